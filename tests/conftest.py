@@ -1,0 +1,23 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) GPU; run with -m gpu")
+    config.addinivalue_line("markers", "slow: long-running (large configs)")
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _native_libs():
+    """Build the CPU-side native libraries (input generator, oracle) once per session."""
+    import ctgen
+    import oracle
+
+    ctgen.build()
+    oracle.build()
