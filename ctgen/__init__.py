@@ -72,6 +72,10 @@ def lib():
         L.ctgen_encrypt.restype = ctypes.c_int
         L.ctgen_encrypt.argtypes = [ctypes.c_int, i64, i64, i64, u64, ctypes.c_int, ctypes.c_int, P,
                                     i64, i64, P, P, ctypes.c_int]
+        L.ctgen_msg_block.restype = None
+        L.ctgen_msg_block.argtypes = [u64, i64, i64, i64, i64, i64, P, ctypes.c_int]
+        L.ctgen_plain_block.restype = None
+        L.ctgen_plain_block.argtypes = [u64, i64, i64, ctypes.c_int, i64, i64, i64, i64, P, ctypes.c_int]
         L.ctgen_uniform_residues.restype = None
         L.ctgen_uniform_residues.argtypes = [u64, u32, i64, P, ctypes.c_int]
         _lib = L
@@ -129,6 +133,19 @@ def plain_matrix(seed: int, N: int, d1: int, rows, cols, log_delta: int) -> np.n
     L = lib()
     return np.array([[L.ctgen_plain(seed, N, d1, int(i), int(j), log_delta) for j in cols] for i in rows],
                     dtype=np.int64)
+
+
+def msg_block(seed: int, d1: int, r0: int, nrows: int, c0: int, ncols: int, nthreads: int = 0) -> np.ndarray:
+    out = np.empty((nrows, ncols), dtype=np.float64)
+    lib().ctgen_msg_block(seed, d1, r0, nrows, c0, ncols, _ptr(out), nthreads)
+    return out
+
+
+def plain_block(seed: int, N: int, d1: int, log_delta: int, r0: int, nrows: int, c0: int, ncols: int,
+                nthreads: int = 0) -> np.ndarray:
+    out = np.empty((nrows, ncols), dtype=np.int64)
+    lib().ctgen_plain_block(seed, N, d1, log_delta, r0, nrows, c0, ncols, _ptr(out), nthreads)
+    return out
 
 
 def U_matrix(seed: int, d2: int, d3: int, bound: int, nthreads: int = 0) -> np.ndarray:

@@ -425,3 +425,25 @@ void ctgen_uniform_residues(uint64_t seed, uint32_t p, int64_t n, uint32_t* out,
 #endif
   for (int64_t i = 0; i < n; ++i) out[i] = (uint32_t)(ctgen_draw64(seed, tag_a(p, 1ULL << 23), (uint64_t)i) % p);
 }
+
+/* Bulk versions (row-major [nrows][ncols] blocks of the d1 x d2 matrices, rows [r0,r0+nrows),
+ * columns [c0,c0+ncols)) for the large-config tests. */
+void ctgen_msg_block(uint64_t seed, int64_t d1, int64_t r0, int64_t nrows, int64_t c0, int64_t ncols, double* out,
+                     int nthreads) {
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(static)
+#endif
+  for (int64_t i = 0; i < nrows; ++i)
+    for (int64_t j = 0; j < ncols; ++j) out[i * ncols + j] = ctgen_msg(seed, d1, r0 + i, c0 + j);
+}
+
+void ctgen_plain_block(uint64_t seed, int64_t N, int64_t d1, int log_delta, int64_t r0, int64_t nrows, int64_t c0,
+                       int64_t ncols, int64_t* out, int nthreads) {
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(static)
+#endif
+  for (int64_t i = 0; i < nrows; ++i)
+    for (int64_t j = 0; j < ncols; ++j) out[i * ncols + j] = ctgen_plain(seed, N, d1, r0 + i, c0 + j, log_delta);
+}

@@ -1,0 +1,156 @@
+/*
+ * ctpt.h — C ABI of the B200 (sm_100a) ciphertext × plaintext matmul library
+ *          (libctpt.so, built from paper_2503_16080_b200/csrc/).
+ *
+ * What it computes.  arXiv 2503.16080, Algorithm 6 step 1:
+ * a matrix M ∈ R^{d1×d2} encrypted column by column in a structured-S format,
+ *     S·A + B ≈ Δ·M (mod q)                  (Lemma le:mat_struct_s),
+ * is multiplied by a known integer plaintext U0 ∈ Z^{d2×d3} as
+ *     (A', B') = (A·U0 mod q, B·U0 mod q),    so that S·A' + B' ≈ Δ·M·U0,
+ * i.e. one Mod-PP-MM_{rows_A,d2,d3} plus one Mod-PP-MM_{d1,d2,d3} (Thm th:pcmm P:1711,
+ * th:pcmm-shs P:1722).  q = p_0·…·p_{L-1} is held in RNS: every product is computed
+ * independently per prime p < 2^31 (the one-product-per-prime structure of Strategy 3,
+ * P:1444–1448).  Rescale (Alg. 6 step 2) is not performed: U is an integer matrix
+ * (scale 1), so the output keeps scale Δ (reading Q3).
+ *
+ * How.  Each 31-bit residue x ∈ [0,p) is split into its four base-2^8 digits (the
+ * signed-digit decomposition of Lemma le:strategy1, with K = 2^8 and
+ * non-negative digits since x ≥ 0); U0's centred residues into balanced int8 digits.
+ * The limb products run on the tcgen05 tensor cores (kind::i8, u8 × s8 → s32 in TMEM);
+ * limb recombination Σ 2^{8ℓ} C_ℓ and the reduction mod p are fused into the epilogue
+ * (P:1385–1388), so only reduced residues are written.
+ *
+ * Formats (Table 1):
+ *   CTPT_RLWE      d1 = N, one key,                  A ∈ Z_q^{N×d2}
+ *   CTPT_SHARED_S  N | d1, one key, S = I ⊗ toep(sk), A ∈ Z_q^{d1×d2}
+ *   CTPT_SHARED_A  N | d1, k = d1/N keys, shared a,  A ∈ Z_q^{N×d2}
+ * rows_A = N (RLWE, shared-a) or d1 (shared-s).  R = rows_A + d1.
+ *
+ * Conventions for every entry point:
+ *  - Residues at the boundary are canonical uint32 in [0, p) (reading Q14).
+ *  - All device memory is allocated and owned by the caller; sizes come from
+ *    ctpt_query_sizes.  The library never allocates or frees device memory and keeps
+ *    no global state besides a per-thread error string.
+ *  - `stream` is a cudaStream_t passed as void*.  All device work is enqueued on it.
+ *    ctpt_layout(validate=0), ctpt_split and ctpt_gemm / ctpt_matmul never synchronise;
+ *    ctpt_plain_precompute* and ctpt_layout(validate=1) synchronise `stream` (they read
+ *    a device-computed value back).
+ *  - Argument validation is synchronous; on a non-OK status nothing was enqueued and
+ *    ctpt_last_error() describes the problem.  Asynchronous CUDA faults surface as
+ *    CTPT_ERR_CUDA on a later call.
+ *  - Calls on distinct streams and distinct buffers may run concurrently.
+ */
+#ifndef CTPT_H_
+#define CTPT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  CTPT_OK = 0,
+  CTPT_ERR_ARG = 1,         /* null pointer, bad enum, bad buffer size                              */
+  CTPT_ERR_SHAPE = 2,       /* Table 1 dimension rules violated, or d2/d3 < 1          */
+  CTPT_ERR_MODULUS = 3,     /* primes must be odd, distinct and 2 < p < 2^31                        */
+  CTPT_ERR_OVERFLOW = 4,    /* exactness bound of the int8 limb products would fail (refuse, never
+                               round: Lemma le:strategy1's d2·‖limb‖·‖limb‖ bound, K = 2^8)          */
+  CTPT_ERR_RANGE = 5,       /* an input residue ≥ p (validate=1), or |U| too large for a shared plane */
+  CTPT_ERR_UNSUPPORTED = 6, /* format / option not implemented (MLWE, structured-A)                  */
+  CTPT_ERR_CUDA = 7         /* a CUDA runtime/driver error (see ctpt_last_error)                    */
+} ctpt_status;
+
+typedef enum { CTPT_RLWE = 0, CTPT_SHARED_S = 1, CTPT_SHARED_A = 2 } ctpt_format;
+
+/* One CP-MM problem, possibly a shard of a larger one:
+ * `primes` may be any subset of the RNS basis and [col_begin, col_end) any block of U's
+ * columns; outputs then hold exactly that shard. */
+typedef struct {
+  int32_t fmt;              /* ctpt_format                                                   */
+  int32_t L;                /* number of primes in `primes` (1..64)                           */
+  int64_t N;                /* ring degree, a power of two                                    */
+  int64_t d1, d2, d3;       /* M ∈ R^{d1×d2}, U ∈ Z^{d2×d3}                                   */
+  const uint32_t* primes;   /* HOST array of L primes                                         */
+  int64_t col_begin;        /* first column of U to multiply (0)                              */
+  int64_t col_end;          /* one past the last column; 0 means d3                          */
+  int32_t kU;               /* int8 digits per U entry, as returned by ctpt_plain_precompute* */
+  int32_t plain_per_prime;  /* 0: one U digit set shared by all primes (ctpt_plain_precompute)
+                               1: per-prime digit sets (ctpt_plain_precompute_rns)            */
+} ctpt_problem;
+
+typedef struct {
+  size_t ctmat_bytes;       /* d_ctmat: 256-byte header + L·R·d2p int32 (K-major stacked [A;B]) */
+  size_t plain_bytes;       /* d_plain for ctpt_plain_precompute: 256 + kU·d3·d2p int8          */
+  size_t plain_rns_bytes;   /* d_plain for ctpt_plain_precompute_rns: 256 + L·4·d3·d2p int8     */
+  size_t workspace_bytes;   /* d_ws for ctpt_matmul / ctpt_split / ctpt_gemm: 4·R·d2p           */
+  size_t out_AU_bytes;      /* L·d3_loc·rows_A uint32                                          */
+  size_t out_BU_bytes;      /* L·d3_loc·d1 uint32                                              */
+  int64_t rows_A, R, d2p, d3_loc;
+} ctpt_sizes;
+
+/* Thread-local description of the last non-OK status (never NULL). */
+const char* ctpt_last_error(void);
+
+/* Library version / build string. */
+const char* ctpt_version(void);
+
+/* Validate `prob` (Table 1 rules, primes, exactness bound for prob->kU; kU=0 is treated as 1)
+ * and fill `out`.  Host only; needs no GPU. */
+ctpt_status ctpt_query_sizes(const ctpt_problem* prob, ctpt_sizes* out);
+
+/* Format layout (column j of A / B are the
+ * coefficients of ciphertext j).  Inputs are the per-column ciphertexts of `prob`'s L primes:
+ *   d_a_polys: uint32 [L][n_a][N], n_a = d2·(k for shared-s, else 1), poly j·k+t = column j chunk t
+ *   d_b_polys: uint32 [L][d2·k][N]
+ * i.e. per prime A and B in column-major order [d2][rows_A] and [d2][d1].
+ * Output d_ctmat (ctmat_bytes): a 256-byte header, then for each prime the stacked matrix
+ * X = [A; B] ∈ Z_p^{R×d2} in row-major (K-major) int32 with row stride d2p = ⌈d2/16⌉·16 and
+ * zero padding.  A pure permutation of int32 values (no limb split; SURVEY.md §8(a) note 2).
+ * validate=1 additionally checks every residue is < p (synchronises; CTPT_ERR_RANGE). */
+ctpt_status ctpt_layout(const ctpt_problem* prob, const uint32_t* d_a_polys, const uint32_t* d_b_polys,
+                        void* d_ctmat, int validate, void* stream);
+
+/* Plaintext precompute ("pre-computation … can be amortized", P:954;
+ * k2 = 1 "when U is low-precision").  d_U: int64 [d2][d3] row-major on the device.
+ * Requires max|U| < min(p)/2 so the centred residue of U is U itself for every prime (else
+ * CTPT_ERR_RANGE: use ctpt_plain_precompute_rns).  Writes kU balanced int8 digit planes
+ * (U^T, K-major, [kU][d3][d2p]) into d_plain and the digit count to *kU_out.  Synchronises. */
+ctpt_status ctpt_plain_precompute(const ctpt_problem* prob, const int64_t* d_U, void* d_plain, int32_t* kU_out,
+                                  void* stream);
+
+/* General plaintext U ∈ Z_q given as canonical residues d_Ures: uint32 [L][d2][d3].
+ * Writes 4 balanced int8 digit planes of each centred residue per prime ([L][4][d3][d2p]),
+ * *kU_out = 4; set prob->plain_per_prime = 1 for the matmul.  Synchronises. */
+ctpt_status ctpt_plain_precompute_rns(const ctpt_problem* prob, const uint32_t* d_Ures, void* d_plain,
+                                      int32_t* kU_out, void* stream);
+
+/* The hot path: (A·U0 mod p, B·U0 mod p) for every prime of `prob` and U columns
+ * [col_begin, col_end) (Alg. 6 step 1).  Per prime: the limb split of X into the
+ * workspace (timed here by design), then the tcgen05 limb GEMM with
+ * the fused recombine + Barrett epilogue (a4, a5).  Outputs in per-column ciphertext layout:
+ *   d_AU: uint32 [L][d3_loc][rows_A], d_BU: uint32 [L][d3_loc][d1]   (output column j is
+ *   ciphertext j of M·U under the same S).
+ * d_ws: workspace_bytes, ws_bytes its size.  Never synchronises. */
+ctpt_status ctpt_matmul(const ctpt_problem* prob, const void* d_ctmat, const void* d_plain, uint32_t* d_AU,
+                        uint32_t* d_BU, void* d_ws, size_t ws_bytes, void* stream);
+
+/* The two stages of ctpt_matmul for prime index l alone (so callers can time them apart):
+ * ctpt_split writes the 4 limb planes of prime l into d_ws; ctpt_gemm consumes them. */
+ctpt_status ctpt_split(const ctpt_problem* prob, int32_t l, const void* d_ctmat, void* d_ws, size_t ws_bytes,
+                       void* stream);
+ctpt_status ctpt_gemm(const ctpt_problem* prob, int32_t l, const void* d_ws, size_t ws_bytes, const void* d_plain,
+                      uint32_t* d_AU_l, uint32_t* d_BU_l, void* stream);
+
+/* Bring-up / diagnostics only (not a product path): the same limb GEMM and epilogue on
+ * CUDA cores, reading the same workspace and plain planes.  Used by the tests to tell a
+ * layout/split bug from a tensor-core descriptor bug. */
+ctpt_status ctpt_gemm_simt(const ctpt_problem* prob, int32_t l, const void* d_ws, size_t ws_bytes,
+                           const void* d_plain, uint32_t* d_AU_l, uint32_t* d_BU_l, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CTPT_H_ */

@@ -1,0 +1,395 @@
+// ctpt.cu — C ABI (include/ctpt.h): validation, size queries, TMA descriptor encoding and
+// kernel launches for the CP-MM hot path on sm_100a.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <climits>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/ctpt.h"
+#include "gemm_tc.cuh"
+#include "kernels.cuh"
+
+using namespace ctpt;
+
+namespace {
+
+thread_local char g_err[512] = "ok";
+
+ctpt_status fail(ctpt_status s, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                          \
+  do {                                                                                          \
+    cudaError_t e_ = (expr);                                                                    \
+    if (e_ != cudaSuccess) return fail(CTPT_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+
+constexpr int kMaxPrimes = 64;
+constexpr size_t kHeader = 256;
+
+struct Dims {
+  int64_t N, d1, d2, d3, k, rows_A, R, d2p, j0, j1, d3_loc;
+  int L;
+};
+
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+ctpt_status check_problem(const ctpt_problem* pb, Dims& d) {
+  if (!pb) return fail(CTPT_ERR_ARG, "problem is NULL");
+  if (pb->fmt < CTPT_RLWE || pb->fmt > CTPT_SHARED_A) return fail(CTPT_ERR_UNSUPPORTED, "unknown format %d", pb->fmt);
+  if (pb->L < 1 || pb->L > kMaxPrimes) return fail(CTPT_ERR_ARG, "L = %d outside 1..%d", pb->L, kMaxPrimes);
+  if (!pb->primes) return fail(CTPT_ERR_ARG, "primes is NULL");
+  if (pb->N < 1 || (pb->N & (pb->N - 1))) return fail(CTPT_ERR_SHAPE, "N = %lld is not a power of two", (long long)pb->N);
+  if (pb->d1 < 1 || pb->d2 < 1 || pb->d3 < 1) return fail(CTPT_ERR_SHAPE, "d1, d2, d3 must be >= 1");
+  // Table 1: RLWE needs d1 = N; shared-s and shared-a need N | d1.
+  if (pb->fmt == CTPT_RLWE && pb->d1 != pb->N) return fail(CTPT_ERR_SHAPE, "RLWE format requires d1 = N");
+  if (pb->d1 % pb->N) return fail(CTPT_ERR_SHAPE, "shared-s / shared-a formats require N | d1");
+  for (int i = 0; i < pb->L; ++i) {
+    const uint32_t p = pb->primes[i];
+    if (p < 3 || !(p & 1u) || p >= (1u << 31)) return fail(CTPT_ERR_MODULUS, "prime %u must be odd and in (2, 2^31)", p);
+    for (int j = 0; j < i; ++j)
+      if (pb->primes[j] == p) return fail(CTPT_ERR_MODULUS, "prime %u repeated", p);
+  }
+  const int64_t c0 = pb->col_begin, c1 = pb->col_end == 0 ? pb->d3 : pb->col_end;
+  if (c0 < 0 || c1 > pb->d3 || c0 >= c1) return fail(CTPT_ERR_SHAPE, "column shard [%lld, %lld) invalid", (long long)c0, (long long)c1);
+  const int kU = pb->kU <= 0 ? 1 : pb->kU;
+  if (kU > 4) return fail(CTPT_ERR_ARG, "kU = %d > 4", kU);
+  // Exactness (Lemma le:strategy1 with K = 2^8): |C_ℓ| ≤ d2 · 255 · 128 must stay < 2^31.
+  if (pb->d2 * 255LL * 128LL >= (1LL << 31)) return fail(CTPT_ERR_OVERFLOW, "d2 = %lld too large for exact int32 limb accumulation (d2 <= 65793)", (long long)pb->d2);
+  d.N = pb->N; d.d1 = pb->d1; d.d2 = pb->d2; d.d3 = pb->d3; d.L = pb->L;
+  d.k = pb->d1 / pb->N;
+  d.rows_A = (pb->fmt == CTPT_SHARED_S) ? pb->d1 : pb->N;
+  d.R = d.rows_A + d.d1;
+  d.d2p = round_up(d.d2, 16);
+  d.j0 = c0; d.j1 = c1; d.d3_loc = c1 - c0;
+  if (d.R > INT32_MAX / 2 || d.d3 > INT32_MAX / 2) return fail(CTPT_ERR_SHAPE, "dimension exceeds TMA coordinate range");
+  return CTPT_OK;
+}
+
+ModP make_modp(uint32_t p) {
+  ModP m;
+  m.p = p;
+  m.mu = static_cast<uint64_t>((static_cast<unsigned __int128>(1) << 64) / p);
+  const uint64_t two56 = 1ULL << 56;
+  m.off = ((two56 + p - 1) / p) * static_cast<uint64_t>(p);
+  return m;
+}
+
+uint32_t pow2mod(int e, uint32_t p) {
+  uint64_t r = 1 % p;
+  for (int i = 0; i < e; ++i) r = (r * 2) % p;
+  return static_cast<uint32_t>(r);
+}
+
+// ---------------------------------------------------------------- TMA descriptors
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 3-D uint8 tensor [dim2][dim1][dim0] with row pitch `pitch1` bytes and plane pitch `pitch2`.
+ctpt_status make_tmap_u8(CUtensorMap* m, const void* base, uint64_t dim0, uint64_t dim1, uint64_t dim2,
+                         uint64_t pitch1, uint64_t pitch2, uint32_t box0, uint32_t box1, uint32_t box2) {
+  auto enc = get_encode();
+  if (!enc) return fail(CTPT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {dim0, dim1, dim2};
+  cuuint64_t strides[2] = {pitch1, pitch2};
+  cuuint32_t box[3] = {box0, box1, box2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CTPT_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+  return CTPT_OK;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+ctpt_status tc_setup() {
+  static cudaError_t e = cudaErrorNotReady;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    e = cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BYTES);
+  });
+  if (e != cudaSuccess) return fail(CTPT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+  return CTPT_OK;
+}
+
+int plane_index(const ctpt_problem* pb, int l, int i) {
+  const int kU = pb->kU <= 0 ? 1 : pb->kU;
+  return pb->plain_per_prime ? l * kU + i : i;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ctpt_last_error(void) { return g_err; }
+
+const char* ctpt_version(void) { return "ctpt 0.1 sm_100a tcgen05 kind::i8 (u8 limbs x s8 U digits)"; }
+
+ctpt_status ctpt_query_sizes(const ctpt_problem* pb, ctpt_sizes* out) {
+  Dims d;
+  ctpt_status s = check_problem(pb, d);
+  if (s != CTPT_OK) return s;
+  if (!out) return fail(CTPT_ERR_ARG, "out is NULL");
+  const int kU = pb->kU <= 0 ? 1 : pb->kU;
+  out->ctmat_bytes = kHeader + static_cast<size_t>(d.L) * d.R * d.d2p * 4;
+  out->plain_bytes = kHeader + static_cast<size_t>(kU) * d.d3 * d.d2p;
+  out->plain_rns_bytes = kHeader + static_cast<size_t>(d.L) * 4 * d.d3 * d.d2p;
+  out->workspace_bytes = static_cast<size_t>(4) * d.R * d.d2p;
+  out->out_AU_bytes = static_cast<size_t>(d.L) * d.d3_loc * d.rows_A * 4;
+  out->out_BU_bytes = static_cast<size_t>(d.L) * d.d3_loc * d.d1 * 4;
+  out->rows_A = d.rows_A;
+  out->R = d.R;
+  out->d2p = d.d2p;
+  out->d3_loc = d.d3_loc;
+  return CTPT_OK;
+}
+
+ctpt_status ctpt_layout(const ctpt_problem* pb, const uint32_t* d_a, const uint32_t* d_b, void* d_ctmat, int validate,
+                        void* stream) {
+  Dims d;
+  ctpt_status s = check_problem(pb, d);
+  if (s != CTPT_OK) return s;
+  if (!d_a || !d_b || !d_ctmat) return fail(CTPT_ERR_ARG, "null device pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* hdr = static_cast<uint8_t*>(d_ctmat);
+  LayoutParams P;
+  memset(&P, 0, sizeof(P));
+  P.a = d_a;
+  P.b = d_b;
+  P.x = reinterpret_cast<uint32_t*>(hdr + kHeader);
+  P.rows_A = d.rows_A;
+  P.d1 = d.d1;
+  P.R = d.R;
+  P.d2 = d.d2;
+  P.d2p = d.d2p;
+  for (int i = 0; i < d.L; ++i) P.p_arr[i] = pb->primes[i];
+  P.validate = validate ? 1 : 0;
+  P.bad_flag = reinterpret_cast<uint32_t*>(hdr);  // header word 0
+  if (validate) CUDA_TRY(cudaMemsetAsync(hdr, 0, 4, st));
+  dim3 grid(static_cast<unsigned>((d.R + 63) / 64), static_cast<unsigned>((d.d2p + 63) / 64), d.L);
+  if (grid.y > 65535) return fail(CTPT_ERR_SHAPE, "d2 too large for the layout grid");
+  k_layout<<<grid, 256, 0, st>>>(P);
+  CUDA_TRY(cudaGetLastError());
+  if (validate) {
+    uint32_t flag = 0;
+    CUDA_TRY(cudaMemcpyAsync(&flag, hdr, 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (flag) return fail(CTPT_ERR_RANGE, "an input residue is >= its prime");
+  }
+  return CTPT_OK;
+}
+
+static ctpt_status plain_common(const ctpt_problem* pb, const int64_t* d_U, const uint32_t* d_Ures, void* d_plain,
+                                int32_t* kU_out, void* stream) {
+  Dims d;
+  ctpt_status s = check_problem(pb, d);
+  if (s != CTPT_OK) return s;
+  if ((!d_U && !d_Ures) || !d_plain || !kU_out) return fail(CTPT_ERR_ARG, "null pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* hdr = static_cast<uint8_t*>(d_plain);
+  PlainParams P;
+  memset(&P, 0, sizeof(P));
+  P.planes = reinterpret_cast<int8_t*>(hdr + kHeader);
+  P.d2 = d.d2;
+  P.d3 = d.d3;
+  P.d2p = d.d2p;
+  int nblk_z = 1;
+  if (d_U) {
+    // max|U| decides k_U (minimal balanced int8 digit count) and whether U's centred
+    // residue is U itself for every prime (needs |U| < p/2).
+    long long init[2] = {LLONG_MAX, LLONG_MIN};
+    CUDA_TRY(cudaMemcpyAsync(hdr, init, 16, cudaMemcpyHostToDevice, st));
+    const int64_t n = d.d2 * d.d3;
+    k_minmax_i64<<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 4096)), 256, 0, st>>>(
+        d_U, n, reinterpret_cast<long long*>(hdr));
+    CUDA_TRY(cudaGetLastError());
+    long long mm[2];
+    CUDA_TRY(cudaMemcpyAsync(mm, hdr, 16, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    uint32_t pmin = pb->primes[0];
+    for (int i = 1; i < d.L; ++i) pmin = std::min(pmin, pb->primes[i]);
+    const long long amax = std::max(mm[1], -mm[0]);
+    if (amax >= static_cast<long long>(pmin / 2))
+      return fail(CTPT_ERR_RANGE, "max|U| = %lld >= min(p)/2: use ctpt_plain_precompute_rns", amax);
+    int kU = 1;
+    // k balanced digits cover [-128·(256^k-1)/255, 127·(256^k-1)/255]
+    while (kU < 4) {
+      const long long span = ((1LL << (8 * kU)) - 1) / 255;
+      if (mm[0] >= -128 * span && mm[1] <= 127 * span) break;
+      ++kU;
+    }
+    P.u = d_U;
+    P.kU = kU;
+    P.rns = 0;
+  } else {
+    P.ures = d_Ures;
+    P.kU = 4;
+    P.rns = 1;
+    for (int i = 0; i < d.L; ++i) P.p_arr[i] = pb->primes[i];
+    nblk_z = d.L;
+  }
+  dim3 grid(static_cast<unsigned>((d.d2p + 31) / 32), static_cast<unsigned>((d.d3 + 31) / 32), nblk_z);
+  if (grid.y > 65535) return fail(CTPT_ERR_SHAPE, "d3 too large for the precompute grid");
+  k_plain<<<grid, 256, 0, st>>>(P);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(st));
+  *kU_out = P.kU;
+  return CTPT_OK;
+}
+
+ctpt_status ctpt_plain_precompute(const ctpt_problem* pb, const int64_t* d_U, void* d_plain, int32_t* kU_out,
+                                  void* stream) {
+  if (!d_U) return fail(CTPT_ERR_ARG, "d_U is NULL");
+  return plain_common(pb, d_U, nullptr, d_plain, kU_out, stream);
+}
+
+ctpt_status ctpt_plain_precompute_rns(const ctpt_problem* pb, const uint32_t* d_Ures, void* d_plain, int32_t* kU_out,
+                                      void* stream) {
+  if (!d_Ures) return fail(CTPT_ERR_ARG, "d_Ures is NULL");
+  return plain_common(pb, nullptr, d_Ures, d_plain, kU_out, stream);
+}
+
+ctpt_status ctpt_split(const ctpt_problem* pb, int32_t l, const void* d_ctmat, void* d_ws, size_t ws_bytes,
+                       void* stream) {
+  Dims d;
+  ctpt_status s = check_problem(pb, d);
+  if (s != CTPT_OK) return s;
+  if (l < 0 || l >= d.L) return fail(CTPT_ERR_ARG, "prime index %d out of range", l);
+  if (!d_ctmat || !d_ws) return fail(CTPT_ERR_ARG, "null device pointer");
+  if (ws_bytes < static_cast<size_t>(4) * d.R * d.d2p) return fail(CTPT_ERR_ARG, "workspace too small");
+  const int64_t n = d.R * d.d2p;  // multiple of 16
+  const uint4* x = reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(d_ctmat) + kHeader) + (l * n) / 4;
+  const int64_t n16 = n / 16;
+  const int blocks = static_cast<int>(std::min<int64_t>((n16 + 255) / 256, static_cast<int64_t>(num_sms()) * 16));
+  k_split<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(x, static_cast<uint4*>(d_ws), n16);
+  CUDA_TRY(cudaGetLastError());
+  return CTPT_OK;
+}
+
+static ctpt_status gemm_common(const ctpt_problem* pb, int32_t l, const void* d_ws, size_t ws_bytes,
+                               const void* d_plain, uint32_t* d_AU_l, uint32_t* d_BU_l, void* stream, bool simt) {
+  Dims d;
+  ctpt_status s = check_problem(pb, d);
+  if (s != CTPT_OK) return s;
+  if (l < 0 || l >= d.L) return fail(CTPT_ERR_ARG, "prime index %d out of range", l);
+  if (!d_ws || !d_plain || !d_AU_l || !d_BU_l) return fail(CTPT_ERR_ARG, "null device pointer");
+  if (ws_bytes < static_cast<size_t>(4) * d.R * d.d2p) return fail(CTPT_ERR_ARG, "workspace too small");
+  const int kU = pb->kU <= 0 ? 1 : pb->kU;
+  const uint32_t p = pb->primes[l];
+  const ModP m = make_modp(p);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int8_t* planes = reinterpret_cast<const int8_t*>(static_cast<const uint8_t*>(d_plain) + kHeader);
+  const int nplanes = pb->plain_per_prime ? d.L * kU : kU;
+  OutParams o;
+  o.AU = d_AU_l;
+  o.BU = d_BU_l;
+  o.rows_A = d.rows_A;
+  o.d1 = d.d1;
+  o.R = d.R;
+  o.d3_loc = d.d3_loc;
+  if (simt) {
+    for (int i = 0; i < kU; ++i) {
+      SimtParams S;
+      S.limbs = static_cast<const uint8_t*>(d_ws);
+      S.uplane = planes + static_cast<int64_t>(plane_index(pb, l, i)) * d.d3 * d.d2p;
+      S.R = d.R;
+      S.d2 = d.d2;
+      S.d2p = d.d2p;
+      S.j_off = d.j0;
+      S.m = m;
+      S.o = o;
+      S.o.accumulate = i > 0;
+      S.o.w = pow2mod(8 * i, p);
+      dim3 grid(static_cast<unsigned>((d.R + 15) / 16), static_cast<unsigned>((d.d3_loc + 15) / 16));
+      k_gemm_simt<<<grid, 256, 0, st>>>(S);
+      CUDA_TRY(cudaGetLastError());
+    }
+    return CTPT_OK;
+  }
+  s = tc_setup();
+  if (s != CTPT_OK) return s;
+  CUtensorMap tmU, tmX;
+  s = make_tmap_u8(&tmU, planes, d.d2, d.d3, nplanes, d.d2p, d.d3 * d.d2p, TC_BLOCK_K, TC_BLOCK_J, 1);
+  if (s != CTPT_OK) return s;
+  s = make_tmap_u8(&tmX, d_ws, d.d2, d.R, 4, d.d2p, d.R * d.d2p, TC_BLOCK_K, TC_BLOCK_R, 4);
+  if (s != CTPT_OK) return s;
+  TcParams P;
+  P.R = d.R;
+  P.d2 = d.d2;
+  P.j_off = static_cast<int32_t>(d.j0);
+  P.num_kb = static_cast<int32_t>((d.d2 + TC_BLOCK_K - 1) / TC_BLOCK_K);
+  P.tiles_j = static_cast<int32_t>((d.d3_loc + TC_BLOCK_J - 1) / TC_BLOCK_J);
+  P.tiles_r = static_cast<int32_t>((d.R + TC_BLOCK_R - 1) / TC_BLOCK_R);
+  const int64_t nt = static_cast<int64_t>(P.tiles_j) * P.tiles_r;
+  if (nt > INT32_MAX) return fail(CTPT_ERR_SHAPE, "too many tiles");
+  P.num_tiles = static_cast<int32_t>(nt);
+  P.m = m;
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(nt, num_sms()));
+  for (int i = 0; i < kU; ++i) {
+    P.plane = plane_index(pb, l, i);
+    P.o = o;
+    P.o.accumulate = i > 0;
+    P.o.w = pow2mod(8 * i, p);
+    k_gemm_tc<<<grid, TC_THREADS, TC_SMEM_BYTES, st>>>(tmU, tmX, P);
+    CUDA_TRY(cudaGetLastError());
+  }
+  return CTPT_OK;
+}
+
+ctpt_status ctpt_gemm(const ctpt_problem* pb, int32_t l, const void* d_ws, size_t ws_bytes, const void* d_plain,
+                      uint32_t* d_AU_l, uint32_t* d_BU_l, void* stream) {
+  return gemm_common(pb, l, d_ws, ws_bytes, d_plain, d_AU_l, d_BU_l, stream, false);
+}
+
+ctpt_status ctpt_gemm_simt(const ctpt_problem* pb, int32_t l, const void* d_ws, size_t ws_bytes, const void* d_plain,
+                           uint32_t* d_AU_l, uint32_t* d_BU_l, void* stream) {
+  return gemm_common(pb, l, d_ws, ws_bytes, d_plain, d_AU_l, d_BU_l, stream, true);
+}
+
+ctpt_status ctpt_matmul(const ctpt_problem* pb, const void* d_ctmat, const void* d_plain, uint32_t* d_AU,
+                        uint32_t* d_BU, void* d_ws, size_t ws_bytes, void* stream) {
+  Dims d;
+  ctpt_status s = check_problem(pb, d);
+  if (s != CTPT_OK) return s;
+  if (!d_AU || !d_BU) return fail(CTPT_ERR_ARG, "null output pointer");
+  for (int l = 0; l < d.L; ++l) {
+    s = ctpt_split(pb, l, d_ctmat, d_ws, ws_bytes, stream);
+    if (s != CTPT_OK) return s;
+    s = ctpt_gemm(pb, l, d_ws, ws_bytes, d_plain, d_AU + static_cast<int64_t>(l) * d.d3_loc * d.rows_A,
+                  d_BU + static_cast<int64_t>(l) * d.d3_loc * d.d1, stream);
+    if (s != CTPT_OK) return s;
+  }
+  return CTPT_OK;
+}
+
+}  // extern "C"

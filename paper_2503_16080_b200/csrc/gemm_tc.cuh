@@ -1,0 +1,197 @@
+// gemm_tc.cuh — the limb GEMM on the 5th-generation tensor cores (SURVEY.md §8(a) a4 + a5).
+//
+// Per prime p, with X = [A; B] ∈ Z_p^{R×d2} split into four u8 limb planes X_ℓ and U0's
+// balanced s8 digit plane U (k_U = 1 per pass):
+//     C_ℓ = X_ℓ · U   over Z (int32, exact: d2·255·128 < 2^31),
+//     out = (C_0 + 2^8 C_1 + 2^16 C_2 + 2^24 C_3) mod p
+//
+// Mapping onto tcgen05.mma.cta_group::1.kind::i8 (D[M×N] += A[M×K]·B[N×K]^T, K-major both):
+//   MMA "A" = U^T tile: 128 output columns j × K        (s8, TMEM lanes = j)
+//   MMA "B" = 4 limb tiles stacked: (ℓ, r) = ℓ·64 + r, 256 × K   (u8)
+//   D = 128 lanes × 256 int32 columns: lane j holds C_ℓ[r][j] at column ℓ·64 + r, so one
+//   epilogue thread owns all four limb sums of its 64 outputs — recombination needs no
+//   data exchange.  One MMA (M=128, N=256, K=32) per 32-byte K step.
+// Tiles: 128 (j) × 64 (r) outputs, K-block 128 bytes, 4-stage TMA→SMEM ring (48 KB/stage),
+// double-buffered TMEM accumulators (2 × 256 columns = all 512).
+// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator, w4–7 epilogue.
+// Persistent: grid = min(#tiles, #SMs); tiles visited in groups of GROUP_J j-tiles so the
+// U panels of a group stay in L2 while the X panels stream.
+#pragma once
+#include <cstdint>
+
+#include "kernels.cuh"
+#include "ptx.cuh"
+
+namespace ctpt {
+
+constexpr int TC_BLOCK_J = 128;   // MMA M (output columns per tile)
+constexpr int TC_BLOCK_R = 64;    // rows of X per tile (× 4 limbs = MMA N = 256)
+constexpr int TC_BLOCK_K = 128;   // bytes of K per stage (one 128-B swizzle row)
+constexpr int TC_STAGES = 4;
+constexpr int TC_MMA_K = 32;      // K per kind::i8 MMA
+constexpr int TC_U_BYTES = TC_BLOCK_J * TC_BLOCK_K;            // 16 KB
+constexpr int TC_X_BYTES = 4 * TC_BLOCK_R * TC_BLOCK_K;        // 32 KB
+constexpr int TC_STAGE_BYTES = TC_U_BYTES + TC_X_BYTES;        // 48 KB
+constexpr int TC_ACC_COLS = 4 * TC_BLOCK_R;                    // 256
+constexpr int TC_THREADS = 256;
+constexpr int TC_SMEM_BYTES = TC_STAGES * TC_STAGE_BYTES + 256 + 1024;
+constexpr int TC_GROUP_J = 16;
+
+struct TcParams {
+  int64_t R, d2;
+  int32_t j_off;      // first U column (col_begin)
+  int32_t plane;      // U digit plane index (3rd TMA coordinate)
+  int32_t num_kb;     // ceil(d2 / 128)
+  int32_t tiles_j, tiles_r;
+  int32_t num_tiles;
+  ModP m;
+  OutParams o;
+};
+
+__device__ __forceinline__ void tc_tile_coords(int32_t tile, const TcParams& P, int32_t& tj, int32_t& tr) {
+  const int32_t per_group = TC_GROUP_J * P.tiles_r;
+  const int32_t g = tile / per_group;
+  const int32_t rem = tile - g * per_group;
+  const int32_t gj = min(TC_GROUP_J, P.tiles_j - g * TC_GROUP_J);
+  tj = g * TC_GROUP_J + rem % gj;
+  tr = rem / gj;
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    k_gemm_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmX,
+              const __grid_constant__ TcParams P) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar_base = sbase + TC_STAGES * TC_STAGE_BYTES;
+  auto full_bar = [&](int s) { return bar_base + 8u * s; };
+  auto empty_bar = [&](int s) { return bar_base + 8u * (TC_STAGES + s); };
+  auto tfull_bar = [&](int b) { return bar_base + 8u * (2 * TC_STAGES + b); };
+  auto tempty_bar = [&](int b) { return bar_base + 8u * (2 * TC_STAGES + 2 + b); };
+  const uint32_t tmem_slot = bar_base + 8u * (2 * TC_STAGES + 4);
+  uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(smem + TC_STAGES * TC_STAGE_BYTES + 8 * (2 * TC_STAGES + 4));
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmU);
+    tma_prefetch(&tmX);
+    for (int s = 0; s < TC_STAGES; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull_bar(b), 1);
+      mbar_init(tempty_bar(b), 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot_ptr;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int32_t tile = blockIdx.x; tile < P.num_tiles; tile += gridDim.x) {
+        int32_t tj, tr;
+        tc_tile_coords(tile, P, tj, tr);
+        for (int32_t kb = 0; kb < P.num_kb; ++kb) {
+          mbar_wait(empty_bar(stage), phase ^ 1);
+          const uint32_t su = sbase + stage * TC_STAGE_BYTES;
+          mbar_arrive_expect_tx(full_bar(stage), TC_STAGE_BYTES);
+          tma_load_3d(su, &tmU, full_bar(stage), kb * TC_BLOCK_K, P.j_off + tj * TC_BLOCK_J, P.plane);
+          tma_load_3d(su + TC_U_BYTES, &tmX, full_bar(stage), kb * TC_BLOCK_K, tr * TC_BLOCK_R, 0);
+          if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_i8(TC_BLOCK_J, TC_ACC_COLS, /*a_signed=*/true, /*b_signed=*/false);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int32_t tile = blockIdx.x; tile < P.num_tiles; tile += gridDim.x) {
+        mbar_wait(tempty_bar(acc), acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * TC_ACC_COLS;
+        for (int32_t kb = 0; kb < P.num_kb; ++kb) {
+          mbar_wait(full_bar(stage), phase);
+          tc_fence_after();
+          const uint32_t su = sbase + stage * TC_STAGE_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < TC_BLOCK_K / TC_MMA_K; ++kk) {
+            const uint64_t ad = umma_desc_sw128(su + kk * TC_MMA_K);
+            const uint64_t bd = umma_desc_sw128(su + TC_U_BYTES + kk * TC_MMA_K);
+            mma_i8(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+          }
+          mma_commit(empty_bar(stage));  // frees the SMEM stage once these MMAs have read it
+          if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(tfull_bar(acc));  // accumulator ready for the epilogue
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------------------------------------------------------- epilogue (128 threads)
+    const int quad = warp & 3;  // TMEM lanes [32·quad, 32·quad + 32)
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    const bool vec_ok = ((P.o.rows_A & 3) == 0) && ((P.o.d1 & 3) == 0) && !P.o.accumulate;
+    for (int32_t tile = blockIdx.x; tile < P.num_tiles; tile += gridDim.x) {
+      int32_t tj, tr;
+      tc_tile_coords(tile, P, tj, tr);
+      mbar_wait(tfull_bar(acc), acc_phase);
+      tc_fence_after();
+      const int64_t j = static_cast<int64_t>(tj) * TC_BLOCK_J + quad * 32 + lane;
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * TC_ACC_COLS;
+#pragma unroll 1
+      for (int c = 0; c < TC_BLOCK_R / 16; ++c) {
+        uint32_t v0[16], v1[16], v2[16], v3[16];
+        tmem_ld16(t_row + 0 * TC_BLOCK_R + c * 16, v0);
+        tmem_ld16(t_row + 1 * TC_BLOCK_R + c * 16, v1);
+        tmem_ld16(t_row + 2 * TC_BLOCK_R + c * 16, v2);
+        tmem_ld16(t_row + 3 * TC_BLOCK_R + c * 16, v3);
+        tmem_ld_wait();
+        uint32_t res[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          res[i] = recombine_mod(static_cast<int32_t>(v0[i]), static_cast<int32_t>(v1[i]),
+                                 static_cast<int32_t>(v2[i]), static_cast<int32_t>(v3[i]), P.m);
+        if (j < P.o.d3_loc) {
+          const int64_t r0 = static_cast<int64_t>(tr) * TC_BLOCK_R + c * 16;
+          const bool in_a = (r0 + 15 < P.o.rows_A), in_b = (r0 >= P.o.rows_A);
+          if (vec_ok && r0 + 15 < P.o.R && (in_a || in_b)) {
+            uint4* q = reinterpret_cast<uint4*>(out_ptr(P.o, j, r0));
+#pragma unroll
+            for (int i = 0; i < 4; ++i) q[i] = make_uint4(res[4 * i], res[4 * i + 1], res[4 * i + 2], res[4 * i + 3]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (r0 + i < P.o.R) store_out(P.o, P.m, j, r0 + i, res[i]);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tempty_bar(acc));
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem_base);
+  }
+}
+
+}  // namespace ctpt

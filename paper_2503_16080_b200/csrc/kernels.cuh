@@ -1,0 +1,238 @@
+// kernels.cuh — the memory-bound kernels of the CP-MM path (layout, plaintext precompute,
+// limb split) and the shared epilogue arithmetic (limb recombination + Barrett reduction).
+#pragma once
+#include <cstdint>
+
+namespace ctpt {
+
+// ------------------------------------------------------------------------------------------
+// Epilogue arithmetic ("compute their sum using integer arithmetic …
+// then reduce it modulo the modulus").
+// ------------------------------------------------------------------------------------------
+struct ModP {
+  uint32_t p;
+  uint64_t mu;   // floor(2^64 / p)
+  uint64_t off;  // p * ceil(2^56 / p): makes t + off non-negative for |t| < 2^56
+};
+
+// r = x mod p for x < 2^64 (Barrett with a 64-bit reciprocal; q_est ∈ {q-1, q}).
+__device__ __forceinline__ uint32_t barrett64(uint64_t x, const ModP& m) {
+  uint64_t q = __umul64hi(x, m.mu);
+  uint64_t r = x - q * m.p;
+  r = (r >= m.p) ? r - m.p : r;
+  r = (r >= m.p) ? r - m.p : r;
+  return static_cast<uint32_t>(r);
+}
+
+// t = C0 + 2^8 C1 + 2^16 C2 + 2^24 C3 (exact in int64), reduced to [0, p).
+__device__ __forceinline__ uint32_t recombine_mod(int32_t c0, int32_t c1, int32_t c2, int32_t c3, const ModP& m) {
+  int64_t t = static_cast<int64_t>(c0) + (static_cast<int64_t>(c1) << 8) + (static_cast<int64_t>(c2) << 16) +
+              (static_cast<int64_t>(c3) << 24);
+  return barrett64(static_cast<uint64_t>(t + static_cast<int64_t>(m.off)), m);
+}
+
+// (prev + w·r) mod p for the k_U > 1 accumulation passes (Σ_i 2^{8i} (A·U_i) mod p).
+__device__ __forceinline__ uint32_t accum_mod(uint32_t prev, uint32_t r, uint32_t w, const ModP& m) {
+  uint64_t x = static_cast<uint64_t>(r) * w + prev;  // < 2^62 + 2^31
+  return barrett64(x, m);
+}
+
+// ------------------------------------------------------------------------------------------
+// Layout: per-column ciphertexts (column-major A [d2][rows_A], B [d2][d1] per prime) →
+// stacked K-major X = [A; B] int32 [R][d2p].  Pure permutation (§8(a) a1).
+// 64x64 tiles through shared memory so both the reads (along r) and writes (along k) coalesce.
+// ------------------------------------------------------------------------------------------
+struct LayoutParams {
+  const uint32_t* a;  // [L][d2][rows_A]
+  const uint32_t* b;  // [L][d2][d1]
+  uint32_t* x;        // [L][R][d2p]
+  int64_t rows_A, d1, R, d2, d2p;
+  const uint32_t* primes_dev;  // unused (primes passed in p_arr)
+  uint32_t p_arr[64];
+  int32_t validate;
+  uint32_t* bad_flag;  // device word, OR-ed with 1 on a residue ≥ p
+};
+
+__global__ void __launch_bounds__(256) k_layout(const __grid_constant__ LayoutParams P) {
+  __shared__ uint32_t tile[64][65];
+  const int l = blockIdx.z;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 64;
+  const int64_t k0 = static_cast<int64_t>(blockIdx.y) * 64;
+  const uint32_t p = P.p_arr[l];
+  const uint32_t* a = P.a + static_cast<int64_t>(l) * P.d2 * P.rows_A;
+  const uint32_t* b = P.b + static_cast<int64_t>(l) * P.d2 * P.d1;
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 x 4
+  bool bad = false;
+  // read: element (k, r) with r fastest
+  for (int kk = ty; kk < 64; kk += 4) {
+    const int64_t k = k0 + kk, r = r0 + tx;
+    uint32_t v = 0;
+    if (k < P.d2 && r < P.R) {
+      v = (r < P.rows_A) ? a[k * P.rows_A + r] : b[k * P.d1 + (r - P.rows_A)];
+      bad |= (v >= p);
+    }
+    tile[kk][tx] = v;
+  }
+  __syncthreads();
+  uint32_t* x = P.x + static_cast<int64_t>(l) * P.R * P.d2p;
+  for (int rr = ty; rr < 64; rr += 4) {
+    const int64_t r = r0 + rr, k = k0 + tx;
+    if (r < P.R && k < P.d2p) x[r * P.d2p + k] = tile[tx][rr];  // zero for k >= d2
+  }
+  if (P.validate && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(P.bad_flag, 1u);
+}
+
+// ------------------------------------------------------------------------------------------
+// Limb split (inside the timed ctpt_matmul): x = Σ_{ℓ<4} x_ℓ 2^{8ℓ},
+// x_ℓ ∈ [0,255] — the digits of Lemma le:strategy1's decomposition with
+// K = 2^8 for a canonical (non-negative) residue.  int32 [n] → uint8 [4][n]; 16 elements per
+// thread: 4 × 16-B loads, an 8-PRMT 4×4 byte transpose per 4 words, 4 × 16-B stores.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void byte_transpose4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint32_t& l0,
+                                                uint32_t& l1, uint32_t& l2, uint32_t& l3) {
+  const uint32_t t0 = __byte_perm(w0, w1, 0x5140), t1 = __byte_perm(w0, w1, 0x7362);
+  const uint32_t t2 = __byte_perm(w2, w3, 0x5140), t3 = __byte_perm(w2, w3, 0x7362);
+  l0 = __byte_perm(t0, t2, 0x5410);
+  l1 = __byte_perm(t0, t2, 0x7632);
+  l2 = __byte_perm(t1, t3, 0x5410);
+  l3 = __byte_perm(t1, t3, 0x7632);
+}
+
+__global__ void __launch_bounds__(256) k_split(const uint4* __restrict__ x, uint4* __restrict__ limbs, int64_t n16) {
+  // n16 = number of 16-element groups; plane stride = n16 uint4
+  for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < n16;
+       g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint4 w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) w[i] = __ldcs(x + 4 * g + i);  // streaming: read once
+    uint32_t o[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) byte_transpose4(w[i].x, w[i].y, w[i].z, w[i].w, o[0][i], o[1][i], o[2][i], o[3][i]);
+#pragma unroll
+    for (int l = 0; l < 4; ++l) limbs[l * n16 + g] = make_uint4(o[l][0], o[l][1], o[l][2], o[l][3]);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Plaintext precompute (§8(a) a2): U int64 [d2][d3] → balanced int8 digits of the centred
+// residue, written transposed (U^T, K-major) as planes [kU][d3][d2p].
+// ------------------------------------------------------------------------------------------
+__global__ void k_minmax_i64(const int64_t* __restrict__ u, int64_t n, long long* mm /*[2]: min, max*/) {
+  long long lo = LLONG_MAX, hi = LLONG_MIN;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    long long v = u[i];
+    lo = v < lo ? v : lo;
+    hi = v > hi ? v : hi;
+  }
+  for (int o = 16; o; o >>= 1) {
+    long long a = __shfl_xor_sync(0xffffffffu, lo, o), b = __shfl_xor_sync(0xffffffffu, hi, o);
+    lo = a < lo ? a : lo;
+    hi = b > hi ? b : hi;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(mm, lo);
+    atomicMax(mm + 1, hi);
+  }
+}
+
+// balanced digit: d = ((x + 128) mod 256) - 128, x <- (x - d) / 256
+__device__ __forceinline__ int8_t balanced_digit(int64_t& x) {
+  const int64_t d = ((x + 128) & 255) - 128;
+  x = (x - d) >> 8;
+  return static_cast<int8_t>(d);
+}
+
+struct PlainParams {
+  const int64_t* u;     // [d2][d3] (int64 mode)
+  const uint32_t* ures; // [L][d2][d3] (rns mode)
+  int8_t* planes;       // [nplanes][d3][d2p]
+  int64_t d2, d3, d2p;
+  int32_t kU;
+  int32_t rns;          // 0: shared planes from int64 U; 1: per-prime planes from residues
+  uint32_t p_arr[64];
+};
+
+// grid: (ceil(d2p/32), ceil(d3/32), L or 1); block 32x8.  Reads coalesce along j, writes along k.
+__global__ void __launch_bounds__(256) k_plain(const __grid_constant__ PlainParams P) {
+  __shared__ int8_t t[4][32][33];
+  const int l = blockIdx.z;
+  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * 32, j0 = static_cast<int64_t>(blockIdx.y) * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int kk = ty; kk < 32; kk += 8) {
+    const int64_t k = k0 + kk, j = j0 + tx;
+    int64_t x = 0;
+    if (k < P.d2 && j < P.d3) {
+      if (P.rns) {
+        const uint32_t p = P.p_arr[l];
+        const uint32_t v = P.ures[(static_cast<int64_t>(l) * P.d2 + k) * P.d3 + j];
+        x = (v > p / 2) ? static_cast<int64_t>(v) - p : static_cast<int64_t>(v);  // centred residue
+      } else {
+        x = P.u[k * P.d3 + j];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) t[i][kk][tx] = (i < P.kU) ? balanced_digit(x) : 0;
+  }
+  __syncthreads();
+  for (int jj = ty; jj < 32; jj += 8) {
+    const int64_t j = j0 + jj, k = k0 + tx;
+    if (j < P.d3 && k < P.d2p) {
+      for (int i = 0; i < P.kU; ++i) {
+        const int64_t plane = static_cast<int64_t>(l) * P.kU + i;
+        P.planes[(plane * P.d3 + j) * P.d2p + k] = t[i][tx][jj];
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Epilogue output routing shared by both GEMMs: row r of the stacked X is row r of A'
+// (r < rows_A) or row r - rows_A of B'; output column j is contiguous (per-column layout).
+// ------------------------------------------------------------------------------------------
+struct OutParams {
+  uint32_t* AU;  // [d3_loc][rows_A]
+  uint32_t* BU;  // [d3_loc][d1]
+  int64_t rows_A, d1, R, d3_loc;
+  uint32_t w;          // 2^{8i} mod p for pass i
+  int32_t accumulate;  // pass i > 0: out = (out + w·r) mod p
+};
+
+__device__ __forceinline__ uint32_t* out_ptr(const OutParams& o, int64_t j, int64_t r) {
+  return (r < o.rows_A) ? o.AU + j * o.rows_A + r : o.BU + j * o.d1 + (r - o.rows_A);
+}
+
+__device__ __forceinline__ void store_out(const OutParams& o, const ModP& m, int64_t j, int64_t r, uint32_t v) {
+  uint32_t* q = out_ptr(o, j, r);
+  if (o.accumulate) v = accum_mod(*q, v, o.w, m);
+  *q = v;
+}
+
+// ------------------------------------------------------------------------------------------
+// CUDA-core bring-up GEMM (diagnostics only): same limb planes, same epilogue.
+// One thread per (j, r) output; block 16 (r) x 16 (j).
+// ------------------------------------------------------------------------------------------
+struct SimtParams {
+  const uint8_t* limbs;  // [4][R][d2p]
+  const int8_t* uplane;  // [d3_total][d2p] plane for this pass
+  int64_t R, d2, d2p, j_off;
+  ModP m;
+  OutParams o;
+};
+
+__global__ void k_gemm_simt(const __grid_constant__ SimtParams P) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * 16 + (threadIdx.x & 15);
+  const int64_t j = static_cast<int64_t>(blockIdx.y) * 16 + (threadIdx.x >> 4);
+  if (r >= P.R || j >= P.o.d3_loc) return;
+  int32_t c[4] = {0, 0, 0, 0};
+  const int8_t* u = P.uplane + (P.j_off + j) * P.d2p;
+  const int64_t plane = P.R * P.d2p;
+  for (int64_t k = 0; k < P.d2; ++k) {
+    const int32_t uk = u[k];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) c[l] += static_cast<int32_t>(P.limbs[l * plane + r * P.d2p + k]) * uk;
+  }
+  store_out(P.o, P.m, j, r, recombine_mod(c[0], c[1], c[2], c[3], P.m));
+}
+
+}  // namespace ctpt

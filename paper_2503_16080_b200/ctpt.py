@@ -1,0 +1,173 @@
+"""Thin ctypes binding of libctpt.so (include/ctpt.h) — argument marshalling only.
+
+Every step of the CP-MM path runs in the library's CUDA kernels; this module only
+turns torch tensors into device pointers and the current CUDA stream into the
+``void* stream`` argument.  There is no CPU fallback: importing this module on a
+machine without the built library raises, and every call that returns a non-OK
+status raises :class:`CtptError`.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+from dataclasses import dataclass
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libctpt.so")
+HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "ctpt.h")
+
+RLWE, SHARED_S, SHARED_A = 0, 1, 2
+STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_SHAPE", 3: "ERR_MODULUS", 4: "ERR_OVERFLOW", 5: "ERR_RANGE",
+          6: "ERR_UNSUPPORTED", 7: "ERR_CUDA"}
+
+
+class CtptError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libctpt.so not built at {LIB_PATH}; run __graft_entry__.build() (no CPU fallback exists)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+
+class Problem(ctypes.Structure):
+    _fields_ = [("fmt", ctypes.c_int32), ("L", ctypes.c_int32), ("N", ctypes.c_int64), ("d1", ctypes.c_int64),
+                ("d2", ctypes.c_int64), ("d3", ctypes.c_int64), ("primes", ctypes.POINTER(ctypes.c_uint32)),
+                ("col_begin", ctypes.c_int64), ("col_end", ctypes.c_int64), ("kU", ctypes.c_int32),
+                ("plain_per_prime", ctypes.c_int32)]
+
+
+class Sizes(ctypes.Structure):
+    _fields_ = [("ctmat_bytes", ctypes.c_size_t), ("plain_bytes", ctypes.c_size_t),
+                ("plain_rns_bytes", ctypes.c_size_t), ("workspace_bytes", ctypes.c_size_t),
+                ("out_AU_bytes", ctypes.c_size_t), ("out_BU_bytes", ctypes.c_size_t), ("rows_A", ctypes.c_int64),
+                ("R", ctypes.c_int64), ("d2p", ctypes.c_int64), ("d3_loc", ctypes.c_int64)]
+
+
+_P = ctypes.c_void_p
+_PP = ctypes.POINTER(Problem)
+_sig = {
+    "ctpt_last_error": (ctypes.c_char_p, []),
+    "ctpt_version": (ctypes.c_char_p, []),
+    "ctpt_query_sizes": (ctypes.c_int, [_PP, ctypes.POINTER(Sizes)]),
+    "ctpt_layout": (ctypes.c_int, [_PP, _P, _P, _P, ctypes.c_int, _P]),
+    "ctpt_plain_precompute": (ctypes.c_int, [_PP, _P, _P, ctypes.POINTER(ctypes.c_int32), _P]),
+    "ctpt_plain_precompute_rns": (ctypes.c_int, [_PP, _P, _P, ctypes.POINTER(ctypes.c_int32), _P]),
+    "ctpt_matmul": (ctypes.c_int, [_PP, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
+    "ctpt_split": (ctypes.c_int, [_PP, ctypes.c_int32, _P, _P, ctypes.c_size_t, _P]),
+    "ctpt_gemm": (ctypes.c_int, [_PP, ctypes.c_int32, _P, ctypes.c_size_t, _P, _P, _P, _P]),
+    "ctpt_gemm_simt": (ctypes.c_int, [_PP, ctypes.c_int32, _P, ctypes.c_size_t, _P, _P, _P, _P]),
+}
+for _name, (_res, _args) in _sig.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+
+def header_symbols() -> list[str]:
+    """Every function name include/ctpt.h declares."""
+    txt = open(HEADER_PATH).read()
+    return sorted(set(re.findall(r"\b(ctpt_[a-z0-9_]+)\s*\(", txt)))
+
+
+def _check(status: int):
+    if status != 0:
+        raise CtptError(status, _lib.ctpt_last_error().decode())
+
+
+def version() -> str:
+    return _lib.ctpt_version().decode()
+
+
+@dataclass
+class Spec:
+    """A CP-MM problem (or shard): format, ring degree, dims, primes, U column block."""
+    fmt: int
+    N: int
+    d1: int
+    d2: int
+    d3: int
+    primes: list
+    col_begin: int = 0
+    col_end: int = 0
+    kU: int = 1
+    plain_per_prime: int = 0
+
+    def cstruct(self) -> Problem:
+        arr = (ctypes.c_uint32 * len(self.primes))(*[int(p) for p in self.primes])
+        pb = Problem(self.fmt, len(self.primes), self.N, self.d1, self.d2, self.d3, arr, self.col_begin,
+                     self.col_end, self.kU, self.plain_per_prime)
+        pb._keep = arr  # keep the host prime array alive with the struct
+        return pb
+
+
+def _ptr(t) -> ctypes.c_void_p:
+    if t is None:
+        return ctypes.c_void_p(0)
+    if isinstance(t, int):
+        return ctypes.c_void_p(t)
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream) -> ctypes.c_void_p:
+    if stream is None:
+        import torch
+
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def query_sizes(spec: Spec) -> Sizes:
+    s = Sizes()
+    pb = spec.cstruct()
+    _check(_lib.ctpt_query_sizes(ctypes.byref(pb), ctypes.byref(s)))
+    return s
+
+
+def layout(spec: Spec, a_polys, b_polys, ctmat, validate: bool = False, stream=None):
+    pb = spec.cstruct()
+    _check(_lib.ctpt_layout(ctypes.byref(pb), _ptr(a_polys), _ptr(b_polys), _ptr(ctmat), int(validate),
+                            _stream(stream)))
+
+
+def plain_precompute(spec: Spec, U, plain, stream=None) -> int:
+    pb = spec.cstruct()
+    kU = ctypes.c_int32(0)
+    _check(_lib.ctpt_plain_precompute(ctypes.byref(pb), _ptr(U), _ptr(plain), ctypes.byref(kU), _stream(stream)))
+    return kU.value
+
+
+def plain_precompute_rns(spec: Spec, Ures, plain, stream=None) -> int:
+    pb = spec.cstruct()
+    kU = ctypes.c_int32(0)
+    _check(_lib.ctpt_plain_precompute_rns(ctypes.byref(pb), _ptr(Ures), _ptr(plain), ctypes.byref(kU),
+                                          _stream(stream)))
+    return kU.value
+
+
+def matmul(spec: Spec, ctmat, plain, AU, BU, ws, stream=None):
+    pb = spec.cstruct()
+    nbytes = ws.numel() * ws.element_size()
+    _check(_lib.ctpt_matmul(ctypes.byref(pb), _ptr(ctmat), _ptr(plain), _ptr(AU), _ptr(BU), _ptr(ws), nbytes,
+                            _stream(stream)))
+
+
+def split(spec: Spec, l: int, ctmat, ws, stream=None):
+    pb = spec.cstruct()
+    _check(_lib.ctpt_split(ctypes.byref(pb), l, _ptr(ctmat), _ptr(ws), ws.numel() * ws.element_size(),
+                           _stream(stream)))
+
+
+def gemm(spec: Spec, l: int, ws, plain, AU_l, BU_l, stream=None, simt: bool = False):
+    pb = spec.cstruct()
+    f = _lib.ctpt_gemm_simt if simt else _lib.ctpt_gemm
+    _check(f(ctypes.byref(pb), l, _ptr(ws), ws.numel() * ws.element_size(), _ptr(plain), _ptr(AU_l), _ptr(BU_l),
+             _stream(stream)))
+
+
+def raw_lib():
+    return _lib

@@ -1,0 +1,79 @@
+"""Device-buffer management around the C ABI (torch is the allocator and stream source).
+
+``CpmmEngine`` owns the caller-side buffers the ABI asks for (ctpt_query_sizes) and
+drives the three calls of the hot path: format layout, plaintext precompute and
+ctpt_matmul.  All arithmetic happens in libctpt.so.
+"""
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+import torch
+
+from . import ctpt
+
+
+def _u32_to_dev(a: np.ndarray, device) -> torch.Tensor:
+    a = np.ascontiguousarray(a, dtype=np.uint32)
+    return torch.from_numpy(a.view(np.int32)).to(device, non_blocking=False)
+
+
+def dev_to_u32(t: torch.Tensor) -> np.ndarray:
+    return t.detach().cpu().numpy().view(np.uint32)
+
+
+class CpmmEngine:
+    def __init__(self, spec: ctpt.Spec, device: str | torch.device = "cuda"):
+        self.device = torch.device(device)
+        self.spec = dataclasses.replace(spec)
+        self.sizes = ctpt.query_sizes(self.spec)
+        self.ws = torch.empty(self.sizes.workspace_bytes, dtype=torch.uint8, device=self.device)
+        self.ctmat = None
+        self.plain = None
+
+    # -- a1: format layout ----------------------------------------------------------------
+    def layout(self, a_polys, b_polys, validate: bool = False) -> torch.Tensor:
+        a = a_polys if isinstance(a_polys, torch.Tensor) else _u32_to_dev(a_polys, self.device)
+        b = b_polys if isinstance(b_polys, torch.Tensor) else _u32_to_dev(b_polys, self.device)
+        if self.ctmat is None:
+            self.ctmat = torch.empty(self.sizes.ctmat_bytes, dtype=torch.uint8, device=self.device)
+        ctpt.layout(self.spec, a, b, self.ctmat, validate=validate)
+        return self.ctmat
+
+    # -- a2: plaintext precompute ------------------------------------------------------------
+    def precompute(self, U) -> int:
+        Ud = U if isinstance(U, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(U, dtype=np.int64))
+        Ud = Ud.to(self.device)
+        self.spec.kU = 4  # size the buffer for the worst case first
+        sz = ctpt.query_sizes(self.spec)
+        self.plain = torch.empty(sz.plain_bytes, dtype=torch.uint8, device=self.device)
+        kU = ctpt.plain_precompute(self.spec, Ud, self.plain)
+        self.spec.kU = kU
+        self.spec.plain_per_prime = 0
+        return kU
+
+    def precompute_rns(self, Ures) -> int:
+        Ud = Ures if isinstance(Ures, torch.Tensor) else _u32_to_dev(Ures, self.device)
+        self.plain = torch.empty(self.sizes.plain_rns_bytes, dtype=torch.uint8, device=self.device)
+        kU = ctpt.plain_precompute_rns(self.spec, Ud, self.plain)
+        self.spec.kU = kU
+        self.spec.plain_per_prime = 1
+        return kU
+
+    # -- a3–a6: the hot path -------------------------------------------------------------------
+    def alloc_outputs(self):
+        AU = torch.empty(self.sizes.out_AU_bytes // 4, dtype=torch.int32, device=self.device)
+        BU = torch.empty(self.sizes.out_BU_bytes // 4, dtype=torch.int32, device=self.device)
+        return AU, BU
+
+    def matmul(self, AU=None, BU=None, stream=None):
+        if AU is None:
+            AU, BU = self.alloc_outputs()
+        ctpt.matmul(self.spec, self.ctmat, self.plain, AU, BU, self.ws, stream=stream)
+        return AU, BU
+
+    def outputs_numpy(self, AU: torch.Tensor, BU: torch.Tensor):
+        L = len(self.spec.primes)
+        d3l = self.sizes.d3_loc
+        return (dev_to_u32(AU).reshape(L, d3l, self.sizes.rows_A), dev_to_u32(BU).reshape(L, d3l, self.spec.d1))

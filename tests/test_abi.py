@@ -1,0 +1,76 @@
+"""The C-ABI library loads, exports every symbol include/ctpt.h declares, and validates
+arguments on the host (no GPU needed: validation and size queries touch no device)."""
+import ctypes
+import os
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def ctpt():
+    import __graft_entry__
+
+    __graft_entry__.build_ctpt()
+    from paper_2503_16080_b200 import ctpt as m
+
+    return m
+
+
+def test_exports_every_header_symbol(ctpt):
+    syms = ctpt.header_symbols()
+    assert "ctpt_matmul" in syms and "ctpt_layout" in syms and "ctpt_plain_precompute" in syms
+    lib = ctypes.CDLL(ctpt.LIB_PATH)
+    for s in syms:
+        assert hasattr(lib, s), f"libctpt.so does not export {s}"
+
+
+def test_version(ctpt):
+    assert "sm_100a" in ctpt.version()
+
+
+def _spec(ctpt, **kw):
+    base = dict(fmt=ctpt.SHARED_A, N=16, d1=64, d2=48, d3=20, primes=[2147418113])
+    base.update(kw)
+    return ctpt.Spec(**base)
+
+
+def test_sizes(ctpt):
+    s = ctpt.query_sizes(_spec(ctpt))
+    assert s.rows_A == 16 and s.R == 80 and s.d2p == 48 and s.d3_loc == 20
+    assert s.ctmat_bytes == 256 + 80 * 48 * 4
+    assert s.workspace_bytes == 4 * 80 * 48
+    assert s.out_AU_bytes == 20 * 16 * 4 and s.out_BU_bytes == 20 * 64 * 4
+    s2 = ctpt.query_sizes(_spec(ctpt, fmt=ctpt.SHARED_S, d2=50, col_begin=3, col_end=11))
+    assert s2.rows_A == 64 and s2.R == 128 and s2.d2p == 64 and s2.d3_loc == 8
+    s3 = ctpt.query_sizes(_spec(ctpt, fmt=ctpt.RLWE, d1=16, primes=[2147418113, 2146959361]))
+    assert s3.out_BU_bytes == 2 * 20 * 16 * 4
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(fmt=0, N=16, d1=32), "ERR_SHAPE"),
+    (dict(N=12, d1=24), "ERR_SHAPE"),
+    (dict(d1=40), "ERR_SHAPE"),
+    (dict(d2=0), "ERR_SHAPE"),
+    (dict(col_begin=5, col_end=5), "ERR_SHAPE"),
+    (dict(col_end=21), "ERR_SHAPE"),
+    (dict(primes=[2147418113, 2147418113]), "ERR_MODULUS"),
+    (dict(primes=[2 ** 31 + 11]), "ERR_MODULUS"),
+    (dict(primes=[1024]), "ERR_MODULUS"),
+    (dict(d2=70000), "ERR_OVERFLOW"),
+    (dict(fmt=7), "ERR_UNSUPPORTED"),
+])
+def test_validation(ctpt, kw, status):
+    with pytest.raises(ctpt.CtptError) as ei:
+        ctpt.query_sizes(_spec(ctpt, **kw))
+    assert str(ei.value).startswith(status)
+
+
+def test_null_pointers_rejected_without_gpu(ctpt):
+    # argument validation happens before any CUDA call
+    lib = ctpt.raw_lib()
+    pb = _spec(ctpt).cstruct()
+    assert lib.ctpt_layout(ctypes.byref(pb), None, None, None, 0, None) == 1
+    assert lib.ctpt_matmul(ctypes.byref(pb), None, None, None, None, None, 0, None) == 1
+    assert b"null" in lib.ctpt_last_error()

@@ -155,3 +155,24 @@ def test_config_table():
     assert c["c3"].R == 20480 and c["c3"].residue_macs == 3 * 20480 * 16384 * 16384
     assert c["c5"].R == 65536 and c["c5"].k == 2
     assert c["c4"].rows_A == 32768 and c["c2"].rows_A == 4096
+
+
+def test_bulk_blocks_match_scalar():
+    N, d1, ld = 16, 64, 30
+    Mb = ctgen.msg_block(4, d1, 3, 10, 2, 5)
+    Pb = ctgen.plain_block(4, N, d1, ld, 3, 10, 2, 5)
+    assert (Mb == ctgen.msg_matrix(4, d1, range(3, 13), range(2, 7))).all()
+    assert (Pb == ctgen.plain_matrix(4, N, d1, range(3, 13), range(2, 7), ld)).all()
+
+
+def test_colmajor_views_equal_format_matrices():
+    import sys, os
+    sys.path.insert(0, os.path.dirname(__file__))
+    from gpu_helpers import colmajor_views
+
+    for fmt, N, k in [(ctgen.RLWE, 16, 1), (ctgen.SHARED_S, 8, 3), (ctgen.SHARED_A, 8, 3)]:
+        d1, d2 = N * k, 7
+        ct = ctgen.encrypt(fmt, N, d1, d2, 0, 20, ctgen.primes(1))
+        A, B = oracle.format_matrices(fmt, N, d1, ct.a_polys[0], ct.b_polys[0])
+        Av, Bv = colmajor_views(fmt, N, d1, d2, ct.a_polys[0], ct.b_polys[0])
+        assert (Av == A.T).all() and (Bv == B.T).all()

@@ -1,0 +1,216 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, bit-exact residues.
+
+Bar: residues are integers, so every compared entry must be
+identical.  Small shapes and configs c1/c2 are compared element by element; the
+large configs on sampled entries, tile-boundary rows/columns, Freivalds and the
+decryption identity (tests/test_gpu_configs.py).
+"""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+sys.path.insert(0, os.path.dirname(__file__))
+
+import ctgen  # noqa: E402
+import oracle  # noqa: E402
+from gpu_helpers import NTHREADS, U_residues, oracle_outputs, run_gpu  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+R, S, A = ctgen.RLWE, ctgen.SHARED_S, ctgen.SHARED_A
+
+SHAPES = [
+    # fmt, N, k, d2, d3, L  — several tiles + ragged tails in every dimension
+    (R, 16, 1, 16, 1, 1),
+    (R, 64, 1, 64, 64, 1),
+    (S, 16, 2, 48, 7, 2),
+    (A, 16, 4, 200, 129, 3),
+    (S, 64, 2, 64, 300, 1),
+    (A, 256, 2, 4112, 64, 1),
+    (R, 256, 1, 129, 130, 2),
+    (A, 8, 4, 33, 5, 1),
+    (S, 4, 8, 128, 128, 1),
+    (A, 1024, 3, 1000, 257, 2),
+]
+
+
+def _check(fmt, N, k, d2, d3, L, seed=0, u_bound=8, simt=False, col_begin=0, col_end=0):
+    d1 = N * k
+    ps = ctgen.primes(L)
+    ct = ctgen.encrypt(fmt, N, d1, d2, seed, 20, ps, nthreads=NTHREADS)
+    U = ctgen.U_matrix(seed, d2, d3, u_bound)
+    (AU, BU), eng = run_gpu(fmt, N, d1, d2, d3, ps, ct.a_polys, ct.b_polys, U=U, simt=simt, col_begin=col_begin,
+                            col_end=col_end)
+    c1 = col_end or d3
+    cols = np.arange(col_begin, c1)
+    for l, p in enumerate(ps):
+        wa, wb = oracle_outputs(fmt, N, d1, ct.a_polys[l], ct.b_polys[l], U, p, cols=cols)
+        assert np.array_equal(AU[l], wa), f"A·U mismatch prime {l}: {np.argwhere(AU[l] != wa)[:5]}"
+        assert np.array_equal(BU[l], wb), f"B·U mismatch prime {l}: {np.argwhere(BU[l] != wb)[:5]}"
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "f%d_N%d_k%d_d2%d_d3%d_L%d" % s)
+def test_shapes_tcgen05(shape):
+    _check(*shape)
+
+
+@pytest.mark.parametrize("shape", SHAPES[:6], ids=lambda s: "f%d_N%d_k%d_d2%d_d3%d_L%d" % s)
+def test_shapes_simt_diagnostic(shape):
+    _check(*shape, simt=True)
+
+
+def test_column_shard():
+    _check(A, 64, 2, 96, 300, 2, col_begin=70, col_end=211)
+
+
+def test_empty_U_columns_zero():
+    # U = 0 → outputs are 0 (degenerate case); U = I → outputs are A and B themselves
+    fmt, N, k, d2 = S, 32, 2, 64
+    d1 = N * k
+    ps = ctgen.primes(1)
+    ct = ctgen.encrypt(fmt, N, d1, d2, 3, 20, ps)
+    (AU, BU), _ = run_gpu(fmt, N, d1, d2, 5, ps, ct.a_polys, ct.b_polys, U=np.zeros((d2, 5), np.int64))
+    assert (AU == 0).all() and (BU == 0).all()
+    (AU, BU), _ = run_gpu(fmt, N, d1, d2, d2, ps, ct.a_polys, ct.b_polys, U=np.eye(d2, dtype=np.int64))
+    A_, B_ = oracle.format_matrices(fmt, N, d1, ct.a_polys[0], ct.b_polys[0])
+    assert np.array_equal(AU[0], A_.T) and np.array_equal(BU[0], B_.T)
+
+
+def test_adversarial_residues_and_digits():
+    """Residues 0, 1, (p±1)/2, p−1 and U at the int8 digit extremes −128 / 127."""
+    fmt, N, k, d2, d3 = A, 64, 2, 384, 96
+    d1 = N * k
+    ps = ctgen.primes(2)
+    rng = np.random.default_rng(0)
+    a = np.empty((2, d2, N), np.uint32)
+    b = np.empty((2, d2 * k, N), np.uint32)
+    for l, p in enumerate(ps):
+        special = np.array([0, 1, (p - 1) // 2, (p + 1) // 2, p - 1, p - 2], dtype=np.uint32)
+        a[l] = special[rng.integers(0, 6, a[l].shape)]
+        b[l] = special[rng.integers(0, 6, b[l].shape)]
+        a[l, :, 0] = p - 1
+    U = rng.choice(np.array([-128, 127, -1, 0, 1], dtype=np.int64), size=(d2, d3))
+    U[:, 0] = -128
+    U[:, 1] = 127
+    (AU, BU), eng = run_gpu(fmt, N, d1, d2, d3, ps, a, b, U=U)
+    assert eng.spec.kU == 1
+    for l, p in enumerate(ps):
+        wa, wb = oracle_outputs(fmt, N, d1, a[l], b[l], U, p)
+        assert np.array_equal(AU[l], wa) and np.array_equal(BU[l], wb)
+
+
+def test_max_d2_int32_bound():
+    """d2 = 65536 (the exactness limit d2·255·128 < 2^31) with every limb and digit at its
+    extreme: C_ℓ reaches −d2·255·128 and must not wrap."""
+    fmt, N, d2, d3 = R, 16, 65536, 16
+    ps = ctgen.primes(1)
+    p = ps[0]
+    a = np.full((1, d2, N), 0xFF_FF_FF & 0, np.uint32)
+    # residues whose bytes are all 255 in limbs 0..2 (p > 2^30, so 2^24·64 + 0xFFFFFF < p)
+    a[:] = (64 << 24) | 0xFFFFFF
+    b = np.full((1, d2, N), p - 1, np.uint32)
+    U = np.full((d2, d3), -128, np.int64)
+    U[:, 1::2] = 127
+    (AU, BU), _ = run_gpu(fmt, N, N, d2, d3, ps, a, b, U=U)
+    wa, wb = oracle_outputs(fmt, N, N, a[0], b[0], U, p)
+    assert np.array_equal(AU[0], wa) and np.array_equal(BU[0], wb)
+
+
+def test_multi_digit_U():
+    """|U| up to 30000 → k_U = 2 balanced digits; the second pass accumulates 2^8·(X·U_1) mod p."""
+    fmt, N, k, d2, d3 = S, 32, 2, 160, 40
+    d1 = N * k
+    ps = ctgen.primes(2)
+    ct = ctgen.encrypt(fmt, N, d1, d2, 5, 20, ps)
+    U = ctgen.U_matrix(5, d2, d3, 30000)
+    (AU, BU), eng = run_gpu(fmt, N, d1, d2, d3, ps, ct.a_polys, ct.b_polys, U=U)
+    assert eng.spec.kU == 2
+    for l, p in enumerate(ps):
+        wa, wb = oracle_outputs(fmt, N, d1, ct.a_polys[l], ct.b_polys[l], U, p)
+        assert np.array_equal(AU[l], wa) and np.array_equal(BU[l], wb)
+
+
+def test_general_U_residues_rns():
+    """U ∈ Z_q given by residues (ctpt_plain_precompute_rns, k_U = 4 per prime)."""
+    fmt, N, k, d2, d3 = A, 32, 3, 130, 70
+    d1 = N * k
+    ps = ctgen.primes(3)
+    ct = ctgen.encrypt(fmt, N, d1, d2, 6, 20, ps)
+    rng = np.random.default_rng(6)
+    Ub = rng.integers(-(2 ** 62), 2 ** 62, (d2, d3), dtype=np.int64)  # |U| ≫ p: a genuine element of Z_q
+    Ures = U_residues(Ub, ps)
+    (AU, BU), eng = run_gpu(fmt, N, d1, d2, d3, ps, ct.a_polys, ct.b_polys, Ures=Ures)
+    assert eng.spec.kU == 4 and eng.spec.plain_per_prime == 1
+    for l, p in enumerate(ps):
+        wa, wb = oracle_outputs(fmt, N, d1, ct.a_polys[l], ct.b_polys[l], Ub, p)
+        assert np.array_equal(AU[l], wa) and np.array_equal(BU[l], wb)
+
+
+def test_validate_flags_out_of_range():
+    from paper_2503_16080_b200 import ctpt
+
+    fmt, N, d2 = R, 16, 32
+    ps = ctgen.primes(1)
+    ct = ctgen.encrypt(fmt, N, N, d2, 0, 20, ps)
+    ct.b_polys[0, 3, 5] = ps[0]  # = p: not a canonical residue
+    with pytest.raises(ctpt.CtptError, match="ERR_RANGE"):
+        run_gpu(fmt, N, N, d2, 4, ps, ct.a_polys, ct.b_polys, U=np.ones((d2, 4), np.int64), validate=True)
+
+
+def test_config1_full_and_decrypt():
+    c = ctgen.CONFIGS["c1"]
+    ps = ctgen.primes(c.L)
+    ct = ctgen.encrypt(c.fmt, c.N, c.d1, c.d2, c.seed, c.log_delta, ps)
+    U = ctgen.U_matrix(c.seed, c.d2, c.d3, c.u_bound)
+    (AU, BU), _ = run_gpu(c.fmt, c.N, c.d1, c.d2, c.d3, ps, ct.a_polys, ct.b_polys, U=U)
+    wa, wb = oracle_outputs(c.fmt, c.N, c.d1, ct.a_polys[0], ct.b_polys[0], U, ps[0])
+    assert np.array_equal(AU[0], wa) and np.array_equal(BU[0], wb)
+    # decryption identity and decode (readings Q15, Q16)
+    sk = [ctgen.sk(c.seed, 0, c.N)]
+    P = ctgen.plain_block(c.seed, c.N, c.d1, c.log_delta, 0, c.d1, 0, c.d2)
+    PU = P.astype(object).dot(U.astype(object))
+    M = ctgen.msg_block(c.seed, c.d1, 0, c.d1, 0, c.d2)
+    MU = M.dot(U.astype(np.float64))
+    dec = np.stack([oracle.decrypt_col(c.fmt, c.N, c.d1, sk, AU[0, j], BU[0, j], ps[0]) for j in range(c.d3)], 1)
+    cen = np.array([[oracle.crt_centred([v], ps) for v in row] for row in dec], dtype=object)
+    assert (cen == PU).all()
+    approx = cen.astype(np.float64) / 2.0 ** c.log_delta
+    assert np.abs(approx - MU).max() <= np.abs(U).max() * c.d2 * 20.5 / 2.0 ** c.log_delta
+
+
+def test_config2_full():
+    """Config c2 (RLWE, N = d = 4096, two primes): every output entry vs the oracle, plus the
+    decryption identity and the 1e-6 decode bound on sampled columns."""
+    c = ctgen.CONFIGS["c2"]
+    ps = ctgen.primes(c.L)
+    ct = ctgen.encrypt(c.fmt, c.N, c.d1, c.d2, c.seed, c.log_delta, ps, nthreads=NTHREADS)
+    U = ctgen.U_matrix(c.seed, c.d2, c.d3, c.u_bound, nthreads=NTHREADS)
+    (AU, BU), _ = run_gpu(c.fmt, c.N, c.d1, c.d2, c.d3, ps, ct.a_polys, ct.b_polys, U=U)
+    for l, p in enumerate(ps):
+        wa, wb = oracle_outputs(c.fmt, c.N, c.d1, ct.a_polys[l], ct.b_polys[l], U, p)
+        assert np.array_equal(AU[l], wa), "A·U mismatch"
+        assert np.array_equal(BU[l], wb), "B·U mismatch"
+    _decrypt_check(c, ps, AU, BU, U, cols=[0, 1, 127, 128, 2049, c.d3 - 1])
+
+
+def _decrypt_check(c, ps, AU, BU, U, cols):
+    """S·A' + B' ≡ (⌊ΔM⌉+E)·U (mod q) exactly on `cols`, and the decoded value is within 1e-6
+    relative of M·U in float64 (readings Q15, Q16)."""
+    nk = c.k if c.fmt == A else 1
+    sks = [ctgen.sk(c.seed, t, c.N) for t in range(nk)]
+    P = ctgen.plain_block(c.seed, c.N, c.d1, c.log_delta, 0, c.d1, 0, c.d2, nthreads=NTHREADS)
+    M = ctgen.msg_block(c.seed, c.d1, 0, c.d1, 0, c.d2, nthreads=NTHREADS)
+    Uc = U[:, cols]
+    PU = P.astype(object).dot(Uc.astype(object)) if c.log_delta > 48 else P.dot(Uc).astype(object)
+    MU = M.dot(Uc.astype(np.float64))
+    worst = 0.0
+    for ci, j in enumerate(cols):
+        decs = np.stack([oracle.decrypt_col(c.fmt, c.N, c.d1, sks, AU[l, j], BU[l, j], p, nthreads=NTHREADS)
+                         for l, p in enumerate(ps)])
+        cen = oracle.crt_centred_array(decs, ps)
+        assert cen == list(PU[:, ci]), f"decryption identity fails in column {j}"
+        approx = np.array([float(v) for v in cen]) / 2.0 ** c.log_delta
+        worst = max(worst, np.abs(approx - MU[:, ci]).max() / np.abs(MU).max())
+    assert worst <= 1e-6, worst
