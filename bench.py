@@ -1,0 +1,372 @@
+#!/usr/bin/env python
+"""Benchmark of the CP-MM hot path (Algorithm 6 step 1) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+
+One "step" = ctpt_matmul over one batch of synthetic input: every RNS prime of the
+configuration, i.e. (A·U mod p, B·U mod p) for all L primes, with the limb split inside
+the step (SURVEY.md §8(a) note 2).  Default workload: config c3 (shared-a, N = 4096,
+k = 4, d1 = d2 = d3 = 16384, L = 3) — the configuration BASELINE.json's metric ("at
+d = 16384") is quoted on.  Prints ONE JSON line on rank 0.
+
+Multi-GPU (torchrun, one rank per GPU): every rank runs its own independent c3 problem
+(seed = rank); there is no collective on the data path, so "scaling" is "weak" and
+value = all ranks' residue-MACs ÷ the max-over-ranks device time.
+
+--impl reference: the CPU oracle (oracle/, schoolbook modular matmul, 128-bit
+accumulation) as it stands, on the host cores, on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ct-pt matmul residue-MACs/s at d=16384 and % of B200 dense INT8 TC peak"
+UNIT = "residue-MAC/s"
+INT8_DATASHEET_MACS = 2.25e15  # dense INT8 4.5 POPS, in MAC/s
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target seconds of oracle work per sample")
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            mp = json.load(f)
+        return mp, "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def workload_desc(c) -> dict:
+    import ctgen
+
+    return {"workload": f"{c.name}: {ctgen.FORMAT_NAMES[c.fmt]} N={c.N} k={c.k} d1={c.d1} d2={c.d2} d3={c.d3} "
+                        f"L={c.L} Δ=2^{c.log_delta} U∈[-{c.u_bound},{c.u_bound}]",
+            "format": ctgen.FORMAT_NAMES[c.fmt], "N": c.N, "d1": c.d1, "d2": c.d2, "d3": c.d3, "L": c.L,
+            "rows_stacked_R": c.R, "seed": c.seed}
+
+
+# ------------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                       "-lms", "100", "-i", str(gpu_index)], stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+
+        sm = [num(r[1]) for r in rows if num(r[1]) is not None]
+        smax = [num(r[2]) for r in rows if num(r[2]) is not None]
+        pw = [num(r[3]) for r in rows if num(r[3]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "power_w_max": max(pw) if pw else None, "samples": len(rows), "reasons": reasons}
+
+
+# ------------------------------------------------------------------------------------ CPU oracle
+def cpu_oracle_rate(c, ct, U, target_s: float):
+    """Residue-MAC/s of the oracle's schoolbook on a bounded sample of workload c: output
+    columns of prime 0 over all R stacked rows and the full d2 contraction."""
+    import oracle
+
+    cores = os.cpu_count() or 1
+    p = ct.primes[0]
+    ra = c.rows_A
+    Ac = ct.a_polys[0].reshape(c.d2, ra)
+    Bc = ct.b_polys[0].reshape(c.d2, c.d1)
+    ncols = max(1, min(cores, c.d3))
+    t0 = time.perf_counter()
+    oracle.modmatmul(Ac, U, p, cols=np.arange(ncols), nthreads=cores)
+    oracle.modmatmul(Bc, U, p, cols=np.arange(ncols), nthreads=cores)
+    dt = time.perf_counter() - t0
+    # scale the sample to ~target_s of work
+    ncols2 = int(min(c.d3, max(ncols, ncols * target_s / max(dt, 1e-3))))
+    ncols2 = max(cores, (ncols2 // cores) * cores) if ncols2 >= cores else ncols2
+    t0 = time.perf_counter()
+    oracle.modmatmul(Ac, U, p, cols=np.arange(ncols2), nthreads=cores)
+    oracle.modmatmul(Bc, U, p, cols=np.arange(ncols2), nthreads=cores)
+    dt = time.perf_counter() - t0
+    macs = c.R * c.d2 * ncols2
+    return {"value": macs / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"prime 0, {ncols2} of {c.d3} output columns x all {c.R} stacked rows x d2={c.d2} "
+                      f"({macs:.3e} residue-MACs, {dt:.1f} s, schoolbook __int128, OpenMP {cores} threads)"}
+
+
+# ------------------------------------------------------------------------------------ inputs
+def make_inputs(c, seed: int, nthreads: int):
+    import ctgen
+
+    ps = ctgen.primes(c.L)
+    t0 = time.perf_counter()
+    ct = ctgen.encrypt(c.fmt, c.N, c.d1, c.d2, seed, c.log_delta, ps, nthreads=nthreads)
+    U = ctgen.U_matrix(seed, c.d2, c.d3, c.u_bound, nthreads=nthreads)
+    return ps, ct, U, time.perf_counter() - t0
+
+
+# ------------------------------------------------------------------------------------ reference arm
+def run_reference(args, rank: int):
+    import ctgen
+
+    if rank != 0:
+        return
+    c = ctgen.CONFIGS[args.config]
+    cores = os.cpu_count() or 1
+    ps, ct, U, _ = make_inputs(c, c.seed, cores)
+    import oracle
+
+    p = ps[0]
+    Ac = ct.a_polys[0].reshape(c.d2, c.rows_A)
+    Bc = ct.b_polys[0].reshape(c.d2, c.d1)
+    # size each step to ~ (a few minutes / (steps + warmup)) of CPU work
+    budget = min(20.0, 150.0 / max(1, args.steps + args.warmup))
+    t0 = time.perf_counter()
+    oracle.modmatmul(Ac, U, p, cols=np.arange(cores), nthreads=cores)
+    oracle.modmatmul(Bc, U, p, cols=np.arange(cores), nthreads=cores)
+    per_col = (time.perf_counter() - t0) / cores
+    ncols = int(max(1, min(c.d3, budget / max(per_col, 1e-6))))
+    times = []
+    for i in range(args.warmup + args.steps):
+        j0 = (i * ncols) % max(1, c.d3 - ncols + 1)
+        cols = np.arange(j0, j0 + ncols)
+        t0 = time.perf_counter()
+        oracle.modmatmul(Ac, U, p, cols=cols, nthreads=cores)
+        oracle.modmatmul(Bc, U, p, cols=cols, nthreads=cores)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    macs = c.R * c.d2 * ncols
+    t = statistics.mean(times)
+    v = macs / t
+    sample = (f"per step: prime 0, {ncols} of {c.d3} output columns x all {c.R} stacked rows x d2={c.d2} "
+              f"({macs:.3e} residue-MACs)")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u128 (schoolbook residues)", "data": "synthetic",
+        "config": workload_desc(c),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+# ------------------------------------------------------------------------------------ our arm
+def run_ours(args, rank: int, world: int, local_rank: int):
+    import torch
+
+    import ctgen
+    from paper_2503_16080_b200 import ctpt
+    from paper_2503_16080_b200.engine import CpmmEngine
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    c = ctgen.CONFIGS[args.config]
+    cores = os.cpu_count() or 1
+    seed = c.seed + rank
+    ps, ct, U, gen_s = make_inputs(c, seed, max(1, cores // world))
+
+    eng = CpmmEngine(ctpt.Spec(c.fmt, c.N, c.d1, c.d2, c.d3, ps), dev)
+    a_dev = torch.from_numpy(ct.a_polys.view(np.int32)).to(dev)
+    b_dev = torch.from_numpy(ct.b_polys.view(np.int32)).to(dev)
+    eng.layout(a_dev, b_dev, validate=True)
+    kU = eng.precompute(U)
+    AU, BU = eng.alloc_outputs()
+    spec, sizes = eng.spec, eng.sizes
+    stream = torch.cuda.current_stream(dev)
+    d3l, ra = sizes.d3_loc, sizes.rows_A
+
+    def step(ev_pairs=None):
+        for l in range(len(ps)):
+            ctpt.split(spec, l, eng.ctmat, eng.ws, stream=stream)
+            if ev_pairs is not None:
+                ev_pairs[l][0].record(stream)
+            ctpt.gemm(spec, l, eng.ws, eng.plain, AU[l * d3l * ra:], BU[l * d3l * c.d1:], stream=stream)
+            if ev_pairs is not None:
+                ev_pairs[l][1].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    # ------------------------------------------------ timed region (device-resident inputs)
+    gemm_ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in ps]
+               for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    clk = ClockSampler(local_rank)
+    time.sleep(0.3)  # let the sampler start
+    t_start.record(stream)
+    for s in range(args.steps):
+        step(gemm_ev[s])
+    t_end.record(stream)
+    torch.cuda.synchronize(dev)
+    clocks = clk.stop()
+    if world > 1:
+        torch.distributed.barrier()
+    elapsed_ms = t_start.elapsed_time(t_end)
+    gemm_ms = [a.elapsed_time(b) for row in gemm_ev for (a, b) in row]
+    if world > 1:
+        t = torch.tensor([elapsed_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+
+    macs_rank = c.residue_macs  # per step
+    value = world * macs_rank * args.steps / (elapsed_ms / 1e3)
+    ms_per_step = elapsed_ms / args.steps
+
+    # ------------------------------------------------ roofline of the dominant kernel (k_gemm_tc)
+    mp, which = peaks()
+    gemm_avg_s = statistics.mean(gemm_ms) / 1e3
+    limb_macs_launch = 4 * kU * c.R * c.d2 * c.d3
+    achieved_tops = 2 * limb_macs_launch / gemm_avg_s / 1e12
+    peak_tops = 2 * float(mp["bf16_tflops_sustained"])  # int8 = 2 x bf16 (guide's nominal ratio), sustained
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "gemm_dram_bytes.json")) as f:
+            traffic = json.load(f).get(c.name)
+    except OSError:
+        pass
+
+    # ------------------------------------------------ end to end through the ABI (host buffers)
+    e2e = run_e2e(args, c, ps, ct, eng, dev, stream)
+
+    gemm_share = sum(gemm_ms) / elapsed_ms
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+        "config": dict(workload_desc(c), **{
+            "l2": f"inputs {sizes.ctmat_bytes * 1.0 / 2**30:.2f} GiB per step > 126 MB L2 (no flush needed)",
+            "parallelism": f"weak: {world} independent problem(s), one per GPU, no data-path collective",
+            "kU": kU, "limb_macs_per_residue_mac": 4 * kU}),
+        "pct_int8_datasheet": 100.0 * value * 4 * kU / world / INT8_DATASHEET_MACS,
+        "roofline": {"bound": "tensor", "achieved": achieved_tops, "peak": peak_tops, "unit": "TOP/s",
+                     "frac": achieved_tops / peak_tops, "traffic": traffic,
+                     "kernel": "k_gemm_tc", "peak_source": f"{which}: 2 x bf16_tflops_sustained (int8/bf16 nominal 2x)",
+                     "per_launch": f"{limb_macs_launch:.4e} limb MACs (4·kU·R·d2·d3, one prime)",
+                     "avg_launch_ms": gemm_avg_s * 1e3, "share_of_step": gemm_share},
+        "e2e": e2e,
+        "gpu_launches": (1 + kU) * len(ps) * args.steps,  # per prime: k_split + kU x k_gemm_tc
+        "clocks": clocks,
+        "input_generation_s": gen_s,
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_oracle_rate(c, ct, U, args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(result))
+
+
+def run_e2e(args, c, ps, ct, eng, dev, stream):
+    """Same metric through the public ABI with HOST buffers: every step copies the ciphertexts
+    from pinned host memory, lays them out, runs ctpt_matmul and reads the outputs back."""
+    import torch
+
+    from paper_2503_16080_b200 import ctpt
+
+    a_h = torch.from_numpy(ct.a_polys.view(np.int32)).pin_memory()
+    b_h = torch.from_numpy(ct.b_polys.view(np.int32)).pin_memory()
+    a_d = torch.empty_like(a_h, device=dev)
+    b_d = torch.empty_like(b_h, device=dev)
+    AU, BU = eng.alloc_outputs()
+    AU_h = torch.empty(AU.shape, dtype=AU.dtype).pin_memory()
+    BU_h = torch.empty(BU.shape, dtype=BU.dtype).pin_memory()
+
+    def step():
+        a_d.copy_(a_h, non_blocking=True)
+        b_d.copy_(b_h, non_blocking=True)
+        ctpt.layout(eng.spec, a_d, b_d, eng.ctmat, stream=stream)
+        ctpt.matmul(eng.spec, eng.ctmat, eng.plain, AU, BU, eng.ws, stream=stream)
+        AU_h.copy_(AU, non_blocking=True)
+        BU_h.copy_(BU, non_blocking=True)
+
+    step()
+    torch.cuda.synchronize(dev)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.e2e_steps):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = t0.elapsed_time(t1) / args.e2e_steps
+    h2d = a_h.numel() * 4 + b_h.numel() * 4
+    d2h = AU_h.numel() * 4 + BU_h.numel() * 4
+    return {"value": c.residue_macs / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": ms, "steps": args.e2e_steps,
+            "path": "pinned H2D -> ctpt_layout -> ctpt_matmul -> D2H, one stream, sequential"}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch
+
+            torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
