@@ -118,23 +118,25 @@ int64_t orc_freivalds(const uint32_t* X, int64_t rows, int64_t d2, const int64_t
 
 /* Negacyclic product by the Toeplitz definition: c = toep(s)·Vec(a), i.e.
  *   c_i = Σ_{j ≤ i} s_{i-j} a_j  −  Σ_{j > i} s_{N+i-j} a_j   (mod p). */
-void orc_negacyclic_mul(const uint32_t* a, const int64_t* s, int64_t N, uint32_t p, uint32_t* out) {
-  for (int64_t i = 0; i < N; ++i) {
-    u128 pos = 0, neg = 0;
-    for (int64_t j = 0; j < N; ++j) {
-      if (j <= i) {
-        int64_t sv = s[i - j];
-        if (sv >= 0) pos += (u128)((uint64_t)a[j] * (uint64_t)sv);
-        else neg += (u128)((uint64_t)a[j] * (uint64_t)(-sv));
-      } else {
-        int64_t sv = s[N + i - j];
-        if (sv >= 0) neg += (u128)((uint64_t)a[j] * (uint64_t)sv);
-        else pos += (u128)((uint64_t)a[j] * (uint64_t)(-sv));
-      }
+static uint32_t negacyclic_coeff(const uint32_t* a, const int64_t* s, int64_t N, uint32_t p, int64_t i) {
+  u128 pos = 0, neg = 0;
+  for (int64_t j = 0; j < N; ++j) {
+    if (j <= i) {
+      int64_t sv = s[i - j];
+      if (sv >= 0) pos += (u128)((uint64_t)a[j] * (uint64_t)sv);
+      else neg += (u128)((uint64_t)a[j] * (uint64_t)(-sv));
+    } else {
+      int64_t sv = s[N + i - j];
+      if (sv >= 0) neg += (u128)((uint64_t)a[j] * (uint64_t)sv);
+      else pos += (u128)((uint64_t)a[j] * (uint64_t)(-sv));
     }
-    uint64_t P = (uint64_t)(pos % p), Q = (uint64_t)(neg % p);
-    out[i] = (uint32_t)((P + p - Q) % p);
   }
+  uint64_t P = (uint64_t)(pos % p), Q = (uint64_t)(neg % p);
+  return (uint32_t)((P + p - Q) % p);
+}
+
+void orc_negacyclic_mul(const uint32_t* a, const int64_t* s, int64_t N, uint32_t p, uint32_t* out) {
+  for (int64_t i = 0; i < N; ++i) out[i] = negacyclic_coeff(a, s, N, p, i);
 }
 
 /* Decryption of one output column in a structured-S format (P:852 Dec; P:1688 identity
@@ -145,17 +147,15 @@ void orc_negacyclic_mul(const uint32_t* a, const int64_t* s, int64_t N, uint32_t
 int orc_decrypt_col(int fmt, int64_t N, int64_t d1, const int64_t* sks, const uint32_t* a_col,
                     const uint32_t* b_col, uint32_t p, uint32_t* out, int nthreads) {
   if (N <= 0 || d1 % N) return -1;
-  const int64_t k = d1 / N;
   set_threads(nthreads);
 #ifdef _OPENMP
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(dynamic, 64)
 #endif
-  for (int64_t t = 0; t < k; ++t) {
+  for (int64_t r = 0; r < d1; ++r) {
+    const int64_t t = r / N, i = r % N;
     const int64_t* key = sks + ((fmt == 2) ? t : 0) * N;
     const uint32_t* a = a_col + ((fmt == 1) ? t * N : 0);
-    uint32_t* o = out + t * N;
-    orc_negacyclic_mul(a, key, N, p, o);
-    for (int64_t i = 0; i < N; ++i) o[i] = (uint32_t)(((uint64_t)o[i] + b_col[t * N + i]) % p);
+    out[r] = (uint32_t)(((uint64_t)negacyclic_coeff(a, key, N, p, i) + b_col[r]) % p);
   }
   return 0;
 }

@@ -1,0 +1,134 @@
+"""GPU parity at BASELINE.json's full sizes (configs c3, c4, c5), in the launch configuration
+bench.py times (ctpt_layout + ctpt_plain_precompute + ctpt_matmul over the config's primes).
+
+The oracle cannot recompute 10^13–10^14 residue MACs, so per prime and per output matrix
+(SURVEY.md §8(c) c5):
+  * two Freivalds trials: (C·v) mod p == (X·(U·v)) mod p, v uniform in Z_p^{d3} (a wrong C
+    survives a trial with probability ≤ 1/p);
+  * exact schoolbook on every entry of rows/columns at tile boundaries (0, 63, 64, 127, 128, …,
+    last) and on random entries;
+and on sampled output columns the decryption identity S·A' + B' ≡ (⌊ΔM⌉+E)·U (mod p) for every
+prime plus the decoded value within 1e-6 relative of M·U in float64 (readings Q15, Q16).
+c5 (68.7 GB of ciphertexts) streams one prime at a time through the same ABI calls.
+"""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+sys.path.insert(0, os.path.dirname(__file__))
+
+import ctgen  # noqa: E402
+import oracle  # noqa: E402
+from gpu_helpers import NTHREADS, colmajor_views, run_gpu  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def _boundary(n, tile):
+    idx = {0, n - 1}
+    for t in range(tile, n, tile):
+        idx.update({t - 1, t})
+        if len(idx) > 10:
+            break
+    return sorted(i for i in idx if 0 <= i < n)
+
+
+def _check_matrix(Xc, U, C, p, rng, name, n_random):
+    """Xc: col-major [d2][rows] ciphertext matrix; C: [d3][rows] GPU output."""
+    d2, rows = Xc.shape
+    d3 = U.shape[1]
+    for trial in range(2):
+        v = rng.integers(0, p, d3, dtype=np.uint64)
+        assert oracle.freivalds(Xc, U, C, p, v, nthreads=NTHREADS) == 0, f"{name}: Freivalds trial {trial} failed"
+    rb = _boundary(rows, 64)
+    cb = _boundary(d3, 128)
+    r_idx = np.concatenate([np.repeat(rb, len(cb)), rng.integers(0, rows, n_random)])
+    j_idx = np.concatenate([np.tile(cb, len(rb)), rng.integers(0, d3, n_random)])
+    want = oracle.modmatmul_entries(Xc, U, p, r_idx, j_idx, nthreads=NTHREADS)
+    got = C[j_idx, r_idx]
+    assert np.array_equal(got, want), f"{name}: {np.count_nonzero(got != want)} sampled entries differ"
+    # every entry of two whole boundary columns
+    cols = np.array([cb[0], cb[-1]])
+    full = oracle.modmatmul(Xc, U, p, cols=cols, nthreads=NTHREADS)
+    assert np.array_equal(C[cols], full), f"{name}: boundary columns differ"
+
+
+def _pu_mod_and_mu(c, U, ps, cols, kblock=2048):
+    """(P·U)[:, cols] mod p for every prime and (M·U)[:, cols] in float64, streaming P and M
+    over blocks of d2 (P = ⌊ΔM⌉ + E from the generator, products by the oracle)."""
+    pu = np.zeros((len(ps), len(cols), c.d1), dtype=np.uint64)
+    mu = np.zeros((c.d1, len(cols)), dtype=np.float64)
+    Uc = U[:, cols]
+    for k0 in range(0, c.d2, kblock):
+        kb = min(kblock, c.d2 - k0)
+        P = ctgen.plain_block(c.seed, c.N, c.d1, c.log_delta, 0, c.d1, k0, kb, nthreads=NTHREADS)  # [d1][kb]
+        M = ctgen.msg_block(c.seed, c.d1, 0, c.d1, k0, kb, nthreads=NTHREADS)
+        mu += M.dot(Uc[k0:k0 + kb].astype(np.float64))
+        Pt = np.ascontiguousarray(P.T)  # [kb][d1] = col-major view of the d1 x kb block
+        for l, p in enumerate(ps):
+            Pm = (Pt % p).astype(np.uint32)
+            part = oracle.modmatmul(Pm, Uc[k0:k0 + kb], p, nthreads=NTHREADS)  # [ncols][d1]
+            pu[l] = (pu[l] + part) % p
+    return pu, mu
+
+
+def _decrypt_and_decode(c, ps, AUc, BUc, U, cols):
+    """AUc[l]: [ncols][rows_A], BUc[l]: [ncols][d1] (GPU outputs on `cols`)."""
+    nk = c.k if c.fmt == ctgen.SHARED_A else 1
+    sks = [ctgen.sk(c.seed, t, c.N) for t in range(nk)]
+    pu, mu = _pu_mod_and_mu(c, U, ps, cols)
+    worst = 0.0
+    scale = np.abs(mu).max()
+    for ci, j in enumerate(cols):
+        decs = []
+        for l, p in enumerate(ps):
+            dec = oracle.decrypt_col(c.fmt, c.N, c.d1, sks, AUc[l][ci], BUc[l][ci], p, nthreads=NTHREADS)
+            assert np.array_equal(dec.astype(np.uint64), pu[l, ci]), f"decryption identity fails: prime {l}, col {j}"
+            decs.append(dec)
+        cen = oracle.crt_centred_array(np.stack(decs), ps)
+        approx = np.array([float(v) for v in cen]) / 2.0 ** c.log_delta
+        worst = max(worst, np.abs(approx - mu[:, ci]).max() / scale)
+    assert worst <= 1e-6, f"decoded relative error {worst:.3e} > 1e-6"
+    return worst
+
+
+def _run_config(name, primes_per_call, n_random, dec_cols):
+    import torch
+
+    c = ctgen.CONFIGS[name]
+    ps_all = ctgen.primes(c.L)
+    U = ctgen.U_matrix(c.seed, c.d2, c.d3, c.u_bound, nthreads=NTHREADS)
+    rng = np.random.default_rng(1234)
+    AUc = [None] * c.L
+    BUc = [None] * c.L
+    for l0 in range(0, c.L, primes_per_call):
+        ps = ps_all[l0:l0 + primes_per_call]
+        ct = ctgen.encrypt(c.fmt, c.N, c.d1, c.d2, c.seed, c.log_delta, ps, nthreads=NTHREADS)
+        (AU, BU), eng = run_gpu(c.fmt, c.N, c.d1, c.d2, c.d3, ps, ct.a_polys, ct.b_polys, U=U, validate=True)
+        del eng
+        torch.cuda.empty_cache()
+        for i, p in enumerate(ps):
+            Ac, Bc = colmajor_views(c.fmt, c.N, c.d1, c.d2, ct.a_polys[i], ct.b_polys[i])
+            _check_matrix(Ac, U, AU[i], p, rng, f"{name} A·U prime {l0 + i}", n_random)
+            _check_matrix(Bc, U, BU[i], p, rng, f"{name} B·U prime {l0 + i}", n_random)
+            AUc[l0 + i] = AU[i][dec_cols].copy()
+            BUc[l0 + i] = BU[i][dec_cols].copy()
+        del ct, AU, BU
+    return _decrypt_and_decode(c, ps_all, AUc, BUc, U, dec_cols)
+
+
+def test_config3_full_size():
+    c = ctgen.CONFIGS["c3"]
+    _run_config("c3", primes_per_call=3, n_random=65536, dec_cols=[0, 127, 128, 8191, c.d3 - 1])
+
+
+def test_config4_full_size():
+    c = ctgen.CONFIGS["c4"]
+    _run_config("c4", primes_per_call=4, n_random=32768, dec_cols=[0, 128, c.d3 - 1])
+
+
+def test_config5_full_size():
+    c = ctgen.CONFIGS["c5"]
+    _run_config("c5", primes_per_call=1, n_random=8192, dec_cols=[0, c.d3 - 1])
