@@ -91,10 +91,14 @@ class ClockSampler:
         self.f.flush()
         rows = []
         with open(self.f.name) as fh:
-            for line in fh:
-                parts = [x.strip() for x in line.split(",")]
-                if len(parts) >= 9:
-                    rows.append(parts)
+            raw = fh.read()
+        for line in raw.splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        if os.environ.get("CTPT_CLOCK_LOG"):
+            with open(os.environ["CTPT_CLOCK_LOG"], "w") as fh:
+                fh.write(self.FIELDS + "\n" + raw)
         os.unlink(self.f.name)
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}

@@ -44,23 +44,28 @@ static void set_threads(int nthreads) {
 void orc_modmatmul_cols(const uint32_t* X, int64_t rows, int64_t d2, const int64_t* U, int64_t d3,
                         const int64_t* cols, int64_t ncols, uint32_t p, uint32_t* out, int nthreads) {
   set_threads(nthreads);
+  /* work items = (output column, block of rows); each row's sum is still taken over k in order */
+  const int64_t RB = 2048;
+  const int64_t nrb = (rows + RB - 1) / RB;
 #ifdef _OPENMP
 #pragma omp parallel
 #endif
   {
-    u128* acc = (u128*)malloc(sizeof(u128) * (size_t)rows);
+    u128* acc = (u128*)malloc(sizeof(u128) * (size_t)RB);
 #ifdef _OPENMP
 #pragma omp for schedule(dynamic, 1)
 #endif
-    for (int64_t c = 0; c < ncols; ++c) {
+    for (int64_t w = 0; w < ncols * nrb; ++w) {
+      const int64_t c = w / nrb, r0 = (w % nrb) * RB;
+      const int64_t r1 = r0 + RB < rows ? r0 + RB : rows;
       const int64_t j = cols[c];
-      memset(acc, 0, sizeof(u128) * (size_t)rows);
+      memset(acc, 0, sizeof(u128) * (size_t)RB);
       for (int64_t k = 0; k < d2; ++k) {
         const uint64_t u = canon(U[k * d3 + j], p);
         const uint32_t* xk = X + k * rows;
-        for (int64_t r = 0; r < rows; ++r) acc[r] += (u128)((uint64_t)xk[r] * u);
+        for (int64_t r = r0; r < r1; ++r) acc[r - r0] += (u128)((uint64_t)xk[r] * u);
       }
-      for (int64_t r = 0; r < rows; ++r) out[c * rows + r] = (uint32_t)(acc[r] % p);
+      for (int64_t r = r0; r < r1; ++r) out[c * rows + r] = (uint32_t)(acc[r - r0] % p);
     }
     free(acc);
   }

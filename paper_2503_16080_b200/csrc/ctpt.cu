@@ -7,11 +7,13 @@
 #include <climits>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
 #include "../../include/ctpt.h"
 #include "gemm_tc.cuh"
+#include "gemm_tc2.cuh"
 #include "kernels.cuh"
 
 using namespace ctpt;
@@ -137,6 +139,8 @@ ctpt_status tc_setup() {
   static std::once_flag once;
   std::call_once(once, [] {
     e = cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BYTES);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_gemm_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, T2_SMEM_BYTES);
   });
   if (e != cudaSuccess) return fail(CTPT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
   return CTPT_OK;
@@ -338,29 +342,44 @@ static ctpt_status gemm_common(const ctpt_problem* pb, int32_t l, const void* d_
   }
   s = tc_setup();
   if (s != CTPT_OK) return s;
+  // Kernel choice.  Under the 1000 W cap the single-CTA kernel sustains more int8 ops
+  // (c3, 100 steps: 2844 TOP/s at 1395 MHz vs 2634 TOP/s at 1140 MHz for the CTA pair, which is
+  // more efficient per clock — 95 % vs 84 % of 8192 MAC/clk/SM — but draws more power per
+  // clock; profiles/r01/power_1cta_vs_2cta.txt), so it is the default; CTPT_GEMM=2cta selects
+  // the pair kernel (tests exercise both).
+  bool pair = false;
+  if (const char* g = getenv("CTPT_GEMM")) pair = (strcmp(g, "2cta") == 0);
+  const int block_j = pair ? T2_BLOCK_J : TC_BLOCK_J;
   CUtensorMap tmU, tmX;
-  s = make_tmap_u8(&tmU, planes, d.d2, d.d3, nplanes, d.d2p, d.d3 * d.d2p, TC_BLOCK_K, TC_BLOCK_J, 1);
+  s = make_tmap_u8(&tmU, planes, d.d2, d.d3, nplanes, d.d2p, d.d3 * d.d2p, TC_BLOCK_K, 128, 1);
   if (s != CTPT_OK) return s;
-  s = make_tmap_u8(&tmX, d_ws, d.d2, d.R, 4, d.d2p, d.R * d.d2p, TC_BLOCK_K, TC_BLOCK_R, 4);
+  s = make_tmap_u8(&tmX, d_ws, d.d2, d.R, 4, d.d2p, d.R * d.d2p, TC_BLOCK_K, TC_BLOCK_R, pair ? 2 : 4);
   if (s != CTPT_OK) return s;
   TcParams P;
   P.R = d.R;
   P.d2 = d.d2;
   P.j_off = static_cast<int32_t>(d.j0);
   P.num_kb = static_cast<int32_t>((d.d2 + TC_BLOCK_K - 1) / TC_BLOCK_K);
-  P.tiles_j = static_cast<int32_t>((d.d3_loc + TC_BLOCK_J - 1) / TC_BLOCK_J);
+  P.tiles_j = static_cast<int32_t>((d.d3_loc + block_j - 1) / block_j);
   P.tiles_r = static_cast<int32_t>((d.R + TC_BLOCK_R - 1) / TC_BLOCK_R);
   const int64_t nt = static_cast<int64_t>(P.tiles_j) * P.tiles_r;
   if (nt > INT32_MAX) return fail(CTPT_ERR_SHAPE, "too many tiles");
   P.num_tiles = static_cast<int32_t>(nt);
+  P.group_j = pair ? T2_GROUP_J_DEFAULT : TC_GROUP_J_DEFAULT;
+  if (const char* g = getenv("CTPT_GROUP_J")) P.group_j = std::max(1, atoi(g));  // tuning knob
   P.m = m;
-  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(nt, num_sms()));
+  const int sms = num_sms();
+  const unsigned grid = pair ? static_cast<unsigned>(2 * std::min<int64_t>(nt, sms / 2))
+                             : static_cast<unsigned>(std::min<int64_t>(nt, sms));
   for (int i = 0; i < kU; ++i) {
     P.plane = plane_index(pb, l, i);
     P.o = o;
     P.o.accumulate = i > 0;
     P.o.w = pow2mod(8 * i, p);
-    k_gemm_tc<<<grid, TC_THREADS, TC_SMEM_BYTES, st>>>(tmU, tmX, P);
+    if (pair)
+      k_gemm_tc2<<<grid, T2_THREADS, T2_SMEM_BYTES, st>>>(tmU, tmX, P);
+    else
+      k_gemm_tc<<<grid, TC_THREADS, TC_SMEM_BYTES, st>>>(tmU, tmX, P);
     CUDA_TRY(cudaGetLastError());
   }
   return CTPT_OK;

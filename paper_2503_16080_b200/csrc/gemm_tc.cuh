@@ -35,7 +35,7 @@ constexpr int TC_STAGE_BYTES = TC_U_BYTES + TC_X_BYTES;        // 48 KB
 constexpr int TC_ACC_COLS = 4 * TC_BLOCK_R;                    // 256
 constexpr int TC_THREADS = 256;
 constexpr int TC_SMEM_BYTES = TC_STAGES * TC_STAGE_BYTES + 256 + 1024;
-constexpr int TC_GROUP_J = 16;
+constexpr int TC_GROUP_J_DEFAULT = 16;  // measured best of {8,16,32,64,128} on c3 (profiles/r01)
 
 struct TcParams {
   int64_t R, d2;
@@ -44,16 +44,17 @@ struct TcParams {
   int32_t num_kb;     // ceil(d2 / 128)
   int32_t tiles_j, tiles_r;
   int32_t num_tiles;
+  int32_t group_j;    // tiles visited in groups of group_j j-tiles (L2 reuse of U panels)
   ModP m;
   OutParams o;
 };
 
 __device__ __forceinline__ void tc_tile_coords(int32_t tile, const TcParams& P, int32_t& tj, int32_t& tr) {
-  const int32_t per_group = TC_GROUP_J * P.tiles_r;
+  const int32_t per_group = P.group_j * P.tiles_r;
   const int32_t g = tile / per_group;
   const int32_t rem = tile - g * per_group;
-  const int32_t gj = min(TC_GROUP_J, P.tiles_j - g * TC_GROUP_J);
-  tj = g * TC_GROUP_J + rem % gj;
+  const int32_t gj = min(P.group_j, P.tiles_j - g * P.group_j);
+  tj = g * P.group_j + rem % gj;
   tr = rem / gj;
 }
 

@@ -51,9 +51,33 @@ def _check(fmt, N, k, d2, d3, L, seed=0, u_bound=8, simt=False, col_begin=0, col
         assert np.array_equal(BU[l], wb), f"B·U mismatch prime {l}: {np.argwhere(BU[l] != wb)[:5]}"
 
 
+@pytest.fixture(params=["1cta", "2cta"])
+def gemm_kernel(request, monkeypatch):
+    """Force the single-CTA (k_gemm_tc) or CTA-pair (k_gemm_tc2) tensor-core kernel."""
+    monkeypatch.setenv("CTPT_GEMM", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "f%d_N%d_k%d_d2%d_d3%d_L%d" % s)
-def test_shapes_tcgen05(shape):
+def test_shapes_tcgen05(shape, gemm_kernel):
     _check(*shape)
+
+
+def test_column_shard_both_kernels(gemm_kernel):
+    _check(S, 128, 2, 160, 600, 1, col_begin=37, col_end=591)
+
+
+def test_multi_digit_U_pair_kernel(monkeypatch):
+    monkeypatch.setenv("CTPT_GEMM", "2cta")
+    fmt, N, k, d2, d3 = A, 64, 2, 256, 300
+    d1 = N * k
+    ps = ctgen.primes(1)
+    ct = ctgen.encrypt(fmt, N, d1, d2, 9, 20, ps)
+    U = ctgen.U_matrix(9, d2, d3, 3000)
+    (AU, BU), eng = run_gpu(fmt, N, d1, d2, d3, ps, ct.a_polys, ct.b_polys, U=U)
+    assert eng.spec.kU == 2
+    wa, wb = oracle_outputs(fmt, N, d1, ct.a_polys[0], ct.b_polys[0], U, ps[0])
+    assert np.array_equal(AU[0], wa) and np.array_equal(BU[0], wb)
 
 
 @pytest.mark.parametrize("shape", SHAPES[:6], ids=lambda s: "f%d_N%d_k%d_d2%d_d3%d_L%d" % s)
