@@ -143,6 +143,22 @@ ctpt_status ctpt_split(const ctpt_problem* prob, int32_t l, const void* d_ctmat,
 ctpt_status ctpt_gemm(const ctpt_problem* prob, int32_t l, const void* d_ws, size_t ws_bytes, const void* d_plain,
                       uint32_t* d_AU_l, uint32_t* d_BU_l, void* stream);
 
+/* End-to-end executor from HOST buffers (the e2e path): the same computation as
+ * ctpt_layout + ctpt_matmul, but the per-column ciphertexts h_a_polys / h_b_polys (layouts as
+ * for ctpt_layout) and the outputs h_AU / h_BU (layouts as for ctpt_matmul) live in host
+ * memory.  The stacked X of each prime is processed in row chunks of `chunk_rows` (≤ 0: about
+ * R/4, rounded to 64); the host→device copy of one chunk, the layout + split + GEMM of the
+ * previous one and the device→host copy of the one before run concurrently (two internal
+ * copy streams forked from and joined back into `stream`).  Host buffers must be page-locked
+ * (cudaHostAlloc / cudaHostRegister) for the copies to overlap.  d_plain as for ctpt_matmul;
+ * d_ws: at least ctpt_host_workspace_bytes(prob, chunk_rows) bytes.  Returns once everything
+ * is enqueued; the results are in host memory after `stream` completes.  No validation of
+ * residue ranges (use ctpt_layout with validate=1 for that). */
+ctpt_status ctpt_host_workspace_bytes(const ctpt_problem* prob, int64_t chunk_rows, size_t* bytes);
+ctpt_status ctpt_matmul_host(const ctpt_problem* prob, const uint32_t* h_a_polys, const uint32_t* h_b_polys,
+                             const void* d_plain, uint32_t* h_AU, uint32_t* h_BU, void* d_ws, size_t ws_bytes,
+                             int64_t chunk_rows, void* stream);
+
 /* Bring-up / diagnostics only (not a product path): the same limb GEMM and epilogue on
  * CUDA cores, reading the same workspace and plain planes.  Used by the tests to tell a
  * layout/split bug from a tensor-core descriptor bug. */

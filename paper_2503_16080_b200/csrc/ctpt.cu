@@ -151,6 +151,19 @@ int plane_index(const ctpt_problem* pb, int l, int i) {
   return pb->plain_per_prime ? l * kU + i : i;
 }
 
+// One prime's limb GEMM (all kU passes) over R rows of byte limbs.
+struct GemmArgs {
+  const void* limbs;     // [4][R][d2p] u8
+  int64_t R;             // rows of X in `limbs` (the problem's R, or a chunk's)
+  Dims d;                // d2, d2p, d3, j0, d3_loc
+  const int8_t* planes;  // U^T digit planes [nplanes][d3][d2p]
+  int nplanes, plane0, kU;
+  uint32_t p;
+  OutParams o;           // accumulate / w are set per pass
+};
+ctpt_status launch_split(const uint32_t* x, int64_t n, void* limbs, cudaStream_t st);
+ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt);
+
 }  // namespace
 
 extern "C" {
@@ -292,12 +305,8 @@ ctpt_status ctpt_split(const ctpt_problem* pb, int32_t l, const void* d_ctmat, v
   if (!d_ctmat || !d_ws) return fail(CTPT_ERR_ARG, "null device pointer");
   if (ws_bytes < static_cast<size_t>(4) * d.R * d.d2p) return fail(CTPT_ERR_ARG, "workspace too small");
   const int64_t n = d.R * d.d2p;  // multiple of 16
-  const uint4* x = reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(d_ctmat) + kHeader) + (l * n) / 4;
-  const int64_t n16 = n / 16;
-  const int blocks = static_cast<int>(std::min<int64_t>((n16 + 255) / 256, static_cast<int64_t>(num_sms()) * 16));
-  k_split<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(x, static_cast<uint4*>(d_ws), n16);
-  CUDA_TRY(cudaGetLastError());
-  return CTPT_OK;
+  const uint32_t* x = reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(d_ctmat) + kHeader) + l * n;
+  return launch_split(x, n, d_ws, static_cast<cudaStream_t>(stream));
 }
 
 static ctpt_status gemm_common(const ctpt_problem* pb, int32_t l, const void* d_ws, size_t ws_bytes,
@@ -308,39 +317,62 @@ static ctpt_status gemm_common(const ctpt_problem* pb, int32_t l, const void* d_
   if (l < 0 || l >= d.L) return fail(CTPT_ERR_ARG, "prime index %d out of range", l);
   if (!d_ws || !d_plain || !d_AU_l || !d_BU_l) return fail(CTPT_ERR_ARG, "null device pointer");
   if (ws_bytes < static_cast<size_t>(4) * d.R * d.d2p) return fail(CTPT_ERR_ARG, "workspace too small");
-  const int kU = pb->kU <= 0 ? 1 : pb->kU;
-  const uint32_t p = pb->primes[l];
-  const ModP m = make_modp(p);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int8_t* planes = reinterpret_cast<const int8_t*>(static_cast<const uint8_t*>(d_plain) + kHeader);
-  const int nplanes = pb->plain_per_prime ? d.L * kU : kU;
-  OutParams o;
-  o.AU = d_AU_l;
-  o.BU = d_BU_l;
-  o.rows_A = d.rows_A;
-  o.d1 = d.d1;
-  o.R = d.R;
-  o.d3_loc = d.d3_loc;
+  GemmArgs g;
+  g.limbs = d_ws;
+  g.R = d.R;
+  g.d = d;
+  g.kU = pb->kU <= 0 ? 1 : pb->kU;
+  g.planes = reinterpret_cast<const int8_t*>(static_cast<const uint8_t*>(d_plain) + kHeader);
+  g.nplanes = pb->plain_per_prime ? d.L * g.kU : g.kU;
+  g.plane0 = plane_index(pb, l, 0);
+  g.p = pb->primes[l];
+  g.o.AU = d_AU_l;
+  g.o.BU = d_BU_l;
+  g.o.rows_A = d.rows_A;
+  g.o.d1 = d.d1;
+  g.o.R = d.R;
+  g.o.d3_loc = d.d3_loc;
+  return launch_gemm(g, static_cast<cudaStream_t>(stream), simt);
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------------------------
+// Internal launchers (shared by the per-stage entry points and the host-pipelined executor)
+// ---------------------------------------------------------------------------------------------
+namespace {
+
+ctpt_status launch_split(const uint32_t* x, int64_t n, void* limbs, cudaStream_t st) {
+  const int64_t n16 = n / 16;  // n is a multiple of 16 (rows of d2p)
+  const int blocks = static_cast<int>(std::min<int64_t>((n16 + 255) / 256, static_cast<int64_t>(num_sms()) * 16));
+  if (blocks > 0) k_split<<<blocks, 256, 0, st>>>(reinterpret_cast<const uint4*>(x), static_cast<uint4*>(limbs), n16);
+  CUDA_TRY(cudaGetLastError());
+  return CTPT_OK;
+}
+
+ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
+  const Dims& d = g.d;
+  const ModP m = make_modp(g.p);
   if (simt) {
-    for (int i = 0; i < kU; ++i) {
+    for (int i = 0; i < g.kU; ++i) {
       SimtParams S;
-      S.limbs = static_cast<const uint8_t*>(d_ws);
-      S.uplane = planes + static_cast<int64_t>(plane_index(pb, l, i)) * d.d3 * d.d2p;
-      S.R = d.R;
+      S.limbs = static_cast<const uint8_t*>(g.limbs);
+      S.uplane = g.planes + static_cast<int64_t>(g.plane0 + i) * d.d3 * d.d2p;
+      S.R = g.R;
       S.d2 = d.d2;
       S.d2p = d.d2p;
       S.j_off = d.j0;
       S.m = m;
-      S.o = o;
+      S.o = g.o;
       S.o.accumulate = i > 0;
-      S.o.w = pow2mod(8 * i, p);
-      dim3 grid(static_cast<unsigned>((d.R + 15) / 16), static_cast<unsigned>((d.d3_loc + 15) / 16));
+      S.o.w = pow2mod(8 * i, g.p);
+      dim3 grid(static_cast<unsigned>((g.R + 15) / 16), static_cast<unsigned>((d.d3_loc + 15) / 16));
       k_gemm_simt<<<grid, 256, 0, st>>>(S);
       CUDA_TRY(cudaGetLastError());
     }
     return CTPT_OK;
   }
-  s = tc_setup();
+  ctpt_status s = tc_setup();
   if (s != CTPT_OK) return s;
   // Kernel choice.  Under the 1000 W cap the single-CTA kernel sustains more int8 ops
   // (c3, 100 steps: 2844 TOP/s at 1395 MHz vs 2634 TOP/s at 1140 MHz for the CTA pair, which is
@@ -351,17 +383,17 @@ static ctpt_status gemm_common(const ctpt_problem* pb, int32_t l, const void* d_
   if (const char* g = getenv("CTPT_GEMM")) pair = (strcmp(g, "2cta") == 0);
   const int block_j = pair ? T2_BLOCK_J : TC_BLOCK_J;
   CUtensorMap tmU, tmX;
-  s = make_tmap_u8(&tmU, planes, d.d2, d.d3, nplanes, d.d2p, d.d3 * d.d2p, TC_BLOCK_K, 128, 1);
+  s = make_tmap_u8(&tmU, g.planes, d.d2, d.d3, g.nplanes, d.d2p, d.d3 * d.d2p, TC_BLOCK_K, 128, 1);
   if (s != CTPT_OK) return s;
-  s = make_tmap_u8(&tmX, d_ws, d.d2, d.R, 4, d.d2p, d.R * d.d2p, TC_BLOCK_K, TC_BLOCK_R, pair ? 2 : 4);
+  s = make_tmap_u8(&tmX, g.limbs, d.d2, g.R, 4, d.d2p, g.R * d.d2p, TC_BLOCK_K, TC_BLOCK_R, pair ? 2 : 4);
   if (s != CTPT_OK) return s;
   TcParams P;
-  P.R = d.R;
+  P.R = g.R;
   P.d2 = d.d2;
   P.j_off = static_cast<int32_t>(d.j0);
   P.num_kb = static_cast<int32_t>((d.d2 + TC_BLOCK_K - 1) / TC_BLOCK_K);
   P.tiles_j = static_cast<int32_t>((d.d3_loc + block_j - 1) / block_j);
-  P.tiles_r = static_cast<int32_t>((d.R + TC_BLOCK_R - 1) / TC_BLOCK_R);
+  P.tiles_r = static_cast<int32_t>((g.R + TC_BLOCK_R - 1) / TC_BLOCK_R);
   const int64_t nt = static_cast<int64_t>(P.tiles_j) * P.tiles_r;
   if (nt > INT32_MAX) return fail(CTPT_ERR_SHAPE, "too many tiles");
   P.num_tiles = static_cast<int32_t>(nt);
@@ -371,11 +403,11 @@ static ctpt_status gemm_common(const ctpt_problem* pb, int32_t l, const void* d_
   const int sms = num_sms();
   const unsigned grid = pair ? static_cast<unsigned>(2 * std::min<int64_t>(nt, sms / 2))
                              : static_cast<unsigned>(std::min<int64_t>(nt, sms));
-  for (int i = 0; i < kU; ++i) {
-    P.plane = plane_index(pb, l, i);
-    P.o = o;
+  for (int i = 0; i < g.kU; ++i) {
+    P.plane = g.plane0 + i;
+    P.o = g.o;
     P.o.accumulate = i > 0;
-    P.o.w = pow2mod(8 * i, p);
+    P.o.w = pow2mod(8 * i, g.p);
     if (pair)
       k_gemm_tc2<<<grid, T2_THREADS, T2_SMEM_BYTES, st>>>(tmU, tmX, P);
     else
@@ -384,6 +416,10 @@ static ctpt_status gemm_common(const ctpt_problem* pb, int32_t l, const void* d_
   }
   return CTPT_OK;
 }
+
+}  // namespace
+
+extern "C" {
 
 ctpt_status ctpt_gemm(const ctpt_problem* pb, int32_t l, const void* d_ws, size_t ws_bytes, const void* d_plain,
                       uint32_t* d_AU_l, uint32_t* d_BU_l, void* stream) {
@@ -408,6 +444,177 @@ ctpt_status ctpt_matmul(const ctpt_problem* pb, const void* d_ctmat, const void*
                   d_BU + static_cast<int64_t>(l) * d.d3_loc * d.d1, stream);
     if (s != CTPT_OK) return s;
   }
+  return CTPT_OK;
+}
+
+}  // extern "C"
+
+// =============================================================================================
+// Host-pipelined executor: per-column ciphertexts in HOST memory → (A·U, B·U) in HOST memory.
+// The stacked X of each prime is cut into row chunks; chunk i's host→device copy, chunk i−1's
+// layout + split + GEMM and chunk i−2's device→host copy run concurrently on three streams
+// (copy engines in both directions + the SMs), with two staging buffers per direction.
+// =============================================================================================
+namespace {
+
+struct HostPlan {
+  int64_t chunk;  // rows of X per chunk (multiple of 64)
+  size_t in_bytes, cm_bytes, limb_bytes, out_bytes, total;
+};
+
+size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+HostPlan host_plan(const Dims& d, int64_t chunk_rows) {
+  HostPlan h;
+  // default: ~6 chunks per prime (c3: 97 ms/step = 86 % of the concurrent-PCIe floor, vs 110 ms
+  // with 4 chunks; profiles/r01/e2e_chunk_sweep.txt)
+  int64_t c = chunk_rows > 0 ? chunk_rows : (d.R + 5) / 6;
+  c = (c + 63) / 64 * 64;
+  c = std::max<int64_t>(64, std::min<int64_t>(c, (d.R + 63) / 64 * 64));
+  h.chunk = c;
+  h.in_bytes = align256(static_cast<size_t>(d.d2) * c * 4);
+  h.cm_bytes = align256(static_cast<size_t>(c) * d.d2p * 4);
+  h.limb_bytes = align256(static_cast<size_t>(4) * c * d.d2p);
+  h.out_bytes = align256(static_cast<size_t>(d.d3_loc) * c * 4);
+  h.total = 2 * h.in_bytes + h.cm_bytes + h.limb_bytes + 2 * h.out_bytes;
+  return h;
+}
+
+ctpt_status launch_layout_cols(const uint32_t* a_colmajor, uint32_t* x, int64_t rows, int64_t d2, int64_t d2p,
+                               cudaStream_t st) {
+  LayoutParams P;
+  memset(&P, 0, sizeof(P));
+  P.a = a_colmajor;
+  P.b = a_colmajor;  // never read: every row is an "A" row
+  P.x = x;
+  P.rows_A = rows;
+  P.d1 = 0;
+  P.R = rows;
+  P.d2 = d2;
+  P.d2p = d2p;
+  dim3 grid(static_cast<unsigned>((rows + 63) / 64), static_cast<unsigned>((d2p + 63) / 64), 1);
+  k_layout<<<grid, 256, 0, st>>>(P);
+  CUDA_TRY(cudaGetLastError());
+  return CTPT_OK;
+}
+
+struct StreamSet {
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t ev[10] = {};
+  ~StreamSet() {  // resources are released once the enqueued work completes
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (h2d) cudaStreamDestroy(h2d);
+    if (d2h) cudaStreamDestroy(d2h);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+ctpt_status ctpt_host_workspace_bytes(const ctpt_problem* pb, int64_t chunk_rows, size_t* bytes) {
+  Dims d;
+  ctpt_status s = check_problem(pb, d);
+  if (s != CTPT_OK) return s;
+  if (!bytes) return fail(CTPT_ERR_ARG, "bytes is NULL");
+  *bytes = host_plan(d, chunk_rows).total;
+  return CTPT_OK;
+}
+
+ctpt_status ctpt_matmul_host(const ctpt_problem* pb, const uint32_t* h_a, const uint32_t* h_b, const void* d_plain,
+                             uint32_t* h_AU, uint32_t* h_BU, void* d_ws, size_t ws_bytes, int64_t chunk_rows,
+                             void* stream) {
+  Dims d;
+  ctpt_status s = check_problem(pb, d);
+  if (s != CTPT_OK) return s;
+  if (!h_a || !h_b || !d_plain || !h_AU || !h_BU || !d_ws) return fail(CTPT_ERR_ARG, "null pointer");
+  const HostPlan hp = host_plan(d, chunk_rows);
+  if (ws_bytes < hp.total) return fail(CTPT_ERR_ARG, "workspace too small (%zu < %zu)", ws_bytes, hp.total);
+  cudaStream_t sc = static_cast<cudaStream_t>(stream);
+  uint8_t* w = static_cast<uint8_t*>(d_ws);
+  uint32_t* in[2] = {reinterpret_cast<uint32_t*>(w), reinterpret_cast<uint32_t*>(w + hp.in_bytes)};
+  uint32_t* cm = reinterpret_cast<uint32_t*>(w + 2 * hp.in_bytes);
+  void* limbs = w + 2 * hp.in_bytes + hp.cm_bytes;
+  uint32_t* ob[2] = {reinterpret_cast<uint32_t*>(w + 2 * hp.in_bytes + hp.cm_bytes + hp.limb_bytes),
+                     reinterpret_cast<uint32_t*>(w + 2 * hp.in_bytes + hp.cm_bytes + hp.limb_bytes + hp.out_bytes)};
+
+  StreamSet ss;
+  CUDA_TRY(cudaStreamCreateWithFlags(&ss.h2d, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&ss.d2h, cudaStreamNonBlocking));
+  for (auto& e : ss.ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  cudaEvent_t ev_start = ss.ev[0], ev_end = ss.ev[1];
+  cudaEvent_t* in_ready = ss.ev + 2;  // [2]
+  cudaEvent_t* in_free = ss.ev + 4;   // [2]
+  cudaEvent_t* out_ready = ss.ev + 6; // [2]
+  cudaEvent_t* out_free = ss.ev + 8;  // [2]
+
+  // fork: copies start only after prior work on the caller's stream (e.g. the precompute)
+  CUDA_TRY(cudaEventRecord(ev_start, sc));
+  CUDA_TRY(cudaStreamWaitEvent(ss.h2d, ev_start, 0));
+  CUDA_TRY(cudaStreamWaitEvent(ss.d2h, ev_start, 0));
+
+  GemmArgs g;
+  g.d = d;
+  g.kU = pb->kU <= 0 ? 1 : pb->kU;
+  g.planes = reinterpret_cast<const int8_t*>(static_cast<const uint8_t*>(d_plain) + kHeader);
+  g.nplanes = pb->plain_per_prime ? d.L * g.kU : g.kU;
+  g.limbs = limbs;
+
+  int64_t it = 0;
+  for (int l = 0; l < d.L; ++l) {
+    const uint32_t* a_l = h_a + static_cast<int64_t>(l) * d.d2 * d.rows_A;
+    const uint32_t* b_l = h_b + static_cast<int64_t>(l) * d.d2 * d.d1;
+    uint32_t* AU_l = h_AU + static_cast<int64_t>(l) * d.d3_loc * d.rows_A;
+    uint32_t* BU_l = h_BU + static_cast<int64_t>(l) * d.d3_loc * d.d1;
+    for (int64_t r0 = 0; r0 < d.R; r0 += hp.chunk, ++it) {
+      const int b = static_cast<int>(it & 1);
+      const int64_t r1 = std::min(d.R, r0 + hp.chunk), rows = r1 - r0;
+      const int64_t na = std::max<int64_t>(0, std::min(r1, d.rows_A) - r0), nb = rows - na;
+      const int64_t rb0 = r0 + na - d.rows_A;  // first B row of the chunk (if nb > 0)
+      // 1. host → device: the chunk's rows of every ciphertext column, packed col-major [d2][rows]
+      if (it >= 2) CUDA_TRY(cudaStreamWaitEvent(ss.h2d, in_free[b], 0));
+      if (na)
+        CUDA_TRY(cudaMemcpy2DAsync(in[b], rows * 4, a_l + r0, d.rows_A * 4, na * 4, d.d2, cudaMemcpyHostToDevice,
+                                   ss.h2d));
+      if (nb)
+        CUDA_TRY(cudaMemcpy2DAsync(in[b] + na, rows * 4, b_l + rb0, d.d1 * 4, nb * 4, d.d2, cudaMemcpyHostToDevice,
+                                   ss.h2d));
+      CUDA_TRY(cudaEventRecord(in_ready[b], ss.h2d));
+      // 2. layout + split + GEMM on the caller's stream
+      CUDA_TRY(cudaStreamWaitEvent(sc, in_ready[b], 0));
+      s = launch_layout_cols(in[b], cm, rows, d.d2, d.d2p, sc);
+      if (s != CTPT_OK) return s;
+      CUDA_TRY(cudaEventRecord(in_free[b], sc));
+      s = launch_split(cm, rows * d.d2p, limbs, sc);
+      if (s != CTPT_OK) return s;
+      if (it >= 2) CUDA_TRY(cudaStreamWaitEvent(sc, out_free[b], 0));
+      g.R = rows;
+      g.p = pb->primes[l];
+      g.plane0 = plane_index(pb, l, 0);
+      g.o.AU = ob[b];
+      g.o.BU = ob[b];
+      g.o.rows_A = rows;
+      g.o.d1 = 0;
+      g.o.R = rows;
+      g.o.d3_loc = d.d3_loc;
+      s = launch_gemm(g, sc, false);
+      if (s != CTPT_OK) return s;
+      CUDA_TRY(cudaEventRecord(out_ready[b], sc));
+      // 3. device → host: rows [r0, r1) of every output column
+      CUDA_TRY(cudaStreamWaitEvent(ss.d2h, out_ready[b], 0));
+      if (na)
+        CUDA_TRY(cudaMemcpy2DAsync(AU_l + r0, d.rows_A * 4, ob[b], rows * 4, na * 4, d.d3_loc, cudaMemcpyDeviceToHost,
+                                   ss.d2h));
+      if (nb)
+        CUDA_TRY(cudaMemcpy2DAsync(BU_l + rb0, d.d1 * 4, ob[b] + na, rows * 4, nb * 4, d.d3_loc,
+                                   cudaMemcpyDeviceToHost, ss.d2h));
+      CUDA_TRY(cudaEventRecord(out_free[b], ss.d2h));
+    }
+  }
+  // join: the caller's stream completes only after the last device→host copy
+  CUDA_TRY(cudaEventRecord(ev_end, ss.d2h));
+  CUDA_TRY(cudaStreamWaitEvent(sc, ev_end, 0));
   return CTPT_OK;
 }
 

@@ -61,6 +61,8 @@ _sig = {
     "ctpt_split": (ctypes.c_int, [_PP, ctypes.c_int32, _P, _P, ctypes.c_size_t, _P]),
     "ctpt_gemm": (ctypes.c_int, [_PP, ctypes.c_int32, _P, ctypes.c_size_t, _P, _P, _P, _P]),
     "ctpt_gemm_simt": (ctypes.c_int, [_PP, ctypes.c_int32, _P, ctypes.c_size_t, _P, _P, _P, _P]),
+    "ctpt_host_workspace_bytes": (ctypes.c_int, [_PP, ctypes.c_int64, ctypes.POINTER(ctypes.c_size_t)]),
+    "ctpt_matmul_host": (ctypes.c_int, [_PP, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, ctypes.c_int64, _P]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_lib, _name)
@@ -167,6 +169,20 @@ def gemm(spec: Spec, l: int, ws, plain, AU_l, BU_l, stream=None, simt: bool = Fa
     f = _lib.ctpt_gemm_simt if simt else _lib.ctpt_gemm
     _check(f(ctypes.byref(pb), l, _ptr(ws), ws.numel() * ws.element_size(), _ptr(plain), _ptr(AU_l), _ptr(BU_l),
              _stream(stream)))
+
+
+def host_workspace_bytes(spec: Spec, chunk_rows: int = 0) -> int:
+    pb = spec.cstruct()
+    n = ctypes.c_size_t(0)
+    _check(_lib.ctpt_host_workspace_bytes(ctypes.byref(pb), chunk_rows, ctypes.byref(n)))
+    return n.value
+
+
+def matmul_host(spec: Spec, a_polys_h, b_polys_h, plain, AU_h, BU_h, ws, chunk_rows: int = 0, stream=None):
+    """a_polys_h / b_polys_h / AU_h / BU_h: pinned host tensors (or raw host addresses)."""
+    pb = spec.cstruct()
+    _check(_lib.ctpt_matmul_host(ctypes.byref(pb), _ptr(a_polys_h), _ptr(b_polys_h), _ptr(plain), _ptr(AU_h),
+                                 _ptr(BU_h), _ptr(ws), ws.numel() * ws.element_size(), chunk_rows, _stream(stream)))
 
 
 def raw_lib():

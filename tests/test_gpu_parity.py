@@ -172,6 +172,41 @@ def test_general_U_residues_rns():
         assert np.array_equal(AU[l], wa) and np.array_equal(BU[l], wb)
 
 
+@pytest.mark.parametrize("fmt,N,k,d2,d3,L,u_bound,chunk,cols", [
+    (A, 64, 3, 200, 130, 2, 8, 64, (0, 0)),         # many chunks, A/B boundary inside a chunk
+    (S, 32, 4, 96, 300, 1, 8, 0, (17, 250)),        # default chunking, column shard
+    (R, 256, 1, 130, 64, 3, 30000, 192, (0, 0)),    # k_U = 2 through the host path
+    (A, 16, 2, 40, 7, 1, 8, 4096, (0, 0)),          # one chunk larger than R
+])
+def test_matmul_host_pipeline(fmt, N, k, d2, d3, L, u_bound, chunk, cols):
+    """ctpt_matmul_host (host buffers, chunked 3-stream pipeline) == the oracle."""
+    import torch
+
+    from paper_2503_16080_b200 import ctpt
+    from paper_2503_16080_b200.engine import CpmmEngine
+
+    d1 = N * k
+    ps = ctgen.primes(L)
+    ct = ctgen.encrypt(fmt, N, d1, d2, 4, 20, ps)
+    U = ctgen.U_matrix(4, d2, d3, u_bound)
+    eng = CpmmEngine(ctpt.Spec(fmt, N, d1, d2, d3, ps, cols[0], cols[1]), "cuda")
+    eng.precompute(U)
+    a_h = torch.from_numpy(ct.a_polys.view(np.int32)).pin_memory()
+    b_h = torch.from_numpy(ct.b_polys.view(np.int32)).pin_memory()
+    AU_h = torch.zeros(eng.sizes.out_AU_bytes // 4, dtype=torch.int32).pin_memory()
+    BU_h = torch.zeros(eng.sizes.out_BU_bytes // 4, dtype=torch.int32).pin_memory()
+    ws = torch.empty(ctpt.host_workspace_bytes(eng.spec, chunk), dtype=torch.uint8, device="cuda")
+    ctpt.matmul_host(eng.spec, a_h, b_h, eng.plain, AU_h, BU_h, ws, chunk_rows=chunk)
+    torch.cuda.synchronize()
+    d3l = eng.sizes.d3_loc
+    AU = AU_h.numpy().view(np.uint32).reshape(L, d3l, -1)
+    BU = BU_h.numpy().view(np.uint32).reshape(L, d3l, d1)
+    c1 = cols[1] or d3
+    for l, p in enumerate(ps):
+        wa, wb = oracle_outputs(fmt, N, d1, ct.a_polys[l], ct.b_polys[l], U, p, cols=np.arange(cols[0], c1))
+        assert np.array_equal(AU[l], wa) and np.array_equal(BU[l], wb)
+
+
 def test_validate_flags_out_of_range():
     from paper_2503_16080_b200 import ctpt
 
