@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target seconds of oracle work per sample")
+    ap.add_argument("--shard", action="store_true",
+                    help="strong scaling: shard ONE problem's (prime, column) units over the ranks "
+                         "(shard.plan_units); host-resident inputs/outputs via ctpt_matmul_host")
     return ap.parse_args()
 
 
@@ -389,6 +392,87 @@ def run_e2e(args, c, ps, ct, eng, dev, stream):
                     "(3 streams) -> pinned host outputs"}
 
 
+def run_sharded(args, rank: int, world: int, local_rank: int):
+    """One problem (e.g. c5: 8 primes, 68.7 GB of ciphertexts) sharded over the ranks by
+    (prime, U-column) units; each rank streams its units from pinned host
+    memory through ctpt_matmul_host (a 1-GPU run streams the primes sequentially) and leaves
+    its output blocks in host memory (the sharded result; shard.run_and_gather is the NCCL
+    gather for device-resident outputs).  Device time, max over ranks; "scaling": "strong"."""
+    import torch
+
+    import ctgen
+    from paper_2503_16080_b200 import ctpt
+    from paper_2503_16080_b200.engine import CpmmEngine
+    from paper_2503_16080_b200.shard import plan_units, primes_needed
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    c = ctgen.CONFIGS[args.config]
+    cores = os.cpu_count() or 1
+    ps = ctgen.primes(c.L)
+    plan = plan_units(c.L, c.d3, world)
+    mine = plan[rank]
+    t0 = time.perf_counter()
+    U = ctgen.U_matrix(c.seed, c.d2, c.d3, c.u_bound, nthreads=max(1, cores // world))
+    host_ct = {}
+    for l in primes_needed(mine):
+        ct = ctgen.encrypt(c.fmt, c.N, c.d1, c.d2, c.seed, c.log_delta, [ps[l]], nthreads=max(1, cores // world))
+        host_ct[l] = (torch.from_numpy(ct.a_polys.view(np.int32)).pin_memory(),
+                      torch.from_numpy(ct.b_polys.view(np.int32)).pin_memory())
+        del ct
+    gen_s = time.perf_counter() - t0
+    eng = CpmmEngine(ctpt.Spec(c.fmt, c.N, c.d1, c.d2, c.d3, [ps[mine[0].l]]), dev)
+    kU = eng.precompute(U)
+    specs, outs = [], []
+    ws_bytes = 0
+    for u in mine:
+        sp = ctpt.Spec(c.fmt, c.N, c.d1, c.d2, c.d3, [ps[u.l]], u.c0, u.c1, kU, 0)
+        sz = ctpt.query_sizes(sp)
+        specs.append(sp)
+        outs.append((torch.empty(sz.out_AU_bytes // 4, dtype=torch.int32).pin_memory(),
+                     torch.empty(sz.out_BU_bytes // 4, dtype=torch.int32).pin_memory()))
+        ws_bytes = max(ws_bytes, ctpt.host_workspace_bytes(sp, 0))
+    hws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        for u, sp, (au, bu) in zip(mine, specs, outs):
+            a_h, b_h = host_ct[u.l]
+            ctpt.matmul_host(sp, a_h, b_h, eng.plain, au, bu, hws, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    clk = ClockSampler(local_rank)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    h2d = sum(host_ct[u.l][0].numel() * 4 + host_ct[u.l][1].numel() * 4 for u in mine)
+    d2h = sum(au.numel() * 4 + bu.numel() * 4 for au, bu in outs)
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": c.residue_macs / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+            "config": dict(workload_desc(c), parallelism=f"sharded over {world} rank(s): "
+                                                        f"{[[(u.l, u.c0, u.c1) for u in us] for us in plan]}",
+                           path="pinned host ciphertexts -> ctpt_matmul_host per unit -> pinned host outputs"),
+            "e2e": {"value": c.residue_macs / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": None, "clocks": clocks, "input_generation_s": gen_s}))
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -403,7 +487,10 @@ def main():
         torch.cuda.set_device(local_rank)
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_ours(args, rank, world, local_rank)
+        if args.shard:
+            run_sharded(args, rank, world, local_rank)
+        else:
+            run_ours(args, rank, world, local_rank)
     finally:
         if world > 1:
             import torch

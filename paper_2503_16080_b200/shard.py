@@ -1,0 +1,118 @@
+"""Multi-GPU sharding of CP-MM — planner, per-rank execution, final gather.
+
+The path partitions naturally: the residue products of different RNS primes are independent
+(one Mod-PP-MM per prime, the structure of Strategy 3), and so are different
+column blocks of U (output column j is output ciphertext j).  A *unit* is
+(prime index l, U columns [c0, c1)).  There is no exchange inside the computation; the only
+communication is the optional final gather of every unit's (A·U, B·U) block to rank 0, issued
+as point-to-point sends right after each unit is computed so the transfer of unit i overlaps
+the compute of unit i+1 (NCCL runs its sends on its own stream).
+
+Layout of the gathered result on rank 0 (the single-GPU layout of ctpt_matmul):
+    AU [L][d3][rows_A], BU [L][d3][d1]; a unit is the contiguous block AU[l, c0:c1].
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable
+
+
+@dataclass(frozen=True)
+class Unit:
+    l: int   # prime index
+    c0: int  # first U column
+    c1: int  # one past the last U column
+
+    @property
+    def ncols(self) -> int:
+        return self.c1 - self.c0
+
+
+def plan_units(L: int, d3: int, world: int) -> list[list[Unit]]:
+    """Per-rank unit lists covering every (prime, column) pair exactly once, with equal
+    residue-MAC counts up to one column.
+    * world | L: rank r takes primes [r·L/world, (r+1)·L/world), all columns (no U split);
+    * otherwise: the (prime, column) pairs in prime-major order are cut into `world` contiguous
+      slices; a rank touches at most ⌈L/world⌉ + 1 primes."""
+    if world < 1 or L < 1 or d3 < 1:
+        raise ValueError("world, L, d3 must be >= 1")
+    if L % world == 0:
+        per = L // world
+        return [[Unit(l, 0, d3) for l in range(r * per, (r + 1) * per)] for r in range(world)]
+    total = L * d3
+    out = []
+    for r in range(world):
+        a, b = total * r // world, total * (r + 1) // world
+        units = []
+        while a < b:
+            l, c = divmod(a, d3)
+            c1 = min(d3, c + (b - a))
+            units.append(Unit(l, c, c1))
+            a += c1 - c
+        out.append(units)
+    return out
+
+
+def primes_needed(units: list[Unit]) -> list[int]:
+    return sorted({u.l for u in units})
+
+
+def run_and_gather(units_per_rank: list[list[Unit]], rank: int, compute: Callable[[Unit], tuple],
+                   out_AU=None, out_BU=None, gather: bool = True, group=None):
+    """Compute this rank's units with `compute(unit) -> (AU_blk [ncols][rows_A], BU_blk [ncols][d1])`
+    (torch tensors on the communication device) and, if `gather`, send them to rank 0, which
+    writes every rank's blocks into out_AU [L][d3][rows_A] / out_BU [L][d3][d1].
+    Returns the list of (unit, AU_blk, BU_blk) computed locally."""
+    import torch.distributed as dist
+
+    mine = []
+    reqs = []
+    for u in units_per_rank[rank]:
+        au, bu = compute(u)
+        mine.append((u, au, bu))
+        if gather and rank != 0:
+            reqs.append(dist.isend(au.contiguous(), dst=0, group=group))
+            reqs.append(dist.isend(bu.contiguous(), dst=0, group=group))
+    if gather and rank == 0:
+        for (u, au, bu) in mine:
+            out_AU[u.l, u.c0:u.c1].copy_(au)
+            out_BU[u.l, u.c0:u.c1].copy_(bu)
+        for src in range(1, len(units_per_rank)):
+            for u in units_per_rank[src]:
+                dist.recv(out_AU[u.l, u.c0:u.c1], src=src, group=group)
+                dist.recv(out_BU[u.l, u.c0:u.c1], src=src, group=group)
+    for r in reqs:
+        r.wait()
+    return mine
+
+
+def gpu_compute_fn(fmt: int, N: int, d1: int, d2: int, d3: int, primes: list, get_ciphertexts: Callable,
+                   U, device):
+    """compute(unit) for one GPU: ctpt_layout + ctpt_plain_precompute + ctpt_matmul on a one-prime,
+    one-column-block Spec.  get_ciphertexts(l) -> (a_polys_l, b_polys_l) of prime l (host numpy or
+    device tensors); prime l's layout is cached across its units."""
+    import torch
+
+    from . import ctpt
+    from .engine import CpmmEngine
+
+    cache = {}
+
+    def compute(u: Unit):
+        key = u.l
+        if key not in cache:
+            cache.clear()
+            eng = CpmmEngine(ctpt.Spec(fmt, N, d1, d2, d3, [primes[u.l]]), device)
+            a, b = get_ciphertexts(u.l)
+            eng.layout(a, b)
+            eng.precompute(U)
+            cache[key] = eng
+        base = cache[key]
+        spec = ctpt.Spec(fmt, N, d1, d2, d3, [primes[u.l]], u.c0, u.c1, base.spec.kU, 0)
+        sizes = ctpt.query_sizes(spec)
+        AU = torch.empty(sizes.out_AU_bytes // 4, dtype=torch.int32, device=device)
+        BU = torch.empty(sizes.out_BU_bytes // 4, dtype=torch.int32, device=device)
+        ctpt.matmul(spec, base.ctmat, base.plain, AU, BU, base.ws)
+        return AU.view(u.ncols, sizes.rows_A), BU.view(u.ncols, d1)
+
+    return compute

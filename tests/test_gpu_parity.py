@@ -207,6 +207,32 @@ def test_matmul_host_pipeline(fmt, N, k, d2, d3, L, u_bound, chunk, cols):
         assert np.array_equal(AU[l], wa) and np.array_equal(BU[l], wb)
 
 
+def test_shard_units_on_one_gpu():
+    """Every unit of a 4-rank plan (L = 3 primes: column-split units) computed through
+    shard.gpu_compute_fn on this GPU and placed as rank 0's gather would place it == the oracle."""
+    import torch
+
+    from paper_2503_16080_b200.shard import gpu_compute_fn, plan_units
+
+    fmt, N, k, d2, d3, L = A, 64, 2, 130, 300, 3
+    d1 = N * k
+    ps = ctgen.primes(L)
+    ct = ctgen.encrypt(fmt, N, d1, d2, 8, 20, ps)
+    U = ctgen.U_matrix(8, d2, d3, 8)
+    compute = gpu_compute_fn(fmt, N, d1, d2, d3, ps, lambda l: (ct.a_polys[l], ct.b_polys[l]), U, "cuda")
+    full_AU = np.zeros((L, d3, N), np.uint32)
+    full_BU = np.zeros((L, d3, d1), np.uint32)
+    for units in plan_units(L, d3, 4):
+        for u in units:
+            au, bu = compute(u)
+            torch.cuda.synchronize()
+            full_AU[u.l, u.c0:u.c1] = au.cpu().numpy().view(np.uint32)
+            full_BU[u.l, u.c0:u.c1] = bu.cpu().numpy().view(np.uint32)
+    for l, p in enumerate(ps):
+        wa, wb = oracle_outputs(fmt, N, d1, ct.a_polys[l], ct.b_polys[l], U, p)
+        assert np.array_equal(full_AU[l], wa) and np.array_equal(full_BU[l], wb)
+
+
 def test_validate_flags_out_of_range():
     from paper_2503_16080_b200 import ctpt
 
