@@ -16,8 +16,26 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libctgen.so")
 
-RLWE, SHARED_S, SHARED_A = 0, 1, 2
-FORMAT_NAMES = {RLWE: "rlwe", SHARED_S: "shared-s", SHARED_A: "shared-a"}
+RLWE, SHARED_S, SHARED_A, STRUCT_A = 0, 1, 2, 3
+FORMAT_NAMES = {RLWE: "rlwe", SHARED_S: "shared-s", SHARED_A: "shared-a", STRUCT_A: "struct-a shared-a"}
+
+
+def n_a_polys(fmt: int, N: int, d1: int, ncols: int) -> int:
+    """Number of a-polynomials a format stores for `ncols` columns: one per (column, chunk) for
+    shared-s, one per column for RLWE / shared-a, one per ROW BLOCK (d1/N, independent of the
+    columns) for structured-A shared-a."""
+    k = d1 // N
+    if fmt == SHARED_S:
+        return ncols * k
+    if fmt == STRUCT_A:
+        return k
+    return ncols
+
+
+def rows_A_of(fmt: int, N: int, d1: int) -> int:
+    """Rows of the matrix A the CP-MM multiplies: d1 (shared-s), N (RLWE, shared-a), 0 for
+    structured-A shared-a, whose Ã is not multiplied (Algorithm 7 step 1)."""
+    return d1 if fmt == SHARED_S else (0 if fmt == STRUCT_A else N)
 
 _lib = None
 
@@ -189,7 +207,7 @@ class Ciphertexts:
 
     @property
     def rows_A(self) -> int:
-        return self.d1 if self.fmt == SHARED_S else self.N
+        return rows_A_of(self.fmt, self.N, self.d1)
 
 
 def encrypt(fmt: int, N: int, d1: int, d2: int, seed: int, log_delta: int, prime_list, col_begin: int = 0,
@@ -201,7 +219,7 @@ def encrypt(fmt: int, N: int, d1: int, d2: int, seed: int, log_delta: int, prime
     k = d1 // N
     ncols = col_end - col_begin
     L = len(prime_list)
-    n_a = ncols * (k if fmt == SHARED_S else 1)
+    n_a = n_a_polys(fmt, N, d1, ncols)
     a = out_a if out_a is not None else np.empty((L, n_a, N), dtype=np.uint32)
     b = out_b if out_b is not None else np.empty((L, ncols * k, N), dtype=np.uint32)
     assert a.dtype == np.uint32 and a.size == L * n_a * N and a.flags["C_CONTIGUOUS"]
@@ -242,7 +260,7 @@ class Config:
 
     @property
     def rows_A(self) -> int:
-        return self.d1 if self.fmt == SHARED_S else self.N
+        return rows_A_of(self.fmt, self.N, self.d1)
 
     @property
     def R(self) -> int:
@@ -259,4 +277,7 @@ CONFIGS = {
     "c3": Config("c3", SHARED_A, 4096, 16384, 16384, 16384, 3, 45, 8),
     "c4": Config("c4", SHARED_S, 8192, 32768, 32768, 4096, 4, 50, 8),
     "c5": Config("c5", SHARED_S, 16384, 32768, 32768, 32768, 8, 60, 8),
+    # Algorithm 7 (CP-MM with precomputation) on c3's shapes in the
+    # structured-A shared-a format — only B·U is computed (R = d1 = 16384 instead of 20480).
+    "c3a": Config("c3a", STRUCT_A, 4096, 16384, 16384, 16384, 3, 45, 8),
 }

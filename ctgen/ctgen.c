@@ -34,6 +34,7 @@
 #define CTGEN_RLWE 0
 #define CTGEN_SHARED_S 1
 #define CTGEN_SHARED_A 2
+#define CTGEN_STRUCT_A 3 /* structured-A shared-a: a_i shared by row block i, sk_j per column */
 
 #define K_SK 1ULL
 #define K_A 2ULL
@@ -345,10 +346,21 @@ int ctgen_negacyclic_ntt(const uint32_t* a, const int8_t* s, int64_t N, uint32_t
  * with local column c = j - col_begin, poly index c*k + t (a: c or c*k+t).
  * Streams use the GLOBAL column index j, so a column range reproduces the same values.
  */
+static int encrypt_struct_a(int64_t N, int64_t d1, uint64_t seed, int log_delta, int L, const uint32_t* primes,
+                            int64_t col_begin, int64_t col_end, uint32_t* a_polys, uint32_t* b_polys);
+
 int ctgen_encrypt(int fmt, int64_t N, int64_t d1, int64_t d2, uint64_t seed, int log_delta, int L,
                   const uint32_t* primes, int64_t col_begin, int64_t col_end, uint32_t* a_polys,
                   uint32_t* b_polys, int nthreads) {
   if (N <= 0 || (N & (N - 1))) return -1;
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+  if (fmt == CTGEN_STRUCT_A) {
+    if (d1 % N) return -2;
+    if (col_begin < 0 || col_end > d2 || col_begin > col_end) return -4;
+    return encrypt_struct_a(N, d1, seed, log_delta, L, primes, col_begin, col_end, a_polys, b_polys);
+  }
   if (d1 % N) return -2;
   if (fmt == CTGEN_RLWE && d1 != N) return -3;
   if (col_begin < 0 || col_end > d2 || col_begin > col_end) return -4;
@@ -446,4 +458,64 @@ void ctgen_plain_block(uint64_t seed, int64_t N, int64_t d1, int log_delta, int6
 #endif
   for (int64_t i = 0; i < nrows; ++i)
     for (int64_t j = 0; j < ncols; ++j) out[i * ncols + j] = ctgen_plain(seed, N, d1, r0 + i, c0 + j, log_delta);
+}
+
+/* ---------------- structured-A shared-a (Algorithm 7) ----------------
+ *   a_i · sk_j + b_{i,j} = P_{i,j}   (i < k = d1/N row blocks, j < d2 columns)
+ * i.e. Ã·S + B = P with Ã = [toep(a_0); …; toep(a_{k−1})] ∈ Z_q^{d1×N} and S = [Vec(sk_j)]_j.
+ * One a-poly per row block (stream A, poly index 2^22 + i: disjoint from the column-indexed
+ * a-parts of the other formats) shared by every column; one ternary key per GLOBAL column j
+ * (stream SK, t = j).  Output: a_polys[l][k][N], b_polys[l][ncols·k][N] (poly c·k + i). */
+static int encrypt_struct_a(int64_t N, int64_t d1, uint64_t seed, int log_delta, int L, const uint32_t* primes,
+                            int64_t col_begin, int64_t col_end, uint32_t* a_polys, uint32_t* b_polys) {
+  const int64_t k = d1 / N;
+  const int64_t ncols = col_end - col_begin;
+  for (int l = 0; l < L; ++l) {
+    const uint32_t p = primes[l];
+    ntt_plan pl;
+    if (ntt_plan_init(&pl, p, N)) return -5;
+    uint32_t* A = a_polys + (int64_t)l * k * N;
+    uint32_t* B = b_polys + (int64_t)l * ncols * k * N;
+    uint32_t* a_hat = (uint32_t*)malloc(sizeof(uint32_t) * N * k);
+    for (int64_t i = 0; i < k; ++i) {
+      for (int64_t c = 0; c < N; ++c) A[i * N + c] = ctgen_a_coeff(seed, p, (1ULL << 22) + (uint64_t)i, (uint64_t)c);
+      memcpy(a_hat + i * N, A + i * N, sizeof(uint32_t) * N);
+      ntt_fwd(&pl, a_hat + i * N);
+    }
+#ifdef _OPENMP
+#pragma omp parallel
+#endif
+    {
+      uint32_t* skh = (uint32_t*)malloc(sizeof(uint32_t) * N);
+      uint32_t* prod = (uint32_t*)malloc(sizeof(uint32_t) * N);
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 4)
+#endif
+      for (int64_t c = 0; c < ncols; ++c) {
+        const int64_t j = col_begin + c;
+        for (int64_t x = 0; x < N; ++x) {
+          int32_t s = ctgen_sk_coeff(seed, (uint64_t)j, (uint64_t)x);
+          skh[x] = s >= 0 ? (uint32_t)s : p - (uint32_t)(-s);
+        }
+        ntt_fwd(&pl, skh);
+        for (int64_t i = 0; i < k; ++i) {
+          for (int64_t x = 0; x < N; ++x) prod[x] = mulmod(a_hat[i * N + x], skh[x], p);
+          ntt_inv(&pl, prod); /* a_i · sk_j */
+          uint32_t* b_out = B + (c * k + i) * N;
+          for (int64_t x = 0; x < N; ++x) {
+            int64_t P = ctgen_plain(seed, N, d1, i * N + x, j, log_delta);
+            int64_t pm = P % (int64_t)p;
+            if (pm < 0) pm += p;
+            uint32_t v = (uint32_t)pm;
+            b_out[x] = v >= prod[x] ? v - prod[x] : v + p - prod[x];
+          }
+        }
+      }
+      free(skh);
+      free(prod);
+    }
+    free(a_hat);
+    ntt_plan_free(&pl);
+  }
+  return 0;
 }

@@ -24,7 +24,14 @@
  *   CTPT_RLWE      d1 = N, one key,                  A ∈ Z_q^{N×d2}
  *   CTPT_SHARED_S  N | d1, one key, S = I ⊗ toep(sk), A ∈ Z_q^{d1×d2}
  *   CTPT_SHARED_A  N | d1, k = d1/N keys, shared a,  A ∈ Z_q^{N×d2}
- * rows_A = N (RLWE, shared-a) or d1 (shared-s).  R = rows_A + d1.
+ *   CTPT_STRUCT_A  N | d1, structured-A shared-a: Ã·S + B ≈ Δ·M with
+ *                  Ã = [toep(a_0); …; toep(a_{k−1})] (k = d1/N polynomials shared by all
+ *                  columns) and a general S = [Vec(sk_j)]_j.  Algorithm 7 (CP-MM with
+ *                  precomputation) step 1 computes only B' = B·U:
+ *                  the output (Ã, B') encrypts M·U under S·U; Ã passes through unchanged
+ *                  (no Rescale, reading Q3), so the library never reads the a-polynomials.
+ * rows_A = N (RLWE, shared-a), d1 (shared-s) or 0 (structured-A).  R = rows_A + d1.
+ * With rows_A = 0 every A-side pointer (d_a_polys, d_AU, h_a_polys, h_AU) may be NULL.
  *
  * Conventions for every entry point:
  *  - Residues at the boundary are canonical uint32 in [0, p) (reading Q14).
@@ -58,11 +65,11 @@ typedef enum {
   CTPT_ERR_OVERFLOW = 4,    /* exactness bound of the int8 limb products would fail (refuse, never
                                round: Lemma le:strategy1's d2·‖limb‖·‖limb‖ bound, K = 2^8)          */
   CTPT_ERR_RANGE = 5,       /* an input residue ≥ p (validate=1), or |U| too large for a shared plane */
-  CTPT_ERR_UNSUPPORTED = 6, /* format / option not implemented (MLWE, structured-A)                  */
+  CTPT_ERR_UNSUPPORTED = 6, /* format / option not implemented (MLWE, MLWE structured-A)             */
   CTPT_ERR_CUDA = 7         /* a CUDA runtime/driver error (see ctpt_last_error)                    */
 } ctpt_status;
 
-typedef enum { CTPT_RLWE = 0, CTPT_SHARED_S = 1, CTPT_SHARED_A = 2 } ctpt_format;
+typedef enum { CTPT_RLWE = 0, CTPT_SHARED_S = 1, CTPT_SHARED_A = 2, CTPT_STRUCT_A = 3 } ctpt_format;
 
 /* One CP-MM problem, possibly a shard of a larger one:
  * `primes` may be any subset of the RNS basis and [col_begin, col_end) any block of U's
@@ -103,6 +110,7 @@ ctpt_status ctpt_query_sizes(const ctpt_problem* prob, ctpt_sizes* out);
 /* Format layout (column j of A / B are the
  * coefficients of ciphertext j).  Inputs are the per-column ciphertexts of `prob`'s L primes:
  *   d_a_polys: uint32 [L][n_a][N], n_a = d2·(k for shared-s, else 1), poly j·k+t = column j chunk t
+ *              (not read, may be NULL, for CTPT_STRUCT_A)
  *   d_b_polys: uint32 [L][d2·k][N]
  * i.e. per prime A and B in column-major order [d2][rows_A] and [d2][d1].
  * Output d_ctmat (ctmat_bytes): a 256-byte header, then for each prime the stacked matrix
@@ -142,6 +150,17 @@ ctpt_status ctpt_split(const ctpt_problem* prob, int32_t l, const void* d_ctmat,
                        void* stream);
 ctpt_status ctpt_gemm(const ctpt_problem* prob, int32_t l, const void* d_ws, size_t ws_bytes, const void* d_plain,
                       uint32_t* d_AU_l, uint32_t* d_BU_l, void* stream);
+
+/* The skinny-U regime (d3_loc ≤ 256 and kU = 1, CP-Mv at d3 = 1,
+ * P:982; Table 4's d3 ∈ {1, 2^6, 2^7}).  For prime index l: the same
+ * (A·U mod p, B·U mod p) as ctpt_split + ctpt_gemm, but the limb split runs inside the GEMM's
+ * load path, reading the int32 residues of d_ctmat exactly once (no workspace): the regime is
+ * HBM-bound and this saves the split's write + re-read.  ctpt_matmul (and ctpt_matmul_host)
+ * choose this kernel automatically for every prime when d3_loc ≤ 256 and kU = 1 (environment
+ * CTPT_SKINNY=off disables that, for A/B measurements).  Outputs as for ctpt_gemm.
+ * CTPT_ERR_UNSUPPORTED when kU ≠ 1 or d3_loc > 256.  Never synchronises. */
+ctpt_status ctpt_gemm_fused(const ctpt_problem* prob, int32_t l, const void* d_ctmat, const void* d_plain,
+                            uint32_t* d_AU_l, uint32_t* d_BU_l, void* stream);
 
 /* End-to-end executor from HOST buffers (the e2e path): the same computation as
  * ctpt_layout + ctpt_matmul, but the per-column ciphertexts h_a_polys / h_b_polys (layouts as

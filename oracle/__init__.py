@@ -11,6 +11,9 @@ What it computes, and where the paper defines it (``P:n`` = PAPER.md line n):
 * ``negacyclic_mul``    c = toep(s)·Vec(a) mod p, C schoolbook
 * ``secret_matrix``     S_RLWE = toep(sk) (P:39), S_sh-s = I ⊗ toep(sk) (P:50),
                         S_sh-a = [toep(sk_0); …; toep(sk_{k-1})] (P:66)
+* ``struct_a_matrices`` structured-A shared-a: Ã = [toep(a_0); …; toep(a_{k-1})] and
+                        S = [Vec(sk_j)]_j with Ã·S + B ≈ M
+* ``su_column``         column j of S·U, the Algorithm 7 output key
 * ``format_matrices``   (A, B) with column j = the coefficients of ciphertext j
                         (P:45–71, P:118–127, P:1071)
 * ``encrypt_small``     b = P − S-part, so that a·sk + b = P
@@ -38,7 +41,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
-RLWE, SHARED_S, SHARED_A = 0, 1, 2
+RLWE, SHARED_S, SHARED_A, STRUCT_A = 0, 1, 2, 3
 
 
 def build(force: bool = False) -> str:
@@ -134,8 +137,11 @@ def negacyclic_mul(a: np.ndarray, s: np.ndarray, p: int) -> np.ndarray:
 # L2 formats with structured S (Table 1)
 # ----------------------------------------------------------------------------------
 def rows_A(fmt: int, N: int, d1: int) -> int:
-    """Row count of A: N for RLWE and shared-a (A ∈ Z_q^{N×d2}, Lemma le:mat_struct_s,
-    P:118–122), d1 for shared-s (A ∈ Z_q^{d1×d2}, P:124–127)."""
+    """Row count of the A the CP-MM multiplies: N for RLWE and shared-a (A ∈ Z_q^{N×d2},
+    Lemma le:mat_struct_s), d1 for shared-s (A ∈ Z_q^{d1×d2}), and 0
+    for structured-A shared-a, where Algorithm 7 multiplies only B."""
+    if fmt == STRUCT_A:
+        return 0
     return d1 if fmt == SHARED_S else N
 
 
@@ -146,7 +152,7 @@ def check_dims(fmt: int, N: int, d1: int) -> None:
     if fmt == RLWE and d1 != N:
         raise ValueError("RLWE format requires d1 = N")
     if d1 % N:
-        raise ValueError("shared-s / shared-a formats require N | d1")
+        raise ValueError("shared-s / shared-a / structured-A formats require N | d1")
 
 
 def secret_matrix(fmt: int, sks, N: int, d1: int) -> np.ndarray:
@@ -174,7 +180,9 @@ def format_matrices(fmt: int, N: int, d1: int, a_polys: np.ndarray, b_polys: np.
     for j in range(ncols):
         for t in range(k):
             B[t * N:(t + 1) * N, j] = b_polys[j * k + t]
-    if fmt == SHARED_S:
+    if fmt == STRUCT_A:  # Ã is not a per-column matrix; Algorithm 7 multiplies B only
+        A = np.empty((0, ncols), dtype=np.uint32)
+    elif fmt == SHARED_S:
         A = np.empty((d1, ncols), dtype=np.uint32)
         for j in range(ncols):
             for t in range(k):
@@ -184,6 +192,26 @@ def format_matrices(fmt: int, N: int, d1: int, a_polys: np.ndarray, b_polys: np.
         for j in range(ncols):
             A[:, j] = a_polys[j]
     return A, B
+
+
+def struct_a_matrices(a_polys, sks):
+    """Structured-A shared-a (P:143–160): Ã = (toep(a_0)^t | … | toep(a_{k-1})^t)^t ∈ Z^{d1×N}
+    from the k row-block polynomials a_i, and S ∈ Z^{N×d2} the horizontal concatenation of
+    Vec(sk_j), so that Ã·S + B ≈ M (mod q).  Small sizes only (dense, object entries)."""
+    At = np.vstack([toeplitz([int(v) for v in a]) for a in a_polys]).astype(object)
+    S = np.stack([np.asarray(s, dtype=np.int64) for s in sks], axis=1).astype(object)
+    return At, S
+
+
+def su_column(sks, U: np.ndarray, j: int) -> np.ndarray:
+    """Column j of S·U with S = [Vec(sk_0) | … | Vec(sk_{d2-1})]: Σ_k U[k][j]·sk_k over Z —
+    the secret of output column j of Algorithm 7 (the key S·U)."""
+    acc = np.zeros(len(sks[0]), dtype=np.int64)
+    for k in range(U.shape[0]):
+        u = int(U[k, j])
+        if u:
+            acc += u * np.asarray(sks[k], dtype=np.int64)
+    return acc
 
 
 def encrypt_small(fmt: int, sks, P: np.ndarray, a_cols: np.ndarray, p: int) -> np.ndarray:
@@ -244,13 +272,17 @@ def freivalds(X_colmajor: np.ndarray, U: np.ndarray, C: np.ndarray, p: int, v: n
 
 def decrypt_col(fmt: int, N: int, d1: int, sks, a_col: np.ndarray, b_col: np.ndarray, p: int,
                 nthreads: int = 0) -> np.ndarray:
-    """S·a + b mod p for one column in a structured-S format."""
+    """S·a + b mod p for one column in a structured-S format.  For
+    structured-A shared-a (fmt 3) it is Ã·key + b: `a_col` holds the k = d1/N shared
+    polynomials a_t (k·N entries) and sks = [key], the column's Vec(sk_j) — or (S·U)_j for an
+    Algorithm 7 output column."""
     k = d1 // N
     nkeys = k if fmt == SHARED_A else 1
     S = np.ascontiguousarray(np.stack([np.asarray(sks[t], dtype=np.int64) for t in range(nkeys)]))
-    a = np.ascontiguousarray(a_col, dtype=np.uint32)
+    a = np.ascontiguousarray(a_col, dtype=np.uint32).ravel()
     b = np.ascontiguousarray(b_col, dtype=np.uint32)
-    assert a.shape[0] == rows_A(fmt, N, d1) and b.shape[0] == d1
+    want_a = d1 if fmt == STRUCT_A else rows_A(fmt, N, d1)
+    assert a.shape[0] == want_a and b.shape[0] == d1
     out = np.empty(d1, dtype=np.uint32)
     rc = lib().orc_decrypt_col(fmt, N, d1, _ptr(S), _ptr(a), _ptr(b), p, _ptr(out), nthreads)
     assert rc == 0

@@ -148,10 +148,15 @@ void orc_negacyclic_mul(const uint32_t* a, const int64_t* s, int64_t N, uint32_t
  * S·(A·U0) + B·U0 = M·U0 mod q):  out = S·a_col + b_col mod p, chunk by chunk:
  *   RLWE / shared-a:  out[tN+i] = (toep(sk_t)·a)_i + b[tN+i]   (a has N entries; t=0 for RLWE)
  *   shared-s:         out[tN+i] = (toep(sk)·a_t)_i + b[tN+i]   (a has d1 entries, chunk t)
- * fmt: 0 RLWE, 1 shared-s, 2 shared-a.  sks: nkeys × N ternary keys (int64). */
+ *   structured-A:     out[tN+i] = (toep(a_t)·key)_i + b[tN+i]  (Ã·S + B; a holds the
+ *                     k = d1/N shared polys a_t, key is the column's secret Vec(sk_j) — or, for an
+ *                     Algorithm 7 output column, the column (S·U)_j of the new key, P:1751–1757;
+ *                     toep(a)·Vec(s) = Vec(a·s) = toep(s)·Vec(a), so the same coefficient formula)
+ * fmt: 0 RLWE, 1 shared-s, 2 shared-a, 3 structured-A.  sks: nkeys × N integer keys (int64;
+ * |key| < 2^31 so every product stays below 2^62). */
 int orc_decrypt_col(int fmt, int64_t N, int64_t d1, const int64_t* sks, const uint32_t* a_col,
                     const uint32_t* b_col, uint32_t p, uint32_t* out, int nthreads) {
-  if (N <= 0 || d1 % N) return -1;
+  if (N <= 0 || d1 % N || fmt < 0 || fmt > 3) return -1;
   set_threads(nthreads);
 #ifdef _OPENMP
 #pragma omp parallel for schedule(dynamic, 64)
@@ -159,7 +164,7 @@ int orc_decrypt_col(int fmt, int64_t N, int64_t d1, const int64_t* sks, const ui
   for (int64_t r = 0; r < d1; ++r) {
     const int64_t t = r / N, i = r % N;
     const int64_t* key = sks + ((fmt == 2) ? t : 0) * N;
-    const uint32_t* a = a_col + ((fmt == 1) ? t * N : 0);
+    const uint32_t* a = a_col + ((fmt == 1 || fmt == 3) ? t * N : 0);
     out[r] = (uint32_t)(((uint64_t)negacyclic_coeff(a, key, N, p, i) + b_col[r]) % p);
   }
   return 0;

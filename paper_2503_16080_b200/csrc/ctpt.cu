@@ -14,6 +14,7 @@
 #include "../../include/ctpt.h"
 #include "gemm_tc.cuh"
 #include "gemm_tc2.cuh"
+#include "gemm_fused.cuh"
 #include "kernels.cuh"
 
 using namespace ctpt;
@@ -48,14 +49,14 @@ int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 ctpt_status check_problem(const ctpt_problem* pb, Dims& d) {
   if (!pb) return fail(CTPT_ERR_ARG, "problem is NULL");
-  if (pb->fmt < CTPT_RLWE || pb->fmt > CTPT_SHARED_A) return fail(CTPT_ERR_UNSUPPORTED, "unknown format %d", pb->fmt);
+  if (pb->fmt < CTPT_RLWE || pb->fmt > CTPT_STRUCT_A) return fail(CTPT_ERR_UNSUPPORTED, "unknown format %d", pb->fmt);
   if (pb->L < 1 || pb->L > kMaxPrimes) return fail(CTPT_ERR_ARG, "L = %d outside 1..%d", pb->L, kMaxPrimes);
   if (!pb->primes) return fail(CTPT_ERR_ARG, "primes is NULL");
   if (pb->N < 1 || (pb->N & (pb->N - 1))) return fail(CTPT_ERR_SHAPE, "N = %lld is not a power of two", (long long)pb->N);
   if (pb->d1 < 1 || pb->d2 < 1 || pb->d3 < 1) return fail(CTPT_ERR_SHAPE, "d1, d2, d3 must be >= 1");
   // Table 1: RLWE needs d1 = N; shared-s and shared-a need N | d1.
   if (pb->fmt == CTPT_RLWE && pb->d1 != pb->N) return fail(CTPT_ERR_SHAPE, "RLWE format requires d1 = N");
-  if (pb->d1 % pb->N) return fail(CTPT_ERR_SHAPE, "shared-s / shared-a formats require N | d1");
+  if (pb->d1 % pb->N) return fail(CTPT_ERR_SHAPE, "shared-s / shared-a / structured-A formats require N | d1");
   for (int i = 0; i < pb->L; ++i) {
     const uint32_t p = pb->primes[i];
     if (p < 3 || !(p & 1u) || p >= (1u << 31)) return fail(CTPT_ERR_MODULUS, "prime %u must be odd and in (2, 2^31)", p);
@@ -70,7 +71,8 @@ ctpt_status check_problem(const ctpt_problem* pb, Dims& d) {
   if (pb->d2 * 255LL * 128LL >= (1LL << 31)) return fail(CTPT_ERR_OVERFLOW, "d2 = %lld too large for exact int32 limb accumulation (d2 <= 65793)", (long long)pb->d2);
   d.N = pb->N; d.d1 = pb->d1; d.d2 = pb->d2; d.d3 = pb->d3; d.L = pb->L;
   d.k = pb->d1 / pb->N;
-  d.rows_A = (pb->fmt == CTPT_SHARED_S) ? pb->d1 : pb->N;
+  // structured-A shared-a (Algorithm 7): only B·U is computed, Ã passes through
+  d.rows_A = (pb->fmt == CTPT_SHARED_S) ? pb->d1 : (pb->fmt == CTPT_STRUCT_A ? 0 : pb->N);
   d.R = d.rows_A + d.d1;
   d.d2p = round_up(d.d2, 16);
   d.j0 = c0; d.j1 = c1; d.d3_loc = c1 - c0;
@@ -141,6 +143,10 @@ ctpt_status tc_setup() {
     e = cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BYTES);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_gemm_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, T2_SMEM_BYTES);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_gemm_fused<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(1));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_gemm_fused<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(2));
   });
   if (e != cudaSuccess) return fail(CTPT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
   return CTPT_OK;
@@ -163,6 +169,17 @@ struct GemmArgs {
 };
 ctpt_status launch_split(const uint32_t* x, int64_t n, void* limbs, cudaStream_t st);
 ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt);
+ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st);
+
+// The skinny regime: d3_loc ≤ 256 columns and one U digit plane.  There
+// the step is HBM-bound and the fused kernel (split inside the GEMM's load path, X read once)
+// replaces split + GEMM.  CTPT_SKINNY=off forces split + GEMM (for A/B measurements).
+constexpr int64_t kFusedMaxD3 = 256;
+bool fused_eligible(const Dims& d, int kU) {
+  if (kU != 1 || d.d3_loc > kFusedMaxD3) return false;
+  const char* e = getenv("CTPT_SKINNY");
+  return !(e && strcmp(e, "off") == 0);
+}
 
 }  // namespace
 
@@ -196,7 +213,7 @@ ctpt_status ctpt_layout(const ctpt_problem* pb, const uint32_t* d_a, const uint3
   Dims d;
   ctpt_status s = check_problem(pb, d);
   if (s != CTPT_OK) return s;
-  if (!d_a || !d_b || !d_ctmat) return fail(CTPT_ERR_ARG, "null device pointer");
+  if ((!d_a && d.rows_A > 0) || !d_b || !d_ctmat) return fail(CTPT_ERR_ARG, "null device pointer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   uint8_t* hdr = static_cast<uint8_t*>(d_ctmat);
   LayoutParams P;
@@ -315,7 +332,7 @@ static ctpt_status gemm_common(const ctpt_problem* pb, int32_t l, const void* d_
   ctpt_status s = check_problem(pb, d);
   if (s != CTPT_OK) return s;
   if (l < 0 || l >= d.L) return fail(CTPT_ERR_ARG, "prime index %d out of range", l);
-  if (!d_ws || !d_plain || !d_AU_l || !d_BU_l) return fail(CTPT_ERR_ARG, "null device pointer");
+  if (!d_ws || !d_plain || (!d_AU_l && d.rows_A > 0) || !d_BU_l) return fail(CTPT_ERR_ARG, "null device pointer");
   if (ws_bytes < static_cast<size_t>(4) * d.R * d.d2p) return fail(CTPT_ERR_ARG, "workspace too small");
   GemmArgs g;
   g.limbs = d_ws;
@@ -417,9 +434,67 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
   return CTPT_OK;
 }
 
+ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st) {
+  const Dims& d = g.d;
+  if (g.kU != 1 || d.d3_loc > kFusedMaxD3) return fail(CTPT_ERR_UNSUPPORTED, "fused kernel needs kU = 1 and d3_loc <= 256");
+  ctpt_status s = tc_setup();
+  if (s != CTPT_OK) return s;
+  CUtensorMap tmU;
+  s = make_tmap_u8(&tmU, g.planes, d.d2, d.d3, g.nplanes, d.d2p, d.d3 * d.d2p, FU_BLOCK_K, 128, 1);
+  if (s != CTPT_OK) return s;
+  FusedParams P;
+  P.x = x;
+  P.R = g.R;
+  P.d2p = d.d2p;
+  P.j_off = static_cast<int32_t>(d.j0);
+  P.plane = g.plane0;
+  P.num_kb = static_cast<int32_t>((d.d2p + FU_BLOCK_K - 1) / FU_BLOCK_K);
+  const int64_t nt = (g.R + FU_BLOCK_R - 1) / FU_BLOCK_R;
+  if (nt > INT32_MAX) return fail(CTPT_ERR_SHAPE, "too many tiles");
+  P.num_tiles = static_cast<int32_t>(nt);
+  P.m = make_modp(g.p);
+  P.o = g.o;
+  P.o.accumulate = 0;
+  P.o.w = 1;
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(nt, num_sms()));
+  if (d.d3_loc <= 128)
+    k_gemm_fused<1><<<grid, FU_THREADS, fu_smem_bytes(1), st>>>(tmU, P);
+  else
+    k_gemm_fused<2><<<grid, FU_THREADS, fu_smem_bytes(2), st>>>(tmU, P);
+  CUDA_TRY(cudaGetLastError());
+  return CTPT_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+ctpt_status ctpt_gemm_fused(const ctpt_problem* pb, int32_t l, const void* d_ctmat, const void* d_plain,
+                            uint32_t* d_AU_l, uint32_t* d_BU_l, void* stream) {
+  Dims d;
+  ctpt_status s = check_problem(pb, d);
+  if (s != CTPT_OK) return s;
+  if (l < 0 || l >= d.L) return fail(CTPT_ERR_ARG, "prime index %d out of range", l);
+  if (!d_ctmat || !d_plain || (!d_AU_l && d.rows_A > 0) || !d_BU_l) return fail(CTPT_ERR_ARG, "null device pointer");
+  GemmArgs g;
+  g.limbs = nullptr;
+  g.R = d.R;
+  g.d = d;
+  g.kU = pb->kU <= 0 ? 1 : pb->kU;
+  g.planes = reinterpret_cast<const int8_t*>(static_cast<const uint8_t*>(d_plain) + kHeader);
+  g.nplanes = pb->plain_per_prime ? d.L * g.kU : g.kU;
+  g.plane0 = plane_index(pb, l, 0);
+  g.p = pb->primes[l];
+  g.o.AU = d_AU_l;
+  g.o.BU = d_BU_l;
+  g.o.rows_A = d.rows_A;
+  g.o.d1 = d.d1;
+  g.o.R = d.R;
+  g.o.d3_loc = d.d3_loc;
+  const uint32_t* x =
+      reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(d_ctmat) + kHeader) + l * d.R * d.d2p;
+  return launch_fused(g, x, static_cast<cudaStream_t>(stream));
+}
 
 ctpt_status ctpt_gemm(const ctpt_problem* pb, int32_t l, const void* d_ws, size_t ws_bytes, const void* d_plain,
                       uint32_t* d_AU_l, uint32_t* d_BU_l, void* stream) {
@@ -436,8 +511,15 @@ ctpt_status ctpt_matmul(const ctpt_problem* pb, const void* d_ctmat, const void*
   Dims d;
   ctpt_status s = check_problem(pb, d);
   if (s != CTPT_OK) return s;
-  if (!d_AU || !d_BU) return fail(CTPT_ERR_ARG, "null output pointer");
+  if ((!d_AU && d.rows_A > 0) || !d_BU) return fail(CTPT_ERR_ARG, "null output pointer");
+  const bool fused = fused_eligible(d, pb->kU <= 0 ? 1 : pb->kU);
   for (int l = 0; l < d.L; ++l) {
+    if (fused) {
+      s = ctpt_gemm_fused(pb, l, d_ctmat, d_plain, d_AU + static_cast<int64_t>(l) * d.d3_loc * d.rows_A,
+                          d_BU + static_cast<int64_t>(l) * d.d3_loc * d.d1, stream);
+      if (s != CTPT_OK) return s;
+      continue;
+    }
     s = ctpt_split(pb, l, d_ctmat, d_ws, ws_bytes, stream);
     if (s != CTPT_OK) return s;
     s = ctpt_gemm(pb, l, d_ws, ws_bytes, d_plain, d_AU + static_cast<int64_t>(l) * d.d3_loc * d.rows_A,
@@ -528,7 +610,7 @@ ctpt_status ctpt_matmul_host(const ctpt_problem* pb, const uint32_t* h_a, const 
   Dims d;
   ctpt_status s = check_problem(pb, d);
   if (s != CTPT_OK) return s;
-  if (!h_a || !h_b || !d_plain || !h_AU || !h_BU || !d_ws) return fail(CTPT_ERR_ARG, "null pointer");
+  if (((!h_a || !h_AU) && d.rows_A > 0) || !h_b || !d_plain || !h_BU || !d_ws) return fail(CTPT_ERR_ARG, "null pointer");
   const HostPlan hp = host_plan(d, chunk_rows);
   if (ws_bytes < hp.total) return fail(CTPT_ERR_ARG, "workspace too small (%zu < %zu)", ws_bytes, hp.total);
   cudaStream_t sc = static_cast<cudaStream_t>(stream);
@@ -560,6 +642,7 @@ ctpt_status ctpt_matmul_host(const ctpt_problem* pb, const uint32_t* h_a, const 
   g.planes = reinterpret_cast<const int8_t*>(static_cast<const uint8_t*>(d_plain) + kHeader);
   g.nplanes = pb->plain_per_prime ? d.L * g.kU : g.kU;
   g.limbs = limbs;
+  const bool fused = fused_eligible(d, g.kU);
 
   int64_t it = 0;
   for (int l = 0; l < d.L; ++l) {
@@ -586,8 +669,10 @@ ctpt_status ctpt_matmul_host(const ctpt_problem* pb, const uint32_t* h_a, const 
       s = launch_layout_cols(in[b], cm, rows, d.d2, d.d2p, sc);
       if (s != CTPT_OK) return s;
       CUDA_TRY(cudaEventRecord(in_free[b], sc));
-      s = launch_split(cm, rows * d.d2p, limbs, sc);
-      if (s != CTPT_OK) return s;
+      if (!fused) {
+        s = launch_split(cm, rows * d.d2p, limbs, sc);
+        if (s != CTPT_OK) return s;
+      }
       if (it >= 2) CUDA_TRY(cudaStreamWaitEvent(sc, out_free[b], 0));
       g.R = rows;
       g.p = pb->primes[l];
@@ -598,7 +683,7 @@ ctpt_status ctpt_matmul_host(const ctpt_problem* pb, const uint32_t* h_a, const 
       g.o.d1 = 0;
       g.o.R = rows;
       g.o.d3_loc = d.d3_loc;
-      s = launch_gemm(g, sc, false);
+      s = fused ? launch_fused(g, cm, sc) : launch_gemm(g, sc, false);
       if (s != CTPT_OK) return s;
       CUDA_TRY(cudaEventRecord(out_ready[b], sc));
       // 3. device → host: rows [r0, r1) of every output column

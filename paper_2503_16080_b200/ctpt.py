@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libctpt.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "ctpt.h")
 
-RLWE, SHARED_S, SHARED_A = 0, 1, 2
+RLWE, SHARED_S, SHARED_A, STRUCT_A = 0, 1, 2, 3
 STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_SHAPE", 3: "ERR_MODULUS", 4: "ERR_OVERFLOW", 5: "ERR_RANGE",
           6: "ERR_UNSUPPORTED", 7: "ERR_CUDA"}
 
@@ -61,6 +61,7 @@ _sig = {
     "ctpt_split": (ctypes.c_int, [_PP, ctypes.c_int32, _P, _P, ctypes.c_size_t, _P]),
     "ctpt_gemm": (ctypes.c_int, [_PP, ctypes.c_int32, _P, ctypes.c_size_t, _P, _P, _P, _P]),
     "ctpt_gemm_simt": (ctypes.c_int, [_PP, ctypes.c_int32, _P, ctypes.c_size_t, _P, _P, _P, _P]),
+    "ctpt_gemm_fused": (ctypes.c_int, [_PP, ctypes.c_int32, _P, _P, _P, _P, _P]),
     "ctpt_host_workspace_bytes": (ctypes.c_int, [_PP, ctypes.c_int64, ctypes.POINTER(ctypes.c_size_t)]),
     "ctpt_matmul_host": (ctypes.c_int, [_PP, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, ctypes.c_int64, _P]),
 }
@@ -169,6 +170,13 @@ def gemm(spec: Spec, l: int, ws, plain, AU_l, BU_l, stream=None, simt: bool = Fa
     f = _lib.ctpt_gemm_simt if simt else _lib.ctpt_gemm
     _check(f(ctypes.byref(pb), l, _ptr(ws), ws.numel() * ws.element_size(), _ptr(plain), _ptr(AU_l), _ptr(BU_l),
              _stream(stream)))
+
+
+def gemm_fused(spec: Spec, l: int, ctmat, plain, AU_l, BU_l, stream=None):
+    """Skinny-U kernel (d3_loc <= 256, kU = 1): split fused into the GEMM's load path."""
+    pb = spec.cstruct()
+    _check(_lib.ctpt_gemm_fused(ctypes.byref(pb), l, _ptr(ctmat), _ptr(plain), _ptr(AU_l), _ptr(BU_l),
+                                _stream(stream)))
 
 
 def host_workspace_bytes(spec: Spec, chunk_rows: int = 0) -> int:

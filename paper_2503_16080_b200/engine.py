@@ -34,7 +34,10 @@ class CpmmEngine:
 
     # -- a1: format layout ----------------------------------------------------------------
     def layout(self, a_polys, b_polys, validate: bool = False) -> torch.Tensor:
-        a = a_polys if isinstance(a_polys, torch.Tensor) else _u32_to_dev(a_polys, self.device)
+        if self.sizes.rows_A == 0:  # structured-A: the a-polynomials are not read (Ã passes through)
+            a = None
+        else:
+            a = a_polys if isinstance(a_polys, torch.Tensor) else _u32_to_dev(a_polys, self.device)
         b = b_polys if isinstance(b_polys, torch.Tensor) else _u32_to_dev(b_polys, self.device)
         if self.ctmat is None:
             self.ctmat = torch.empty(self.sizes.ctmat_bytes, dtype=torch.uint8, device=self.device)
@@ -63,7 +66,7 @@ class CpmmEngine:
 
     # -- a3–a6: the hot path -------------------------------------------------------------------
     def alloc_outputs(self):
-        AU = torch.empty(self.sizes.out_AU_bytes // 4, dtype=torch.int32, device=self.device)
+        AU = torch.empty(max(1, self.sizes.out_AU_bytes // 4), dtype=torch.int32, device=self.device)
         BU = torch.empty(self.sizes.out_BU_bytes // 4, dtype=torch.int32, device=self.device)
         return AU, BU
 
@@ -76,4 +79,6 @@ class CpmmEngine:
     def outputs_numpy(self, AU: torch.Tensor, BU: torch.Tensor):
         L = len(self.spec.primes)
         d3l = self.sizes.d3_loc
-        return (dev_to_u32(AU).reshape(L, d3l, self.sizes.rows_A), dev_to_u32(BU).reshape(L, d3l, self.spec.d1))
+        ra = self.sizes.rows_A
+        AUn = dev_to_u32(AU)[:L * d3l * ra].reshape(L, d3l, ra)
+        return AUn, dev_to_u32(BU).reshape(L, d3l, self.spec.d1)

@@ -55,7 +55,8 @@ def colmajor_views(fmt, N, d1, d2, a_polys_l, b_polys_l):
     """Column-major A [d2][rows_A] and B [d2][d1] views of one prime's per-column ciphertexts
     (no copy: poly j*k+t of column j is contiguous)."""
     ra = oracle.rows_A(fmt, N, d1)
-    return a_polys_l.reshape(d2, ra), b_polys_l.reshape(d2, d1)
+    A = np.empty((d2, 0), np.uint32) if ra == 0 else a_polys_l.reshape(d2, ra)  # structured-A: no A·U
+    return A, b_polys_l.reshape(d2, d1)
 
 
 def U_residues(U: np.ndarray, primes) -> np.ndarray:

@@ -74,3 +74,15 @@ def test_null_pointers_rejected_without_gpu(ctpt):
     assert lib.ctpt_layout(ctypes.byref(pb), None, None, None, 0, None) == 1
     assert lib.ctpt_matmul(ctypes.byref(pb), None, None, None, None, None, 0, None) == 1
     assert b"null" in lib.ctpt_last_error()
+
+
+def test_fused_refuses_wide_or_multidigit_U_without_gpu(ctpt):
+    # the skinny kernel's eligibility (d3_loc <= 256, kU = 1) is checked before any CUDA call
+    lib = ctpt.raw_lib()
+    fake = ctypes.c_void_p(256)  # never dereferenced
+    pb = _spec(ctpt, d3=300).cstruct()
+    assert lib.ctpt_gemm_fused(ctypes.byref(pb), 0, fake, fake, fake, fake, None) == 6
+    pb = _spec(ctpt, d3=300, col_begin=10, col_end=266, kU=2).cstruct()
+    assert lib.ctpt_gemm_fused(ctypes.byref(pb), 0, fake, fake, fake, fake, None) == 6
+    pb = _spec(ctpt, d3=20).cstruct()
+    assert lib.ctpt_gemm_fused(ctypes.byref(pb), 1, fake, fake, fake, fake, None) == 1  # prime index

@@ -74,17 +74,24 @@ def _pu_mod_and_mu(c, U, ps, cols, kblock=2048):
     return pu, mu
 
 
-def _decrypt_and_decode(c, ps, AUc, BUc, U, cols):
-    """AUc[l]: [ncols][rows_A], BUc[l]: [ncols][d1] (GPU outputs on `cols`)."""
-    nk = c.k if c.fmt == ctgen.SHARED_A else 1
-    sks = [ctgen.sk(c.seed, t, c.N) for t in range(nk)]
+def _decrypt_and_decode(c, ps, AUc, BUc, U, cols, a_polys_sa=None):
+    """AUc[l]: [ncols][rows_A], BUc[l]: [ncols][d1] (GPU outputs on `cols`); a_polys_sa[l]: the
+    structured-A format's k shared polynomials per prime (Ã passes through Algorithm 7)."""
+    if c.fmt == ctgen.STRUCT_A:  # column j decrypts under (S·U)_j (Algorithm 7, P:1751–1757)
+        allk = [ctgen.sk(c.seed, t, c.N) for t in range(c.d2)]
+        keys = {j: [oracle.su_column(allk, U, j)] for j in cols}
+    else:
+        nk = c.k if c.fmt == ctgen.SHARED_A else 1
+        sks = [ctgen.sk(c.seed, t, c.N) for t in range(nk)]
+        keys = {j: sks for j in cols}
     pu, mu = _pu_mod_and_mu(c, U, ps, cols)
     worst = 0.0
     scale = np.abs(mu).max()
     for ci, j in enumerate(cols):
         decs = []
         for l, p in enumerate(ps):
-            dec = oracle.decrypt_col(c.fmt, c.N, c.d1, sks, AUc[l][ci], BUc[l][ci], p, nthreads=NTHREADS)
+            a_part = a_polys_sa[l] if c.fmt == ctgen.STRUCT_A else AUc[l][ci]
+            dec = oracle.decrypt_col(c.fmt, c.N, c.d1, keys[j], a_part, BUc[l][ci], p, nthreads=NTHREADS)
             assert np.array_equal(dec.astype(np.uint64), pu[l, ci]), f"decryption identity fails: prime {l}, col {j}"
             decs.append(dec)
         cen = oracle.crt_centred_array(np.stack(decs), ps)
@@ -103,6 +110,7 @@ def _run_config(name, primes_per_call, n_random, dec_cols):
     rng = np.random.default_rng(1234)
     AUc = [None] * c.L
     BUc = [None] * c.L
+    a_sa = [None] * c.L
     for l0 in range(0, c.L, primes_per_call):
         ps = ps_all[l0:l0 + primes_per_call]
         ct = ctgen.encrypt(c.fmt, c.N, c.d1, c.d2, c.seed, c.log_delta, ps, nthreads=NTHREADS)
@@ -111,12 +119,14 @@ def _run_config(name, primes_per_call, n_random, dec_cols):
         torch.cuda.empty_cache()
         for i, p in enumerate(ps):
             Ac, Bc = colmajor_views(c.fmt, c.N, c.d1, c.d2, ct.a_polys[i], ct.b_polys[i])
-            _check_matrix(Ac, U, AU[i], p, rng, f"{name} A·U prime {l0 + i}", n_random)
+            if c.rows_A:
+                _check_matrix(Ac, U, AU[i], p, rng, f"{name} A·U prime {l0 + i}", n_random)
             _check_matrix(Bc, U, BU[i], p, rng, f"{name} B·U prime {l0 + i}", n_random)
             AUc[l0 + i] = AU[i][dec_cols].copy()
             BUc[l0 + i] = BU[i][dec_cols].copy()
+            a_sa[l0 + i] = ct.a_polys[i].copy()
         del ct, AU, BU
-    return _decrypt_and_decode(c, ps_all, AUc, BUc, U, dec_cols)
+    return _decrypt_and_decode(c, ps_all, AUc, BUc, U, dec_cols, a_sa)
 
 
 def test_config3_full_size():
@@ -129,6 +139,51 @@ def test_config4_full_size():
     _run_config("c4", primes_per_call=4, n_random=32768, dec_cols=[0, 128, c.d3 - 1])
 
 
+def test_config3a_struct_a_full_size():
+    """SURVEY.md §8(f) row 2 at c3's sizes: Algorithm 7 in structured-A shared-a (R = d1 = 16384)."""
+    c = ctgen.CONFIGS["c3a"]
+    _run_config("c3a", primes_per_call=3, n_random=32768, dec_cols=[0, 128, c.d3 - 1])
+
+
 def test_config5_full_size():
     c = ctgen.CONFIGS["c5"]
     _run_config("c5", primes_per_call=1, n_random=8192, dec_cols=[0, c.d3 - 1])
+
+
+def test_config4_skinny_sweep_full_size(monkeypatch):
+    """SURVEY.md §8(f) row 1 at full size: config c4's ciphertexts (shared-s, N = 8192,
+    d1 = d2 = 32768, R = 65536; one prime) times a U with d3_loc ∈ {1, 64, 128, 256} — Table 4's
+    d3 values and CP-Mv — through ctpt_matmul, which takes the fused skinny
+    kernel; Freivalds + boundary/random entries + whole boundary columns per output matrix."""
+    import dataclasses
+
+    import torch
+
+    from paper_2503_16080_b200 import ctpt
+
+    monkeypatch.delenv("CTPT_SKINNY", raising=False)
+    c = ctgen.CONFIGS["c4"]
+    ps = ctgen.primes(1)
+    p = ps[0]
+    d3 = 256
+    ct = ctgen.encrypt(c.fmt, c.N, c.d1, c.d2, c.seed, c.log_delta, ps, nthreads=NTHREADS)
+    U = ctgen.U_matrix(c.seed, c.d2, d3, c.u_bound, nthreads=NTHREADS)
+    from paper_2503_16080_b200.engine import CpmmEngine, dev_to_u32
+
+    eng = CpmmEngine(ctpt.Spec(c.fmt, c.N, c.d1, c.d2, d3, ps), "cuda")
+    eng.layout(ct.a_polys, ct.b_polys, validate=True)
+    eng.precompute(U)
+    Ac, Bc = colmajor_views(c.fmt, c.N, c.d1, c.d2, ct.a_polys[0], ct.b_polys[0])
+    rng = np.random.default_rng(77)
+    for c0, c1 in [(0, 1), (0, 64), (0, 128), (0, 256), (100, 229)]:
+        sp = dataclasses.replace(eng.spec, col_begin=c0, col_end=c1)
+        sz = ctpt.query_sizes(sp)
+        AU = torch.empty(sz.out_AU_bytes // 4, dtype=torch.int32, device="cuda")
+        BU = torch.empty(sz.out_BU_bytes // 4, dtype=torch.int32, device="cuda")
+        ctpt.matmul(sp, eng.ctmat, eng.plain, AU, BU, eng.ws)
+        torch.cuda.synchronize()
+        AUn = dev_to_u32(AU).reshape(c1 - c0, c.rows_A)
+        BUn = dev_to_u32(BU).reshape(c1 - c0, c.d1)
+        Us = np.ascontiguousarray(U[:, c0:c1])
+        _check_matrix(Ac, Us, AUn, p, rng, f"c4-skinny A·U cols [{c0},{c1})", 8192)
+        _check_matrix(Bc, Us, BUn, p, rng, f"c4-skinny B·U cols [{c0},{c1})", 8192)

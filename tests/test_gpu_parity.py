@@ -19,7 +19,7 @@ from gpu_helpers import NTHREADS, U_residues, oracle_outputs, run_gpu  # noqa: E
 
 pytestmark = pytest.mark.gpu
 
-R, S, A = ctgen.RLWE, ctgen.SHARED_S, ctgen.SHARED_A
+R, S, A, SA = ctgen.RLWE, ctgen.SHARED_S, ctgen.SHARED_A, ctgen.STRUCT_A
 
 SHAPES = [
     # fmt, N, k, d2, d3, L  — several tiles + ragged tails in every dimension
@@ -33,6 +33,8 @@ SHAPES = [
     (A, 8, 4, 33, 5, 1),
     (S, 4, 8, 128, 128, 1),
     (A, 1024, 3, 1000, 257, 2),
+    (SA, 64, 3, 300, 260, 2),    # structured-A shared-a (Algorithm 7): only B·U
+    (SA, 16, 5, 130, 100, 1),
 ]
 
 
@@ -51,20 +53,102 @@ def _check(fmt, N, k, d2, d3, L, seed=0, u_bound=8, simt=False, col_begin=0, col
         assert np.array_equal(BU[l], wb), f"B·U mismatch prime {l}: {np.argwhere(BU[l] != wb)[:5]}"
 
 
-@pytest.fixture(params=["1cta", "2cta"])
+@pytest.fixture(params=["1cta", "2cta", "fused"])
 def gemm_kernel(request, monkeypatch):
-    """Force the single-CTA (k_gemm_tc) or CTA-pair (k_gemm_tc2) tensor-core kernel."""
-    monkeypatch.setenv("CTPT_GEMM", request.param)
+    """Force the single-CTA (k_gemm_tc) or CTA-pair (k_gemm_tc2) tensor-core kernel after a
+    separate split (CTPT_SKINNY=off), or leave ctpt_matmul's default, which takes the fused
+    skinny kernel (k_gemm_fused) whenever d3_loc <= 256 and kU = 1."""
+    if request.param == "fused":
+        monkeypatch.delenv("CTPT_SKINNY", raising=False)
+    else:
+        monkeypatch.setenv("CTPT_SKINNY", "off")
+        monkeypatch.setenv("CTPT_GEMM", request.param)
     return request.param
 
 
 @pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "f%d_N%d_k%d_d2%d_d3%d_L%d" % s)
 def test_shapes_tcgen05(shape, gemm_kernel):
+    if gemm_kernel == "fused" and shape[4] > 256:
+        pytest.skip("d3 > 256 never takes the fused kernel")
     _check(*shape)
 
 
 def test_column_shard_both_kernels(gemm_kernel):
     _check(S, 128, 2, 160, 600, 1, col_begin=37, col_end=591)
+    _check(A, 64, 3, 300, 600, 2, col_begin=300, col_end=555)  # d3_loc = 255: fused when allowed
+
+
+# ------------------------------------------------------------------ skinny regime (§8(f) row 1)
+SKINNY = [
+    # fmt, N, k, d2, d3, L — d3 across the fused kernel's range: 1 (CP-Mv), < 128, = 128,
+    # one past (two MMA groups), 256; ragged R and d2 (not multiples of 64 / 128)
+    (S, 64, 3, 1000, 1, 2),
+    (R, 512, 1, 130, 2, 1),
+    (A, 128, 4, 520, 64, 1),
+    (S, 32, 5, 384, 128, 1),
+    (A, 16, 3, 77, 129, 2),
+    (R, 1024, 1, 2056, 200, 1),
+    (S, 128, 2, 640, 256, 1),
+    (A, 8, 2, 16, 256, 1),       # R = 24 rows < one tile
+    (SA, 256, 2, 700, 1, 2),     # Algorithm 7 CP-Mv (P:1770): the output is a shared-s vector
+]
+
+
+@pytest.mark.parametrize("shape", SKINNY, ids=lambda s: "f%d_N%d_k%d_d2%d_d3%d_L%d" % s)
+def test_skinny_fused(shape, monkeypatch):
+    monkeypatch.delenv("CTPT_SKINNY", raising=False)
+    _check(*shape)
+
+
+def test_skinny_fused_direct_entry_point():
+    """ctpt_gemm_fused per prime (the stage entry point) == the oracle; and it refuses
+    d3_loc > 256 with ERR_UNSUPPORTED."""
+    import torch
+
+    from paper_2503_16080_b200 import ctpt
+    from paper_2503_16080_b200.engine import CpmmEngine
+
+    fmt, N, k, d2, d3, L = S, 64, 2, 300, 100, 2
+    d1 = N * k
+    ps = ctgen.primes(L)
+    ct = ctgen.encrypt(fmt, N, d1, d2, 11, 20, ps)
+    U = ctgen.U_matrix(11, d2, d3, 8)
+    eng = CpmmEngine(ctpt.Spec(fmt, N, d1, d2, d3, ps), "cuda")
+    eng.layout(ct.a_polys, ct.b_polys)
+    eng.precompute(U)
+    AU, BU = eng.alloc_outputs()
+    ra = eng.sizes.rows_A
+    for l in range(L):
+        ctpt.gemm_fused(eng.spec, l, eng.ctmat, eng.plain, AU[l * d3 * ra:], BU[l * d3 * d1:])
+    torch.cuda.synchronize()
+    AUn, BUn = eng.outputs_numpy(AU, BU)
+    for l, p in enumerate(ps):
+        wa, wb = oracle_outputs(fmt, N, d1, ct.a_polys[l], ct.b_polys[l], U, p)
+        assert np.array_equal(AUn[l], wa) and np.array_equal(BUn[l], wb)
+    big = ctpt.Spec(fmt, N, d1, d2, 300, ps)
+    with pytest.raises(ctpt.CtptError, match="ERR_UNSUPPORTED"):
+        ctpt.gemm_fused(big, 0, eng.ctmat, eng.plain, AU, BU)
+
+
+def test_skinny_adversarial_residues(monkeypatch):
+    """The fused split on residues 0, 1, (p±1)/2, p−1, p−2 with U digits at −128 / 127 and
+    d2 = 65536 (the int32 exactness limit) — C_ℓ reaches ±d2·255·128."""
+    monkeypatch.delenv("CTPT_SKINNY", raising=False)
+    fmt, N, d2, d3 = R, 64, 65536, 130
+    ps = ctgen.primes(1)
+    p = ps[0]
+    rng = np.random.default_rng(3)
+    special = np.array([0, 1, (p - 1) // 2, (p + 1) // 2, p - 1, p - 2, (64 << 24) | 0xFFFFFF], dtype=np.uint32)
+    a = special[rng.integers(0, len(special), (1, d2, N))]
+    b = special[rng.integers(0, len(special), (1, d2, N))]
+    a[0, :, 0] = (64 << 24) | 0xFFFFFF
+    U = rng.choice(np.array([-128, 127, -1, 0, 1], dtype=np.int64), size=(d2, d3))
+    U[:, 0] = -128
+    U[:, 129] = 127
+    (AU, BU), eng = run_gpu(fmt, N, N, d2, d3, ps, a, b, U=U)
+    assert eng.spec.kU == 1
+    wa, wb = oracle_outputs(fmt, N, N, a[0], b[0], U, p)
+    assert np.array_equal(AU[0], wa) and np.array_equal(BU[0], wb)
 
 
 def test_multi_digit_U_pair_kernel(monkeypatch):
@@ -177,6 +261,8 @@ def test_general_U_residues_rns():
     (S, 32, 4, 96, 300, 1, 8, 0, (17, 250)),        # default chunking, column shard
     (R, 256, 1, 130, 64, 3, 30000, 192, (0, 0)),    # k_U = 2 through the host path
     (A, 16, 2, 40, 7, 1, 8, 4096, (0, 0)),          # one chunk larger than R
+    (S, 64, 3, 300, 256, 2, 8, 128, (0, 0)),        # fused skinny kernel on each chunk
+    (R, 512, 1, 200, 600, 1, 8, 320, (100, 101)),   # d3_loc = 1 (CP-Mv) column shard
 ])
 def test_matmul_host_pipeline(fmt, N, k, d2, d3, L, u_bound, chunk, cols):
     """ctpt_matmul_host (host buffers, chunked 3-stream pipeline) == the oracle."""
@@ -299,3 +385,24 @@ def _decrypt_check(c, ps, AU, BU, U, cols):
         approx = np.array([float(v) for v in cen]) / 2.0 ** c.log_delta
         worst = max(worst, np.abs(approx - MU[:, ci]).max() / np.abs(MU).max())
     assert worst <= 1e-6, worst
+
+
+def test_struct_a_algorithm7_decrypts():
+    """Algorithm 7 end to end on the GPU: B' = B·U from ctpt_matmul; then Ã·(S·U) + B' ≡
+    (⌊ΔM⌉+E)·U (mod p) for every output column and prime."""
+    fmt, N, k, d2, d3, L = SA, 32, 3, 96, 20, 2
+    d1 = N * k
+    ps = ctgen.primes(L)
+    ct = ctgen.encrypt(fmt, N, d1, d2, 12, 20, ps)
+    U = ctgen.U_matrix(12, d2, d3, 8)
+    (AU, BU), eng = run_gpu(fmt, N, d1, d2, d3, ps, ct.a_polys, ct.b_polys, U=U)
+    assert AU.shape == (L, d3, 0) and eng.sizes.out_AU_bytes == 0
+    sks = [ctgen.sk(12, j, N) for j in range(d2)]
+    P = ctgen.plain_matrix(12, N, d1, range(d1), range(d2), 20)
+    PU = P.astype(object).dot(U.astype(object))
+    for l, p in enumerate(ps):
+        wa, wb = oracle_outputs(fmt, N, d1, ct.a_polys[l], ct.b_polys[l], U, p)
+        assert np.array_equal(BU[l], wb)
+        for j in range(d3):
+            dec = oracle.decrypt_col(fmt, N, d1, [oracle.su_column(sks, U, j)], ct.a_polys[l], BU[l, j], p)
+            assert [int(x) for x in dec] == [int(v) % p for v in PU[:, j]]
