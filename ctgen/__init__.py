@@ -83,6 +83,10 @@ def lib():
         L.ctgen_u.argtypes = [u64, i64, i64, i64, i64]
         L.ctgen_U.restype = None
         L.ctgen_U.argtypes = [u64, i64, i64, i64, P, ctypes.c_int]
+        L.ctgen_U_real.restype = None
+        L.ctgen_U_real.argtypes = [u64, i64, i64, u64, P, P, ctypes.c_int]
+        L.ctgen_u_real.restype = ctypes.c_double
+        L.ctgen_u_real.argtypes = [u64, i64, i64, i64]
         L.ctgen_uniform.restype = u64
         L.ctgen_uniform.argtypes = [u64, u64, u64, u64]
         L.ctgen_negacyclic_ntt.restype = ctypes.c_int
@@ -171,6 +175,19 @@ def U_matrix(seed: int, d2: int, d3: int, bound: int, nthreads: int = 0) -> np.n
     out = np.empty((d2, d3), dtype=np.int64)
     lib().ctgen_U(seed, d2, d3, bound, _ptr(out), nthreads)
     return out
+
+
+def U_real(seed: int, d2: int, d3: int, scale: int, nthreads: int = 0):
+    """Real U ∈ [-1,1)^{d2×d3} (53-bit grid) and its encoding U0 = ⌊scale·U⌉ (Alg. 6 REQUIRE,
+    P:1697) as exact int64 — the input of the Rescale workloads (scale = Δ_U)."""
+    real = np.empty((d2, d3), dtype=np.float64)
+    enc = np.empty((d2, d3), dtype=np.int64)
+    lib().ctgen_U_real(seed, d2, d3, int(scale), _ptr(real), _ptr(enc), nthreads)
+    return real, enc
+
+
+def u_real(seed: int, d3: int, k: int, j: int) -> float:
+    return lib().ctgen_u_real(seed, d3, k, j)
 
 
 def uniform(seed: int, stream: int, n: int, mod: int) -> np.ndarray:

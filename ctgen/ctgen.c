@@ -42,6 +42,7 @@
 #define K_M 4ULL
 #define K_U 5ULL
 #define K_R 6ULL /* generic stream for test vectors (Freivalds r, etc.) */
+#define K_UR 7ULL /* real-valued U for the Rescale workloads (uniform 53-bit grid on [-1,1)) */
 
 static inline uint64_t splitmix64(uint64_t x) {
   x += 0x9E3779B97F4A7C15ULL;
@@ -183,6 +184,33 @@ void ctgen_U(uint64_t seed, int64_t d2, int64_t d3, int64_t bound, int64_t* out,
 #endif
   for (int64_t k = 0; k < d2; ++k)
     for (int64_t j = 0; j < d3; ++j) out[k * d3 + j] = ctgen_u(seed, d3, k, j, bound);
+}
+
+/* Real U ∈ [-1,1)^{d2×d3} on the 53-bit grid (stream K_UR, idx k*d3 + j), and its encoding
+ * U0 = ⌊scale · U⌉ (Alg. 6 REQUIRE: U0 = ⌊Δ·U⌉; ties up) for an arbitrary
+ * integer scale < 2^62 (e.g. Δ_U = the rescaling prime), computed exactly in 128-bit:
+ * scale·U = scale·v·2^-52 with v = r53 - 2^52, so ⌊scale·U + 1/2⌋ = (scale·v + 2^51) >> 52. */
+double ctgen_u_real(uint64_t seed, int64_t d3, int64_t k, int64_t j) {
+  uint64_t r53 = ctgen_draw64(seed, K_UR << 56, (uint64_t)(k * d3 + j)) >> 11;
+  return ldexp((double)((int64_t)r53 - (1LL << 52)), -52);
+}
+
+void ctgen_U_real(uint64_t seed, int64_t d2, int64_t d3, uint64_t scale, double* out_real, int64_t* out_enc,
+                  int nthreads) {
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(static)
+#endif
+  for (int64_t k = 0; k < d2; ++k)
+    for (int64_t j = 0; j < d3; ++j) {
+      uint64_t r53 = ctgen_draw64(seed, K_UR << 56, (uint64_t)(k * d3 + j)) >> 11;
+      int64_t v = (int64_t)r53 - (1LL << 52);
+      if (out_real) out_real[k * d3 + j] = ldexp((double)v, -52);
+      if (out_enc) {
+        __int128 t = (__int128)scale * v + ((__int128)1 << 51);
+        out_enc[k * d3 + j] = (int64_t)(t >> 52); /* arithmetic shift = floor */
+      }
+    }
 }
 
 uint64_t ctgen_uniform(uint64_t seed, uint64_t stream, uint64_t idx, uint64_t mod) {

@@ -85,15 +85,23 @@ typedef struct {
   int32_t kU;               /* int8 digits per U entry, as returned by ctpt_plain_precompute* */
   int32_t plain_per_prime;  /* 0: one U digit set shared by all primes (ctpt_plain_precompute)
                                1: per-prime digit sets (ctpt_plain_precompute_rns)            */
+  int32_t rescale;          /* 0: outputs are (A·U, B·U) mod every prime (Alg. 6 step 1).
+                               1: ctpt_matmul also performs Alg. 6 / Alg. 7 step 2, Rescale
+                               (P:1681), dividing by q_1 = primes[L−1] (the paper's
+                               "q_1 ≈ Δ that divides q"): outputs hold ⌊x / q_1⌉ mod
+                               p_l for the first L−1 primes only, x ∈ Z_q the exact product.
+                               Needs L ≥ 2 and the whole prime set; the per-prime entry points
+                               and ctpt_matmul_host return CTPT_ERR_UNSUPPORTED.            */
 } ctpt_problem;
 
 typedef struct {
   size_t ctmat_bytes;       /* d_ctmat: 256-byte header + L·R·d2p int32 (K-major stacked [A;B]) */
   size_t plain_bytes;       /* d_plain for ctpt_plain_precompute: 256 + kU·d3·d2p int8          */
   size_t plain_rns_bytes;   /* d_plain for ctpt_plain_precompute_rns: 256 + L·4·d3·d2p int8     */
-  size_t workspace_bytes;   /* d_ws for ctpt_matmul / ctpt_split / ctpt_gemm: 4·R·d2p           */
-  size_t out_AU_bytes;      /* L·d3_loc·rows_A uint32                                          */
-  size_t out_BU_bytes;      /* L·d3_loc·d1 uint32                                              */
+  size_t workspace_bytes;   /* d_ws for ctpt_matmul / ctpt_split / ctpt_gemm: 4·R·d2p (with
+                               rescale: ⌈4·R·d2p⌉_256 + 4·R·d3_loc for the last prime's product) */
+  size_t out_AU_bytes;      /* L_out·d3_loc·rows_A uint32 (L_out = L, or L − 1 with rescale)    */
+  size_t out_BU_bytes;      /* L_out·d3_loc·d1 uint32                                          */
   int64_t rows_A, R, d2p, d3_loc;
 } ctpt_sizes;
 
@@ -135,7 +143,8 @@ ctpt_status ctpt_plain_precompute_rns(const ctpt_problem* prob, const uint32_t* 
                                       int32_t* kU_out, void* stream);
 
 /* The hot path: (A·U0 mod p, B·U0 mod p) for every prime of `prob` and U columns
- * [col_begin, col_end) (Alg. 6 step 1).  Per prime: the limb split of X into the
+ * [col_begin, col_end) (Alg. 6 step 1), and with prob->rescale = 1 the RNS Rescale by
+ * the last prime fused into the other primes' epilogues (step 2).  Per prime: the limb split of X into the
  * workspace (timed here by design), then the tcgen05 limb GEMM with
  * the fused recombine + Barrett epilogue (a4, a5).  Outputs in per-column ciphertext layout:
  *   d_AU: uint32 [L][d3_loc][rows_A], d_BU: uint32 [L][d3_loc][d1]   (output column j is

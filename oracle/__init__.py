@@ -21,6 +21,8 @@ What it computes, and where the paper defines it (``P:n`` = PAPER.md line n):
                         (Alg. 6 step 1; Thm th:pcmm P:1711, th:pcmm-shs P:1722)
 * ``decrypt_cols``      S·A' + B' mod p (identity at P:1688)
 * ``crt_centred``       centred CRT over the RNS basis (reading Q14)
+* ``rescale_last``      Rescale(x) = ⌊x / q_1⌉ mod q/q_1 with q_1 the last prime
+                        (Alg. 6 step 2 P:1705), exact integers
 * ``precision_bits``    log‖M‖∞ − log‖M − M̃‖∞ (P:1340–1343)
 * ``freivalds``         probabilistic check of C = X·U mod p (test protocol)
 
@@ -314,6 +316,29 @@ def crt_centred_array(res: np.ndarray, primes) -> list:
     """res: [L][n] residues → list of n exact centred integers."""
     res = np.asarray(res)
     return [crt_centred([int(res[l, i]) for l in range(res.shape[0])], primes) for i in range(res.shape[1])]
+
+
+def round_div(x: int, d: int) -> int:
+    """⌊x/d⌉ = ⌊x/d + 1/2⌋ for integers, d > 0 (P:803), exactly: ⌊(2x + d) / (2d)⌋."""
+    return (2 * int(x) + int(d)) // (2 * int(d))
+
+
+def rescale_last(res: np.ndarray, primes) -> np.ndarray:
+    """Rescale: (A, B) ↦ (⌊A/Δ⌉, ⌊B/Δ⌉) with Δ replaced by q_1 = primes[-1], a
+    divisor of q ("choose q_1 ≈ Δ that divides q and replace q/Δ by q/q_1").
+    res: canonical residues [L][n] of elements x ∈ Z_q; returns the residues [L−1][n] of
+    ⌊x/q_1⌉ mod q/q_1 — the plain definition: CRT to the exact integer, divide, round.
+    (The result does not depend on the representative of x: x + q gives + q/q_1.)"""
+    res = np.asarray(res)
+    L, n = res.shape
+    q1 = int(primes[-1])
+    out = np.empty((L - 1, n), dtype=np.uint32)
+    for i in range(n):
+        x = crt_centred([int(res[l, i]) for l in range(L)], primes)
+        y = round_div(x, q1)
+        for l in range(L - 1):
+            out[l, i] = y % int(primes[l])
+    return out
 
 
 def precision_bits(M_ref: np.ndarray, M_approx: np.ndarray) -> float:

@@ -43,6 +43,7 @@ constexpr size_t kHeader = 256;
 struct Dims {
   int64_t N, d1, d2, d3, k, rows_A, R, d2p, j0, j1, d3_loc;
   int L;
+  int L_out;  // primes in the outputs: L, or L − 1 after an RNS Rescale by the last prime
 };
 
 int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
@@ -76,8 +77,22 @@ ctpt_status check_problem(const ctpt_problem* pb, Dims& d) {
   d.R = d.rows_A + d.d1;
   d.d2p = round_up(d.d2, 16);
   d.j0 = c0; d.j1 = c1; d.d3_loc = c1 - c0;
+  if (pb->rescale != 0 && pb->rescale != 1) return fail(CTPT_ERR_ARG, "rescale must be 0 or 1");
+  if (pb->rescale && pb->L < 2) return fail(CTPT_ERR_ARG, "Rescale by the last prime needs L >= 2 primes");
+  d.L_out = pb->rescale ? pb->L - 1 : pb->L;
   if (d.R > INT32_MAX / 2 || d.d3 > INT32_MAX / 2) return fail(CTPT_ERR_SHAPE, "dimension exceeds TMA coordinate range");
   return CTPT_OK;
+}
+
+size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+// d_ws of ctpt_matmul: the 4 limb planes of one prime [4][R][d2p] u8, then (Rescale only) the
+// last prime's product per column [d3_loc][R] u32.
+size_t ws_limb_bytes(const Dims& d) { return static_cast<size_t>(4) * d.R * d.d2p; }
+size_t ws_bytes_needed(const ctpt_problem* pb, const Dims& d) {
+  size_t n = ws_limb_bytes(d);
+  if (pb->rescale) n = align256(n) + static_cast<size_t>(4) * d.R * d.d3_loc;
+  return n;
 }
 
 ModP make_modp(uint32_t p) {
@@ -87,6 +102,16 @@ ModP make_modp(uint32_t p) {
   const uint64_t two56 = 1ULL << 56;
   m.off = ((two56 + p - 1) / p) * static_cast<uint64_t>(p);
   return m;
+}
+
+uint32_t powmod_u32(uint32_t b, uint32_t e, uint32_t p) {
+  uint64_t r = 1 % p, x = b % p;
+  while (e) {
+    if (e & 1) r = r * x % p;
+    x = x * x % p;
+    e >>= 1;
+  }
+  return static_cast<uint32_t>(r);
 }
 
 uint32_t pow2mod(int e, uint32_t p) {
@@ -198,9 +223,9 @@ ctpt_status ctpt_query_sizes(const ctpt_problem* pb, ctpt_sizes* out) {
   out->ctmat_bytes = kHeader + static_cast<size_t>(d.L) * d.R * d.d2p * 4;
   out->plain_bytes = kHeader + static_cast<size_t>(kU) * d.d3 * d.d2p;
   out->plain_rns_bytes = kHeader + static_cast<size_t>(d.L) * 4 * d.d3 * d.d2p;
-  out->workspace_bytes = static_cast<size_t>(4) * d.R * d.d2p;
-  out->out_AU_bytes = static_cast<size_t>(d.L) * d.d3_loc * d.rows_A * 4;
-  out->out_BU_bytes = static_cast<size_t>(d.L) * d.d3_loc * d.d1 * 4;
+  out->workspace_bytes = ws_bytes_needed(pb, d);
+  out->out_AU_bytes = static_cast<size_t>(d.L_out) * d.d3_loc * d.rows_A * 4;
+  out->out_BU_bytes = static_cast<size_t>(d.L_out) * d.d3_loc * d.d1 * 4;
   out->rows_A = d.rows_A;
   out->R = d.R;
   out->d2p = d.d2p;
@@ -331,10 +356,11 @@ static ctpt_status gemm_common(const ctpt_problem* pb, int32_t l, const void* d_
   Dims d;
   ctpt_status s = check_problem(pb, d);
   if (s != CTPT_OK) return s;
+  if (pb->rescale) return fail(CTPT_ERR_UNSUPPORTED, "Rescale needs every prime: use ctpt_matmul");
   if (l < 0 || l >= d.L) return fail(CTPT_ERR_ARG, "prime index %d out of range", l);
   if (!d_ws || !d_plain || (!d_AU_l && d.rows_A > 0) || !d_BU_l) return fail(CTPT_ERR_ARG, "null device pointer");
   if (ws_bytes < static_cast<size_t>(4) * d.R * d.d2p) return fail(CTPT_ERR_ARG, "workspace too small");
-  GemmArgs g;
+  GemmArgs g{};
   g.limbs = d_ws;
   g.R = d.R;
   g.d = d;
@@ -383,6 +409,7 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
       S.o = g.o;
       S.o.accumulate = i > 0;
       S.o.w = pow2mod(8 * i, g.p);
+      if (i < g.kU - 1) S.o.xlast = nullptr;
       dim3 grid(static_cast<unsigned>((g.R + 15) / 16), static_cast<unsigned>((d.d3_loc + 15) / 16));
       k_gemm_simt<<<grid, 256, 0, st>>>(S);
       CUDA_TRY(cudaGetLastError());
@@ -425,6 +452,7 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
     P.o = g.o;
     P.o.accumulate = i > 0;
     P.o.w = pow2mod(8 * i, g.p);
+    if (i < g.kU - 1) P.o.xlast = nullptr;  // Rescale on the final pass only
     if (pair)
       k_gemm_tc2<<<grid, T2_THREADS, T2_SMEM_BYTES, st>>>(tmU, tmX, P);
     else
@@ -474,9 +502,10 @@ ctpt_status ctpt_gemm_fused(const ctpt_problem* pb, int32_t l, const void* d_ctm
   Dims d;
   ctpt_status s = check_problem(pb, d);
   if (s != CTPT_OK) return s;
+  if (pb->rescale) return fail(CTPT_ERR_UNSUPPORTED, "Rescale needs every prime: use ctpt_matmul");
   if (l < 0 || l >= d.L) return fail(CTPT_ERR_ARG, "prime index %d out of range", l);
   if (!d_ctmat || !d_plain || (!d_AU_l && d.rows_A > 0) || !d_BU_l) return fail(CTPT_ERR_ARG, "null device pointer");
-  GemmArgs g;
+  GemmArgs g{};
   g.limbs = nullptr;
   g.R = d.R;
   g.d = d;
@@ -511,19 +540,65 @@ ctpt_status ctpt_matmul(const ctpt_problem* pb, const void* d_ctmat, const void*
   Dims d;
   ctpt_status s = check_problem(pb, d);
   if (s != CTPT_OK) return s;
-  if ((!d_AU && d.rows_A > 0) || !d_BU) return fail(CTPT_ERR_ARG, "null output pointer");
+  if ((!d_AU && d.rows_A > 0) || !d_BU || !d_ctmat || !d_plain) return fail(CTPT_ERR_ARG, "null pointer");
   const bool fused = fused_eligible(d, pb->kU <= 0 ? 1 : pb->kU);
-  for (int l = 0; l < d.L; ++l) {
-    if (fused) {
-      s = ctpt_gemm_fused(pb, l, d_ctmat, d_plain, d_AU + static_cast<int64_t>(l) * d.d3_loc * d.rows_A,
-                          d_BU + static_cast<int64_t>(l) * d.d3_loc * d.d1, stream);
-      if (s != CTPT_OK) return s;
-      continue;
-    }
-    s = ctpt_split(pb, l, d_ctmat, d_ws, ws_bytes, stream);
+  if (!fused && !d_ws) return fail(CTPT_ERR_ARG, "null workspace");
+  if (!fused || pb->rescale) {
+    const size_t need = ws_bytes_needed(pb, d);
+    if (ws_bytes < need) return fail(CTPT_ERR_ARG, "workspace too small (%zu < %zu)", ws_bytes, need);
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint32_t* X0 = reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(d_ctmat) + kHeader);
+  uint32_t* xlast = pb->rescale
+                        ? reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(d_ws) + align256(ws_limb_bytes(d)))
+                        : nullptr;
+  // one prime's product (fused skinny kernel, or split + limb GEMM) into the outputs `o`
+  auto run = [&](int l, const OutParams& o) -> ctpt_status {
+    GemmArgs g{};
+    g.d = d;
+    g.R = d.R;
+    g.kU = pb->kU <= 0 ? 1 : pb->kU;
+    g.planes = reinterpret_cast<const int8_t*>(static_cast<const uint8_t*>(d_plain) + kHeader);
+    g.nplanes = pb->plain_per_prime ? d.L * g.kU : g.kU;
+    g.plane0 = plane_index(pb, l, 0);
+    g.p = pb->primes[l];
+    g.o = o;
+    const uint32_t* x = X0 + static_cast<int64_t>(l) * d.R * d.d2p;
+    if (fused) return launch_fused(g, x, st);
+    ctpt_status s2 = launch_split(x, d.R * d.d2p, d_ws, st);
+    if (s2 != CTPT_OK) return s2;
+    g.limbs = d_ws;
+    return launch_gemm(g, st, false);
+  };
+  if (pb->rescale) {
+    // RNS Rescale by q_1 = p_{L−1} (Alg. 6 step 2 / Alg. 7 step 2): the last
+    // prime's product first, kept per column [d3_loc][R] in the workspace; the other primes'
+    // epilogues then emit ⌊x / p_{L−1}⌉ mod p_l directly.
+    OutParams o{};
+    o.AU = xlast;
+    o.BU = xlast;
+    o.rows_A = d.R;
+    o.d1 = 0;
+    o.R = d.R;
+    o.d3_loc = d.d3_loc;
+    s = run(d.L - 1, o);
     if (s != CTPT_OK) return s;
-    s = ctpt_gemm(pb, l, d_ws, ws_bytes, d_plain, d_AU + static_cast<int64_t>(l) * d.d3_loc * d.rows_A,
-                  d_BU + static_cast<int64_t>(l) * d.d3_loc * d.d1, stream);
+  }
+  for (int l = 0; l < d.L_out; ++l) {
+    OutParams o{};
+    o.AU = d_AU ? d_AU + static_cast<int64_t>(l) * d.d3_loc * d.rows_A : nullptr;
+    o.BU = d_BU + static_cast<int64_t>(l) * d.d3_loc * d.d1;
+    o.rows_A = d.rows_A;
+    o.d1 = d.d1;
+    o.R = d.R;
+    o.d3_loc = d.d3_loc;
+    if (pb->rescale) {
+      const uint32_t pl = pb->primes[d.L - 1], p = pb->primes[l];
+      o.xlast = xlast;
+      o.p_last = pl;
+      o.p_last_inv = powmod_u32(pl % p, p - 2, p);  // p prime (Fermat)
+    }
+    s = run(l, o);
     if (s != CTPT_OK) return s;
   }
   return CTPT_OK;
@@ -543,8 +618,6 @@ struct HostPlan {
   int64_t chunk;  // rows of X per chunk (multiple of 64)
   size_t in_bytes, cm_bytes, limb_bytes, out_bytes, total;
 };
-
-size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
 HostPlan host_plan(const Dims& d, int64_t chunk_rows) {
   HostPlan h;
@@ -610,6 +683,7 @@ ctpt_status ctpt_matmul_host(const ctpt_problem* pb, const uint32_t* h_a, const 
   Dims d;
   ctpt_status s = check_problem(pb, d);
   if (s != CTPT_OK) return s;
+  if (pb->rescale) return fail(CTPT_ERR_UNSUPPORTED, "ctpt_matmul_host does not Rescale (use ctpt_matmul)");
   if (((!h_a || !h_AU) && d.rows_A > 0) || !h_b || !d_plain || !h_BU || !d_ws) return fail(CTPT_ERR_ARG, "null pointer");
   const HostPlan hp = host_plan(d, chunk_rows);
   if (ws_bytes < hp.total) return fail(CTPT_ERR_ARG, "workspace too small (%zu < %zu)", ws_bytes, hp.total);
@@ -636,7 +710,7 @@ ctpt_status ctpt_matmul_host(const ctpt_problem* pb, const uint32_t* h_a, const 
   CUDA_TRY(cudaStreamWaitEvent(ss.h2d, ev_start, 0));
   CUDA_TRY(cudaStreamWaitEvent(ss.d2h, ev_start, 0));
 
-  GemmArgs g;
+  GemmArgs g{};
   g.d = d;
   g.kU = pb->kU <= 0 ? 1 : pb->kU;
   g.planes = reinterpret_cast<const int8_t*>(static_cast<const uint8_t*>(d_plain) + kHeader);

@@ -146,7 +146,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int quad = warp & 3;  // TMEM lanes [32·quad, 32·quad + 32)
     int acc = 0;
     uint32_t acc_phase = 0;
-    const bool vec_ok = ((P.o.rows_A & 3) == 0) && ((P.o.d1 & 3) == 0) && !P.o.accumulate;
     for (int32_t tile = blockIdx.x; tile < P.num_tiles; tile += gridDim.x) {
       int32_t tj, tr;
       tc_tile_coords(tile, P, tj, tr);
@@ -169,16 +168,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                                  static_cast<int32_t>(v2[i]), static_cast<int32_t>(v3[i]), P.m);
         if (j < P.o.d3_loc) {
           const int64_t r0 = static_cast<int64_t>(tr) * TC_BLOCK_R + c * 16;
-          const bool in_a = (r0 + 15 < P.o.rows_A), in_b = (r0 >= P.o.rows_A);
-          if (vec_ok && r0 + 15 < P.o.R && (in_a || in_b)) {
-            uint4* q = reinterpret_cast<uint4*>(out_ptr(P.o, j, r0));
-#pragma unroll
-            for (int i = 0; i < 4; ++i) q[i] = make_uint4(res[4 * i], res[4 * i + 1], res[4 * i + 2], res[4 * i + 3]);
-          } else {
-#pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if (r0 + i < P.o.R) store_out(P.o, P.m, j, r0 + i, res[i]);
-          }
+          store16(P.o, P.m, j, r0, res);
         }
       }
       tc_fence_before();

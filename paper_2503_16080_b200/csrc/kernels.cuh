@@ -196,16 +196,68 @@ struct OutParams {
   int64_t rows_A, d1, R, d3_loc;
   uint32_t w;          // 2^{8i} mod p for pass i
   int32_t accumulate;  // pass i > 0: out = (out + w·r) mod p
+  // RNS Rescale by the last prime q_1 = p_L of the basis (Alg. 6/7 step 2),
+  // applied on the final pass when xlast != nullptr: xlast = the product's residues mod p_L,
+  // per column [d3_loc][R] (stacked rows); out = (x − [x]_{p_L}) · p_L^{-1} mod p.
+  const uint32_t* xlast;
+  uint32_t p_last, p_last_inv;
 };
 
 __device__ __forceinline__ uint32_t* out_ptr(const OutParams& o, int64_t j, int64_t r) {
   return (r < o.rows_A) ? o.AU + j * o.rows_A + r : o.BU + j * o.d1 + (r - o.rows_A);
 }
 
+// y = ⌊x / p_L⌉ mod p from x mod p (v) and x mod p_L (xl): with c the centred residue of x mod
+// p_L, (x − c)/p_L is the rounded quotient (p_L odd: no ties) and ≡ (v − c)·p_L^{-1} (mod p).
+__device__ __forceinline__ uint32_t rescale_last(uint32_t v, uint32_t xl, const OutParams& o, const ModP& m) {
+  const int64_t c = (xl > (o.p_last >> 1)) ? static_cast<int64_t>(xl) - o.p_last : static_cast<int64_t>(xl);
+  const uint32_t cm = barrett64(static_cast<uint64_t>(c + (static_cast<int64_t>(m.p) << 32)), m);
+  uint32_t d = v + (m.p - cm);
+  d = (d >= m.p) ? d - m.p : d;
+  return barrett64(static_cast<uint64_t>(d) * o.p_last_inv, m);
+}
+
 __device__ __forceinline__ void store_out(const OutParams& o, const ModP& m, int64_t j, int64_t r, uint32_t v) {
   uint32_t* q = out_ptr(o, j, r);
   if (o.accumulate) v = accum_mod(*q, v, o.w, m);
+  if (o.xlast) v = rescale_last(v, o.xlast[j * o.R + r], o, m);
   *q = v;
+}
+
+// Store 16 consecutive rows r0..r0+15 of output column j (one epilogue thread's TMEM chunk):
+// 4 × 16-byte stores when the 16 rows lie inside A' or inside B' and both are 4-aligned.
+__device__ __forceinline__ void store16(const OutParams& o, const ModP& m, int64_t j, int64_t r0, uint32_t (&res)[16]) {
+  const bool in_a = (r0 + 15 < o.rows_A), in_b = (r0 >= o.rows_A);
+  if (((o.rows_A & 3) == 0) && ((o.d1 & 3) == 0) && r0 + 15 < o.R && (in_a || in_b)) {
+    uint4* q = reinterpret_cast<uint4*>(out_ptr(o, j, r0));
+    if (o.accumulate) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint4 pv = q[i];
+        res[4 * i] = accum_mod(pv.x, res[4 * i], o.w, m);
+        res[4 * i + 1] = accum_mod(pv.y, res[4 * i + 1], o.w, m);
+        res[4 * i + 2] = accum_mod(pv.z, res[4 * i + 2], o.w, m);
+        res[4 * i + 3] = accum_mod(pv.w, res[4 * i + 3], o.w, m);
+      }
+    }
+    if (o.xlast) {
+      const uint4* xl = reinterpret_cast<const uint4*>(o.xlast + j * o.R + r0);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint4 x = xl[i];
+        res[4 * i] = rescale_last(res[4 * i], x.x, o, m);
+        res[4 * i + 1] = rescale_last(res[4 * i + 1], x.y, o, m);
+        res[4 * i + 2] = rescale_last(res[4 * i + 2], x.z, o, m);
+        res[4 * i + 3] = rescale_last(res[4 * i + 3], x.w, o, m);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) q[i] = make_uint4(res[4 * i], res[4 * i + 1], res[4 * i + 2], res[4 * i + 3]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (r0 + i < o.R) store_out(o, m, j, r0 + i, res[i]);
+  }
 }
 
 // ------------------------------------------------------------------------------------------

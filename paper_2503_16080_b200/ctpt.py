@@ -38,7 +38,7 @@ class Problem(ctypes.Structure):
     _fields_ = [("fmt", ctypes.c_int32), ("L", ctypes.c_int32), ("N", ctypes.c_int64), ("d1", ctypes.c_int64),
                 ("d2", ctypes.c_int64), ("d3", ctypes.c_int64), ("primes", ctypes.POINTER(ctypes.c_uint32)),
                 ("col_begin", ctypes.c_int64), ("col_end", ctypes.c_int64), ("kU", ctypes.c_int32),
-                ("plain_per_prime", ctypes.c_int32)]
+                ("plain_per_prime", ctypes.c_int32), ("rescale", ctypes.c_int32)]
 
 
 class Sizes(ctypes.Structure):
@@ -99,11 +99,12 @@ class Spec:
     col_end: int = 0
     kU: int = 1
     plain_per_prime: int = 0
+    rescale: int = 0
 
     def cstruct(self) -> Problem:
         arr = (ctypes.c_uint32 * len(self.primes))(*[int(p) for p in self.primes])
         pb = Problem(self.fmt, len(self.primes), self.N, self.d1, self.d2, self.d3, arr, self.col_begin,
-                     self.col_end, self.kU, self.plain_per_prime)
+                     self.col_end, self.kU, self.plain_per_prime, self.rescale)
         pb._keep = arr  # keep the host prime array alive with the struct
         return pb
 

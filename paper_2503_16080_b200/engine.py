@@ -77,7 +77,7 @@ class CpmmEngine:
         return AU, BU
 
     def outputs_numpy(self, AU: torch.Tensor, BU: torch.Tensor):
-        L = len(self.spec.primes)
+        L = len(self.spec.primes) - self.spec.rescale  # Rescale drops the last prime
         d3l = self.sizes.d3_loc
         ra = self.sizes.rows_A
         AUn = dev_to_u32(AU)[:L * d3l * ra].reshape(L, d3l, ra)

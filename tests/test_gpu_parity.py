@@ -406,3 +406,51 @@ def test_struct_a_algorithm7_decrypts():
         for j in range(d3):
             dec = oracle.decrypt_col(fmt, N, d1, [oracle.su_column(sks, U, j)], ct.a_polys[l], BU[l, j], p)
             assert [int(x) for x in dec] == [int(v) % p for v in PU[:, j]]
+
+
+# ------------------------------------------------------------------ RNS Rescale (§8(f) row 3)
+RESCALE = [
+    # fmt, N, k, d2, d3, L, U: "real" (U0 = ⌊q_1·U⌉ as residues, kU = 4) or "int" (|U| ≤ 8, kU = 1)
+    (S, 64, 2, 300, 200, 3, "real"),
+    (A, 32, 3, 130, 70, 2, "real"),
+    (R, 128, 1, 96, 40, 4, "int"),      # kU = 1 → fused skinny kernel + Rescale epilogue
+    (SA, 16, 3, 77, 300, 3, "int"),     # structured-A (Algorithm 7 step 2), split + GEMM path
+    (A, 8, 3, 50, 33, 2, "real"),       # R = 32: one partial tile
+]
+
+
+def _rescale_check(fmt, N, k, d2, d3, L, ukind, seed=21):
+    d1 = N * k
+    ps = ctgen.primes(L)
+    ct = ctgen.encrypt(fmt, N, d1, d2, seed, 20, ps, nthreads=NTHREADS)
+    if ukind == "real":
+        _, U0 = ctgen.U_real(seed, d2, d3, ps[-1])
+        (AU, BU), eng = run_gpu(fmt, N, d1, d2, d3, ps, ct.a_polys, ct.b_polys, Ures=U_residues(U0, ps), rescale=1)
+        assert eng.spec.kU == 4
+    else:
+        U0 = ctgen.U_matrix(seed, d2, d3, 8)
+        (AU, BU), eng = run_gpu(fmt, N, d1, d2, d3, ps, ct.a_polys, ct.b_polys, U=U0, rescale=1)
+        assert eng.spec.kU == 1
+    assert AU.shape[0] == L - 1 and BU.shape[0] == L - 1
+    ra = eng.sizes.rows_A
+    prods = []
+    for l, p in enumerate(ps):
+        wa, wb = oracle_outputs(fmt, N, d1, ct.a_polys[l], ct.b_polys[l], U0, p)
+        prods.append(np.concatenate([wa, wb], axis=1).reshape(-1))
+    want = oracle.rescale_last(np.stack(prods), ps).reshape(L - 1, d3, ra + d1)
+    got = np.concatenate([AU, BU], axis=2)
+    bad = np.argwhere(got != want)
+    assert bad.size == 0, f"{len(bad)} rescaled residues differ, first {bad[:5]}"
+
+
+@pytest.mark.parametrize("case", RESCALE, ids=lambda s: "f%d_N%d_k%d_d2%d_d3%d_L%d_%s" % s)
+def test_rescale_fused_epilogue(case, monkeypatch):
+    monkeypatch.delenv("CTPT_SKINNY", raising=False)
+    _rescale_check(*case)
+
+
+def test_rescale_pair_kernel(monkeypatch):
+    monkeypatch.setenv("CTPT_GEMM", "2cta")
+    monkeypatch.setenv("CTPT_SKINNY", "off")
+    _rescale_check(S, 32, 2, 200, 300, 3, "real")
+    _rescale_check(R, 64, 1, 64, 100, 2, "int")
