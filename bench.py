@@ -296,7 +296,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "config": dict(workload_desc(c), **{
             "l2": f"inputs {sizes.ctmat_bytes * 1.0 / 2**30:.2f} GiB per step > 126 MB L2 (no flush needed)",
             "parallelism": f"weak: {world} independent problem(s), one per GPU, no data-path collective",
-            "kU": kU, "limb_macs_per_residue_mac": 4 * kU}),
+            "kU": kU, "limb_macs_per_residue_mac": 4 * kU,
+            "u_plane": (f"u8: U+{eng.spec.u_offset} (ctpt_plain_precompute_unsigned)" if eng.spec.u_unsigned
+                        else "s8 balanced digits")}),
         "pct_int8_datasheet": 100.0 * value * 4 * kU / world / INT8_DATASHEET_MACS,
         "roofline": {"bound": "tensor", "achieved": achieved_tops, "peak": peak_tops, "unit": "TOP/s",
                      "frac": achieved_tops / peak_tops, "traffic": traffic,
@@ -304,7 +306,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                      "per_launch": f"{limb_macs_launch:.4e} limb MACs (4·kU·R·d2·d3, one prime)",
                      "avg_launch_ms": gemm_avg_s * 1e3, "share_of_step": gemm_share},
         "e2e": e2e,
-        "gpu_launches": (1 + kU) * len(ps) * args.steps,  # per prime: k_split + kU x k_gemm_tc
+        "gpu_launches": (1 + kU) * len(ps) * args.steps,  # per prime: k_split[_rows] + kU x k_gemm_tc
         "clocks": clocks,
         "input_generation_s": gen_s,
     }

@@ -92,6 +92,10 @@ typedef struct {
                                p_l for the first L−1 primes only, x ∈ Z_q the exact product.
                                Needs L ≥ 2 and the whole prime set; the per-prime entry points
                                and ctpt_matmul_host return CTPT_ERR_UNSUPPORTED.            */
+  int32_t u_unsigned;       /* 1: the digit plane holds U' = U + u_offset ∈ [0, 255] as u8
+                               (ctpt_plain_precompute_unsigned; kU = 1, shared plane, d2 ≤ 33025)
+                               and the limb MMAs run u8 × u8; 0: balanced s8 digits.          */
+  int32_t u_offset;         /* the offset ctpt_plain_precompute_unsigned returned (≥ 0)        */
 } ctpt_problem;
 
 typedef struct {
@@ -135,6 +139,19 @@ ctpt_status ctpt_layout(const ctpt_problem* prob, const uint32_t* d_a_polys, con
  * (U^T, K-major, [kU][d3][d2p]) into d_plain and the digit count to *kU_out.  Synchronises. */
 ctpt_status ctpt_plain_precompute(const ctpt_problem* prob, const int64_t* d_U, void* d_plain, int32_t* kU_out,
                                   void* stream);
+
+/* Unsigned-U plaintext precompute: the same U as ctpt_plain_precompute, stored as ONE u8 plane
+ * U' = U + u_offset ∈ [0, 255] with u_offset = max(0, −min U) (*u_offset_out).  The product is
+ * unchanged — X·U = X·U' − u_offset·(Σ_k X[r][k]) — and ctpt_split forms the per-row sums while
+ * it reads X, so the epilogue subtracts u_offset·Σ_k X[r][k] mod p (an O(R) correction, the
+ * same bookkeeping as the paper's chop with digits of one sign).  Why: the tensor
+ * cores' switching energy depends on the operand bits, and at the 1000 W cap a non-negative
+ * small U (no sign-extended high bits) sustains ≈ 5 % more int8 ops
+ * (profiles/r01/power_operands_c3gemm.jsonl).  Then set prob->kU = 1, prob->u_unsigned = 1,
+ * prob->u_offset = *u_offset_out.  CTPT_ERR_RANGE when max U + u_offset > 255,
+ * CTPT_ERR_OVERFLOW when d2 > 33025 (u8·u8 limb products).  Synchronises. */
+ctpt_status ctpt_plain_precompute_unsigned(const ctpt_problem* prob, const int64_t* d_U, void* d_plain,
+                                           int32_t* u_offset_out, void* stream);
 
 /* General plaintext U ∈ Z_q given as canonical residues d_Ures: uint32 [L][d2][d3].
  * Writes 4 balanced int8 digit planes of each centred residue per prime ([L][4][d3][d2p]),

@@ -80,6 +80,11 @@ ctpt_status check_problem(const ctpt_problem* pb, Dims& d) {
   if (pb->rescale != 0 && pb->rescale != 1) return fail(CTPT_ERR_ARG, "rescale must be 0 or 1");
   if (pb->rescale && pb->L < 2) return fail(CTPT_ERR_ARG, "Rescale by the last prime needs L >= 2 primes");
   d.L_out = pb->rescale ? pb->L - 1 : pb->L;
+  if (pb->u_unsigned) {
+    // u8 × u8 limb products: |C_ℓ| ≤ d2·255·255 must stay < 2^31 (the int32 accumulator)
+    if (kU != 1 || pb->plain_per_prime) return fail(CTPT_ERR_ARG, "unsigned-U planes need kU = 1 and shared planes");
+    if (pb->d2 * 255LL * 255LL >= (1LL << 31)) return fail(CTPT_ERR_OVERFLOW, "d2 = %lld too large for unsigned-U planes (d2 <= 33025)", (long long)pb->d2);
+  }
   if (d.R > INT32_MAX / 2 || d.d3 > INT32_MAX / 2) return fail(CTPT_ERR_SHAPE, "dimension exceeds TMA coordinate range");
   return CTPT_OK;
 }
@@ -88,11 +93,19 @@ size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
 // d_ws of ctpt_matmul: the 4 limb planes of one prime [4][R][d2p] u8, then (Rescale only) the
 // last prime's product per column [d3_loc][R] u32.
+// d_ws of ctpt_matmul / ctpt_split / ctpt_gemm, in this order:
+//   limbs   [4][R][d2p] u8                      (one prime's byte-limb planes)
+//   rowcorr [R] u32        (unsigned-U mode with u_offset ≠ 0: u_offset·Σ_k X[r][k] mod p)
+//   xlast   [d3_loc][R] u32 (rescale: the last prime's product)
+bool needs_rowcorr(const ctpt_problem* pb) { return pb->u_unsigned && pb->u_offset != 0; }
 size_t ws_limb_bytes(const Dims& d) { return static_cast<size_t>(4) * d.R * d.d2p; }
+size_t ws_corr_off(const Dims& d) { return align256(ws_limb_bytes(d)); }
+size_t ws_xlast_off(const ctpt_problem* pb, const Dims& d) {
+  return ws_corr_off(d) + (needs_rowcorr(pb) ? align256(static_cast<size_t>(4) * d.R) : 0);
+}
 size_t ws_bytes_needed(const ctpt_problem* pb, const Dims& d) {
-  size_t n = ws_limb_bytes(d);
-  if (pb->rescale) n = align256(n) + static_cast<size_t>(4) * d.R * d.d3_loc;
-  return n;
+  if (!needs_rowcorr(pb) && !pb->rescale) return ws_limb_bytes(d);
+  return ws_xlast_off(pb, d) + (pb->rescale ? static_cast<size_t>(4) * d.R * d.d3_loc : 0);
 }
 
 ModP make_modp(uint32_t p) {
@@ -189,10 +202,14 @@ struct GemmArgs {
   Dims d;                // d2, d2p, d3, j0, d3_loc
   const int8_t* planes;  // U^T digit planes [nplanes][d3][d2p]
   int nplanes, plane0, kU;
+  int u_unsigned;        // U plane is u8 (U + u_offset)
   uint32_t p;
   OutParams o;           // accumulate / w are set per pass
 };
 ctpt_status launch_split(const uint32_t* x, int64_t n, void* limbs, cudaStream_t st);
+// the limb split of `rows` rows of X for prime p; in the unsigned-U mode it also writes rowcorr
+ctpt_status launch_split_prime(const ctpt_problem* pb, const uint32_t* x, int64_t rows, int64_t d2p, uint32_t p,
+                               void* limbs, uint32_t* rowcorr, cudaStream_t st);
 ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt);
 ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st);
 
@@ -200,8 +217,8 @@ ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st);
 // the step is HBM-bound and the fused kernel (split inside the GEMM's load path, X read once)
 // replaces split + GEMM.  CTPT_SKINNY=off forces split + GEMM (for A/B measurements).
 constexpr int64_t kFusedMaxD3 = 256;
-bool fused_eligible(const Dims& d, int kU) {
-  if (kU != 1 || d.d3_loc > kFusedMaxD3) return false;
+bool fused_eligible(const Dims& d, int kU, const ctpt_problem* pb) {
+  if (kU != 1 || d.d3_loc > kFusedMaxD3 || needs_rowcorr(pb)) return false;
   const char* e = getenv("CTPT_SKINNY");
   return !(e && strcmp(e, "off") == 0);
 }
@@ -269,7 +286,7 @@ ctpt_status ctpt_layout(const ctpt_problem* pb, const uint32_t* d_a, const uint3
 }
 
 static ctpt_status plain_common(const ctpt_problem* pb, const int64_t* d_U, const uint32_t* d_Ures, void* d_plain,
-                                int32_t* kU_out, void* stream) {
+                                int32_t* kU_out, void* stream, int32_t* u_offset_out = nullptr) {
   Dims d;
   ctpt_status s = check_problem(pb, d);
   if (s != CTPT_OK) return s;
@@ -295,10 +312,24 @@ static ctpt_status plain_common(const ctpt_problem* pb, const int64_t* d_U, cons
     long long mm[2];
     CUDA_TRY(cudaMemcpyAsync(mm, hdr, 16, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
+    if (u_offset_out) {
+      // unsigned-U plane: U' = U + u_offset ∈ [0, 255], u_offset = max(0, −min U)
+      const long long off = mm[0] < 0 ? -mm[0] : 0;
+      if (mm[1] + off > 255)
+        return fail(CTPT_ERR_RANGE, "max(U) - min(U, 0) = %lld > 255: no single unsigned plane", mm[1] + off);
+      if (d.d2 * 255LL * 255LL >= (1LL << 31))
+        return fail(CTPT_ERR_OVERFLOW, "d2 = %lld too large for unsigned-U planes (d2 <= 33025)", (long long)d.d2);
+      P.u = d_U;
+      P.kU = 1;
+      P.rns = 0;
+      P.unsigned_plane = 1;
+      P.u_offset = off;
+      *u_offset_out = static_cast<int32_t>(off);
+    }
     uint32_t pmin = pb->primes[0];
     for (int i = 1; i < d.L; ++i) pmin = std::min(pmin, pb->primes[i]);
     const long long amax = std::max(mm[1], -mm[0]);
-    if (amax >= static_cast<long long>(pmin / 2))
+    if (!u_offset_out && amax >= static_cast<long long>(pmin / 2))
       return fail(CTPT_ERR_RANGE, "max|U| = %lld >= min(p)/2: use ctpt_plain_precompute_rns", amax);
     int kU = 1;
     // k balanced digits cover [-128·(256^k-1)/255, 127·(256^k-1)/255]
@@ -307,9 +338,11 @@ static ctpt_status plain_common(const ctpt_problem* pb, const int64_t* d_U, cons
       if (mm[0] >= -128 * span && mm[1] <= 127 * span) break;
       ++kU;
     }
-    P.u = d_U;
-    P.kU = kU;
-    P.rns = 0;
+    if (!u_offset_out) {
+      P.u = d_U;
+      P.kU = kU;
+      P.rns = 0;
+    }
   } else {
     P.ures = d_Ures;
     P.kU = 4;
@@ -332,6 +365,13 @@ ctpt_status ctpt_plain_precompute(const ctpt_problem* pb, const int64_t* d_U, vo
   return plain_common(pb, d_U, nullptr, d_plain, kU_out, stream);
 }
 
+ctpt_status ctpt_plain_precompute_unsigned(const ctpt_problem* pb, const int64_t* d_U, void* d_plain,
+                                           int32_t* u_offset_out, void* stream) {
+  if (!d_U || !u_offset_out) return fail(CTPT_ERR_ARG, "null pointer");
+  int32_t kU = 0;
+  return plain_common(pb, d_U, nullptr, d_plain, &kU, stream, u_offset_out);
+}
+
 ctpt_status ctpt_plain_precompute_rns(const ctpt_problem* pb, const uint32_t* d_Ures, void* d_plain, int32_t* kU_out,
                                       void* stream) {
   if (!d_Ures) return fail(CTPT_ERR_ARG, "d_Ures is NULL");
@@ -345,10 +385,11 @@ ctpt_status ctpt_split(const ctpt_problem* pb, int32_t l, const void* d_ctmat, v
   if (s != CTPT_OK) return s;
   if (l < 0 || l >= d.L) return fail(CTPT_ERR_ARG, "prime index %d out of range", l);
   if (!d_ctmat || !d_ws) return fail(CTPT_ERR_ARG, "null device pointer");
-  if (ws_bytes < static_cast<size_t>(4) * d.R * d.d2p) return fail(CTPT_ERR_ARG, "workspace too small");
+  if (ws_bytes < ws_bytes_needed(pb, d)) return fail(CTPT_ERR_ARG, "workspace too small");
   const int64_t n = d.R * d.d2p;  // multiple of 16
   const uint32_t* x = reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(d_ctmat) + kHeader) + l * n;
-  return launch_split(x, n, d_ws, static_cast<cudaStream_t>(stream));
+  uint32_t* corr = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(d_ws) + ws_corr_off(d));
+  return launch_split_prime(pb, x, d.R, d.d2p, pb->primes[l], d_ws, corr, static_cast<cudaStream_t>(stream));
 }
 
 static ctpt_status gemm_common(const ctpt_problem* pb, int32_t l, const void* d_ws, size_t ws_bytes,
@@ -359,9 +400,11 @@ static ctpt_status gemm_common(const ctpt_problem* pb, int32_t l, const void* d_
   if (pb->rescale) return fail(CTPT_ERR_UNSUPPORTED, "Rescale needs every prime: use ctpt_matmul");
   if (l < 0 || l >= d.L) return fail(CTPT_ERR_ARG, "prime index %d out of range", l);
   if (!d_ws || !d_plain || (!d_AU_l && d.rows_A > 0) || !d_BU_l) return fail(CTPT_ERR_ARG, "null device pointer");
-  if (ws_bytes < static_cast<size_t>(4) * d.R * d.d2p) return fail(CTPT_ERR_ARG, "workspace too small");
+  if (ws_bytes < ws_bytes_needed(pb, d)) return fail(CTPT_ERR_ARG, "workspace too small");
   GemmArgs g{};
   g.limbs = d_ws;
+  g.u_unsigned = pb->u_unsigned;
+  if (needs_rowcorr(pb)) g.o.rowcorr = reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(d_ws) + ws_corr_off(d));
   g.R = d.R;
   g.d = d;
   g.kU = pb->kU <= 0 ? 1 : pb->kU;
@@ -385,6 +428,18 @@ static ctpt_status gemm_common(const ctpt_problem* pb, int32_t l, const void* d_
 // ---------------------------------------------------------------------------------------------
 namespace {
 
+ctpt_status launch_split_prime(const ctpt_problem* pb, const uint32_t* x, int64_t rows, int64_t d2p, uint32_t p,
+                               void* limbs, uint32_t* rowcorr, cudaStream_t st) {
+  if (!needs_rowcorr(pb)) return launch_split(x, rows * d2p, limbs, st);
+  const int64_t off = pb->u_offset;
+  const uint32_t off_mod = static_cast<uint32_t>(((off % static_cast<int64_t>(p)) + p) % p);
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(rows, INT32_MAX)));
+  k_split_rows<<<blocks, 256, 0, st>>>(reinterpret_cast<const uint4*>(x), static_cast<uint4*>(limbs), rowcorr, rows,
+                                        d2p / 16, p, off_mod);
+  CUDA_TRY(cudaGetLastError());
+  return CTPT_OK;
+}
+
 ctpt_status launch_split(const uint32_t* x, int64_t n, void* limbs, cudaStream_t st) {
   const int64_t n16 = n / 16;  // n is a multiple of 16 (rows of d2p)
   const int blocks = static_cast<int>(std::min<int64_t>((n16 + 255) / 256, static_cast<int64_t>(num_sms()) * 16));
@@ -405,6 +460,7 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
       S.d2 = d.d2;
       S.d2p = d.d2p;
       S.j_off = d.j0;
+      S.u_unsigned = g.u_unsigned;
       S.m = m;
       S.o = g.o;
       S.o.accumulate = i > 0;
@@ -442,6 +498,7 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
   if (nt > INT32_MAX) return fail(CTPT_ERR_SHAPE, "too many tiles");
   P.num_tiles = static_cast<int32_t>(nt);
   P.group_j = pair ? T2_GROUP_J_DEFAULT : TC_GROUP_J_DEFAULT;
+  P.u_unsigned = g.u_unsigned;
   if (const char* g = getenv("CTPT_GROUP_J")) P.group_j = std::max(1, atoi(g));  // tuning knob
   P.m = m;
   const int sms = num_sms();
@@ -480,6 +537,7 @@ ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st) 
   const int64_t nt = (g.R + FU_BLOCK_R - 1) / FU_BLOCK_R;
   if (nt > INT32_MAX) return fail(CTPT_ERR_SHAPE, "too many tiles");
   P.num_tiles = static_cast<int32_t>(nt);
+  P.u_unsigned = g.u_unsigned;
   P.m = make_modp(g.p);
   P.o = g.o;
   P.o.accumulate = 0;
@@ -503,10 +561,12 @@ ctpt_status ctpt_gemm_fused(const ctpt_problem* pb, int32_t l, const void* d_ctm
   ctpt_status s = check_problem(pb, d);
   if (s != CTPT_OK) return s;
   if (pb->rescale) return fail(CTPT_ERR_UNSUPPORTED, "Rescale needs every prime: use ctpt_matmul");
+  if (needs_rowcorr(pb)) return fail(CTPT_ERR_UNSUPPORTED, "the fused kernel does not form row sums (u_offset != 0)");
   if (l < 0 || l >= d.L) return fail(CTPT_ERR_ARG, "prime index %d out of range", l);
   if (!d_ctmat || !d_plain || (!d_AU_l && d.rows_A > 0) || !d_BU_l) return fail(CTPT_ERR_ARG, "null device pointer");
   GemmArgs g{};
   g.limbs = nullptr;
+  g.u_unsigned = pb->u_unsigned;
   g.R = d.R;
   g.d = d;
   g.kU = pb->kU <= 0 ? 1 : pb->kU;
@@ -541,7 +601,7 @@ ctpt_status ctpt_matmul(const ctpt_problem* pb, const void* d_ctmat, const void*
   ctpt_status s = check_problem(pb, d);
   if (s != CTPT_OK) return s;
   if ((!d_AU && d.rows_A > 0) || !d_BU || !d_ctmat || !d_plain) return fail(CTPT_ERR_ARG, "null pointer");
-  const bool fused = fused_eligible(d, pb->kU <= 0 ? 1 : pb->kU);
+  const bool fused = fused_eligible(d, pb->kU <= 0 ? 1 : pb->kU, pb);
   if (!fused && !d_ws) return fail(CTPT_ERR_ARG, "null workspace");
   if (!fused || pb->rescale) {
     const size_t need = ws_bytes_needed(pb, d);
@@ -550,7 +610,7 @@ ctpt_status ctpt_matmul(const ctpt_problem* pb, const void* d_ctmat, const void*
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const uint32_t* X0 = reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(d_ctmat) + kHeader);
   uint32_t* xlast = pb->rescale
-                        ? reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(d_ws) + align256(ws_limb_bytes(d)))
+                        ? reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(d_ws) + ws_xlast_off(pb, d))
                         : nullptr;
   // one prime's product (fused skinny kernel, or split + limb GEMM) into the outputs `o`
   auto run = [&](int l, const OutParams& o) -> ctpt_status {
@@ -562,12 +622,15 @@ ctpt_status ctpt_matmul(const ctpt_problem* pb, const void* d_ctmat, const void*
     g.nplanes = pb->plain_per_prime ? d.L * g.kU : g.kU;
     g.plane0 = plane_index(pb, l, 0);
     g.p = pb->primes[l];
+    g.u_unsigned = pb->u_unsigned;
     g.o = o;
     const uint32_t* x = X0 + static_cast<int64_t>(l) * d.R * d.d2p;
     if (fused) return launch_fused(g, x, st);
-    ctpt_status s2 = launch_split(x, d.R * d.d2p, d_ws, st);
+    uint32_t* corr = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(d_ws) + ws_corr_off(d));
+    ctpt_status s2 = launch_split_prime(pb, x, d.R, d.d2p, g.p, d_ws, corr, st);
     if (s2 != CTPT_OK) return s2;
     g.limbs = d_ws;
+    if (needs_rowcorr(pb)) g.o.rowcorr = corr;
     return launch_gemm(g, st, false);
   };
   if (pb->rescale) {
@@ -616,7 +679,7 @@ namespace {
 
 struct HostPlan {
   int64_t chunk;  // rows of X per chunk (multiple of 64)
-  size_t in_bytes, cm_bytes, limb_bytes, out_bytes, total;
+  size_t in_bytes, cm_bytes, limb_bytes, out_bytes, corr_bytes, total;
 };
 
 HostPlan host_plan(const Dims& d, int64_t chunk_rows) {
@@ -631,7 +694,8 @@ HostPlan host_plan(const Dims& d, int64_t chunk_rows) {
   h.cm_bytes = align256(static_cast<size_t>(c) * d.d2p * 4);
   h.limb_bytes = align256(static_cast<size_t>(4) * c * d.d2p);
   h.out_bytes = align256(static_cast<size_t>(d.d3_loc) * c * 4);
-  h.total = 2 * h.in_bytes + h.cm_bytes + h.limb_bytes + 2 * h.out_bytes;
+  h.corr_bytes = align256(static_cast<size_t>(c) * 4);  // rowcorr of a chunk (unsigned-U mode)
+  h.total = 2 * h.in_bytes + h.cm_bytes + h.limb_bytes + 2 * h.out_bytes + h.corr_bytes;
   return h;
 }
 
@@ -694,6 +758,7 @@ ctpt_status ctpt_matmul_host(const ctpt_problem* pb, const uint32_t* h_a, const 
   void* limbs = w + 2 * hp.in_bytes + hp.cm_bytes;
   uint32_t* ob[2] = {reinterpret_cast<uint32_t*>(w + 2 * hp.in_bytes + hp.cm_bytes + hp.limb_bytes),
                      reinterpret_cast<uint32_t*>(w + 2 * hp.in_bytes + hp.cm_bytes + hp.limb_bytes + hp.out_bytes)};
+  uint32_t* corr = reinterpret_cast<uint32_t*>(w + 2 * hp.in_bytes + hp.cm_bytes + hp.limb_bytes + 2 * hp.out_bytes);
 
   StreamSet ss;
   CUDA_TRY(cudaStreamCreateWithFlags(&ss.h2d, cudaStreamNonBlocking));
@@ -716,7 +781,9 @@ ctpt_status ctpt_matmul_host(const ctpt_problem* pb, const uint32_t* h_a, const 
   g.planes = reinterpret_cast<const int8_t*>(static_cast<const uint8_t*>(d_plain) + kHeader);
   g.nplanes = pb->plain_per_prime ? d.L * g.kU : g.kU;
   g.limbs = limbs;
-  const bool fused = fused_eligible(d, g.kU);
+  g.u_unsigned = pb->u_unsigned;
+  if (needs_rowcorr(pb)) g.o.rowcorr = corr;
+  const bool fused = fused_eligible(d, g.kU, pb);
 
   int64_t it = 0;
   for (int l = 0; l < d.L; ++l) {
@@ -744,7 +811,7 @@ ctpt_status ctpt_matmul_host(const ctpt_problem* pb, const uint32_t* h_a, const 
       if (s != CTPT_OK) return s;
       CUDA_TRY(cudaEventRecord(in_free[b], sc));
       if (!fused) {
-        s = launch_split(cm, rows * d.d2p, limbs, sc);
+        s = launch_split_prime(pb, cm, rows, d.d2p, pb->primes[l], limbs, corr, sc);
         if (s != CTPT_OK) return s;
       }
       if (it >= 2) CUDA_TRY(cudaStreamWaitEvent(sc, out_free[b], 0));

@@ -45,6 +45,7 @@ struct FusedParams {
   int32_t plane;       // U digit plane (3rd TMA coordinate)
   int32_t num_kb;      // ceil(d2p / 128)
   int32_t num_tiles;   // ceil(R / 64)
+  int32_t u_unsigned;  // U plane is u8 (U + u_offset) instead of balanced s8 digits
   ModP m;
   OutParams o;         // d3_loc ≤ 128·NG
 };
@@ -117,7 +118,7 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_i8(128, FU_ACC_COLS, /*a_signed=*/true, /*b_signed=*/false);
+      const uint32_t idesc = idesc_i8(128, FU_ACC_COLS, /*a_signed=*/!P.u_unsigned, /*b_signed=*/false);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;

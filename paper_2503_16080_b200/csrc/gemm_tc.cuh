@@ -45,6 +45,7 @@ struct TcParams {
   int32_t tiles_j, tiles_r;
   int32_t num_tiles;
   int32_t group_j;    // tiles visited in groups of group_j j-tiles (L2 reuse of U panels)
+  int32_t u_unsigned; // U plane is u8 (U + u_offset) instead of balanced s8 digits
   ModP m;
   OutParams o;
 };
@@ -115,7 +116,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_i8(TC_BLOCK_J, TC_ACC_COLS, /*a_signed=*/true, /*b_signed=*/false);
+      const uint32_t idesc = idesc_i8(TC_BLOCK_J, TC_ACC_COLS, /*a_signed=*/!P.u_unsigned, /*b_signed=*/false);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;

@@ -112,7 +112,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer (leader only)
     if (rank == 0 && lane == 0) {
-      constexpr uint32_t idesc = idesc_i8(T2_BLOCK_J, T2_ACC_COLS, /*a_signed=*/true, /*b_signed=*/false);
+      const uint32_t idesc = idesc_i8(T2_BLOCK_J, T2_ACC_COLS, /*a_signed=*/!P.u_unsigned, /*b_signed=*/false);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;

@@ -113,6 +113,44 @@ __global__ void __launch_bounds__(256) k_split(const uint4* __restrict__ x, uint
   }
 }
 
+// The same split for the unsigned-U mode, one 256-thread block per row of X ([R][d2p]; c3: 64
+// residues per thread), which also forms rowcorr[r] = u_offset·Σ_k x[r][k] mod p (Σ < 2^47) for
+// the epilogue's correction.  Blocks per row keep the grid fine-grained (R blocks) so the
+// HBM-bound pass has no tail wave.
+__global__ void __launch_bounds__(256) k_split_rows(const uint4* __restrict__ x, uint4* __restrict__ limbs,
+                                                   uint32_t* __restrict__ rowcorr, int64_t R, int64_t d2p16,
+                                                   uint32_t p, uint32_t off_mod_p) {
+  __shared__ uint64_t part[8];
+  const int64_t n16 = R * d2p16;  // 16-element groups in the plane
+  for (int64_t r = blockIdx.x; r < R; r += gridDim.x) {
+    uint64_t sum = 0;
+    for (int64_t c = threadIdx.x; c < d2p16; c += blockDim.x) {
+      const int64_t g = r * d2p16 + c;
+      uint4 w[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) w[i] = __ldcs(x + 4 * g + i);
+      uint32_t o[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        sum += static_cast<uint64_t>(w[i].x) + w[i].y + w[i].z + w[i].w;
+        byte_transpose4(w[i].x, w[i].y, w[i].z, w[i].w, o[0][i], o[1][i], o[2][i], o[3][i]);
+      }
+#pragma unroll
+      for (int l = 0; l < 4; ++l) limbs[l * n16 + g] = make_uint4(o[l][0], o[l][1], o[l][2], o[l][3]);
+    }
+#pragma unroll
+    for (int s = 16; s; s >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, s);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint64_t t = 0;
+      for (int w = 0; w < (blockDim.x >> 5); ++w) t += part[w];
+      rowcorr[r] = static_cast<uint32_t>((t % p) * off_mod_p % p);
+    }
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------------------------------------------
 // Plaintext precompute (§8(a) a2): U int64 [d2][d3] → balanced int8 digits of the centred
 // residue, written transposed (U^T, K-major) as planes [kU][d3][d2p].
@@ -150,6 +188,8 @@ struct PlainParams {
   int64_t d2, d3, d2p;
   int32_t kU;
   int32_t rns;          // 0: shared planes from int64 U; 1: per-prime planes from residues
+  int32_t unsigned_plane;  // 1: one u8 plane holding U + u_offset ∈ [0, 255] (int64 mode, kU = 1)
+  int64_t u_offset;
   uint32_t p_arr[64];
 };
 
@@ -171,8 +211,12 @@ __global__ void __launch_bounds__(256) k_plain(const __grid_constant__ PlainPara
         x = P.u[k * P.d3 + j];
       }
     }
+    if (P.unsigned_plane) {
+      t[0][kk][tx] = (k < P.d2 && j < P.d3) ? static_cast<int8_t>(static_cast<uint8_t>(x + P.u_offset)) : 0;
+    } else {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) t[i][kk][tx] = (i < P.kU) ? balanced_digit(x) : 0;
+      for (int i = 0; i < 4; ++i) t[i][kk][tx] = (i < P.kU) ? balanced_digit(x) : 0;
+    }
   }
   __syncthreads();
   for (int jj = ty; jj < 32; jj += 8) {
@@ -201,6 +245,9 @@ struct OutParams {
   // per column [d3_loc][R] (stacked rows); out = (x − [x]_{p_L}) · p_L^{-1} mod p.
   const uint32_t* xlast;
   uint32_t p_last, p_last_inv;
+  // Unsigned-U mode (planes hold U' = U + u_offset ≥ 0): X·U = X·U' − u_offset·Σ_k X[r][k], so
+  // the epilogue subtracts rowcorr[r] = u_offset·Σ_k X[r][k] mod p (nullptr: nothing to subtract).
+  const uint32_t* rowcorr;
 };
 
 __device__ __forceinline__ uint32_t* out_ptr(const OutParams& o, int64_t j, int64_t r) {
@@ -217,8 +264,11 @@ __device__ __forceinline__ uint32_t rescale_last(uint32_t v, uint32_t xl, const 
   return barrett64(static_cast<uint64_t>(d) * o.p_last_inv, m);
 }
 
+__device__ __forceinline__ uint32_t sub_mod(uint32_t a, uint32_t b, uint32_t p) { return a >= b ? a - b : a + (p - b); }
+
 __device__ __forceinline__ void store_out(const OutParams& o, const ModP& m, int64_t j, int64_t r, uint32_t v) {
   uint32_t* q = out_ptr(o, j, r);
+  if (o.rowcorr) v = sub_mod(v, o.rowcorr[r], m.p);
   if (o.accumulate) v = accum_mod(*q, v, o.w, m);
   if (o.xlast) v = rescale_last(v, o.xlast[j * o.R + r], o, m);
   *q = v;
@@ -230,6 +280,17 @@ __device__ __forceinline__ void store16(const OutParams& o, const ModP& m, int64
   const bool in_a = (r0 + 15 < o.rows_A), in_b = (r0 >= o.rows_A);
   if (((o.rows_A & 3) == 0) && ((o.d1 & 3) == 0) && r0 + 15 < o.R && (in_a || in_b)) {
     uint4* q = reinterpret_cast<uint4*>(out_ptr(o, j, r0));
+    if (o.rowcorr) {
+      const uint4* rc = reinterpret_cast<const uint4*>(o.rowcorr + r0);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint4 c = rc[i];
+        res[4 * i] = sub_mod(res[4 * i], c.x, m.p);
+        res[4 * i + 1] = sub_mod(res[4 * i + 1], c.y, m.p);
+        res[4 * i + 2] = sub_mod(res[4 * i + 2], c.z, m.p);
+        res[4 * i + 3] = sub_mod(res[4 * i + 3], c.w, m.p);
+      }
+    }
     if (o.accumulate) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -268,6 +329,7 @@ struct SimtParams {
   const uint8_t* limbs;  // [4][R][d2p]
   const int8_t* uplane;  // [d3_total][d2p] plane for this pass
   int64_t R, d2, d2p, j_off;
+  int32_t u_unsigned;    // plane holds u8 values (U + u_offset)
   ModP m;
   OutParams o;
 };
@@ -280,7 +342,7 @@ __global__ void k_gemm_simt(const __grid_constant__ SimtParams P) {
   const int8_t* u = P.uplane + (P.j_off + j) * P.d2p;
   const int64_t plane = P.R * P.d2p;
   for (int64_t k = 0; k < P.d2; ++k) {
-    const int32_t uk = u[k];
+    const int32_t uk = P.u_unsigned ? static_cast<int32_t>(static_cast<uint8_t>(u[k])) : static_cast<int32_t>(u[k]);
 #pragma unroll
     for (int l = 0; l < 4; ++l) c[l] += static_cast<int32_t>(P.limbs[l * plane + r * P.d2p + k]) * uk;
   }

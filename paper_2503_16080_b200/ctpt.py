@@ -38,7 +38,8 @@ class Problem(ctypes.Structure):
     _fields_ = [("fmt", ctypes.c_int32), ("L", ctypes.c_int32), ("N", ctypes.c_int64), ("d1", ctypes.c_int64),
                 ("d2", ctypes.c_int64), ("d3", ctypes.c_int64), ("primes", ctypes.POINTER(ctypes.c_uint32)),
                 ("col_begin", ctypes.c_int64), ("col_end", ctypes.c_int64), ("kU", ctypes.c_int32),
-                ("plain_per_prime", ctypes.c_int32), ("rescale", ctypes.c_int32)]
+                ("plain_per_prime", ctypes.c_int32), ("rescale", ctypes.c_int32),
+                ("u_unsigned", ctypes.c_int32), ("u_offset", ctypes.c_int32)]
 
 
 class Sizes(ctypes.Structure):
@@ -57,6 +58,7 @@ _sig = {
     "ctpt_layout": (ctypes.c_int, [_PP, _P, _P, _P, ctypes.c_int, _P]),
     "ctpt_plain_precompute": (ctypes.c_int, [_PP, _P, _P, ctypes.POINTER(ctypes.c_int32), _P]),
     "ctpt_plain_precompute_rns": (ctypes.c_int, [_PP, _P, _P, ctypes.POINTER(ctypes.c_int32), _P]),
+    "ctpt_plain_precompute_unsigned": (ctypes.c_int, [_PP, _P, _P, ctypes.POINTER(ctypes.c_int32), _P]),
     "ctpt_matmul": (ctypes.c_int, [_PP, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
     "ctpt_split": (ctypes.c_int, [_PP, ctypes.c_int32, _P, _P, ctypes.c_size_t, _P]),
     "ctpt_gemm": (ctypes.c_int, [_PP, ctypes.c_int32, _P, ctypes.c_size_t, _P, _P, _P, _P]),
@@ -100,11 +102,14 @@ class Spec:
     kU: int = 1
     plain_per_prime: int = 0
     rescale: int = 0
+    u_unsigned: int = 0
+    u_offset: int = 0
 
     def cstruct(self) -> Problem:
         arr = (ctypes.c_uint32 * len(self.primes))(*[int(p) for p in self.primes])
         pb = Problem(self.fmt, len(self.primes), self.N, self.d1, self.d2, self.d3, arr, self.col_begin,
-                     self.col_end, self.kU, self.plain_per_prime, self.rescale)
+                     self.col_end, self.kU, self.plain_per_prime, self.rescale, self.u_unsigned,
+                     self.u_offset)
         pb._keep = arr  # keep the host prime array alive with the struct
         return pb
 
@@ -143,6 +148,15 @@ def plain_precompute(spec: Spec, U, plain, stream=None) -> int:
     kU = ctypes.c_int32(0)
     _check(_lib.ctpt_plain_precompute(ctypes.byref(pb), _ptr(U), _ptr(plain), ctypes.byref(kU), _stream(stream)))
     return kU.value
+
+
+def plain_precompute_unsigned(spec: Spec, U, plain, stream=None) -> int:
+    """One u8 plane U + u_offset (returns u_offset); raises CtptError(ERR_RANGE) when U spans > 255."""
+    pb = spec.cstruct()
+    off = ctypes.c_int32(0)
+    _check(_lib.ctpt_plain_precompute_unsigned(ctypes.byref(pb), _ptr(U), _ptr(plain), ctypes.byref(off),
+                                               _stream(stream)))
+    return off.value
 
 
 def plain_precompute_rns(spec: Spec, Ures, plain, stream=None) -> int:

@@ -45,23 +45,48 @@ class CpmmEngine:
         return self.ctmat
 
     # -- a2: plaintext precompute ------------------------------------------------------------
-    def precompute(self, U) -> int:
+    def precompute(self, U, unsigned: str = "auto") -> int:
+        """U's digit planes.  unsigned="auto" stores one u8 plane U + u_offset when the problem is
+        in the GEMM regime (d3_loc > 256: lower tensor-core switching power under the power cap)
+        and U spans ≤ 255 values; "never" forces balanced s8 digits; "always" requires the u8 plane."""
         Ud = U if isinstance(U, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(U, dtype=np.int64))
         Ud = Ud.to(self.device)
         self.spec.kU = 4  # size the buffer for the worst case first
+        self.spec.u_unsigned, self.spec.u_offset = 0, 0
         sz = ctpt.query_sizes(self.spec)
         self.plain = torch.empty(sz.plain_bytes, dtype=torch.uint8, device=self.device)
+        self.spec.plain_per_prime = 0
+        want_u8 = unsigned == "always" or (unsigned == "auto" and self.sizes.d3_loc > 256 and self.spec.d2 <= 33025)
+        if want_u8:
+            self.spec.kU = 1
+            try:
+                off = ctpt.plain_precompute_unsigned(self.spec, Ud, self.plain)
+                self.spec.u_unsigned, self.spec.u_offset = 1, off
+                self._resize_ws()
+                return 1
+            except ctpt.CtptError:
+                if unsigned == "always":
+                    raise
+                self.spec.kU = 4
         kU = ctpt.plain_precompute(self.spec, Ud, self.plain)
         self.spec.kU = kU
-        self.spec.plain_per_prime = 0
+        self._resize_ws()
         return kU
+
+    def _resize_ws(self):
+        """The workspace depends on the plane mode (row sums) — re-query once the mode is known."""
+        self.sizes = ctpt.query_sizes(self.spec)
+        if self.ws.numel() < self.sizes.workspace_bytes:
+            self.ws = torch.empty(self.sizes.workspace_bytes, dtype=torch.uint8, device=self.device)
 
     def precompute_rns(self, Ures) -> int:
         Ud = Ures if isinstance(Ures, torch.Tensor) else _u32_to_dev(Ures, self.device)
         self.plain = torch.empty(self.sizes.plain_rns_bytes, dtype=torch.uint8, device=self.device)
+        self.spec.u_unsigned, self.spec.u_offset = 0, 0
         kU = ctpt.plain_precompute_rns(self.spec, Ud, self.plain)
         self.spec.kU = kU
         self.spec.plain_per_prime = 1
+        self._resize_ws()
         return kU
 
     # -- a3–a6: the hot path -------------------------------------------------------------------

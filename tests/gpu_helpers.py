@@ -13,7 +13,7 @@ NTHREADS = os.cpu_count() or 8
 
 
 def run_gpu(fmt, N, d1, d2, d3, primes, a_polys, b_polys, U=None, Ures=None, col_begin=0, col_end=0, simt=False,
-            validate=True, rescale=0):
+            validate=True, rescale=0, unsigned="auto"):
     import torch
 
     from paper_2503_16080_b200 import ctpt
@@ -24,7 +24,7 @@ def run_gpu(fmt, N, d1, d2, d3, primes, a_polys, b_polys, U=None, Ures=None, col
     if Ures is not None:
         eng.precompute_rns(Ures)
     else:
-        eng.precompute(U)
+        eng.precompute(U, unsigned=unsigned)
     if simt:
         AU, BU = eng.alloc_outputs()
         L = len(primes)

@@ -38,13 +38,15 @@ SHAPES = [
 ]
 
 
-def _check(fmt, N, k, d2, d3, L, seed=0, u_bound=8, simt=False, col_begin=0, col_end=0):
+def _check(fmt, N, k, d2, d3, L, seed=0, u_bound=8, simt=False, col_begin=0, col_end=0, unsigned="auto",
+           U=None):
     d1 = N * k
     ps = ctgen.primes(L)
     ct = ctgen.encrypt(fmt, N, d1, d2, seed, 20, ps, nthreads=NTHREADS)
-    U = ctgen.U_matrix(seed, d2, d3, u_bound)
+    if U is None:
+        U = ctgen.U_matrix(seed, d2, d3, u_bound)
     (AU, BU), eng = run_gpu(fmt, N, d1, d2, d3, ps, ct.a_polys, ct.b_polys, U=U, simt=simt, col_begin=col_begin,
-                            col_end=col_end)
+                            col_end=col_end, unsigned=unsigned)
     c1 = col_end or d3
     cols = np.arange(col_begin, c1)
     for l, p in enumerate(ps):
@@ -70,7 +72,63 @@ def gemm_kernel(request, monkeypatch):
 def test_shapes_tcgen05(shape, gemm_kernel):
     if gemm_kernel == "fused" and shape[4] > 256:
         pytest.skip("d3 > 256 never takes the fused kernel")
-    _check(*shape)
+    _check(*shape, unsigned="never")
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "f%d_N%d_k%d_d2%d_d3%d_L%d" % s)
+def test_shapes_unsigned_U(shape, gemm_kernel):
+    """The unsigned-U plane (U + u_offset as u8, u8 × u8 MMAs, row-sum correction in the
+    epilogue) through both tensor-core kernels; the fused kernel only takes it with offset 0."""
+    if gemm_kernel == "fused":
+        pytest.skip("u_offset != 0 never takes the fused kernel")
+    _check(*shape, unsigned="always")
+
+
+@pytest.mark.parametrize("lo,hi", [(-128, 127), (0, 255), (3, 200), (-1, 0), (0, 0)])
+def test_unsigned_U_ranges(lo, hi, monkeypatch):
+    """u_offset = max(0, −min U) for every admissible span, incl. offset 0 (no correction; the
+    fused skinny kernel then runs u8 × u8) and U = 0."""
+    monkeypatch.delenv("CTPT_SKINNY", raising=False)
+    rng = np.random.default_rng(hi - lo)
+    for d3 in (100, 300):
+        U = rng.integers(lo, hi + 1, (260, d3)).astype(np.int64)
+        _check(A, 64, 3, 260, d3, 2, U=U, unsigned="always")
+
+
+def test_unsigned_U_refusals():
+    from paper_2503_16080_b200 import ctpt
+
+    fmt, N, d2 = R, 16, 64
+    ps = ctgen.primes(1)
+    ct = ctgen.encrypt(fmt, N, N, d2, 0, 20, ps)
+    with pytest.raises(ctpt.CtptError, match="ERR_RANGE"):
+        run_gpu(fmt, N, N, d2, 4, ps, ct.a_polys, ct.b_polys, U=np.full((d2, 4), 256, np.int64), unsigned="always")
+    with pytest.raises(ctpt.CtptError, match="ERR_RANGE"):
+        U = np.zeros((d2, 4), np.int64)
+        U[0, 0], U[1, 1] = -100, 200
+        run_gpu(fmt, N, N, d2, 4, ps, ct.a_polys, ct.b_polys, U=U, unsigned="always")
+    # "auto" falls back to balanced digits and stays exact
+    U = np.zeros((d2, 300), np.int64)
+    U[0, 0], U[1, 1] = -100, 200
+    (AU, BU), eng = run_gpu(fmt, N, N, d2, 300, ps, ct.a_polys, ct.b_polys, U=U)
+    assert eng.spec.u_unsigned == 0
+    wa, wb = oracle_outputs(fmt, N, N, ct.a_polys[0], ct.b_polys[0], U, ps[0])
+    assert np.array_equal(AU[0], wa) and np.array_equal(BU[0], wb)
+
+
+def test_unsigned_U_max_d2_bound():
+    """d2 = 33025 (the u8·u8 exactness limit) with every limb at 255 and U' at 255."""
+    fmt, N, d2, d3 = R, 16, 33025, 300
+    ps = ctgen.primes(1)
+    p = ps[0]
+    a = np.full((1, d2, N), (64 << 24) | 0xFFFFFF, np.uint32)
+    b = np.full((1, d2, N), p - 1, np.uint32)
+    U = np.full((d2, d3), 127, np.int64)
+    U[:, ::2] = -128
+    (AU, BU), eng = run_gpu(fmt, N, N, d2, d3, ps, a, b, U=U, unsigned="always")
+    assert eng.spec.u_unsigned == 1 and eng.spec.u_offset == 128
+    wa, wb = oracle_outputs(fmt, N, N, a[0], b[0], U, p)
+    assert np.array_equal(AU[0], wa) and np.array_equal(BU[0], wb)
 
 
 def test_column_shard_both_kernels(gemm_kernel):
@@ -263,6 +321,7 @@ def test_general_U_residues_rns():
     (A, 16, 2, 40, 7, 1, 8, 4096, (0, 0)),          # one chunk larger than R
     (S, 64, 3, 300, 256, 2, 8, 128, (0, 0)),        # fused skinny kernel on each chunk
     (R, 512, 1, 200, 600, 1, 8, 320, (100, 101)),   # d3_loc = 1 (CP-Mv) column shard
+    (A, 64, 4, 300, 520, 2, 8, 192, (0, 0)),        # unsigned-U plane: row sums per chunk
 ])
 def test_matmul_host_pipeline(fmt, N, k, d2, d3, L, u_bound, chunk, cols):
     """ctpt_matmul_host (host buffers, chunked 3-stream pipeline) == the oracle."""
