@@ -19,6 +19,7 @@ accumulation) as it stands, on the host cores, on a bounded sample of the same w
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import statistics
@@ -428,7 +429,7 @@ def run_sharded(args, rank: int, world: int, local_rank: int):
     specs, outs = [], []
     ws_bytes = 0
     for u in mine:
-        sp = ctpt.Spec(c.fmt, c.N, c.d1, c.d2, c.d3, [ps[u.l]], u.c0, u.c1, kU, 0)
+        sp = dataclasses.replace(eng.spec, primes=[ps[u.l]], col_begin=u.c0, col_end=u.c1)
         sz = ctpt.query_sizes(sp)
         specs.append(sp)
         outs.append((torch.empty(sz.out_AU_bytes // 4, dtype=torch.int32).pin_memory(),

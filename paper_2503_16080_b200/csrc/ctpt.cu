@@ -163,6 +163,21 @@ ctpt_status make_tmap_u8(CUtensorMap* m, const void* base, uint64_t dim0, uint64
   return CTPT_OK;
 }
 
+// 2-D tensor [dim1][dim0] of `esize`-byte elements, row pitch dim0·esize, no swizzle.
+ctpt_status make_tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, uint32_t esize, uint64_t dim0,
+                         uint64_t dim1, uint32_t box0, uint32_t box1) {
+  auto enc = get_encode();
+  if (!enc) return fail(CTPT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {dim0, dim1};
+  cuuint64_t strides[1] = {dim0 * esize};
+  cuuint32_t box[2] = {box0, box1};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CTPT_ERR_CUDA, "cuTensorMapEncodeTiled (2d) failed (%d)", static_cast<int>(r));
+  return CTPT_OK;
+}
+
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -182,9 +197,13 @@ ctpt_status tc_setup() {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_gemm_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, T2_SMEM_BYTES);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_gemm_fused<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(1));
+      e = cudaFuncSetAttribute(k_gemm_fused<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(1, false));
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_gemm_fused<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(2));
+      e = cudaFuncSetAttribute(k_gemm_fused<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(2, false));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_gemm_fused<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(1, true));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_gemm_fused<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(2, true));
   });
   if (e != cudaSuccess) return fail(CTPT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
   return CTPT_OK;
@@ -543,10 +562,19 @@ ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st) 
   P.o.accumulate = 0;
   P.o.w = 1;
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>(nt, num_sms()));
-  if (d.d3_loc <= 128)
-    k_gemm_fused<1><<<grid, FU_THREADS, fu_smem_bytes(1), st>>>(tmU, P);
-  else
-    k_gemm_fused<2><<<grid, FU_THREADS, fu_smem_bytes(2), st>>>(tmU, P);
+  // raw X by TMA (default) or by converter-thread loads (CTPT_FUSED_LOAD=regs, for A/B runs)
+  bool tma_x = true;
+  if (const char* e = getenv("CTPT_FUSED_LOAD")) tma_x = strcmp(e, "regs") != 0;
+  CUtensorMap tmX;
+  s = make_tmap_2d(&tmX, x, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, d.d2p, g.R, FU_BLOCK_K, FU_BLOCK_R);
+  if (s != CTPT_OK) return s;
+  if (d.d3_loc <= 128) {
+    if (tma_x) k_gemm_fused<1, true><<<grid, FU_THREADS, fu_smem_bytes(1, true), st>>>(tmU, tmX, P);
+    else k_gemm_fused<1, false><<<grid, FU_THREADS, fu_smem_bytes(1, false), st>>>(tmU, tmX, P);
+  } else {
+    if (tma_x) k_gemm_fused<2, true><<<grid, FU_THREADS, fu_smem_bytes(2, true), st>>>(tmU, tmX, P);
+    else k_gemm_fused<2, false><<<grid, FU_THREADS, fu_smem_bytes(2, false), st>>>(tmU, tmX, P);
+  }
   CUDA_TRY(cudaGetLastError());
   return CTPT_OK;
 }

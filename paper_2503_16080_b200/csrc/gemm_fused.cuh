@@ -34,9 +34,17 @@ constexpr int FU_THREADS = 512;
 constexpr int FU_CONV_WARP0 = 8;
 constexpr int FU_CONV_WARPS = 8;
 constexpr int FU_ROWS_PER_WARP = FU_BLOCK_R / FU_CONV_WARPS; // 8
-__host__ __device__ constexpr int fu_stages(int ng) { return ng == 1 ? 4 : 3; }
+constexpr int FU_RAW_BYTES = FU_BLOCK_R * FU_BLOCK_K * 4;   // one raw int32 X tile: 32 KB
+// Two ways to feed the converters (template TMA_X):
+//   false: each converter thread loads its residues into registers, two K-blocks ahead;
+//   true:  a TMA producer streams raw int32 X tiles into a ring of RAW stages (96–128 KB in
+//          flight per SM, no register cost) and converters read them with LDS.128.
+__host__ __device__ constexpr int fu_stages(int ng, bool tma_x) { return tma_x ? 2 : (ng == 1 ? 4 : 3); }
+__host__ __device__ constexpr int fu_raw_stages(int ng, bool tma_x) { return tma_x ? (ng == 1 ? 4 : 3) : 0; }
 __host__ __device__ constexpr int fu_stage_bytes(int ng) { return ng * FU_U_BYTES + FU_X_BYTES; }
-__host__ __device__ constexpr int fu_smem_bytes(int ng) { return fu_stages(ng) * fu_stage_bytes(ng) + 256 + 1024; }
+__host__ __device__ constexpr int fu_smem_bytes(int ng, bool tma_x) {
+  return fu_stages(ng, tma_x) * fu_stage_bytes(ng) + fu_raw_stages(ng, tma_x) * FU_RAW_BYTES + 256 + 1024;
+}
 
 struct FusedParams {
   const uint32_t* x;   // stacked K-major X of this prime (or chunk): [R][d2p] int32 residues
@@ -57,22 +65,28 @@ __device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
-template <int NG>
+template <int NG, bool TMA_X>
 __global__ void __launch_bounds__(FU_THREADS, 1)
-    k_gemm_fused(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ FusedParams P) {
-  constexpr int STAGES = fu_stages(NG);
+    k_gemm_fused(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmX,
+                 const __grid_constant__ FusedParams P) {
+  constexpr int STAGES = fu_stages(NG, TMA_X);
+  constexpr int RAW = fu_raw_stages(NG, TMA_X);
   constexpr int STAGE_BYTES = fu_stage_bytes(NG);
   constexpr int NBUF = (NG == 1) ? 2 : 1;  // accumulator buffers (NBUF·NG·256 ≤ 512 columns)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
-  const uint32_t bar_base = sbase + STAGES * STAGE_BYTES;
+  const uint32_t raw_base = sbase + STAGES * STAGE_BYTES;
+  const uint32_t bar_base = raw_base + RAW * FU_RAW_BYTES;
   auto full_bar = [&](int s) { return bar_base + 8u * s; };
   auto empty_bar = [&](int s) { return bar_base + 8u * (STAGES + s); };
   auto tfull_bar = [&](int b) { return bar_base + 8u * (2 * STAGES + b); };
   auto tempty_bar = [&](int b) { return bar_base + 8u * (2 * STAGES + 2 + b); };
   const uint32_t tmem_slot = bar_base + 8u * (2 * STAGES + 4);
-  uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(smem + STAGES * STAGE_BYTES + 8 * (2 * STAGES + 4));
+  uint32_t* tmem_slot_ptr =
+      reinterpret_cast<uint32_t*>(smem + STAGES * STAGE_BYTES + RAW * FU_RAW_BYTES + 8 * (2 * STAGES + 4));
+  auto raw_full = [&](int s) { return bar_base + 8u * (2 * STAGES + 5 + s); };
+  auto raw_empty = [&](int s) { return bar_base + 8u * (2 * STAGES + 5 + RAW + s); };
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -91,6 +105,11 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
       mbar_init(tfull_bar(b), 1);
       mbar_init(tempty_bar(b), 128);
     }
+    for (int s = 0; s < RAW; ++s) {
+      mbar_init(raw_full(s), 1);
+      mbar_init(raw_empty(s), FU_CONV_WARPS);
+    }
+    if (TMA_X) tma_prefetch(&tmX);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -146,6 +165,20 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
         if (++acc == NBUF) { acc = 0; acc_phase ^= 1; }
       }
     }
+  } else if (warp == 3) {
+    // ---------------------------------------------------------------- raw X TMA producer
+    if (TMA_X && lane == 0) {
+      int rs = 0;
+      uint32_t rphase = 0;
+      for (int64_t it = 0; it < n_it; ++it) {
+        const int32_t tr = static_cast<int32_t>(blockIdx.x) + static_cast<int32_t>(it / P.num_kb) * gridDim.x;
+        const int32_t kb = static_cast<int32_t>(it % P.num_kb);
+        mbar_wait(raw_empty(rs), rphase ^ 1);
+        mbar_arrive_expect_tx(raw_full(rs), FU_RAW_BYTES);
+        tma_load_2d(raw_base + rs * FU_RAW_BYTES, &tmX, raw_full(rs), kb * FU_BLOCK_K, tr * FU_BLOCK_R);
+        if (++rs == RAW) { rs = 0; rphase ^= 1; }
+      }
+    }
   } else if (warp >= 4 && warp < 8) {
     // ---------------------------------------------------------------- epilogue (128 threads)
     const int quad = warp & 3;
@@ -189,6 +222,38 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
     // of the K-block (one coalesced 512-B row segment per warp instruction).  Loads run two
     // iterations ahead of the stores (registers ra / rb).
     const int cw = warp - FU_CONV_WARP0;
+    if constexpr (TMA_X) {
+      int stage = 0, rs = 0;
+      uint32_t phase = 0, rphase = 0;
+      for (int64_t it = 0; it < n_it; ++it) {
+        mbar_wait(raw_full(rs), rphase);
+        uint4 r[FU_ROWS_PER_WARP];
+        const uint32_t sraw = raw_base + rs * FU_RAW_BYTES;
+#pragma unroll
+        for (int i = 0; i < FU_ROWS_PER_WARP; ++i) r[i] = lds128(sraw + (cw + FU_CONV_WARPS * i) * 512 + lane * 16);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(raw_empty(rs));  // values are in registers: the raw tile may refill
+        if (++rs == RAW) { rs = 0; rphase ^= 1; }
+        mbar_wait(empty_bar(stage), phase ^ 1);
+        const uint32_t sx = sbase + stage * STAGE_BYTES + NG * FU_U_BYTES;
+#pragma unroll
+        for (int i = 0; i < FU_ROWS_PER_WARP; ++i) {
+          const int row = cw + FU_CONV_WARPS * i;
+          uint32_t l0, l1, l2, l3;
+          byte_transpose4(r[i].x, r[i].y, r[i].z, r[i].w, l0, l1, l2, l3);
+          const uint32_t off =
+              static_cast<uint32_t>(row) * 128u + ((((lane >> 2) ^ (row & 7)) << 4) | ((lane & 3) << 2));
+          sts32(sx + 0 * FU_BLOCK_R * 128 + off, l0);
+          sts32(sx + 1 * FU_BLOCK_R * 128 + off, l1);
+          sts32(sx + 2 * FU_BLOCK_R * 128 + off, l2);
+          sts32(sx + 3 * FU_BLOCK_R * 128 + off, l3);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(full_bar(stage));
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    } else {
     auto load = [&](int64_t it, uint4 (&r)[FU_ROWS_PER_WARP]) {
       const int32_t tr = static_cast<int32_t>(blockIdx.x) + static_cast<int32_t>(it / P.num_kb) * gridDim.x;
       const int64_t k = static_cast<int64_t>(it % P.num_kb) * FU_BLOCK_K + 4 * lane;
@@ -231,6 +296,7 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
         store(rb);
         if (it + 3 < n_it) load(it + 3, rb);
       }
+    }
     }
   }
 

@@ -13,6 +13,8 @@ Layout of the gathered result on rank 0 (the single-GPU layout of ctpt_matmul):
 """
 from __future__ import annotations
 
+import dataclasses
+
 from dataclasses import dataclass
 from typing import Callable
 
@@ -108,7 +110,8 @@ def gpu_compute_fn(fmt: int, N: int, d1: int, d2: int, d3: int, primes: list, ge
             eng.precompute(U)
             cache[key] = eng
         base = cache[key]
-        spec = ctpt.Spec(fmt, N, d1, d2, d3, [primes[u.l]], u.c0, u.c1, base.spec.kU, 0)
+        # the unit's column block of the base problem (keeps the plane mode: kU, u_unsigned, u_offset)
+        spec = dataclasses.replace(base.spec, col_begin=u.c0, col_end=u.c1)
         sizes = ctpt.query_sizes(spec)
         AU = torch.empty(sizes.out_AU_bytes // 4, dtype=torch.int32, device=device)
         BU = torch.empty(sizes.out_BU_bytes // 4, dtype=torch.int32, device=device)

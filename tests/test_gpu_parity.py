@@ -152,9 +152,12 @@ SKINNY = [
 ]
 
 
+@pytest.mark.parametrize("load", ["tma", "regs"])
 @pytest.mark.parametrize("shape", SKINNY, ids=lambda s: "f%d_N%d_k%d_d2%d_d3%d_L%d" % s)
-def test_skinny_fused(shape, monkeypatch):
+def test_skinny_fused(shape, load, monkeypatch):
+    """Both ways of feeding the fused kernel's converters: raw X tiles by TMA, or register loads."""
     monkeypatch.delenv("CTPT_SKINNY", raising=False)
+    monkeypatch.setenv("CTPT_FUSED_LOAD", load)
     _check(*shape)
 
 

@@ -33,7 +33,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--d3", default="1,64,128,256")
-    ap.add_argument("--paths", default="fused,split+gemm")
+    ap.add_argument("--paths", default="fused,fused-regs,split+gemm")
     args = ap.parse_args()
 
     import torch
@@ -67,10 +67,12 @@ def main():
         BU = torch.empty(sz.out_BU_bytes // 4, dtype=torch.int32, device="cuda")
         ra = sz.rows_A
         for path in args.paths.split(","):
+            os.environ["CTPT_FUSED_LOAD"] = "regs" if path == "fused-regs" else "tma"
+
             def step(evs=None):
                 for l in range(len(ps)):
                     au, bu = AU[l * d3 * ra:], BU[l * d3 * c.d1:]
-                    if path == "fused":
+                    if path.startswith("fused"):
                         if evs is not None:
                             evs[l][0].record(stream)
                         ctpt.gemm_fused(sp, l, eng.ctmat, eng.plain, au, bu, stream=stream)
@@ -101,7 +103,7 @@ def main():
             print(json.dumps({
                 "sweep": "skinny", "path": path, "d3": d3, "L": len(ps), "R": R, "d2": d2,
                 "ms_per_step": ms_step, "residue_macs_per_s": macs / (ms_step / 1e3),
-                "kernel": "k_gemm_fused" if path == "fused" else "k_gemm_tc (after k_split)",
+                "kernel": ("k_gemm_fused" if path.startswith("fused") else "k_gemm_tc (after k_split)"),
                 "avg_launch_ms": k_ms,
                 "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
                              "frac": gbs / hbm_peak, "per_launch_bytes": alg_bytes},
