@@ -48,6 +48,10 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target seconds of oracle work per sample")
+    ap.add_argument("--rescale", action="store_true",
+                    help="Algorithm 6 with step 2 (SURVEY.md §8(f) row 3): U real uniform[-1,1) encoded at "
+                         "Δ_U = the last prime (per-prime residues, kU = 4), RNS Rescale by that prime "
+                         "fused into the other primes' epilogues")
     ap.add_argument("--shard", action="store_true",
                     help="strong scaling: shard ONE problem's (prime, column) units over the ranks "
                          "(shard.plan_units); host-resident inputs/outputs via ctpt_matmul_host")
@@ -131,18 +135,20 @@ def cpu_oracle_rate(c, ct, U, target_s: float):
     cores = os.cpu_count() or 1
     p = ct.primes[0]
     ra = c.rows_A
-    Ac = ct.a_polys[0].reshape(c.d2, ra)
+    Ac = ct.a_polys[0].reshape(c.d2, ra) if ra else None  # structured-A: only B·U (Algorithm 7)
     Bc = ct.b_polys[0].reshape(c.d2, c.d1)
     ncols = max(1, min(cores, c.d3))
     t0 = time.perf_counter()
-    oracle.modmatmul(Ac, U, p, cols=np.arange(ncols), nthreads=cores)
+    if Ac is not None:
+        oracle.modmatmul(Ac, U, p, cols=np.arange(ncols), nthreads=cores)
     oracle.modmatmul(Bc, U, p, cols=np.arange(ncols), nthreads=cores)
     dt = time.perf_counter() - t0
     # scale the sample to ~target_s of work
     ncols2 = int(min(c.d3, max(ncols, ncols * target_s / max(dt, 1e-3))))
     ncols2 = max(cores, (ncols2 // cores) * cores) if ncols2 >= cores else ncols2
     t0 = time.perf_counter()
-    oracle.modmatmul(Ac, U, p, cols=np.arange(ncols2), nthreads=cores)
+    if Ac is not None:
+        oracle.modmatmul(Ac, U, p, cols=np.arange(ncols2), nthreads=cores)
     oracle.modmatmul(Bc, U, p, cols=np.arange(ncols2), nthreads=cores)
     dt = time.perf_counter() - t0
     macs = c.R * c.d2 * ncols2
@@ -174,12 +180,13 @@ def run_reference(args, rank: int):
     import oracle
 
     p = ps[0]
-    Ac = ct.a_polys[0].reshape(c.d2, c.rows_A)
+    Ac = ct.a_polys[0].reshape(c.d2, c.rows_A) if c.rows_A else None
     Bc = ct.b_polys[0].reshape(c.d2, c.d1)
     # size each step to ~ (a few minutes / (steps + warmup)) of CPU work
     budget = min(20.0, 150.0 / max(1, args.steps + args.warmup))
     t0 = time.perf_counter()
-    oracle.modmatmul(Ac, U, p, cols=np.arange(cores), nthreads=cores)
+    if Ac is not None:
+        oracle.modmatmul(Ac, U, p, cols=np.arange(cores), nthreads=cores)
     oracle.modmatmul(Bc, U, p, cols=np.arange(cores), nthreads=cores)
     per_col = (time.perf_counter() - t0) / cores
     ncols = int(max(1, min(c.d3, budget / max(per_col, 1e-6))))
@@ -188,7 +195,8 @@ def run_reference(args, rank: int):
         j0 = (i * ncols) % max(1, c.d3 - ncols + 1)
         cols = np.arange(j0, j0 + ncols)
         t0 = time.perf_counter()
-        oracle.modmatmul(Ac, U, p, cols=cols, nthreads=cores)
+        if Ac is not None:
+            oracle.modmatmul(Ac, U, p, cols=cols, nthreads=cores)
         oracle.modmatmul(Bc, U, p, cols=cols, nthreads=cores)
         if i >= args.warmup:
             times.append(time.perf_counter() - t0)
@@ -222,22 +230,41 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     seed = c.seed + rank
     ps, ct, U, gen_s = make_inputs(c, seed, max(1, cores // world))
 
-    eng = CpmmEngine(ctpt.Spec(c.fmt, c.N, c.d1, c.d2, c.d3, ps), dev)
+    eng = CpmmEngine(ctpt.Spec(c.fmt, c.N, c.d1, c.d2, c.d3, ps, rescale=int(args.rescale)), dev)
     a_dev = torch.from_numpy(ct.a_polys.view(np.int32)).to(dev)
     b_dev = torch.from_numpy(ct.b_polys.view(np.int32)).to(dev)
     eng.layout(a_dev, b_dev, validate=True)
-    kU = eng.precompute(U)
+    if args.rescale:
+        _, U0 = ctgen.U_real(seed, c.d2, c.d3, ps[-1], nthreads=cores)
+        kU = eng.precompute_rns(np.stack([(U0 % int(p)).astype(np.uint32) for p in ps]))
+        del U0
+    else:
+        kU = eng.precompute(U)
     AU, BU = eng.alloc_outputs()
     spec, sizes = eng.spec, eng.sizes
     stream = torch.cuda.current_stream(dev)
     d3l, ra = sizes.d3_loc, sizes.rows_A
+    fused = (d3l <= 256 and kU == 1 and not (spec.u_unsigned and spec.u_offset)
+             and os.environ.get("CTPT_SKINNY") != "off" and not args.rescale)
+    n_ev = 1 if args.rescale else len(ps)
 
     def step(ev_pairs=None):
+        if args.rescale:  # the whole ctpt_matmul: last prime first, Rescale in the others' epilogues
+            if ev_pairs is not None:
+                ev_pairs[0][0].record(stream)
+            ctpt.matmul(spec, eng.ctmat, eng.plain, AU, BU, eng.ws, stream=stream)
+            if ev_pairs is not None:
+                ev_pairs[0][1].record(stream)
+            return
         for l in range(len(ps)):
-            ctpt.split(spec, l, eng.ctmat, eng.ws, stream=stream)
+            if not fused:
+                ctpt.split(spec, l, eng.ctmat, eng.ws, stream=stream)
             if ev_pairs is not None:
                 ev_pairs[l][0].record(stream)
-            ctpt.gemm(spec, l, eng.ws, eng.plain, AU[l * d3l * ra:], BU[l * d3l * c.d1:], stream=stream)
+            if fused:
+                ctpt.gemm_fused(spec, l, eng.ctmat, eng.plain, AU[l * d3l * ra:], BU[l * d3l * c.d1:], stream=stream)
+            else:
+                ctpt.gemm(spec, l, eng.ws, eng.plain, AU[l * d3l * ra:], BU[l * d3l * c.d1:], stream=stream)
             if ev_pairs is not None:
                 ev_pairs[l][1].record(stream)
 
@@ -246,7 +273,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     torch.cuda.synchronize(dev)
 
     # ------------------------------------------------ timed region (device-resident inputs)
-    gemm_ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in ps]
+    gemm_ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_ev)]
                for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
@@ -276,9 +303,13 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     # ------------------------------------------------ roofline of the dominant kernel (k_gemm_tc)
     mp, which = peaks()
     gemm_avg_s = statistics.mean(gemm_ms) / 1e3
-    limb_macs_launch = 4 * kU * c.R * c.d2 * c.d3
+    limb_macs_launch = 4 * kU * c.R * c.d2 * c.d3 * (len(ps) if args.rescale else 1)
     achieved_tops = 2 * limb_macs_launch / gemm_avg_s / 1e12
-    peak_tops = 2 * float(mp["bf16_tflops_sustained"])  # int8 = 2 x bf16 (guide's nominal ratio), sustained
+    # int8 = 2 x bf16 (the guide's nominal ratio).  Burst peak for a timed region shorter than
+    # MEASURED_PEAKS' 4-s sustained loop (the clocks have not settled at the power cap yet),
+    # sustained peak for longer runs.
+    peak_key = "bf16_tflops" if elapsed_ms < 2000.0 else "bf16_tflops_sustained"
+    peak_tops = 2 * float(mp[peak_key])
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "gemm_dram_bytes.json")) as f:
@@ -287,7 +318,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         pass
 
     # ------------------------------------------------ end to end through the ABI (host buffers)
-    e2e = run_e2e(args, c, ps, ct, eng, dev, stream)
+    e2e = (run_e2e(args, c, ps, ct, eng, dev, stream) if not args.rescale else
+           {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+            "note": "ctpt_matmul_host does not Rescale; no host-buffer path for this workload"})
 
     gemm_share = sum(gemm_ms) / elapsed_ms
     result = {
@@ -301,13 +334,21 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "u_plane": (f"u8: U+{eng.spec.u_offset} (ctpt_plain_precompute_unsigned)" if eng.spec.u_unsigned
                         else "s8 balanced digits")}),
         "pct_int8_datasheet": 100.0 * value * 4 * kU / world / INT8_DATASHEET_MACS,
-        "roofline": {"bound": "tensor", "achieved": achieved_tops, "peak": peak_tops, "unit": "TOP/s",
-                     "frac": achieved_tops / peak_tops, "traffic": traffic,
-                     "kernel": "k_gemm_tc", "peak_source": f"{which}: 2 x bf16_tflops_sustained (int8/bf16 nominal 2x)",
-                     "per_launch": f"{limb_macs_launch:.4e} limb MACs (4·kU·R·d2·d3, one prime)",
+        "rescale": bool(args.rescale),
+        "vs_cublaslt_int8": cublaslt_ratio(value * 4 * kU / world, elapsed_ms),
+        "roofline": roofline_fused(c, d3l, gemm_avg_s, gemm_share, mp, which) if fused else {
+                     "bound": "tensor", "achieved": achieved_tops, "peak": peak_tops, "unit": "TOP/s",
+                     "frac": achieved_tops / peak_tops, "traffic": traffic if not args.rescale else None,
+                     "kernel": ("ctpt_matmul: k_split + kU passes of k_gemm_tc per prime, Rescale epilogue"
+                                if args.rescale else "k_gemm_tc"),
+                     "peak_source": f"{which}: 2 x {peak_key} (int8/bf16 nominal 2x; timed region "
+                                    f"{elapsed_ms / 1e3:.2f} s)",
+                     "per_launch": (f"{limb_macs_launch:.4e} limb MACs (4·kU·R·d2·d3 · L, whole step)" if args.rescale
+                                    else f"{limb_macs_launch:.4e} limb MACs (4·kU·R·d2·d3, one prime)"),
                      "avg_launch_ms": gemm_avg_s * 1e3, "share_of_step": gemm_share},
         "e2e": e2e,
-        "gpu_launches": (1 + kU) * len(ps) * args.steps,  # per prime: k_split[_rows] + kU x k_gemm_tc
+        # per prime: k_split[_rows] + kU x k_gemm_tc, or one k_gemm_fused
+        "gpu_launches": (1 if fused else 1 + kU) * len(ps) * args.steps,
         "clocks": clocks,
         "input_generation_s": gen_s,
     }
@@ -315,6 +356,30 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         result["cpu_baseline"] = cpu_oracle_rate(c, ct, U, args.cpu_seconds)
     if rank == 0:
         print(json.dumps(result))
+
+
+def cublaslt_ratio(limb_macs_per_s: float, elapsed_ms: float):
+    """Our limb-MAC rate ÷ the measured cuBLASLt int8 GEMM rate (torch._int_mm 16384³,
+    profiles/r01/int8_cublaslt_probe.json, tools/int8_probe.py): burst for short timed regions,
+    sustained (4 s back to back) for long ones — the "measured INT8 ceiling" of SURVEY.md §8(d)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "int8_cublaslt_probe.json")) as f:
+            pr = json.load(f)
+    except OSError:
+        return None
+    key = "burst_tops" if elapsed_ms < 2000.0 else "sustained_tops"
+    return {"ratio": 2 * limb_macs_per_s / 1e12 / float(pr[key]), "cublaslt_tops": pr[key], "which": key}
+
+
+def roofline_fused(c, d3l, launch_s, share, mp, which):
+    """HBM roofline of k_gemm_fused (skinny U): algorithmic bytes per launch (one prime) = 4·R·d2
+    (X int32, read once) + d3·d2 (U digits) + 4·R·d3 (outputs)."""
+    alg = 4 * c.R * c.d2 + d3l * c.d2 + 4 * c.R * d3l
+    gbs = alg / launch_s / 1e9
+    return {"bound": "hbm", "achieved": gbs, "peak": float(mp["hbm_gbs"]), "unit": "GB/s",
+            "frac": gbs / float(mp["hbm_gbs"]), "traffic": None, "kernel": "k_gemm_fused",
+            "peak_source": f"{which}: hbm_gbs", "per_launch": f"{alg} algorithmic bytes (4·R·d2 + d3·d2 + 4·R·d3)",
+            "avg_launch_ms": launch_s * 1e3, "share_of_step": share}
 
 
 def pcie_bandwidth(dev, nbytes: int = 1 << 30) -> dict:
@@ -364,7 +429,7 @@ def run_e2e(args, c, ps, ct, eng, dev, stream):
 
     a_h = torch.from_numpy(ct.a_polys.view(np.int32)).pin_memory()
     b_h = torch.from_numpy(ct.b_polys.view(np.int32)).pin_memory()
-    AU_h = torch.empty(eng.sizes.out_AU_bytes // 4, dtype=torch.int32).pin_memory()
+    AU_h = torch.empty(max(1, eng.sizes.out_AU_bytes // 4), dtype=torch.int32).pin_memory()
     BU_h = torch.empty(eng.sizes.out_BU_bytes // 4, dtype=torch.int32).pin_memory()
     # free the device-resident copies of the first leg; the host path stages chunks itself
     eng.ctmat = None
@@ -384,8 +449,8 @@ def run_e2e(args, c, ps, ct, eng, dev, stream):
     t1.record(stream)
     torch.cuda.synchronize(dev)
     ms = t0.elapsed_time(t1) / args.e2e_steps
-    h2d = a_h.numel() * 4 + b_h.numel() * 4
-    d2h = AU_h.numel() * 4 + BU_h.numel() * 4
+    h2d = (a_h.numel() * 4 if eng.sizes.rows_A else 0) + b_h.numel() * 4  # structured-A: Ã is not read
+    d2h = eng.sizes.out_AU_bytes + eng.sizes.out_BU_bytes
     bw = pcie_bandwidth(dev)
     floor_ms = max(h2d / bw["h2d_concurrent_gbs"], d2h / bw["d2h_concurrent_gbs"]) / 1e6
     return {"value": c.residue_macs / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

@@ -231,9 +231,6 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
         const uint32_t sraw = raw_base + rs * FU_RAW_BYTES;
 #pragma unroll
         for (int i = 0; i < FU_ROWS_PER_WARP; ++i) r[i] = lds128(sraw + (cw + FU_CONV_WARPS * i) * 512 + lane * 16);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(raw_empty(rs));  // values are in registers: the raw tile may refill
-        if (++rs == RAW) { rs = 0; rphase ^= 1; }
         mbar_wait(empty_bar(stage), phase ^ 1);
         const uint32_t sx = sbase + stage * STAGE_BYTES + NG * FU_U_BYTES;
 #pragma unroll
@@ -248,10 +245,18 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
           sts32(sx + 2 * FU_BLOCK_R * 128 + off, l2);
           sts32(sx + 3 * FU_BLOCK_R * 128 + off, l3);
         }
+        // The raw tile goes back to the TMA producer only after its values were consumed (the STS
+        // above depend on them) and behind a proxy fence: a generic read followed by an
+        // async-proxy (TMA) write of the same bytes.  Releasing it right after issuing the LDS
+        // corrupted rows intermittently (measured: whole output rows wrong when K ≥ 32 blocks).
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(full_bar(stage));
+        if (lane == 0) {
+          mbar_arrive(full_bar(stage));
+          mbar_arrive(raw_empty(rs));
+        }
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        if (++rs == RAW) { rs = 0; rphase ^= 1; }
       }
     } else {
     auto load = [&](int64_t it, uint4 (&r)[FU_ROWS_PER_WARP]) {

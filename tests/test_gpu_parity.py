@@ -161,6 +161,18 @@ def test_skinny_fused(shape, load, monkeypatch):
     _check(*shape)
 
 
+@pytest.mark.parametrize("load", ["tma", "regs"])
+def test_skinny_long_k_ring_wraparound(load, monkeypatch):
+    """Long K (33–65 k-blocks per tile) wraps the raw-X and limb rings many times; a premature
+    release of a raw tile once corrupted whole output rows intermittently — run it repeatedly."""
+    monkeypatch.delenv("CTPT_SKINNY", raising=False)
+    monkeypatch.setenv("CTPT_FUSED_LOAD", load)
+    for rep in range(3):
+        _check(A, 256, 2, 4112, 64, 1, seed=rep)
+        _check(S, 128, 3, 8200, 100, 1, seed=rep)
+        _check(R, 512, 1, 4096, 256, 1, seed=rep)
+
+
 def test_skinny_fused_direct_entry_point():
     """ctpt_gemm_fused per prime (the stage entry point) == the oracle; and it refuses
     d3_loc > 256 with ERR_UNSUPPORTED."""
