@@ -565,6 +565,9 @@ ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st) 
   // raw X by TMA (default) or by converter-thread loads (CTPT_FUSED_LOAD=regs, for A/B runs)
   bool tma_x = true;
   if (const char* e = getenv("CTPT_FUSED_LOAD")) tma_x = strcmp(e, "regs") != 0;
+  // L2 prefetch distance for the raw X ring (iterations ahead of the TMA into shared memory)
+  P.l2_prefetch = 4;
+  if (const char* e = getenv("CTPT_FUSED_PF")) P.l2_prefetch = std::max(0, atoi(e));
   CUtensorMap tmX;
   s = make_tmap_2d(&tmX, x, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, d.d2p, g.R, FU_BLOCK_K, FU_BLOCK_R);
   if (s != CTPT_OK) return s;

@@ -54,6 +54,7 @@ struct FusedParams {
   int32_t num_kb;      // ceil(d2p / 128)
   int32_t num_tiles;   // ceil(R / 64)
   int32_t u_unsigned;  // U plane is u8 (U + u_offset) instead of balanced s8 digits
+  int32_t l2_prefetch; // raw X tiles prefetched into L2 this many iterations ahead of their TMA (0: off)
   ModP m;
   OutParams o;         // d3_loc ≤ 128·NG
 };
@@ -170,9 +171,23 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
     if (TMA_X && lane == 0) {
       int rs = 0;
       uint32_t rphase = 0;
+      auto coords = [&](int64_t it, int32_t& c0, int32_t& c1) {
+        c1 = (static_cast<int32_t>(blockIdx.x) + static_cast<int32_t>(it / P.num_kb) * gridDim.x) * FU_BLOCK_R;
+        c0 = static_cast<int32_t>(it % P.num_kb) * FU_BLOCK_K;
+      };
+      for (int64_t it = 0; it < P.l2_prefetch && it < n_it; ++it) {
+        int32_t c0, c1;
+        coords(it, c0, c1);
+        tma_prefetch_l2_2d(&tmX, c0, c1);
+      }
       for (int64_t it = 0; it < n_it; ++it) {
         const int32_t tr = static_cast<int32_t>(blockIdx.x) + static_cast<int32_t>(it / P.num_kb) * gridDim.x;
         const int32_t kb = static_cast<int32_t>(it % P.num_kb);
+        if (P.l2_prefetch > 0 && it + P.l2_prefetch < n_it) {
+          int32_t c0, c1;
+          coords(it + P.l2_prefetch, c0, c1);
+          tma_prefetch_l2_2d(&tmX, c0, c1);
+        }
         mbar_wait(raw_empty(rs), rphase ^ 1);
         mbar_arrive_expect_tx(raw_full(rs), FU_RAW_BYTES);
         tma_load_2d(raw_base + rs * FU_RAW_BYTES, &tmX, raw_full(rs), kb * FU_BLOCK_K, tr * FU_BLOCK_R);
@@ -227,36 +242,38 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
       uint32_t phase = 0, rphase = 0;
       for (int64_t it = 0; it < n_it; ++it) {
         mbar_wait(raw_full(rs), rphase);
-        uint4 r[FU_ROWS_PER_WARP];
         const uint32_t sraw = raw_base + rs * FU_RAW_BYTES;
+        uint32_t lw[FU_ROWS_PER_WARP][4];
 #pragma unroll
-        for (int i = 0; i < FU_ROWS_PER_WARP; ++i) r[i] = lds128(sraw + (cw + FU_CONV_WARPS * i) * 512 + lane * 16);
+        for (int i = 0; i < FU_ROWS_PER_WARP; ++i) {
+          const uint4 v = lds128(sraw + (cw + FU_CONV_WARPS * i) * 512 + lane * 16);
+          byte_transpose4(v.x, v.y, v.z, v.w, lw[i][0], lw[i][1], lw[i][2], lw[i][3]);
+        }
+        // Hand the raw tile back to the TMA producer as soon as its values are CONSUMED (the
+        // byte transposes above depend on every LDS), behind a proxy fence (a generic read
+        // followed by an async-proxy write of the same bytes), and before waiting for a free limb
+        // stage — so the raw ring keeps streaming while the MMAs drain.  Releasing it right after
+        // merely issuing the LDS corrupted whole output rows intermittently (K ≥ 32 blocks).
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(raw_empty(rs));
+        if (++rs == RAW) { rs = 0; rphase ^= 1; }
         mbar_wait(empty_bar(stage), phase ^ 1);
         const uint32_t sx = sbase + stage * STAGE_BYTES + NG * FU_U_BYTES;
 #pragma unroll
         for (int i = 0; i < FU_ROWS_PER_WARP; ++i) {
           const int row = cw + FU_CONV_WARPS * i;
-          uint32_t l0, l1, l2, l3;
-          byte_transpose4(r[i].x, r[i].y, r[i].z, r[i].w, l0, l1, l2, l3);
           const uint32_t off =
               static_cast<uint32_t>(row) * 128u + ((((lane >> 2) ^ (row & 7)) << 4) | ((lane & 3) << 2));
-          sts32(sx + 0 * FU_BLOCK_R * 128 + off, l0);
-          sts32(sx + 1 * FU_BLOCK_R * 128 + off, l1);
-          sts32(sx + 2 * FU_BLOCK_R * 128 + off, l2);
-          sts32(sx + 3 * FU_BLOCK_R * 128 + off, l3);
+          sts32(sx + 0 * FU_BLOCK_R * 128 + off, lw[i][0]);
+          sts32(sx + 1 * FU_BLOCK_R * 128 + off, lw[i][1]);
+          sts32(sx + 2 * FU_BLOCK_R * 128 + off, lw[i][2]);
+          sts32(sx + 3 * FU_BLOCK_R * 128 + off, lw[i][3]);
         }
-        // The raw tile goes back to the TMA producer only after its values were consumed (the STS
-        // above depend on them) and behind a proxy fence: a generic read followed by an
-        // async-proxy (TMA) write of the same bytes.  Releasing it right after issuing the LDS
-        // corrupted rows intermittently (measured: whole output rows wrong when K ≥ 32 blocks).
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(full_bar(stage));
-          mbar_arrive(raw_empty(rs));
-        }
+        if (lane == 0) mbar_arrive(full_bar(stage));
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        if (++rs == RAW) { rs = 0; rphase ^= 1; }
       }
     } else {
     auto load = [&](int64_t it, uint4 (&r)[FU_ROWS_PER_WARP]) {

@@ -68,6 +68,10 @@ def main():
         ra = sz.rows_A
         for path in args.paths.split(","):
             os.environ["CTPT_FUSED_LOAD"] = "regs" if path == "fused-regs" else "tma"
+            if path.startswith("fused-pf"):  # fused-pf<N>: L2 prefetch distance N
+                os.environ["CTPT_FUSED_PF"] = path[len("fused-pf"):]
+            else:
+                os.environ.pop("CTPT_FUSED_PF", None)
 
             def step(evs=None):
                 for l in range(len(ps)):
