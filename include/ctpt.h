@@ -188,6 +188,27 @@ ctpt_status ctpt_gemm(const ctpt_problem* prob, int32_t l, const void* d_ws, siz
 ctpt_status ctpt_gemm_fused(const ctpt_problem* prob, int32_t l, const void* d_ctmat, const void* d_plain,
                             uint32_t* d_AU_l, uint32_t* d_BU_l, void* stream);
 
+/* Mod-PP-MM_{q; M, K, Nc} in RNS — the paper's plaintext modular product (notation P:1685,
+ * "Mod-PP-MM_{q; d1,d2,d3}"), which CC-MM (Alg. 8: "≈ 12 fp-PP-MM calls",
+ * P:1599) and the RGSW product (Alg. 9) reduce to, with operands that are full
+ * residues on BOTH sides:  Z = X·Y mod p for every prime p of `primes` (q = Π p).
+ *   d_X:   uint32 [L][M][ldx] row-major canonical residues, ldx = K rounded up to 16 (from
+ *          ctpt_modmatmul_sizes), the padding columns zero.  Read directly (no layout pass).
+ *   d_Y:   uint32 [L][K][Nc] row-major canonical residues; ctpt_modmatmul_precompute turns it
+ *          into per-prime balanced-digit planes in d_plain (4 digits: 16 limb MACs per residue
+ *          MAC) — done once when Y is reused (synchronises).
+ *   d_ZT:  uint32 [L][Nc][M]: Z TRANSPOSED (column j of Z contiguous), like every output here.
+ *   d_ws:  ws_bytes from ctpt_modmatmul_sizes.
+ * Exact (Lemma le:strategy1 with K = 2^8): K ≤ 65793, else CTPT_ERR_OVERFLOW.  Never
+ * synchronises.  Same kernels as ctpt_matmul (the degenerate format "structured-A, N = 1"). */
+ctpt_status ctpt_modmatmul_sizes(int32_t L, const uint32_t* primes, int64_t M, int64_t K, int64_t Nc, int64_t* ldx,
+                                 size_t* plain_bytes, size_t* ws_bytes);
+ctpt_status ctpt_modmatmul_precompute(int32_t L, const uint32_t* primes, int64_t M, int64_t K, int64_t Nc,
+                                      const uint32_t* d_Y, void* d_plain, void* stream);
+ctpt_status ctpt_modmatmul(int32_t L, const uint32_t* primes, int64_t M, int64_t K, int64_t Nc, const uint32_t* d_X,
+                           int64_t ldx, const void* d_plain, uint32_t* d_ZT, void* d_ws, size_t ws_bytes,
+                           void* stream);
+
 /* End-to-end executor from HOST buffers (the e2e path): the same computation as
  * ctpt_layout + ctpt_matmul, but the per-column ciphertexts h_a_polys / h_b_polys (layouts as
  * for ctpt_layout) and the outputs h_AU / h_BU (layouts as for ctpt_matmul) live in host

@@ -626,12 +626,70 @@ ctpt_status ctpt_gemm_simt(const ctpt_problem* pb, int32_t l, const void* d_ws, 
   return gemm_common(pb, l, d_ws, ws_bytes, d_plain, d_AU_l, d_BU_l, stream, true);
 }
 
+static ctpt_status matmul_impl(const ctpt_problem* pb, const Dims& d, const uint32_t* X0, const void* d_plain,
+                               uint32_t* d_AU, uint32_t* d_BU, void* d_ws, size_t ws_bytes, void* stream);
+
 ctpt_status ctpt_matmul(const ctpt_problem* pb, const void* d_ctmat, const void* d_plain, uint32_t* d_AU,
                         uint32_t* d_BU, void* d_ws, size_t ws_bytes, void* stream) {
   Dims d;
   ctpt_status s = check_problem(pb, d);
   if (s != CTPT_OK) return s;
   if ((!d_AU && d.rows_A > 0) || !d_BU || !d_ctmat || !d_plain) return fail(CTPT_ERR_ARG, "null pointer");
+  const uint32_t* X0 = reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(d_ctmat) + kHeader);
+  return matmul_impl(pb, d, X0, d_plain, d_AU, d_BU, d_ws, ws_bytes, stream);
+}
+
+// Mod-PP-MM_{q; M, K, Nc} in RNS as the degenerate problem "structured-A with N = 1": rows_A = 0,
+// d1 = M, d2 = K, d3 = Nc, general per-prime Y planes (k_U = 4).
+static ctpt_problem modmm_problem(int32_t L, const uint32_t* primes, int64_t M, int64_t K, int64_t Nc) {
+  ctpt_problem pb{};
+  pb.fmt = CTPT_STRUCT_A;
+  pb.L = L;
+  pb.N = 1;
+  pb.d1 = M;
+  pb.d2 = K;
+  pb.d3 = Nc;
+  pb.primes = primes;
+  pb.kU = 4;
+  pb.plain_per_prime = 1;
+  return pb;
+}
+
+ctpt_status ctpt_modmatmul_sizes(int32_t L, const uint32_t* primes, int64_t M, int64_t K, int64_t Nc,
+                                 int64_t* ldx, size_t* plain_bytes, size_t* ws_bytes) {
+  ctpt_problem pb = modmm_problem(L, primes, M, K, Nc);
+  Dims d;
+  ctpt_status s = check_problem(&pb, d);
+  if (s != CTPT_OK) return s;
+  if (!ldx || !plain_bytes || !ws_bytes) return fail(CTPT_ERR_ARG, "null pointer");
+  *ldx = d.d2p;
+  *plain_bytes = kHeader + static_cast<size_t>(d.L) * 4 * d.d3 * d.d2p;
+  *ws_bytes = ws_bytes_needed(&pb, d);
+  return CTPT_OK;
+}
+
+ctpt_status ctpt_modmatmul_precompute(int32_t L, const uint32_t* primes, int64_t M, int64_t K, int64_t Nc,
+                                      const uint32_t* d_Y, void* d_plain, void* stream) {
+  ctpt_problem pb = modmm_problem(L, primes, M, K, Nc);
+  int32_t kU = 0;
+  return ctpt_plain_precompute_rns(&pb, d_Y, d_plain, &kU, stream);
+}
+
+ctpt_status ctpt_modmatmul(int32_t L, const uint32_t* primes, int64_t M, int64_t K, int64_t Nc, const uint32_t* d_X,
+                           int64_t ldx, const void* d_plain, uint32_t* d_ZT, void* d_ws, size_t ws_bytes,
+                           void* stream) {
+  ctpt_problem pb = modmm_problem(L, primes, M, K, Nc);
+  Dims d;
+  ctpt_status s = check_problem(&pb, d);
+  if (s != CTPT_OK) return s;
+  if (!d_X || !d_plain || !d_ZT) return fail(CTPT_ERR_ARG, "null pointer");
+  if (ldx != d.d2p) return fail(CTPT_ERR_SHAPE, "ldx = %lld must be K rounded up to 16 (%lld)", (long long)ldx, (long long)d.d2p);
+  return matmul_impl(&pb, d, d_X, d_plain, nullptr, d_ZT, d_ws, ws_bytes, stream);
+}
+
+static ctpt_status matmul_impl(const ctpt_problem* pb, const Dims& d, const uint32_t* X0, const void* d_plain,
+                               uint32_t* d_AU, uint32_t* d_BU, void* d_ws, size_t ws_bytes, void* stream) {
+  ctpt_status s = CTPT_OK;
   const bool fused = fused_eligible(d, pb->kU <= 0 ? 1 : pb->kU, pb);
   if (!fused && !d_ws) return fail(CTPT_ERR_ARG, "null workspace");
   if (!fused || pb->rescale) {
@@ -639,7 +697,6 @@ ctpt_status ctpt_matmul(const ctpt_problem* pb, const void* d_ctmat, const void*
     if (ws_bytes < need) return fail(CTPT_ERR_ARG, "workspace too small (%zu < %zu)", ws_bytes, need);
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const uint32_t* X0 = reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(d_ctmat) + kHeader);
   uint32_t* xlast = pb->rescale
                         ? reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(d_ws) + ws_xlast_off(pb, d))
                         : nullptr;

@@ -64,6 +64,13 @@ _sig = {
     "ctpt_gemm": (ctypes.c_int, [_PP, ctypes.c_int32, _P, ctypes.c_size_t, _P, _P, _P, _P]),
     "ctpt_gemm_simt": (ctypes.c_int, [_PP, ctypes.c_int32, _P, ctypes.c_size_t, _P, _P, _P, _P]),
     "ctpt_gemm_fused": (ctypes.c_int, [_PP, ctypes.c_int32, _P, _P, _P, _P, _P]),
+    "ctpt_modmatmul_sizes": (ctypes.c_int, [ctypes.c_int32, _P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                            ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_size_t),
+                                            ctypes.POINTER(ctypes.c_size_t)]),
+    "ctpt_modmatmul_precompute": (ctypes.c_int, [ctypes.c_int32, _P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                                 _P, _P, _P]),
+    "ctpt_modmatmul": (ctypes.c_int, [ctypes.c_int32, _P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _P,
+                                      ctypes.c_int64, _P, _P, _P, ctypes.c_size_t, _P]),
     "ctpt_host_workspace_bytes": (ctypes.c_int, [_PP, ctypes.c_int64, ctypes.POINTER(ctypes.c_size_t)]),
     "ctpt_matmul_host": (ctypes.c_int, [_PP, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, ctypes.c_int64, _P]),
 }
@@ -192,6 +199,32 @@ def gemm_fused(spec: Spec, l: int, ctmat, plain, AU_l, BU_l, stream=None):
     pb = spec.cstruct()
     _check(_lib.ctpt_gemm_fused(ctypes.byref(pb), l, _ptr(ctmat), _ptr(plain), _ptr(AU_l), _ptr(BU_l),
                                 _stream(stream)))
+
+
+def _primes_arr(primes):
+    return (ctypes.c_uint32 * len(primes))(*[int(p) for p in primes])
+
+
+def modmatmul_sizes(primes, M: int, K: int, Nc: int):
+    """(ldx, plain_bytes, ws_bytes) for Mod-PP-MM_{M,K,Nc} over `primes`."""
+    arr = _primes_arr(primes)
+    ldx, pb_, ws = ctypes.c_int64(0), ctypes.c_size_t(0), ctypes.c_size_t(0)
+    _check(_lib.ctpt_modmatmul_sizes(len(primes), ctypes.cast(arr, _P), M, K, Nc, ctypes.byref(ldx),
+                                     ctypes.byref(pb_), ctypes.byref(ws)))
+    return ldx.value, pb_.value, ws.value
+
+
+def modmatmul_precompute(primes, M: int, K: int, Nc: int, Y, plain, stream=None):
+    arr = _primes_arr(primes)
+    _check(_lib.ctpt_modmatmul_precompute(len(primes), ctypes.cast(arr, _P), M, K, Nc, _ptr(Y), _ptr(plain),
+                                          _stream(stream)))
+
+
+def modmatmul(primes, M: int, K: int, Nc: int, X, ldx: int, plain, ZT, ws, stream=None):
+    """Z^T = (X·Y mod p)^T per prime: X [L][M][ldx], Z^T [L][Nc][M] device tensors."""
+    arr = _primes_arr(primes)
+    _check(_lib.ctpt_modmatmul(len(primes), ctypes.cast(arr, _P), M, K, Nc, _ptr(X), ldx, _ptr(plain), _ptr(ZT),
+                               _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)))
 
 
 def host_workspace_bytes(spec: Spec, chunk_rows: int = 0) -> int:

@@ -86,3 +86,17 @@ def test_fused_refuses_wide_or_multidigit_U_without_gpu(ctpt):
     assert lib.ctpt_gemm_fused(ctypes.byref(pb), 0, fake, fake, fake, fake, None) == 6
     pb = _spec(ctpt, d3=20).cstruct()
     assert lib.ctpt_gemm_fused(ctypes.byref(pb), 1, fake, fake, fake, fake, None) == 1  # prime index
+
+
+def test_modmatmul_sizes_and_ldx_check_without_gpu(ctpt):
+    """Mod-PP-MM entry points validate on the host: ldx = K rounded up to 16, d2 overflow."""
+    ps = [2147418113, 2146959361]
+    ldx, plain, ws = ctpt.modmatmul_sizes(ps, 100, 77, 50)
+    assert ldx == 80 and plain == 256 + 2 * 4 * 50 * 80 and ws == 4 * 100 * 80
+    lib = ctpt.raw_lib()
+    arr = (ctypes.c_uint32 * 2)(*ps)
+    fake = ctypes.c_void_p(256)
+    assert lib.ctpt_modmatmul(2, ctypes.cast(arr, ctypes.c_void_p), 100, 77, 50, fake, 77, fake, fake, fake,
+                              1 << 20, None) == 2  # ERR_SHAPE: ldx must be 80
+    with pytest.raises(ctpt.CtptError, match="ERR_OVERFLOW"):
+        ctpt.modmatmul_sizes(ps, 10, 70000, 10)

@@ -528,3 +528,36 @@ def test_rescale_pair_kernel(monkeypatch):
     monkeypatch.setenv("CTPT_SKINNY", "off")
     _rescale_check(S, 32, 2, 200, 300, 3, "real")
     _rescale_check(R, 64, 1, 64, 100, 2, "int")
+
+
+# ------------------------------------------------------------------ Mod-PP-MM entry point (§8(f) row 4)
+@pytest.mark.parametrize("M,K,Nc,L", [(100, 77, 50, 1), (300, 1000, 257, 2), (64, 16, 1, 3), (1000, 2049, 300, 2),
+                                      (33, 4112, 129, 1)])
+def test_modmatmul_full_residues(M, K, Nc, L):
+    """Z = X·Y mod p with X and Y full residues on both sides (the Mod-PP-MM stage of Alg. 8/9)."""
+    import torch
+
+    from paper_2503_16080_b200 import ctpt
+
+    ps = ctgen.primes(L)
+    ldx, plain_bytes, ws_bytes = ctpt.modmatmul_sizes(ps, M, K, Nc)
+    rng = np.random.default_rng(M + K + Nc)
+    X = np.zeros((L, M, ldx), np.uint32)
+    Y = np.empty((L, K, Nc), np.uint32)
+    for l, p in enumerate(ps):
+        X[l, :, :K] = rng.integers(0, p, (M, K))
+        Y[l] = rng.integers(0, p, (K, Nc))
+        X[l, 0, :K] = p - 1  # extreme residues
+        Y[l, :, 0] = p - 1
+    Xd = torch.from_numpy(X.view(np.int32)).cuda()
+    Yd = torch.from_numpy(Y.view(np.int32)).cuda()
+    plain = torch.empty(plain_bytes, dtype=torch.uint8, device="cuda")
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device="cuda")
+    ZT = torch.empty(L * Nc * M, dtype=torch.int32, device="cuda")
+    ctpt.modmatmul_precompute(ps, M, K, Nc, Yd, plain)
+    ctpt.modmatmul(ps, M, K, Nc, Xd, ldx, plain, ZT, ws)
+    torch.cuda.synchronize()
+    got = ZT.cpu().numpy().view(np.uint32).reshape(L, Nc, M)
+    for l, p in enumerate(ps):
+        want = oracle.modmatmul(np.ascontiguousarray(X[l, :, :K].T), Y[l].astype(np.int64), p, nthreads=NTHREADS)
+        assert np.array_equal(got[l], want), f"prime {l}: {np.count_nonzero(got[l] != want)} entries differ"
