@@ -193,6 +193,21 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
         tma_load_2d(raw_base + rs * FU_RAW_BYTES, &tmX, raw_full(rs), kb * FU_BLOCK_K, tr * FU_BLOCK_R);
         if (++rs == RAW) { rs = 0; rphase ^= 1; }
       }
+    } else if (!TMA_X && lane == 0 && P.l2_prefetch > 0) {
+      // register-load variant: keep the converters' upcoming tiles streaming into L2 (no shared
+      // memory used), paced by the MMA's progress through the limb stages
+      auto prefetch = [&](int64_t it) {
+        const int32_t c1 = (static_cast<int32_t>(blockIdx.x) + static_cast<int32_t>(it / P.num_kb) * gridDim.x) * FU_BLOCK_R;
+        tma_prefetch_l2_2d(&tmX, static_cast<int32_t>(it % P.num_kb) * FU_BLOCK_K, c1);
+      };
+      for (int64_t it = 0; it < P.l2_prefetch && it < n_it; ++it) prefetch(it);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t it = 0; it + P.l2_prefetch < n_it; ++it) {
+        mbar_wait(empty_bar(stage), phase ^ 1);
+        prefetch(it + P.l2_prefetch);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
     }
   } else if (warp >= 4 && warp < 8) {
     // ---------------------------------------------------------------- epilogue (128 threads)
