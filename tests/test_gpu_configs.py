@@ -187,3 +187,66 @@ def test_config4_skinny_sweep_full_size(monkeypatch):
         Us = np.ascontiguousarray(U[:, c0:c1])
         _check_matrix(Ac, Us, AUn, p, rng, f"c4-skinny A·U cols [{c0},{c1})", 8192)
         _check_matrix(Bc, Us, BUn, p, rng, f"c4-skinny B·U cols [{c0},{c1})", 8192)
+
+
+def test_config3_rescale_full_size():
+    """Algorithm 6 WITH step 2 at c3's sizes (bench.py --rescale): U real uniform[-1,1) encoded at
+    Δ_U = q_1 = the last prime (k_U = 4 per-prime digit planes), RNS Rescale by q_1 fused into the
+    other primes' epilogues.  Sampled entries (tile boundaries + random) against the oracle's
+    products for all three primes followed by its plain Rescale ⌊x/q_1⌉; on sampled columns the
+    decryption under the two remaining primes is within the Rescale bound (h+1)/2 of (P·U0)/q_1
+    and decodes to M·U within 1e-6 relative (readings Q27, Q28)."""
+    from fractions import Fraction
+
+    c = ctgen.CONFIGS["c3"]
+    ps = ctgen.primes(c.L)
+    q1 = ps[-1]
+    ct = ctgen.encrypt(c.fmt, c.N, c.d1, c.d2, c.seed, c.log_delta, ps, nthreads=NTHREADS)
+    Ur, U0 = ctgen.U_real(c.seed, c.d2, c.d3, q1, nthreads=NTHREADS)
+    Ures = np.stack([(U0 % int(p)).astype(np.uint32) for p in ps])
+    (AU, BU), eng = run_gpu(c.fmt, c.N, c.d1, c.d2, c.d3, ps, ct.a_polys, ct.b_polys, Ures=Ures, rescale=1)
+    del Ures
+    assert eng.spec.kU == 4 and AU.shape[0] == c.L - 1
+    rng = np.random.default_rng(99)
+    ra = c.rows_A
+    for name, rows, gpu in (("A", ra, AU), ("B", c.d1, BU)):
+        rb = _boundary(rows, 64)
+        cb = _boundary(c.d3, 128)
+        r_idx = np.concatenate([np.repeat(rb, len(cb)), rng.integers(0, rows, 8192)])
+        j_idx = np.concatenate([np.tile(cb, len(rb)), rng.integers(0, c.d3, 8192)])
+        prods = []
+        for l, p in enumerate(ps):
+            Ac, Bc = colmajor_views(c.fmt, c.N, c.d1, c.d2, ct.a_polys[l], ct.b_polys[l])
+            Xc = Ac if name == "A" else Bc
+            prods.append(oracle.modmatmul_entries(Xc, U0, p, r_idx, j_idx, nthreads=NTHREADS))
+        want = oracle.rescale_last(np.stack(prods), ps)
+        for l in range(c.L - 1):
+            got = gpu[l][j_idx, r_idx]
+            assert np.array_equal(got, want[l]), f"{name}: {np.count_nonzero(got != want[l])} rescaled entries differ"
+    # decryption + decode on sampled columns
+    cols = [0, 4097, c.d3 - 1]
+    nk = c.k if c.fmt == ctgen.SHARED_A else 1
+    sks = [ctgen.sk(c.seed, t, c.N) for t in range(nk)]
+    h = max(int(np.abs(s).sum()) for s in sks)
+    pu = np.zeros((c.L, len(cols), c.d1), dtype=np.uint64)  # (P·U0)[:, cols] mod each prime
+    mu = np.zeros((c.d1, len(cols)))
+    Uc = U0[:, cols]
+    for k0 in range(0, c.d2, 2048):
+        P = ctgen.plain_block(c.seed, c.N, c.d1, c.log_delta, 0, c.d1, k0, 2048, nthreads=NTHREADS)
+        M = ctgen.msg_block(c.seed, c.d1, 0, c.d1, k0, 2048, nthreads=NTHREADS)
+        mu += M.dot(Ur[k0:k0 + 2048, cols])
+        Pt = np.ascontiguousarray(P.T)
+        for l, p in enumerate(ps):
+            part = oracle.modmatmul((Pt % p).astype(np.uint32), Uc[k0:k0 + 2048], p, nthreads=NTHREADS)
+            pu[l] = (pu[l] + part) % p
+    worst = 0.0
+    for ci, j in enumerate(cols):
+        decs = np.stack([oracle.decrypt_col(c.fmt, c.N, c.d1, sks, AU[l][j], BU[l][j], ps[l], nthreads=NTHREADS)
+                         for l in range(c.L - 1)])
+        cen = oracle.crt_centred_array(decs, ps[:2])
+        exact = oracle.crt_centred_array(pu[:, ci, :], ps)  # P·U0 exactly (|P·U0| < q/2)
+        for i in range(0, c.d1, 97):
+            assert abs(Fraction(cen[i]) - Fraction(exact[i], q1)) <= Fraction(h + 1, 2), (j, i)
+        approx = np.array([float(v) for v in cen]) / 2.0 ** c.log_delta
+        worst = max(worst, np.abs(approx - mu[:, ci]).max() / np.abs(mu).max())
+    assert worst <= 1e-6, worst
