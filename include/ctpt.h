@@ -182,7 +182,7 @@ ctpt_status ctpt_gemm(const ctpt_problem* prob, int32_t l, const void* d_ws, siz
  * (A·U mod p, B·U mod p) as ctpt_split + ctpt_gemm, but the limb split runs inside the GEMM's
  * load path, reading the int32 residues of d_ctmat exactly once (no workspace): the regime is
  * HBM-bound and this saves the split's write + re-read.  ctpt_matmul (and ctpt_matmul_host)
- * choose this kernel automatically for every prime when d3_loc ≤ 256 and kU = 1 (environment
+ * choose this kernel automatically for every prime when 32 < d3_loc ≤ 256 and kU = 1 (environment
  * CTPT_SKINNY=off disables that, for A/B measurements).  Outputs as for ctpt_gemm.
  * CTPT_ERR_UNSUPPORTED when kU ≠ 1 or d3_loc > 256.  Never synchronises. */
 ctpt_status ctpt_gemm_fused(const ctpt_problem* prob, int32_t l, const void* d_ctmat, const void* d_plain,
@@ -208,6 +208,16 @@ ctpt_status ctpt_modmatmul_precompute(int32_t L, const uint32_t* primes, int64_t
 ctpt_status ctpt_modmatmul(int32_t L, const uint32_t* primes, int64_t M, int64_t K, int64_t Nc, const uint32_t* d_X,
                            int64_t ldx, const void* d_plain, uint32_t* d_ZT, void* d_ws, size_t ws_bytes,
                            void* stream);
+
+/* The very-skinny regime (d3_loc ≤ 32, kU = 1; CP-Mv at d3 = 1) for prime l:
+ * the int32 residues of d_ctmat are fed to the tensor cores as raw bytes against an expanded
+ * U_exp (U's digits spread to byte position ℓ of every 4-byte group, built in d_ws), so every
+ * limb product comes out of ONE byte-level contraction with no limb split at all; work is split
+ * over K with exact int32 partials in d_ws (ws_bytes from ctpt_query_sizes).  ctpt_matmul
+ * takes this kernel automatically when d3_loc ≤ 32 (CTPT_MV=off disables that).  Outputs as for
+ * ctpt_gemm.  CTPT_ERR_UNSUPPORTED when kU ≠ 1, d3_loc > 32 or u_offset ≠ 0.  Never synchronises. */
+ctpt_status ctpt_gemm_mv(const ctpt_problem* prob, int32_t l, const void* d_ctmat, const void* d_plain,
+                         uint32_t* d_AU_l, uint32_t* d_BU_l, void* d_ws, size_t ws_bytes, void* stream);
 
 /* End-to-end executor from HOST buffers (the e2e path): the same computation as
  * ctpt_layout + ctpt_matmul, but the per-column ciphertexts h_a_polys / h_b_polys (layouts as

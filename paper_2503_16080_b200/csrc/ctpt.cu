@@ -15,6 +15,7 @@
 #include "gemm_tc.cuh"
 #include "gemm_tc2.cuh"
 #include "gemm_fused.cuh"
+#include "gemm_mv.cuh"
 #include "kernels.cuh"
 
 using namespace ctpt;
@@ -103,9 +104,17 @@ size_t ws_corr_off(const Dims& d) { return align256(ws_limb_bytes(d)); }
 size_t ws_xlast_off(const ctpt_problem* pb, const Dims& d) {
   return ws_corr_off(d) + (needs_rowcorr(pb) ? align256(static_cast<size_t>(4) * d.R) : 0);
 }
+size_t mv_ws_bytes(const Dims& d);
+size_t ws_base_bytes(const ctpt_problem* pb, const Dims& d) {
+  if (needs_rowcorr(pb) || pb->rescale)
+    return ws_xlast_off(pb, d) + (pb->rescale ? static_cast<size_t>(4) * d.R * d.d3_loc : 0);
+  return ws_limb_bytes(d);
+}
+// the very-skinny kernel's U_exp + split partials + tickets live after everything else
+size_t ws_mv_off(const ctpt_problem* pb, const Dims& d) { return align256(ws_base_bytes(pb, d)); }
 size_t ws_bytes_needed(const ctpt_problem* pb, const Dims& d) {
-  if (!needs_rowcorr(pb) && !pb->rescale) return ws_limb_bytes(d);
-  return ws_xlast_off(pb, d) + (pb->rescale ? static_cast<size_t>(4) * d.R * d.d3_loc : 0);
+  if (d.d3_loc <= 32) return ws_mv_off(pb, d) + mv_ws_bytes(d);
+  return ws_base_bytes(pb, d);
 }
 
 ModP make_modp(uint32_t p) {
@@ -200,6 +209,10 @@ ctpt_status tc_setup() {
       e = cudaFuncSetAttribute(k_gemm_fused<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(1, false));
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_gemm_fused<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(2, false));
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_gemm_fused<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(1, true));
     if (e == cudaSuccess)
@@ -236,11 +249,48 @@ ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st);
 // the step is HBM-bound and the fused kernel (split inside the GEMM's load path, X read once)
 // replaces split + GEMM.  CTPT_SKINNY=off forces split + GEMM (for A/B measurements).
 constexpr int64_t kFusedMaxD3 = 256;
+// The very-skinny regime (d3_loc ≤ 32): raw residue bytes straight into the MMA (gemm_mv.cuh).
+// CTPT_MV=off falls back to the converter kernel (for A/B measurements).
+constexpr int64_t kMvMaxD3 = 32;
+int mv_nc(const Dims& d) {  // N = 4·d3p, d3p ∈ {4, 8, 16, 32}
+  int d3p = 4;
+  while (d3p < d.d3_loc) d3p *= 2;
+  return 4 * d3p;
+}
+struct MvPlan {
+  int nc, splits;
+  int32_t tiles, num_kb;
+  size_t ue_off, part_off, ticket_off, total;
+};
+MvPlan mv_plan(const Dims& d) {
+  MvPlan m;
+  m.nc = mv_nc(d);
+  m.tiles = static_cast<int32_t>((d.R + MV_BLOCK_R - 1) / MV_BLOCK_R);
+  m.num_kb = static_cast<int32_t>(4 * d.d2p / MV_BLOCK_K + ((4 * d.d2p) % MV_BLOCK_K ? 1 : 0));
+  const int target = 12 * num_sms();
+  int s = static_cast<int>((target + m.tiles - 1) / m.tiles);
+  s = std::max(1, std::min(s, std::max(1, m.num_kb / 8)));
+  m.splits = s;
+  m.ue_off = 0;
+  m.part_off = align256(static_cast<size_t>(m.nc) * 4 * d.d2p);
+  const size_t part = m.splits > 1 ? static_cast<size_t>(m.tiles) * m.splits * m.nc * MV_BLOCK_R * 4 : 0;
+  m.ticket_off = m.part_off + align256(part);
+  m.total = m.ticket_off + align256(static_cast<size_t>(m.tiles) * 4);
+  return m;
+}
+bool mv_eligible(const Dims& d, int kU, const ctpt_problem* pb);
+
 bool fused_eligible(const Dims& d, int kU, const ctpt_problem* pb) {
   if (kU != 1 || d.d3_loc > kFusedMaxD3 || needs_rowcorr(pb)) return false;
   const char* e = getenv("CTPT_SKINNY");
   return !(e && strcmp(e, "off") == 0);
 }
+bool mv_eligible(const Dims& d, int kU, const ctpt_problem* pb) {
+  if (!fused_eligible(d, kU, pb) || d.d3_loc > kMvMaxD3) return false;
+  const char* e = getenv("CTPT_MV");
+  return !(e && strcmp(e, "off") == 0);
+}
+size_t mv_ws_bytes(const Dims& d) { return mv_plan(d).total; }
 
 }  // namespace
 
@@ -582,9 +632,86 @@ ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st) 
   return CTPT_OK;
 }
 
+// The very-skinny kernel for one prime: expand U into U_exp in the workspace, zero the tickets,
+// run k_gemm_mv<NC>.  `mv_ws` points at the MvPlan region of the workspace.
+ctpt_status launch_mv(const GemmArgs& g, const uint32_t* x, void* mv_ws, cudaStream_t st) {
+  const Dims& d = g.d;
+  if (g.kU != 1 || d.d3_loc > kMvMaxD3) return fail(CTPT_ERR_UNSUPPORTED, "mv kernel needs kU = 1 and d3_loc <= 32");
+  ctpt_status s = tc_setup();
+  if (s != CTPT_OK) return s;
+  Dims dd = d;
+  dd.R = g.R;
+  const MvPlan mp = mv_plan(dd);
+  uint8_t* w = static_cast<uint8_t*>(mv_ws);
+  uint32_t* ue = reinterpret_cast<uint32_t*>(w + mp.ue_off);
+  const int8_t* plane = g.planes + static_cast<int64_t>(g.plane0) * d.d3 * d.d2p;
+  const int d3p = mp.nc / 4;
+  dim3 eg(static_cast<unsigned>(std::min<int64_t>((d.d2p + 255) / 256, 1024)), static_cast<unsigned>(mp.nc));
+  k_expand_u<<<eg, 256, 0, st>>>(plane, d.d2p, static_cast<int32_t>(d.j0), static_cast<int32_t>(d.d3_loc), d3p, ue);
+  CUDA_TRY(cudaGetLastError());
+  if (mp.splits > 1) CUDA_TRY(cudaMemsetAsync(w + mp.ticket_off, 0, static_cast<size_t>(mp.tiles) * 4, st));
+  CUtensorMap tmX, tmUe;
+  const uint64_t kbytes = static_cast<uint64_t>(4) * d.d2p;
+  s = make_tmap_u8(&tmX, x, kbytes, g.R, 1, kbytes, kbytes * g.R, MV_BLOCK_K, MV_BLOCK_R, 1);
+  if (s != CTPT_OK) return s;
+  s = make_tmap_u8(&tmUe, ue, kbytes, mp.nc, 1, kbytes, kbytes * mp.nc, MV_BLOCK_K, mp.nc, 1);
+  if (s != CTPT_OK) return s;
+  MvParams P{};
+  P.num_kb = mp.num_kb;
+  P.num_tiles = mp.tiles;
+  P.splits = mp.splits;
+  P.u_unsigned = g.u_unsigned;
+  P.partial = reinterpret_cast<int32_t*>(w + mp.part_off);
+  P.tickets = reinterpret_cast<uint32_t*>(w + mp.ticket_off);
+  P.m = make_modp(g.p);
+  P.o = g.o;
+  P.o.accumulate = 0;
+  P.o.w = 1;
+  const int64_t units = static_cast<int64_t>(mp.tiles) * mp.splits;
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(units, num_sms()));
+  switch (mp.nc) {
+    case 16: k_gemm_mv<16><<<grid, MV_THREADS, MV_SMEM_BYTES, st>>>(tmX, tmUe, P); break;
+    case 32: k_gemm_mv<32><<<grid, MV_THREADS, MV_SMEM_BYTES, st>>>(tmX, tmUe, P); break;
+    case 64: k_gemm_mv<64><<<grid, MV_THREADS, MV_SMEM_BYTES, st>>>(tmX, tmUe, P); break;
+    default: k_gemm_mv<128><<<grid, MV_THREADS, MV_SMEM_BYTES, st>>>(tmX, tmUe, P); break;
+  }
+  CUDA_TRY(cudaGetLastError());
+  return CTPT_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+ctpt_status ctpt_gemm_mv(const ctpt_problem* pb, int32_t l, const void* d_ctmat, const void* d_plain,
+                         uint32_t* d_AU_l, uint32_t* d_BU_l, void* d_ws, size_t ws_bytes, void* stream) {
+  Dims d;
+  ctpt_status s = check_problem(pb, d);
+  if (s != CTPT_OK) return s;
+  if (pb->rescale) return fail(CTPT_ERR_UNSUPPORTED, "Rescale needs every prime: use ctpt_matmul");
+  if (needs_rowcorr(pb)) return fail(CTPT_ERR_UNSUPPORTED, "the mv kernel does not form row sums (u_offset != 0)");
+  if (l < 0 || l >= d.L) return fail(CTPT_ERR_ARG, "prime index %d out of range", l);
+  if (!d_ctmat || !d_plain || (!d_AU_l && d.rows_A > 0) || !d_BU_l || !d_ws) return fail(CTPT_ERR_ARG, "null pointer");
+  if (ws_bytes < ws_bytes_needed(pb, d)) return fail(CTPT_ERR_ARG, "workspace too small");
+  GemmArgs g{};
+  g.R = d.R;
+  g.d = d;
+  g.kU = pb->kU <= 0 ? 1 : pb->kU;
+  g.u_unsigned = pb->u_unsigned;
+  g.planes = reinterpret_cast<const int8_t*>(static_cast<const uint8_t*>(d_plain) + kHeader);
+  g.nplanes = pb->plain_per_prime ? d.L * g.kU : g.kU;
+  g.plane0 = plane_index(pb, l, 0);
+  g.p = pb->primes[l];
+  g.o.AU = d_AU_l;
+  g.o.BU = d_BU_l;
+  g.o.rows_A = d.rows_A;
+  g.o.d1 = d.d1;
+  g.o.R = d.R;
+  g.o.d3_loc = d.d3_loc;
+  const uint32_t* x =
+      reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(d_ctmat) + kHeader) + l * d.R * d.d2p;
+  return launch_mv(g, x, static_cast<uint8_t*>(d_ws) + ws_mv_off(pb, d), static_cast<cudaStream_t>(stream));
+}
 
 ctpt_status ctpt_gemm_fused(const ctpt_problem* pb, int32_t l, const void* d_ctmat, const void* d_plain,
                             uint32_t* d_AU_l, uint32_t* d_BU_l, void* stream) {
@@ -691,8 +818,9 @@ static ctpt_status matmul_impl(const ctpt_problem* pb, const Dims& d, const uint
                                uint32_t* d_AU, uint32_t* d_BU, void* d_ws, size_t ws_bytes, void* stream) {
   ctpt_status s = CTPT_OK;
   const bool fused = fused_eligible(d, pb->kU <= 0 ? 1 : pb->kU, pb);
-  if (!fused && !d_ws) return fail(CTPT_ERR_ARG, "null workspace");
-  if (!fused || pb->rescale) {
+  const bool mv = mv_eligible(d, pb->kU <= 0 ? 1 : pb->kU, pb);
+  if ((!fused || mv) && !d_ws) return fail(CTPT_ERR_ARG, "null workspace");
+  if (!fused || mv || pb->rescale) {
     const size_t need = ws_bytes_needed(pb, d);
     if (ws_bytes < need) return fail(CTPT_ERR_ARG, "workspace too small (%zu < %zu)", ws_bytes, need);
   }
@@ -713,6 +841,7 @@ static ctpt_status matmul_impl(const ctpt_problem* pb, const Dims& d, const uint
     g.u_unsigned = pb->u_unsigned;
     g.o = o;
     const uint32_t* x = X0 + static_cast<int64_t>(l) * d.R * d.d2p;
+    if (mv) return launch_mv(g, x, static_cast<uint8_t*>(d_ws) + ws_mv_off(pb, d), st);
     if (fused) return launch_fused(g, x, st);
     uint32_t* corr = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(d_ws) + ws_corr_off(d));
     ctpt_status s2 = launch_split_prime(pb, x, d.R, d.d2p, g.p, d_ws, corr, st);

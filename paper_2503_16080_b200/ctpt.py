@@ -64,6 +64,7 @@ _sig = {
     "ctpt_gemm": (ctypes.c_int, [_PP, ctypes.c_int32, _P, ctypes.c_size_t, _P, _P, _P, _P]),
     "ctpt_gemm_simt": (ctypes.c_int, [_PP, ctypes.c_int32, _P, ctypes.c_size_t, _P, _P, _P, _P]),
     "ctpt_gemm_fused": (ctypes.c_int, [_PP, ctypes.c_int32, _P, _P, _P, _P, _P]),
+    "ctpt_gemm_mv": (ctypes.c_int, [_PP, ctypes.c_int32, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
     "ctpt_modmatmul_sizes": (ctypes.c_int, [ctypes.c_int32, _P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                             ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_size_t),
                                             ctypes.POINTER(ctypes.c_size_t)]),
@@ -199,6 +200,13 @@ def gemm_fused(spec: Spec, l: int, ctmat, plain, AU_l, BU_l, stream=None):
     pb = spec.cstruct()
     _check(_lib.ctpt_gemm_fused(ctypes.byref(pb), l, _ptr(ctmat), _ptr(plain), _ptr(AU_l), _ptr(BU_l),
                                 _stream(stream)))
+
+
+def gemm_mv(spec: Spec, l: int, ctmat, plain, AU_l, BU_l, ws, stream=None):
+    """Very-skinny kernel (d3_loc <= 32, kU = 1): raw residue bytes against an expanded U."""
+    pb = spec.cstruct()
+    _check(_lib.ctpt_gemm_mv(ctypes.byref(pb), l, _ptr(ctmat), _ptr(plain), _ptr(AU_l), _ptr(BU_l), _ptr(ws),
+                             ws.numel() * ws.element_size(), _stream(stream)))
 
 
 def _primes_arr(primes):

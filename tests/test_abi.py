@@ -40,7 +40,9 @@ def test_sizes(ctpt):
     s = ctpt.query_sizes(_spec(ctpt))
     assert s.rows_A == 16 and s.R == 80 and s.d2p == 48 and s.d3_loc == 20
     assert s.ctmat_bytes == 256 + 80 * 48 * 4
-    assert s.workspace_bytes == 4 * 80 * 48
+    # d3 = 20 ≤ 32: the limb planes, then the raw-byte kernel's U_exp (NC = 4·32 rows × 4·d2p bytes)
+    assert s.workspace_bytes >= 4 * 80 * 48 + 128 * 4 * 48
+    assert ctpt.query_sizes(_spec(ctpt, d3=40)).workspace_bytes == 4 * 80 * 48
     assert s.out_AU_bytes == 20 * 16 * 4 and s.out_BU_bytes == 20 * 64 * 4
     s2 = ctpt.query_sizes(_spec(ctpt, fmt=ctpt.SHARED_S, d2=50, col_begin=3, col_end=11))
     assert s2.rows_A == 64 and s2.R == 128 and s2.d2p == 64 and s2.d3_loc == 8

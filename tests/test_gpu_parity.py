@@ -155,10 +155,64 @@ SKINNY = [
 @pytest.mark.parametrize("load", ["tma", "regs"])
 @pytest.mark.parametrize("shape", SKINNY, ids=lambda s: "f%d_N%d_k%d_d2%d_d3%d_L%d" % s)
 def test_skinny_fused(shape, load, monkeypatch):
-    """Both ways of feeding the fused kernel's converters: raw X tiles by TMA, or register loads."""
+    """Both ways of feeding the fused kernel's converters: raw X tiles by TMA, or register loads
+    (CTPT_MV=off keeps d3 <= 32 on the converter kernel too)."""
     monkeypatch.delenv("CTPT_SKINNY", raising=False)
+    monkeypatch.setenv("CTPT_MV", "off")
     monkeypatch.setenv("CTPT_FUSED_LOAD", load)
     _check(*shape)
+
+
+MV = [
+    # fmt, N, k, d2, d3, L — the raw-byte kernel (d3 <= 32): every padded width NC = 16/32/64/128,
+    # ragged R and d2, K split into several units per tile (exact int32 partials + tickets)
+    (S, 64, 3, 1000, 1, 2),
+    (R, 512, 1, 130, 2, 1),
+    (A, 128, 4, 520, 4, 1),
+    (S, 32, 5, 384, 5, 2),
+    (A, 16, 3, 77, 8, 1),
+    (R, 1024, 1, 2056, 16, 1),
+    (S, 128, 2, 640, 17, 1),
+    (A, 8, 2, 16, 31, 1),        # R = 24 rows < one tile, one K block
+    (SA, 256, 3, 4112, 32, 2),   # structured-A, long K
+    (S, 1024, 4, 8200, 3, 1),    # R = 8192: 64 tiles, several K splits each
+]
+
+
+@pytest.mark.parametrize("shape", MV, ids=lambda s: "f%d_N%d_k%d_d2%d_d3%d_L%d" % s)
+def test_mv_raw_bytes(shape, monkeypatch):
+    monkeypatch.delenv("CTPT_SKINNY", raising=False)
+    monkeypatch.delenv("CTPT_MV", raising=False)
+    _check(*shape)
+    _check(*shape, seed=1)  # the tickets were left at zero for the next launch
+
+
+def test_mv_column_shard_and_entry_point(monkeypatch):
+    """A 1..32-column block [col_begin, col_end) of a wider U through ctpt_gemm_mv, per prime."""
+    import torch
+
+    from paper_2503_16080_b200 import ctpt
+    from paper_2503_16080_b200.engine import CpmmEngine
+
+    monkeypatch.delenv("CTPT_MV", raising=False)
+    fmt, N, k, d2, d3, L = A, 64, 4, 700, 300, 2
+    d1 = N * k
+    ps = ctgen.primes(L)
+    ct = ctgen.encrypt(fmt, N, d1, d2, 13, 20, ps)
+    U = ctgen.U_matrix(13, d2, d3, 8)
+    for c0, c1 in [(0, 1), (77, 78), (250, 282), (5, 21)]:
+        eng = CpmmEngine(ctpt.Spec(fmt, N, d1, d2, d3, ps, c0, c1), "cuda")
+        eng.layout(ct.a_polys, ct.b_polys)
+        eng.precompute(U)
+        AU, BU = eng.alloc_outputs()
+        ra, n = eng.sizes.rows_A, c1 - c0
+        for l in range(L):
+            ctpt.gemm_mv(eng.spec, l, eng.ctmat, eng.plain, AU[l * n * ra:], BU[l * n * d1:], eng.ws)
+        torch.cuda.synchronize()
+        AUn, BUn = eng.outputs_numpy(AU, BU)
+        for l, p in enumerate(ps):
+            wa, wb = oracle_outputs(fmt, N, d1, ct.a_polys[l], ct.b_polys[l], U, p, cols=np.arange(c0, c1))
+            assert np.array_equal(AUn[l], wa) and np.array_equal(BUn[l], wb), (c0, c1, l)
 
 
 @pytest.mark.parametrize("load", ["tma", "regs"])

@@ -32,8 +32,10 @@ def main():
     ap.add_argument("--L", type=int, default=4)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--d3", default="1,64,128,256")
-    ap.add_argument("--paths", default="fused,fused-regs,split+gemm")
+    ap.add_argument("--d3", default="1,16,32,64,128,256")
+    ap.add_argument("--paths", default="auto,fused,split+gemm",
+                    help="auto = ctpt_matmul's choice per prime (mv for d3 <= 32, else fused); fused = the "
+                         "converter kernel (ctpt_gemm_fused); mv = ctpt_gemm_mv; split+gemm")
     args = ap.parse_args()
 
     import torch
@@ -58,6 +60,11 @@ def main():
     assert kU == 1
     stream = torch.cuda.current_stream()
     R, d2 = c.R, c.d2
+    import dataclasses
+
+    ws_need = max(ctpt.query_sizes(dataclasses.replace(eng.spec, col_begin=0, col_end=x)).workspace_bytes for x in d3s)
+    if eng.ws.numel() < ws_need:
+        eng.ws = torch.empty(ws_need, dtype=torch.uint8, device="cuda")
     for d3 in d3s:
         import dataclasses
 
@@ -78,7 +85,11 @@ def main():
             def step(evs=None):
                 for l in range(len(ps)):
                     au, bu = AU[l * d3 * ra:], BU[l * d3 * c.d1:]
-                    if path.startswith("fused"):
+                    if path == "mv" or (path == "auto" and d3 <= 32):
+                        if evs is not None:
+                            evs[l][0].record(stream)
+                        ctpt.gemm_mv(sp, l, eng.ctmat, eng.plain, au, bu, eng.ws, stream=stream)
+                    elif path.startswith("fused") or path == "auto":
                         if evs is not None:
                             evs[l][0].record(stream)
                         ctpt.gemm_fused(sp, l, eng.ctmat, eng.plain, au, bu, stream=stream)
@@ -109,7 +120,8 @@ def main():
             print(json.dumps({
                 "sweep": "skinny", "path": path, "d3": d3, "L": len(ps), "R": R, "d2": d2,
                 "ms_per_step": ms_step, "residue_macs_per_s": macs / (ms_step / 1e3),
-                "kernel": ("k_gemm_fused" if path.startswith("fused") else "k_gemm_tc (after k_split)"),
+                "kernel": ("k_gemm_mv" if path == "mv" or (path == "auto" and d3 <= 32) else
+                           "k_gemm_fused" if path.startswith("fused") or path == "auto" else "k_gemm_tc (after k_split)"),
                 "avg_launch_ms": k_ms,
                 "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
                              "frac": gbs / hbm_peak, "per_launch_bytes": alg_bytes},
