@@ -1008,17 +1008,9 @@ ctpt_status ctpt_matmul_host(const ctpt_problem* pb, const uint32_t* h_a, const 
     const uint32_t* b_l = h_b + static_cast<int64_t>(l) * d.d2 * d.d1;
     uint32_t* AU_l = h_AU + static_cast<int64_t>(l) * d.d3_loc * d.rows_A;
     uint32_t* BU_l = h_BU + static_cast<int64_t>(l) * d.d3_loc * d.d1;
-    // Tapered schedule: the very first and very last chunks of the whole call are a quarter
-    // size, so the device→host engine starts (and the host→device engine's idle tail ends)
-    // a quarter-chunk after the start (before the end) instead of a whole chunk.
-    const int64_t small = std::max<int64_t>(64, (hp.chunk / 4 + 63) / 64 * 64);
-    for (int64_t r0 = 0, step = 0; r0 < d.R; r0 += step, ++it) {
+    for (int64_t r0 = 0; r0 < d.R; r0 += hp.chunk, ++it) {
       const int b = static_cast<int>(it & 1);
-      step = hp.chunk;
-      if (l == 0 && r0 == 0) step = small;                                   // first chunk of the call
-      if (l == d.L - 1 && d.R - r0 > small && d.R - r0 <= hp.chunk) step = d.R - r0 - small;  // next-to-last
-      if (l == d.L - 1 && d.R - r0 <= small) step = d.R - r0;               // last chunk
-      const int64_t r1 = std::min(d.R, r0 + step), rows = r1 - r0;
+      const int64_t r1 = std::min(d.R, r0 + hp.chunk), rows = r1 - r0;
       const int64_t na = std::max<int64_t>(0, std::min(r1, d.rows_A) - r0), nb = rows - na;
       const int64_t rb0 = r0 + na - d.rows_A;  // first B row of the chunk (if nb > 0)
       // 1. host → device: the chunk's rows of every ciphertext column, packed col-major [d2][rows]
