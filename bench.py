@@ -382,6 +382,16 @@ def roofline_fused(c, d3l, launch_s, share, mp, which):
             "avg_launch_ms": launch_s * 1e3, "share_of_step": share}
 
 
+def host_launches(c, n_units: int, kU: int, spec_is_split: bool) -> int:
+    """Kernels ctpt_matmul_host launches per call for n_units one-prime units: per row chunk
+    (R/6 rounded up to 64, the library default) k_layout + (k_split[_rows] + kU × k_gemm_tc, or one
+    fused kernel)."""
+    chunk = ((c.R + 5) // 6 + 63) // 64 * 64
+    n_chunks = (c.R + chunk - 1) // chunk
+    per_chunk = 1 + ((1 + kU) if spec_is_split else 1)
+    return n_units * n_chunks * per_chunk
+
+
 def pcie_bandwidth(dev, nbytes: int = 1 << 30) -> dict:
     """Pinned host<->device copy bandwidth (GB/s): each direction alone and both at once on
     two streams — the floor of the e2e path, whose every step moves its inputs and outputs."""
@@ -538,7 +548,8 @@ def run_sharded(args, rank: int, world: int, local_rank: int):
                            path="pinned host ciphertexts -> ctpt_matmul_host per unit -> pinned host outputs"),
             "e2e": {"value": c.residue_macs / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
-            "gpu_launches": None, "clocks": clocks, "input_generation_s": gen_s}))
+            "gpu_launches": host_launches(c, len(mine), kU, spec_is_split=(c.d3 > 256)) * args.steps,
+            "clocks": clocks, "input_generation_s": gen_s}))
 
 
 def main():

@@ -896,7 +896,7 @@ namespace {
 
 struct HostPlan {
   int64_t chunk;  // rows of X per chunk (multiple of 64)
-  size_t in_bytes, cm_bytes, limb_bytes, out_bytes, corr_bytes, total;
+  size_t in_bytes, cm_bytes, limb_bytes, out_bytes, corr_bytes, mv_bytes, total;
 };
 
 HostPlan host_plan(const Dims& d, int64_t chunk_rows) {
@@ -912,7 +912,10 @@ HostPlan host_plan(const Dims& d, int64_t chunk_rows) {
   h.limb_bytes = align256(static_cast<size_t>(4) * c * d.d2p);
   h.out_bytes = align256(static_cast<size_t>(d.d3_loc) * c * 4);
   h.corr_bytes = align256(static_cast<size_t>(c) * 4);  // rowcorr of a chunk (unsigned-U mode)
-  h.total = 2 * h.in_bytes + h.cm_bytes + h.limb_bytes + 2 * h.out_bytes + h.corr_bytes;
+  Dims dc = d;
+  dc.R = c;
+  h.mv_bytes = d.d3_loc <= kMvMaxD3 ? align256(mv_plan(dc).total) : 0;  // very-skinny kernel, per chunk
+  h.total = 2 * h.in_bytes + h.cm_bytes + h.limb_bytes + 2 * h.out_bytes + h.corr_bytes + h.mv_bytes;
   return h;
 }
 
@@ -976,6 +979,7 @@ ctpt_status ctpt_matmul_host(const ctpt_problem* pb, const uint32_t* h_a, const 
   uint32_t* ob[2] = {reinterpret_cast<uint32_t*>(w + 2 * hp.in_bytes + hp.cm_bytes + hp.limb_bytes),
                      reinterpret_cast<uint32_t*>(w + 2 * hp.in_bytes + hp.cm_bytes + hp.limb_bytes + hp.out_bytes)};
   uint32_t* corr = reinterpret_cast<uint32_t*>(w + 2 * hp.in_bytes + hp.cm_bytes + hp.limb_bytes + 2 * hp.out_bytes);
+  uint8_t* mvws = w + 2 * hp.in_bytes + hp.cm_bytes + hp.limb_bytes + 2 * hp.out_bytes + hp.corr_bytes;
 
   StreamSet ss;
   CUDA_TRY(cudaStreamCreateWithFlags(&ss.h2d, cudaStreamNonBlocking));
@@ -1001,6 +1005,7 @@ ctpt_status ctpt_matmul_host(const ctpt_problem* pb, const uint32_t* h_a, const 
   g.u_unsigned = pb->u_unsigned;
   if (needs_rowcorr(pb)) g.o.rowcorr = corr;
   const bool fused = fused_eligible(d, g.kU, pb);
+  const bool mv = mv_eligible(d, g.kU, pb);
 
   int64_t it = 0;
   for (int l = 0; l < d.L; ++l) {
@@ -1041,7 +1046,7 @@ ctpt_status ctpt_matmul_host(const ctpt_problem* pb, const uint32_t* h_a, const 
       g.o.d1 = 0;
       g.o.R = rows;
       g.o.d3_loc = d.d3_loc;
-      s = fused ? launch_fused(g, cm, sc) : launch_gemm(g, sc, false);
+      s = mv ? launch_mv(g, cm, mvws, sc) : fused ? launch_fused(g, cm, sc) : launch_gemm(g, sc, false);
       if (s != CTPT_OK) return s;
       CUDA_TRY(cudaEventRecord(out_ready[b], sc));
       // 3. device → host: rows [r0, r1) of every output column
