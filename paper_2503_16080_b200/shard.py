@@ -115,6 +115,8 @@ def gpu_compute_fn(fmt: int, N: int, d1: int, d2: int, d3: int, primes: list, ge
         sizes = ctpt.query_sizes(spec)
         AU = torch.empty(sizes.out_AU_bytes // 4, dtype=torch.int32, device=device)
         BU = torch.empty(sizes.out_BU_bytes // 4, dtype=torch.int32, device=device)
+        if base.ws.numel() < sizes.workspace_bytes:  # a narrow unit (<= 32 columns) takes the raw-byte kernel
+            base.ws = torch.empty(sizes.workspace_bytes, dtype=torch.uint8, device=device)
         ctpt.matmul(spec, base.ctmat, base.plain, AU, BU, base.ws)
         return AU.view(u.ncols, sizes.rows_A), BU.view(u.ncols, d1)
 

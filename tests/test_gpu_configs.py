@@ -180,6 +180,8 @@ def test_config4_skinny_sweep_full_size(monkeypatch):
         sz = ctpt.query_sizes(sp)
         AU = torch.empty(sz.out_AU_bytes // 4, dtype=torch.int32, device="cuda")
         BU = torch.empty(sz.out_BU_bytes // 4, dtype=torch.int32, device="cuda")
+        if eng.ws.numel() < sz.workspace_bytes:  # d3_loc <= 32 adds the raw-byte kernel's U_exp + partials
+            eng.ws = torch.empty(sz.workspace_bytes, dtype=torch.uint8, device="cuda")
         ctpt.matmul(sp, eng.ctmat, eng.plain, AU, BU, eng.ws)
         torch.cuda.synchronize()
         AUn = dev_to_u32(AU).reshape(c1 - c0, c.rows_A)
