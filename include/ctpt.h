@@ -46,6 +46,12 @@
  *    ctpt_last_error() describes the problem.  Asynchronous CUDA faults surface as
  *    CTPT_ERR_CUDA on a later call.
  *  - Calls on distinct streams and distinct buffers may run concurrently.
+ *  - Kernel-choice knobs for A/B measurements only (environment, read at every call; the
+ *    defaults are the measured best): CTPT_GEMM=2cta (CTA-pair GEMM instead of single-CTA),
+ *    CTPT_SKINNY=off (no fused skinny kernels), CTPT_MV=off (no raw-byte kernel for d3 ≤ 32),
+ *    CTPT_FUSED_LOAD=regs (converter register loads instead of the TMA raw ring),
+ *    CTPT_FUSED_PF=n (L2 prefetch distance in the fused kernel), CTPT_GROUP_J=n (GEMM raster
+ *    group).  None of them changes a result.
  */
 #ifndef CTPT_H_
 #define CTPT_H_

@@ -47,7 +47,6 @@ struct LayoutParams {
   const uint32_t* b;  // [L][d2][d1]
   uint32_t* x;        // [L][R][d2p]
   int64_t rows_A, d1, R, d2, d2p;
-  const uint32_t* primes_dev;  // unused (primes passed in p_arr)
   uint32_t p_arr[64];
   int32_t validate;
   uint32_t* bad_flag;  // device word, OR-ed with 1 on a residue ≥ p

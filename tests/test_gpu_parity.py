@@ -257,11 +257,14 @@ def test_skinny_fused_direct_entry_point():
         ctpt.gemm_fused(big, 0, eng.ctmat, eng.plain, AU, BU)
 
 
-def test_skinny_adversarial_residues(monkeypatch):
-    """The fused split on residues 0, 1, (p±1)/2, p−1, p−2 with U digits at −128 / 127 and
-    d2 = 65536 (the int32 exactness limit) — C_ℓ reaches ±d2·255·128."""
+@pytest.mark.parametrize("d3", [130, 20])
+def test_skinny_adversarial_residues(d3, monkeypatch):
+    """The fused split (d3 = 130) and the raw-byte kernel (d3 = 20, K split into exact partials)
+    on residues 0, 1, (p±1)/2, p−1, p−2 with U digits at −128 / 127 and d2 = 65536 (the int32
+    exactness limit) — C_ℓ reaches ±d2·255·128."""
     monkeypatch.delenv("CTPT_SKINNY", raising=False)
-    fmt, N, d2, d3 = R, 64, 65536, 130
+    monkeypatch.delenv("CTPT_MV", raising=False)
+    fmt, N, d2 = R, 64, 65536
     ps = ctgen.primes(1)
     p = ps[0]
     rng = np.random.default_rng(3)
@@ -271,7 +274,7 @@ def test_skinny_adversarial_residues(monkeypatch):
     a[0, :, 0] = (64 << 24) | 0xFFFFFF
     U = rng.choice(np.array([-128, 127, -1, 0, 1], dtype=np.int64), size=(d2, d3))
     U[:, 0] = -128
-    U[:, 129] = 127
+    U[:, d3 - 1] = 127
     (AU, BU), eng = run_gpu(fmt, N, N, d2, d3, ps, a, b, U=U)
     assert eng.spec.kU == 1
     wa, wb = oracle_outputs(fmt, N, N, a[0], b[0], U, p)
