@@ -336,6 +336,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "pct_int8_datasheet": 100.0 * value * 4 * kU / world / INT8_DATASHEET_MACS,
         "rescale": bool(args.rescale),
         "vs_cublaslt_int8": cublaslt_ratio(value * 4 * kU / world, elapsed_ms),
+        # % of the clock-normalised peak 148 SMs × 8192 int8 MAC/clk × the median
+        # SM clock sampled during the timed region (how busy the tensor pipe is per clock)
+        "pct_int8_clock_normalised": (100.0 * value * 4 * kU / world / (148 * 8192 * clocks["sm_mhz"] * 1e6)
+                                      if clocks.get("sm_mhz") else None),
         "roofline": roofline_fused(c, d3l, gemm_avg_s, gemm_share, mp, which) if fused else {
                      "bound": "tensor", "achieved": achieved_tops, "peak": peak_tops, "unit": "TOP/s",
                      "frac": achieved_tops / peak_tops, "traffic": traffic if not args.rescale else None,

@@ -121,3 +121,70 @@ def gpu_compute_fn(fmt: int, N: int, d1: int, d2: int, d3: int, primes: list, ge
         return AU.view(u.ncols, sizes.rows_A), BU.view(u.ncols, d1)
 
     return compute
+
+
+# ----------------------------------------------------------------------------------------------
+# Fused compute + gather over peer memory (NVLink / NVSwitch on one node)
+# ----------------------------------------------------------------------------------------------
+def share_gather_buffers(out_AU, out_BU, rank: int, group=None):
+    """Rank 0's output buffers mapped into every rank's address space (CUDA IPC through torch's
+    tensor-sharing reductions; on one node with NVLink the mapping is peer memory).  Rank 0 passes
+    its tensors, the others pass None; every rank gets (AU, BU) tensors aliasing rank 0's memory."""
+    import torch.distributed as dist
+    from torch.multiprocessing.reductions import reduce_tensor
+
+    obj = [None]
+    if rank == 0:
+        obj[0] = (reduce_tensor(out_AU), reduce_tensor(out_BU))
+    dist.broadcast_object_list(obj, src=0, group=group)
+    if rank == 0:
+        return out_AU, out_BU
+    (fa, aa), (fb, ab) = obj[0]
+    return fa(*aa), fb(*ab)
+
+
+def run_fused_gather(units_per_rank: list[list[Unit]], rank: int, compute_into: Callable, peer_AU, peer_BU,
+                     group=None):
+    """Every rank computes its units with `compute_into(unit, AU_dst, BU_dst)`, whose kernels'
+    epilogues store the reduced residues DIRECTLY into rank 0's gathered layout
+    (peer_AU [L][d3][rows_A], peer_BU [L][d3][d1], mapped by share_gather_buffers): the transfer
+    over NVLink is the GEMM's own stores, tile by tile, with no staging copy and no collective.
+    A unit's block peer_AU[l, c0:c1] is contiguous, so it is a plain output pointer for
+    ctpt_matmul.  Ends with a device sync and a barrier, after which rank 0 holds the result."""
+    import torch
+    import torch.distributed as dist
+
+    for u in units_per_rank[rank]:
+        compute_into(u, peer_AU[u.l, u.c0:u.c1], peer_BU[u.l, u.c0:u.c1])
+    torch.cuda.synchronize()
+    dist.barrier(group=group)
+
+
+def gpu_compute_into_fn(fmt: int, N: int, d1: int, d2: int, d3: int, primes: list, get_ciphertexts: Callable, U,
+                        device):
+    """compute_into(unit, AU_dst, BU_dst) for one GPU: ctpt_layout + precompute once per prime,
+    then ctpt_matmul on the unit's column block writing into the (possibly peer-mapped)
+    destination blocks."""
+    import torch
+
+    from . import ctpt
+    from .engine import CpmmEngine
+
+    cache = {}
+
+    def compute_into(u: Unit, AU_dst, BU_dst):
+        if u.l not in cache:
+            cache.clear()
+            eng = CpmmEngine(ctpt.Spec(fmt, N, d1, d2, d3, [primes[u.l]]), device)
+            a, b = get_ciphertexts(u.l)
+            eng.layout(a, b)
+            eng.precompute(U)
+            cache[u.l] = eng
+        base = cache[u.l]
+        spec = dataclasses.replace(base.spec, col_begin=u.c0, col_end=u.c1)
+        sizes = ctpt.query_sizes(spec)
+        if base.ws.numel() < sizes.workspace_bytes:
+            base.ws = torch.empty(sizes.workspace_bytes, dtype=torch.uint8, device=device)
+        ctpt.matmul(spec, base.ctmat, base.plain, AU_dst, BU_dst, base.ws)
+
+    return compute_into
