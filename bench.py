@@ -55,6 +55,10 @@ def parse():
     ap.add_argument("--shard", action="store_true",
                     help="strong scaling: shard ONE problem's (prime, column) units over the ranks "
                          "(shard.plan_units); host-resident inputs/outputs via ctpt_matmul_host")
+    ap.add_argument("--gather", default="host", choices=["host", "ipc"],
+                    help="with --shard: 'host' = host-resident streaming (ctpt_matmul_host); 'ipc' = "
+                         "device-resident units whose GEMM epilogues write straight into rank 0's "
+                         "gathered output through peer (IPC) mappings — the fused compute + gather")
     return ap.parse_args()
 
 
@@ -556,6 +560,102 @@ def run_sharded(args, rank: int, world: int, local_rank: int):
             "clocks": clocks, "input_generation_s": gen_s}))
 
 
+def run_sharded_ipc(args, rank: int, world: int, local_rank: int):
+    """One problem sharded over the ranks by (prime, U-column) units with the
+    FUSED gather: every rank's inputs are device-resident (one laid-out X per prime it needs) and
+    its GEMM epilogues store the output residues directly into rank 0's gathered [L][d3][rows]
+    buffers, mapped into every rank by CUDA IPC (peer memory over NVLink on a multi-GPU node).
+    Timed: barrier → all units → device sync → barrier, max over ranks; "scaling": "strong"."""
+    import torch
+
+    import ctgen
+    from paper_2503_16080_b200 import ctpt
+    from paper_2503_16080_b200.engine import CpmmEngine
+    from paper_2503_16080_b200.shard import plan_units, primes_needed, share_gather_buffers
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    c = ctgen.CONFIGS[args.config]
+    cores = os.cpu_count() or 1
+    ps = ctgen.primes(c.L)
+    plan = plan_units(c.L, c.d3, world)
+    mine = plan[rank]
+    t0 = time.perf_counter()
+    U = ctgen.U_matrix(c.seed, c.d2, c.d3, c.u_bound, nthreads=max(1, cores // world))
+    engines = {}
+    shared_ws = None  # one workspace for all of this rank's primes (units run one after another)
+    for l in primes_needed(mine):
+        ct = ctgen.encrypt(c.fmt, c.N, c.d1, c.d2, c.seed, c.log_delta, [ps[l]], nthreads=max(1, cores // world))
+        eng = CpmmEngine(ctpt.Spec(c.fmt, c.N, c.d1, c.d2, c.d3, [ps[l]]), dev)
+        if shared_ws is None:
+            shared_ws = eng.ws
+        else:
+            eng.ws = shared_ws
+            torch.cuda.empty_cache()
+        eng.layout(ct.a_polys, ct.b_polys)
+        del ct
+        eng.precompute(U)
+        engines[l] = eng
+    gen_s = time.perf_counter() - t0
+    ra = c.rows_A
+    out_AU = torch.empty((c.L, c.d3, ra), dtype=torch.int32, device=dev) if rank == 0 else None
+    out_BU = torch.empty((c.L, c.d3, c.d1), dtype=torch.int32, device=dev) if rank == 0 else None
+    peer_AU, peer_BU = share_gather_buffers(out_AU, out_BU, rank) if world > 1 else (out_AU, out_BU)
+    specs = []
+    for u in mine:
+        eng = engines[u.l]
+        sp = dataclasses.replace(eng.spec, col_begin=u.c0, col_end=u.c1)
+        need = ctpt.query_sizes(sp).workspace_bytes
+        if shared_ws.numel() < need:
+            shared_ws = torch.empty(need, dtype=torch.uint8, device=dev)
+        specs.append(sp)
+    for eng in engines.values():
+        eng.ws = shared_ws
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        for u, sp in zip(mine, specs):
+            eng = engines[u.l]
+            ctpt.matmul(sp, eng.ctmat, eng.plain, peer_AU[u.l, u.c0:u.c1], peer_BU[u.l, u.c0:u.c1], eng.ws,
+                        stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    clk = ClockSampler(local_rank)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()  # every rank's stores into rank 0's buffers have landed
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    kU = engines[mine[0].l].spec.kU
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": c.residue_macs / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+            "config": dict(workload_desc(c), parallelism=f"sharded over {world} rank(s), fused gather (IPC peer "
+                                                        f"stores from the GEMM epilogues): "
+                                                        f"{[[(u.l, u.c0, u.c1) for u in us] for us in plan]}",
+                           path="device-resident laid-out X per prime -> ctpt_matmul per unit -> rank 0's "
+                                "gathered output"),
+            "e2e": {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                    "note": "device-resident inputs; see --gather host for the host-buffer path"},
+            "gpu_launches": (2 if c.d3 > 256 else 1) * len(mine) * args.steps if kU == 1 else None,
+            "clocks": clocks, "input_generation_s": gen_s}))
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -570,7 +670,9 @@ def main():
         torch.cuda.set_device(local_rank)
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        if args.shard:
+        if args.shard and args.gather == "ipc":
+            run_sharded_ipc(args, rank, world, local_rank)
+        elif args.shard:
             run_sharded(args, rank, world, local_rank)
         else:
             run_ours(args, rank, world, local_rank)
