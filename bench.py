@@ -594,7 +594,14 @@ def run_sharded_ipc(args, rank: int, world: int, local_rank: int):
             torch.cuda.empty_cache()
         eng.layout(ct.a_polys, ct.b_polys)
         del ct
-        eng.precompute(U)
+        if not engines:
+            eng.precompute(U)
+        else:  # the same U for every prime: share the first engine's digit planes
+            first = next(iter(engines.values()))
+            eng.plain = first.plain
+            eng.spec = dataclasses.replace(eng.spec, kU=first.spec.kU, u_unsigned=first.spec.u_unsigned,
+                                           u_offset=first.spec.u_offset)
+            eng.sizes = ctpt.query_sizes(eng.spec)
         engines[l] = eng
     gen_s = time.perf_counter() - t0
     ra = c.rows_A
