@@ -67,7 +67,7 @@ typedef enum {
   CTPT_OK = 0,
   CTPT_ERR_ARG = 1,         /* null pointer, bad enum, bad buffer size                              */
   CTPT_ERR_SHAPE = 2,       /* Table 1 dimension rules violated, or d2/d3 < 1          */
-  CTPT_ERR_MODULUS = 3,     /* primes must be odd, distinct and 2 < p < 2^31                        */
+  CTPT_ERR_MODULUS = 3,     /* moduli must be distinct odd primes, 2 < p < 2^31                       */
   CTPT_ERR_OVERFLOW = 4,    /* exactness bound of the int8 limb products would fail (refuse, never
                                round: Lemma le:strategy1's d2·‖limb‖·‖limb‖ bound, K = 2^8)          */
   CTPT_ERR_RANGE = 5,       /* an input residue ≥ p (validate=1), or |U| too large for a shared plane */

@@ -49,6 +49,35 @@ struct Dims {
 
 int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
+// Deterministic Miller–Rabin for n < 2^32 (witnesses 2, 7, 61 suffice below 4,759,123,141):
+// the moduli must be primes — the Rescale inverts q_1 modulo each of them (Fermat), and the RNS
+// result is only meaningful for pairwise coprime moduli.
+bool is_prime_u32(uint32_t n) {
+  if (n < 2) return false;
+  for (uint32_t q : {2u, 3u, 5u, 7u, 11u, 13u}) {
+    if (n == q) return true;
+    if (n % q == 0) return false;
+  }
+  auto mulmod = [n](uint64_t a, uint64_t b) { return a * b % n; };
+  uint32_t d = n - 1;
+  int r = 0;
+  while (!(d & 1)) { d >>= 1; ++r; }
+  for (uint64_t a : {2ull, 7ull, 61ull}) {
+    if (a % n == 0) continue;
+    uint64_t x = 1, b = a % n;
+    for (uint32_t e = d; e; e >>= 1, b = mulmod(b, b))
+      if (e & 1) x = mulmod(x, b);
+    if (x == 1 || x == n - 1) continue;
+    bool comp = true;
+    for (int i = 1; i < r && comp; ++i) {
+      x = mulmod(x, x);
+      if (x == n - 1) comp = false;
+    }
+    if (comp) return false;
+  }
+  return true;
+}
+
 ctpt_status check_problem(const ctpt_problem* pb, Dims& d) {
   if (!pb) return fail(CTPT_ERR_ARG, "problem is NULL");
   if (pb->fmt < CTPT_RLWE || pb->fmt > CTPT_STRUCT_A) return fail(CTPT_ERR_UNSUPPORTED, "unknown format %d", pb->fmt);
@@ -62,6 +91,7 @@ ctpt_status check_problem(const ctpt_problem* pb, Dims& d) {
   for (int i = 0; i < pb->L; ++i) {
     const uint32_t p = pb->primes[i];
     if (p < 3 || !(p & 1u) || p >= (1u << 31)) return fail(CTPT_ERR_MODULUS, "prime %u must be odd and in (2, 2^31)", p);
+    if (!is_prime_u32(p)) return fail(CTPT_ERR_MODULUS, "modulus %u is not prime", p);
     for (int j = 0; j < i; ++j)
       if (pb->primes[j] == p) return fail(CTPT_ERR_MODULUS, "prime %u repeated", p);
   }
@@ -92,12 +122,11 @@ ctpt_status check_problem(const ctpt_problem* pb, Dims& d) {
 
 size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
-// d_ws of ctpt_matmul: the 4 limb planes of one prime [4][R][d2p] u8, then (Rescale only) the
-// last prime's product per column [d3_loc][R] u32.
 // d_ws of ctpt_matmul / ctpt_split / ctpt_gemm, in this order:
 //   limbs   [4][R][d2p] u8                      (one prime's byte-limb planes)
 //   rowcorr [R] u32        (unsigned-U mode with u_offset ≠ 0: u_offset·Σ_k X[r][k] mod p)
 //   xlast   [d3_loc][R] u32 (rescale: the last prime's product)
+//   mv      U_exp + K-split partials + tickets   (d3_loc ≤ 32: the raw-byte kernel, MvPlan)
 bool needs_rowcorr(const ctpt_problem* pb) { return pb->u_unsigned && pb->u_offset != 0; }
 size_t ws_limb_bytes(const Dims& d) { return static_cast<size_t>(4) * d.R * d.d2p; }
 size_t ws_corr_off(const Dims& d) { return align256(ws_limb_bytes(d)); }

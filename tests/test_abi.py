@@ -31,7 +31,7 @@ def test_version(ctpt):
 
 
 def _spec(ctpt, **kw):
-    base = dict(fmt=ctpt.SHARED_A, N=16, d1=64, d2=48, d3=20, primes=[2147418113])
+    base = dict(fmt=ctpt.SHARED_A, N=16, d1=64, d2=48, d3=20, primes=[2147352577])
     base.update(kw)
     return ctpt.Spec(**base)
 
@@ -46,7 +46,7 @@ def test_sizes(ctpt):
     assert s.out_AU_bytes == 20 * 16 * 4 and s.out_BU_bytes == 20 * 64 * 4
     s2 = ctpt.query_sizes(_spec(ctpt, fmt=ctpt.SHARED_S, d2=50, col_begin=3, col_end=11))
     assert s2.rows_A == 64 and s2.R == 128 and s2.d2p == 64 and s2.d3_loc == 8
-    s3 = ctpt.query_sizes(_spec(ctpt, fmt=ctpt.RLWE, d1=16, primes=[2147418113, 2146959361]))
+    s3 = ctpt.query_sizes(_spec(ctpt, fmt=ctpt.RLWE, d1=16, primes=[2147352577, 2146959361]))
     assert s3.out_BU_bytes == 2 * 20 * 16 * 4
 
 
@@ -57,9 +57,11 @@ def test_sizes(ctpt):
     (dict(d2=0), "ERR_SHAPE"),
     (dict(col_begin=5, col_end=5), "ERR_SHAPE"),
     (dict(col_end=21), "ERR_SHAPE"),
-    (dict(primes=[2147418113, 2147418113]), "ERR_MODULUS"),
+    (dict(primes=[2147352577, 2147352577]), "ERR_MODULUS"),
     (dict(primes=[2 ** 31 + 11]), "ERR_MODULUS"),
     (dict(primes=[1024]), "ERR_MODULUS"),
+    (dict(primes=[2147352577, 2147352577 - 2]), "ERR_MODULUS"),  # odd composite (divisible by 5)
+    (dict(primes=[2147352577, 1 << 30 | 1]), "ERR_MODULUS"),      # 2^30 + 1 = 5^2 · 13 · 41 · 61 · 1321
     (dict(d2=70000), "ERR_OVERFLOW"),
     (dict(fmt=7), "ERR_UNSUPPORTED"),
 ])
@@ -92,7 +94,7 @@ def test_fused_refuses_wide_or_multidigit_U_without_gpu(ctpt):
 
 def test_modmatmul_sizes_and_ldx_check_without_gpu(ctpt):
     """Mod-PP-MM entry points validate on the host: ldx = K rounded up to 16, d2 overflow."""
-    ps = [2147418113, 2146959361]
+    ps = [2147352577, 2146959361]
     ldx, plain, ws = ctpt.modmatmul_sizes(ps, 100, 77, 50)
     assert ldx == 80 and plain == 256 + 2 * 4 * 50 * 80 and ws == 4 * 100 * 80
     lib = ctpt.raw_lib()

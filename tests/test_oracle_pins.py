@@ -17,7 +17,7 @@ import pytest
 import oracle
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_fixtures.json")))
-P31 = 2147418113  # a prime < 2^31, ≡ 1 mod 2^16 (checked in test_ctgen)
+P31 = 2147352577  # a prime < 2^31, ≡ 1 mod 2^16 (checked in test_ctgen)
 
 
 # ------------------------------------------------------------------ rounding / encoding
