@@ -35,6 +35,7 @@ SHAPES = [
     (A, 1024, 3, 1000, 257, 2),
     (SA, 64, 3, 300, 260, 2),    # structured-A shared-a (Algorithm 7): only B·U
     (SA, 16, 5, 130, 100, 1),
+    (S, 16, 2, 48, 300, 8),      # L = 8 primes (config c5's basis) on a small shape
 ]
 
 
