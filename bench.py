@@ -131,9 +131,11 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------ CPU oracle
-def cpu_oracle_rate(c, ct, U, target_s: float):
+def cpu_oracle_rate(c, ct, U, target_s: float, gpu_out=None):
     """Residue-MAC/s of the oracle's schoolbook on a bounded sample of workload c: output
-    columns of prime 0 over all R stacked rows and the full d2 contraction."""
+    columns of prime 0 over all R stacked rows and the full d2 contraction.  With gpu_out =
+    (AU [d3][rows_A], BU [d3][d1]) of prime 0 from the timed run, the same oracle outputs also give
+    a parity verdict on the sampled columns (every entry compared)."""
     import oracle
 
     cores = os.cpu_count() or 1
@@ -151,14 +153,21 @@ def cpu_oracle_rate(c, ct, U, target_s: float):
     ncols2 = int(min(c.d3, max(ncols, ncols * target_s / max(dt, 1e-3))))
     ncols2 = max(cores, (ncols2 // cores) * cores) if ncols2 >= cores else ncols2
     t0 = time.perf_counter()
-    if Ac is not None:
-        oracle.modmatmul(Ac, U, p, cols=np.arange(ncols2), nthreads=cores)
-    oracle.modmatmul(Bc, U, p, cols=np.arange(ncols2), nthreads=cores)
+    wa = oracle.modmatmul(Ac, U, p, cols=np.arange(ncols2), nthreads=cores) if Ac is not None else None
+    wb = oracle.modmatmul(Bc, U, p, cols=np.arange(ncols2), nthreads=cores)
     dt = time.perf_counter() - t0
     macs = c.R * c.d2 * ncols2
-    return {"value": macs / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"prime 0, {ncols2} of {c.d3} output columns x all {c.R} stacked rows x d2={c.d2} "
-                      f"({macs:.3e} residue-MACs, {dt:.1f} s, schoolbook __int128, OpenMP {cores} threads)"}
+    out = {"value": macs / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+           "sample": f"prime 0, {ncols2} of {c.d3} output columns x all {c.R} stacked rows x d2={c.d2} "
+                     f"({macs:.3e} residue-MACs, {dt:.1f} s, schoolbook __int128, OpenMP {cores} threads)"}
+    if gpu_out is not None:
+        ga, gb = gpu_out
+        bad = int(np.count_nonzero(gb[:ncols2] != wb))
+        if wa is not None:
+            bad += int(np.count_nonzero(ga[:ncols2] != wa))
+        out["parity_on_sample"] = {"entries": int(ncols2 * c.R), "mismatches": bad,
+                                   "verdict": "bit-exact" if bad == 0 else "MISMATCH"}
+    return out
 
 
 # ------------------------------------------------------------------------------------ inputs
@@ -361,7 +370,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "input_generation_s": gen_s,
     }
     if rank == 0 and not args.no_cpu_baseline:
-        result["cpu_baseline"] = cpu_oracle_rate(c, ct, U, args.cpu_seconds)
+        gpu0 = None
+        if not args.rescale:  # prime 0's outputs of the last timed step, for the sampled parity verdict
+            n0 = d3l * ra
+            gpu0 = (AU[:n0].cpu().numpy().view(np.uint32).reshape(d3l, ra),
+                    BU[:d3l * c.d1].cpu().numpy().view(np.uint32).reshape(d3l, c.d1))
+        result["cpu_baseline"] = cpu_oracle_rate(c, ct, U, args.cpu_seconds, gpu0)
     if rank == 0:
         print(json.dumps(result))
 
