@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="run each prime's limb split and GEMM back to back on one stream")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target seconds of oracle work per sample")
     ap.add_argument("--rescale", action="store_true",
@@ -261,6 +263,17 @@ def run_ours(args, rank: int, world: int, local_rank: int):
              and os.environ.get("CTPT_SKINNY") != "off" and not args.rescale)
     n_ev = 1 if args.rescale else len(ps)
 
+    mv = fused and d3l <= 32 and os.environ.get("CTPT_MV") != "off"
+    # Split/GEMM overlap (split path): the limb split of prime l+1 runs on a side stream into the
+    # other of two workspaces while prime l's GEMM runs (the split needs no shared memory and
+    # little SM time, so it co-resides with the persistent GEMM); gemm(l) waits on split(l).
+    overlap = (not fused) and (not args.rescale) and not args.no_overlap
+    ws2 = [eng.ws, torch.empty_like(eng.ws)] if overlap else [eng.ws]
+    side = torch.cuda.Stream(dev) if overlap else stream
+    ev_split = [torch.cuda.Event() for _ in range(2)]
+    ev_free = [torch.cuda.Event() for _ in range(2)]
+    counter = [0]
+
     def step(ev_pairs=None):
         if args.rescale:  # the whole ctpt_matmul: last prime first, Rescale in the others' epilogues
             if ev_pairs is not None:
@@ -270,14 +283,26 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                 ev_pairs[0][1].record(stream)
             return
         for l in range(len(ps)):
+            au, bu = AU[l * d3l * ra:], BU[l * d3l * c.d1:]
             if not fused:
-                ctpt.split(spec, l, eng.ctmat, eng.ws, stream=stream)
+                b = counter[0] % len(ws2)
+                counter[0] += 1
+                if overlap:
+                    side.wait_event(ev_free[b])  # the GEMM that last read ws2[b] has finished
+                ctpt.split(spec, l, eng.ctmat, ws2[b], stream=side)
+                if overlap:
+                    ev_split[b].record(side)
+                    stream.wait_event(ev_split[b])
             if ev_pairs is not None:
                 ev_pairs[l][0].record(stream)
-            if fused:
-                ctpt.gemm_fused(spec, l, eng.ctmat, eng.plain, AU[l * d3l * ra:], BU[l * d3l * c.d1:], stream=stream)
+            if mv:
+                ctpt.gemm_mv(spec, l, eng.ctmat, eng.plain, au, bu, eng.ws, stream=stream)
+            elif fused:
+                ctpt.gemm_fused(spec, l, eng.ctmat, eng.plain, au, bu, stream=stream)
             else:
-                ctpt.gemm(spec, l, eng.ws, eng.plain, AU[l * d3l * ra:], BU[l * d3l * c.d1:], stream=stream)
+                ctpt.gemm(spec, l, ws2[b], eng.plain, au, bu, stream=stream)
+                if overlap:
+                    ev_free[b].record(stream)
             if ev_pairs is not None:
                 ev_pairs[l][1].record(stream)
 
@@ -295,6 +320,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     clk = ClockSampler(local_rank)
     time.sleep(0.3)  # let the sampler start
     t_start.record(stream)
+    if overlap:
+        side.wait_event(t_start)  # the first split belongs to the timed region
     for s in range(args.steps):
         step(gemm_ev[s])
     t_end.record(stream)
@@ -353,7 +380,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         # SM clock sampled during the timed region (how busy the tensor pipe is per clock)
         "pct_int8_clock_normalised": (100.0 * value * 4 * kU / world / (148 * 8192 * clocks["sm_mhz"] * 1e6)
                                       if clocks.get("sm_mhz") else None),
-        "roofline": roofline_fused(c, d3l, gemm_avg_s, gemm_share, mp, which) if fused else {
+        "roofline": roofline_fused(c, d3l, gemm_avg_s, gemm_share, mp, which, "k_gemm_mv" if mv else "k_gemm_fused")
+        if fused else {
                      "bound": "tensor", "achieved": achieved_tops, "peak": peak_tops, "unit": "TOP/s",
                      "frac": achieved_tops / peak_tops, "traffic": traffic if not args.rescale else None,
                      "kernel": ("ctpt_matmul: k_split + kU passes of k_gemm_tc per prime, Rescale epilogue"
@@ -364,8 +392,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                                     else f"{limb_macs_launch:.4e} limb MACs (4·kU·R·d2·d3, one prime)"),
                      "avg_launch_ms": gemm_avg_s * 1e3, "share_of_step": gemm_share},
         "e2e": e2e,
-        # per prime: k_split[_rows] + kU x k_gemm_tc, or one k_gemm_fused
-        "gpu_launches": (1 if fused else 1 + kU) * len(ps) * args.steps,
+        # per prime: k_split[_rows] + kU x k_gemm_tc, or one k_gemm_fused / k_gemm_mv (+ k_expand_u)
+        "gpu_launches": (2 if mv else 1 if fused else 1 + kU) * len(ps) * args.steps,
+        "split_overlap": overlap,
         "clocks": clocks,
         "input_generation_s": gen_s,
     }
@@ -393,13 +422,13 @@ def cublaslt_ratio(limb_macs_per_s: float, elapsed_ms: float):
     return {"ratio": 2 * limb_macs_per_s / 1e12 / float(pr[key]), "cublaslt_tops": pr[key], "which": key}
 
 
-def roofline_fused(c, d3l, launch_s, share, mp, which):
+def roofline_fused(c, d3l, launch_s, share, mp, which, kernel="k_gemm_fused"):
     """HBM roofline of k_gemm_fused (skinny U): algorithmic bytes per launch (one prime) = 4·R·d2
     (X int32, read once) + d3·d2 (U digits) + 4·R·d3 (outputs)."""
     alg = 4 * c.R * c.d2 + d3l * c.d2 + 4 * c.R * d3l
     gbs = alg / launch_s / 1e9
     return {"bound": "hbm", "achieved": gbs, "peak": float(mp["hbm_gbs"]), "unit": "GB/s",
-            "frac": gbs / float(mp["hbm_gbs"]), "traffic": None, "kernel": "k_gemm_fused",
+            "frac": gbs / float(mp["hbm_gbs"]), "traffic": None, "kernel": kernel,
             "peak_source": f"{which}: hbm_gbs", "per_launch": f"{alg} algorithmic bytes (4·R·d2 + d3·d2 + 4·R·d3)",
             "avg_launch_ms": launch_s * 1e3, "share_of_step": share}
 
