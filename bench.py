@@ -46,8 +46,9 @@ def parse():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--no-overlap", action="store_true",
-                    help="run each prime's limb split and GEMM back to back on one stream")
+    ap.add_argument("--overlap", action="store_true",
+                    help="experiment: run prime l+1's limb split on a side stream during prime l's GEMM "
+                         "(measured slower; default off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target seconds of oracle work per sample")
     ap.add_argument("--rescale", action="store_true",
@@ -267,7 +268,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     # Split/GEMM overlap (split path): the limb split of prime l+1 runs on a side stream into the
     # other of two workspaces while prime l's GEMM runs (the split needs no shared memory and
     # little SM time, so it co-resides with the persistent GEMM); gemm(l) waits on split(l).
-    overlap = (not fused) and (not args.rescale) and not args.no_overlap
+    # Measured (profiles/r01/split_overlap_experiment): with the overlap the GEMM slows from 14.05 to
+    # 16.05 ms per launch — the co-resident split costs it far more than the 0.45 ms it hides —
+    # so it is off unless asked for (--overlap).
+    overlap = (not fused) and (not args.rescale) and args.overlap
     ws2 = [eng.ws, torch.empty_like(eng.ws)] if overlap else [eng.ws]
     side = torch.cuda.Stream(dev) if overlap else stream
     ev_split = [torch.cuda.Event() for _ in range(2)]
