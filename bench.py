@@ -326,8 +326,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     t_start.record(stream)
     if overlap:
         side.wait_event(t_start)  # the first split belongs to the timed region
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    step_ev[0].record(stream)
     for s in range(args.steps):
         step(gemm_ev[s])
+        step_ev[s + 1].record(stream)
     t_end.record(stream)
     torch.cuda.synchronize(dev)
     clocks = clk.stop()
@@ -335,6 +338,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         torch.distributed.barrier()
     elapsed_ms = t_start.elapsed_time(t_end)
     gemm_ms = [a.elapsed_time(b) for row in gemm_ev for (a, b) in row]
+    step_ms = [step_ev[i].elapsed_time(step_ev[i + 1]) for i in range(args.steps)]
     if world > 1:
         t = torch.tensor([elapsed_ms], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -371,6 +375,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+        # per-step device times (the paper reports the mean of 10 runs)
+        "step_ms_stats": {"mean": statistics.mean(step_ms), "median": statistics.median(step_ms),
+                          "min": min(step_ms), "max": max(step_ms)},
         "config": dict(workload_desc(c), **{
             "l2": f"inputs {sizes.ctmat_bytes * 1.0 / 2**30:.2f} GiB per step > 126 MB L2 (no flush needed)",
             "parallelism": f"weak: {world} independent problem(s), one per GPU, no data-path collective",
