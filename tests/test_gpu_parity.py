@@ -619,3 +619,44 @@ def test_modmatmul_full_residues(M, K, Nc, L):
     for l, p in enumerate(ps):
         want = oracle.modmatmul(np.ascontiguousarray(X[l, :, :K].T), Y[l].astype(np.int64), p, nthreads=NTHREADS)
         assert np.array_equal(got[l], want), f"prime {l}: {np.count_nonzero(got[l] != want)} entries differ"
+
+
+# ------------------------------------------------------------------ CUDA graph capture
+@pytest.mark.parametrize("shape", [(R, 64, 1, 64, 64, 1), (A, 64, 3, 300, 20, 2), (S, 32, 2, 200, 300, 2)],
+                         ids=["c1_fused", "mv", "split_gemm"])
+def test_matmul_is_graph_capturable(shape, monkeypatch):
+    """ctpt_matmul never synchronises or allocates, so a CUDA graph can capture it (every kernel
+    path: fused, raw-byte with its memset + U expansion, split + GEMM) and replay it: the replayed
+    outputs equal the oracle, and a replay after changing the inputs in place recomputes them."""
+    import torch
+
+    from paper_2503_16080_b200 import ctpt
+    from paper_2503_16080_b200.engine import CpmmEngine
+
+    monkeypatch.delenv("CTPT_MV", raising=False)
+    fmt, N, k, d2, d3, L = shape
+    d1 = N * k
+    ps = ctgen.primes(L)
+    eng = CpmmEngine(ctpt.Spec(fmt, N, d1, d2, d3, ps), "cuda")
+    U = ctgen.U_matrix(3, d2, d3, 8)
+    AU, BU = eng.alloc_outputs()
+    s = torch.cuda.Stream()
+    for seed in (3, 4):
+        ct = ctgen.encrypt(fmt, N, d1, d2, seed, 20, ps)
+        eng.layout(ct.a_polys, ct.b_polys)
+        if seed == 3:
+            eng.precompute(U)
+            with torch.cuda.stream(s):
+                ctpt.matmul(eng.spec, eng.ctmat, eng.plain, AU, BU, eng.ws, stream=s)  # warm-up
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                ctpt.matmul(eng.spec, eng.ctmat, eng.plain, AU, BU, eng.ws, stream=s)
+        AU.zero_()
+        BU.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        AUn, BUn = eng.outputs_numpy(AU, BU)
+        for l, p in enumerate(ps):
+            wa, wb = oracle_outputs(fmt, N, d1, ct.a_polys[l], ct.b_polys[l], U, p)
+            assert np.array_equal(AUn[l], wa) and np.array_equal(BUn[l], wb), (seed, l)
