@@ -29,7 +29,9 @@ What it computes, and where the paper defines it (``P:n`` = PAPER.md line n):
 Every function is pinned by tests/test_oracle_pins.py against things the paper
 or mathematics fix (closed forms, SPEC/paper examples, brute force in exact
 Python integers).  The paper prints no numeric worked example for CP-MM
-(SURVEY.md §8(c) c4), so no function pins against a printed CP-MM output.
+(SURVEY.md §8(c) c4), so no function pins against a printed CP-MM output: against printed
+values the CP-MM functions are "parity unpinned"; each is pinned by the
+identities and brute-force cases listed in the tests instead.
 """
 from __future__ import annotations
 
