@@ -606,6 +606,8 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
   }
   P.u_unsigned = g.u_unsigned;
   if (const char* g = getenv("CTPT_GROUP_J")) P.group_j = std::max(1, atoi(g));  // tuning knob
+  P.l2_pf = 0;
+  if (const char* g = getenv("CTPT_GEMM_PF")) P.l2_pf = std::max(0, atoi(g));     // tuning knob
   P.m = m;
   const int sms = num_sms();
   const unsigned grid = pair ? static_cast<unsigned>(2 * std::min<int64_t>(nt, sms / 2))

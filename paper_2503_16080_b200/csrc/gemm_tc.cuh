@@ -46,6 +46,7 @@ struct TcParams {
   int32_t num_tiles;
   int32_t group_j;    // tiles visited in groups of group_j j-tiles (L2 reuse of U panels)
   int32_t u_unsigned; // U plane is u8 (U + u_offset) instead of balanced s8 digits
+  int32_t l2_pf;      // prefetch the operands of the iteration this far ahead into L2 (0: off)
   ModP m;
   OutParams o;
 };
@@ -100,10 +101,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      // L2 prefetch of the (tile, k-block) iteration l2_pf ahead of the TMA loads: covers the
+      // DRAM latency of first-touch X / U panels that a 4-stage shared-memory ring cannot
+      int32_t pf_tile = blockIdx.x, pf_kb = 0;
+      auto pf_advance = [&]() {
+        if (++pf_kb == P.num_kb) { pf_kb = 0; pf_tile += gridDim.x; }
+      };
+      auto pf_issue = [&]() {
+        if (pf_tile < P.num_tiles) {
+          int32_t ptj, ptr;
+          tc_tile_coords(pf_tile, P, ptj, ptr);
+          tma_prefetch_l2_3d(&tmX, pf_kb * TC_BLOCK_K, ptr * TC_BLOCK_R, 0);
+          tma_prefetch_l2_3d(&tmU, pf_kb * TC_BLOCK_K, P.j_off + ptj * TC_BLOCK_J, P.plane);
+        }
+      };
+      for (int32_t i = 0; i < P.l2_pf; ++i) { pf_issue(); pf_advance(); }
       for (int32_t tile = blockIdx.x; tile < P.num_tiles; tile += gridDim.x) {
         int32_t tj, tr;
         tc_tile_coords(tile, P, tj, tr);
         for (int32_t kb = 0; kb < P.num_kb; ++kb) {
+          if (P.l2_pf > 0) { pf_issue(); pf_advance(); }
           mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t su = sbase + stage * TC_STAGE_BYTES;
           mbar_arrive_expect_tx(full_bar(stage), TC_STAGE_BYTES);
