@@ -234,18 +234,16 @@ ctpt_status tc_setup() {
     e = cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BYTES);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_gemm_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, T2_SMEM_BYTES);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_gemm_fused<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(1, false));
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_gemm_fused<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(2, false));
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_gemm_fused<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(1, true));
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_gemm_fused<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(2, true));
+#define CTPT_FU_ATTR(NG, MODE) \
+    if (e == cudaSuccess)      \
+      e = cudaFuncSetAttribute(k_gemm_fused<NG, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(NG, MODE));
+    CTPT_FU_ATTR(1, FU_REGS)
+    CTPT_FU_ATTR(2, FU_REGS)
+    CTPT_FU_ATTR(1, FU_TMA)
+    CTPT_FU_ATTR(2, FU_TMA)
+    CTPT_FU_ATTR(1, FU_HYBRID)
+    CTPT_FU_ATTR(2, FU_HYBRID)
+#undef CTPT_FU_ATTR
   });
   if (e != cudaSuccess) return fail(CTPT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
   return CTPT_OK;
@@ -651,22 +649,33 @@ ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st) 
   P.o.accumulate = 0;
   P.o.w = 1;
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>(nt, num_sms()));
-  // raw X by TMA (default) or by converter-thread loads (CTPT_FUSED_LOAD=regs, for A/B runs)
-  bool tma_x = true;
-  if (const char* e = getenv("CTPT_FUSED_LOAD")) tma_x = strcmp(e, "regs") != 0;
+  // how the converters get X: TMA raw ring (default), half TMA / half register loads
+  // (CTPT_FUSED_LOAD=hybrid) or register loads only (=regs) — for A/B runs
+  int mode = FU_TMA;
+  if (const char* e = getenv("CTPT_FUSED_LOAD")) {
+    if (strcmp(e, "regs") == 0) mode = FU_REGS;
+    if (strcmp(e, "hybrid") == 0) mode = FU_HYBRID;
+  }
   // L2 prefetch distance for the raw X ring (iterations ahead of the TMA into shared memory)
   P.l2_prefetch = 0;  // measured: any L2 prefetch distance (2..16) lowered the fused kernel 5–35 %
   if (const char* e = getenv("CTPT_FUSED_PF")) P.l2_prefetch = std::max(0, atoi(e));
   CUtensorMap tmX;
-  s = make_tmap_2d(&tmX, x, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, d.d2p, g.R, FU_BLOCK_K, FU_BLOCK_R);
+  s = make_tmap_2d(&tmX, x, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, d.d2p, g.R, FU_BLOCK_K,
+                   static_cast<uint32_t>(fu_raw_rows(mode)));
   if (s != CTPT_OK) return s;
-  if (d.d3_loc <= 128) {
-    if (tma_x) k_gemm_fused<1, true><<<grid, FU_THREADS, fu_smem_bytes(1, true), st>>>(tmU, tmX, P);
-    else k_gemm_fused<1, false><<<grid, FU_THREADS, fu_smem_bytes(1, false), st>>>(tmU, tmX, P);
+  const int ng = d.d3_loc <= 128 ? 1 : 2;
+#define CTPT_FU_LAUNCH(NG, MODE) \
+  k_gemm_fused<NG, MODE><<<grid, FU_THREADS, fu_smem_bytes(NG, MODE), st>>>(tmU, tmX, P)
+  if (ng == 1) {
+    if (mode == FU_TMA) CTPT_FU_LAUNCH(1, FU_TMA);
+    else if (mode == FU_HYBRID) CTPT_FU_LAUNCH(1, FU_HYBRID);
+    else CTPT_FU_LAUNCH(1, FU_REGS);
   } else {
-    if (tma_x) k_gemm_fused<2, true><<<grid, FU_THREADS, fu_smem_bytes(2, true), st>>>(tmU, tmX, P);
-    else k_gemm_fused<2, false><<<grid, FU_THREADS, fu_smem_bytes(2, false), st>>>(tmU, tmX, P);
+    if (mode == FU_TMA) CTPT_FU_LAUNCH(2, FU_TMA);
+    else if (mode == FU_HYBRID) CTPT_FU_LAUNCH(2, FU_HYBRID);
+    else CTPT_FU_LAUNCH(2, FU_REGS);
   }
+#undef CTPT_FU_LAUNCH
   CUDA_TRY(cudaGetLastError());
   return CTPT_OK;
 }

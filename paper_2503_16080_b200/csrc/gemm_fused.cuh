@@ -34,16 +34,23 @@ constexpr int FU_THREADS = 512;
 constexpr int FU_CONV_WARP0 = 8;
 constexpr int FU_CONV_WARPS = 8;
 constexpr int FU_ROWS_PER_WARP = FU_BLOCK_R / FU_CONV_WARPS; // 8
-constexpr int FU_RAW_BYTES = FU_BLOCK_R * FU_BLOCK_K * 4;   // one raw int32 X tile: 32 KB
-// Two ways to feed the converters (template TMA_X):
-//   false: each converter thread loads its residues into registers, two K-blocks ahead;
-//   true:  a TMA producer streams raw int32 X tiles into a ring of RAW stages (96–128 KB in
-//          flight per SM, no register cost) and converters read them with LDS.128.
-__host__ __device__ constexpr int fu_stages(int ng, bool tma_x) { return tma_x ? 2 : (ng == 1 ? 4 : 3); }
-__host__ __device__ constexpr int fu_raw_stages(int ng, bool tma_x) { return tma_x ? (ng == 1 ? 4 : 3) : 0; }
+// Three ways to feed the converters (template MODE):
+//   FU_REGS:   each converter thread loads its residues into registers, two K-blocks ahead;
+//   FU_TMA:    a TMA producer streams raw int32 X tiles (64 rows) into a ring of RAW stages
+//              (96–128 KB in flight per SM, no register cost), converters read them with LDS.128;
+//   FU_HYBRID: rows 0–31 of every tile through the TMA ring (32-row raw tiles, twice as many
+//              stages in the same bytes), rows 32–63 by register loads — half the raw
+//              shared-memory round trip (the kernel is bound by shared-memory bandwidth).
+constexpr int FU_REGS = 0, FU_TMA = 1, FU_HYBRID = 2;
+__host__ __device__ constexpr int fu_raw_rows(int mode) { return mode == FU_HYBRID ? 32 : FU_BLOCK_R; }
+__host__ __device__ constexpr int fu_raw_bytes(int mode) { return fu_raw_rows(mode) * FU_BLOCK_K * 4; }
+__host__ __device__ constexpr int fu_stages(int ng, int mode) { return mode != FU_REGS ? 2 : (ng == 1 ? 4 : 3); }
+__host__ __device__ constexpr int fu_raw_stages(int ng, int mode) {
+  return mode == FU_REGS ? 0 : ((ng == 1 ? 128 : 96) * 1024) / fu_raw_bytes(mode);
+}
 __host__ __device__ constexpr int fu_stage_bytes(int ng) { return ng * FU_U_BYTES + FU_X_BYTES; }
-__host__ __device__ constexpr int fu_smem_bytes(int ng, bool tma_x) {
-  return fu_stages(ng, tma_x) * fu_stage_bytes(ng) + fu_raw_stages(ng, tma_x) * FU_RAW_BYTES + 256 + 1024;
+__host__ __device__ constexpr int fu_smem_bytes(int ng, int mode) {
+  return fu_stages(ng, mode) * fu_stage_bytes(ng) + fu_raw_stages(ng, mode) * fu_raw_bytes(mode) + 256 + 1024;
 }
 
 struct FusedParams {
@@ -66,26 +73,29 @@ __device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
-template <int NG, bool TMA_X>
+template <int NG, int MODE>
 __global__ void __launch_bounds__(FU_THREADS, 1)
     k_gemm_fused(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmX,
                  const __grid_constant__ FusedParams P) {
-  constexpr int STAGES = fu_stages(NG, TMA_X);
-  constexpr int RAW = fu_raw_stages(NG, TMA_X);
+  constexpr bool TMA_X = MODE != FU_REGS;
+  constexpr int STAGES = fu_stages(NG, MODE);
+  constexpr int RAW = fu_raw_stages(NG, MODE);
+  constexpr int RAW_BYTES = fu_raw_bytes(MODE);
+  constexpr int RAW_WARPS = MODE == FU_HYBRID ? 4 : (MODE == FU_TMA ? FU_CONV_WARPS : 0);
   constexpr int STAGE_BYTES = fu_stage_bytes(NG);
   constexpr int NBUF = (NG == 1) ? 2 : 1;  // accumulator buffers (NBUF·NG·256 ≤ 512 columns)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
   const uint32_t raw_base = sbase + STAGES * STAGE_BYTES;
-  const uint32_t bar_base = raw_base + RAW * FU_RAW_BYTES;
+  const uint32_t bar_base = raw_base + RAW * RAW_BYTES;
   auto full_bar = [&](int s) { return bar_base + 8u * s; };
   auto empty_bar = [&](int s) { return bar_base + 8u * (STAGES + s); };
   auto tfull_bar = [&](int b) { return bar_base + 8u * (2 * STAGES + b); };
   auto tempty_bar = [&](int b) { return bar_base + 8u * (2 * STAGES + 2 + b); };
   const uint32_t tmem_slot = bar_base + 8u * (2 * STAGES + 4);
   uint32_t* tmem_slot_ptr =
-      reinterpret_cast<uint32_t*>(smem + STAGES * STAGE_BYTES + RAW * FU_RAW_BYTES + 8 * (2 * STAGES + 4));
+      reinterpret_cast<uint32_t*>(smem + STAGES * STAGE_BYTES + RAW * RAW_BYTES + 8 * (2 * STAGES + 4));
   auto raw_full = [&](int s) { return bar_base + 8u * (2 * STAGES + 5 + s); };
   auto raw_empty = [&](int s) { return bar_base + 8u * (2 * STAGES + 5 + RAW + s); };
 
@@ -108,7 +118,7 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
     }
     for (int s = 0; s < RAW; ++s) {
       mbar_init(raw_full(s), 1);
-      mbar_init(raw_empty(s), FU_CONV_WARPS);
+      mbar_init(raw_empty(s), RAW_WARPS);
     }
     if (TMA_X) tma_prefetch(&tmX);
     fence_mbar_init();
@@ -189,8 +199,8 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
           tma_prefetch_l2_2d(&tmX, c0, c1);
         }
         mbar_wait(raw_empty(rs), rphase ^ 1);
-        mbar_arrive_expect_tx(raw_full(rs), FU_RAW_BYTES);
-        tma_load_2d(raw_base + rs * FU_RAW_BYTES, &tmX, raw_full(rs), kb * FU_BLOCK_K, tr * FU_BLOCK_R);
+        mbar_arrive_expect_tx(raw_full(rs), RAW_BYTES);
+        tma_load_2d(raw_base + rs * RAW_BYTES, &tmX, raw_full(rs), kb * FU_BLOCK_K, tr * FU_BLOCK_R);
         if (++rs == RAW) { rs = 0; rphase ^= 1; }
       }
     } else if (!TMA_X && lane == 0 && P.l2_prefetch > 0) {
@@ -252,16 +262,44 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
     // of the K-block (one coalesced 512-B row segment per warp instruction).  Loads run two
     // iterations ahead of the stores (registers ra / rb).
     const int cw = warp - FU_CONV_WARP0;
-    if constexpr (TMA_X) {
-      int stage = 0, rs = 0;
-      uint32_t phase = 0, rphase = 0;
+    // this warp's 8 rows of every 64-row tile: raw-ring warps take rows [0, 8·RAW_WARPS) with
+    // stride RAW_WARPS, register warps the remaining rows with stride (8 − RAW_WARPS)
+    const bool from_raw = cw < RAW_WARPS;
+    const int rw = from_raw ? cw : cw - RAW_WARPS;                  // index within its group
+    const int rstride = from_raw ? RAW_WARPS : FU_CONV_WARPS - RAW_WARPS;
+    const int rbase = from_raw ? 0 : FU_ROWS_PER_WARP * RAW_WARPS;  // first row of its group
+    int stage = 0;
+    uint32_t phase = 0;
+    // store the limb words of this warp's 8 rows into the next limb stage (SWIZZLE_128B
+    // K-major: 16-B chunk c of row r at chunk position c ^ (r & 7)) and arrive on its barrier
+    auto store = [&](const uint32_t (&lw)[FU_ROWS_PER_WARP][4]) {
+      mbar_wait(empty_bar(stage), phase ^ 1);
+      const uint32_t sx = sbase + stage * STAGE_BYTES + NG * FU_U_BYTES;
+#pragma unroll
+      for (int i = 0; i < FU_ROWS_PER_WARP; ++i) {
+        const int row = rbase + rw + rstride * i;
+        const uint32_t off =
+            static_cast<uint32_t>(row) * 128u + ((((lane >> 2) ^ (row & 7)) << 4) | ((lane & 3) << 2));
+        sts32(sx + 0 * FU_BLOCK_R * 128 + off, lw[i][0]);
+        sts32(sx + 1 * FU_BLOCK_R * 128 + off, lw[i][1]);
+        sts32(sx + 2 * FU_BLOCK_R * 128 + off, lw[i][2]);
+        sts32(sx + 3 * FU_BLOCK_R * 128 + off, lw[i][3]);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(full_bar(stage));
+      if (++stage == STAGES) { stage = 0; phase ^= 1; }
+    };
+    if (from_raw) {
+      int rs = 0;
+      uint32_t rphase = 0;
       for (int64_t it = 0; it < n_it; ++it) {
         mbar_wait(raw_full(rs), rphase);
-        const uint32_t sraw = raw_base + rs * FU_RAW_BYTES;
+        const uint32_t sraw = raw_base + rs * RAW_BYTES;
         uint32_t lw[FU_ROWS_PER_WARP][4];
 #pragma unroll
         for (int i = 0; i < FU_ROWS_PER_WARP; ++i) {
-          const uint4 v = lds128(sraw + (cw + FU_CONV_WARPS * i) * 512 + lane * 16);
+          const uint4 v = lds128(sraw + (rw + rstride * i) * 512 + lane * 16);
           byte_transpose4(v.x, v.y, v.z, v.w, lw[i][0], lw[i][1], lw[i][2], lw[i][3]);
         }
         // Hand the raw tile back to the TMA producer as soon as its values are CONSUMED (the
@@ -273,67 +311,37 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(raw_empty(rs));
         if (++rs == RAW) { rs = 0; rphase ^= 1; }
-        mbar_wait(empty_bar(stage), phase ^ 1);
-        const uint32_t sx = sbase + stage * STAGE_BYTES + NG * FU_U_BYTES;
-#pragma unroll
-        for (int i = 0; i < FU_ROWS_PER_WARP; ++i) {
-          const int row = cw + FU_CONV_WARPS * i;
-          const uint32_t off =
-              static_cast<uint32_t>(row) * 128u + ((((lane >> 2) ^ (row & 7)) << 4) | ((lane & 3) << 2));
-          sts32(sx + 0 * FU_BLOCK_R * 128 + off, lw[i][0]);
-          sts32(sx + 1 * FU_BLOCK_R * 128 + off, lw[i][1]);
-          sts32(sx + 2 * FU_BLOCK_R * 128 + off, lw[i][2]);
-          sts32(sx + 3 * FU_BLOCK_R * 128 + off, lw[i][3]);
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(full_bar(stage));
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        store(lw);
       }
     } else {
-    auto load = [&](int64_t it, uint4 (&r)[FU_ROWS_PER_WARP]) {
-      const int32_t tr = static_cast<int32_t>(blockIdx.x) + static_cast<int32_t>(it / P.num_kb) * gridDim.x;
-      const int64_t k = static_cast<int64_t>(it % P.num_kb) * FU_BLOCK_K + 4 * lane;
+      auto load = [&](int64_t it, uint4 (&r)[FU_ROWS_PER_WARP]) {
+        const int32_t tr = static_cast<int32_t>(blockIdx.x) + static_cast<int32_t>(it / P.num_kb) * gridDim.x;
+        const int64_t k = static_cast<int64_t>(it % P.num_kb) * FU_BLOCK_K + 4 * lane;
 #pragma unroll
-      for (int i = 0; i < FU_ROWS_PER_WARP; ++i) {
-        const int64_t row = static_cast<int64_t>(tr) * FU_BLOCK_R + cw + FU_CONV_WARPS * i;
-        r[i] = (row < P.R && k < P.d2p) ? __ldcs(reinterpret_cast<const uint4*>(P.x + row * P.d2p + k))
-                                        : make_uint4(0u, 0u, 0u, 0u);
-      }
-    };
-    int stage = 0;
-    uint32_t phase = 0;
-    auto store = [&](const uint4 (&r)[FU_ROWS_PER_WARP]) {
-      mbar_wait(empty_bar(stage), phase ^ 1);
-      const uint32_t sx = sbase + stage * STAGE_BYTES + NG * FU_U_BYTES;
+        for (int i = 0; i < FU_ROWS_PER_WARP; ++i) {
+          const int64_t row = static_cast<int64_t>(tr) * FU_BLOCK_R + rbase + rw + rstride * i;
+          r[i] = (row < P.R && k < P.d2p) ? __ldcs(reinterpret_cast<const uint4*>(P.x + row * P.d2p + k))
+                                          : make_uint4(0u, 0u, 0u, 0u);
+        }
+      };
+      auto convert_store = [&](const uint4 (&r)[FU_ROWS_PER_WARP]) {
+        uint32_t lw[FU_ROWS_PER_WARP][4];
 #pragma unroll
-      for (int i = 0; i < FU_ROWS_PER_WARP; ++i) {
-        const int row = cw + FU_CONV_WARPS * i;  // 0..63 inside the tile
-        uint32_t l0, l1, l2, l3;
-        byte_transpose4(r[i].x, r[i].y, r[i].z, r[i].w, l0, l1, l2, l3);
-        // SWIZZLE_128B K-major: 16-B chunk c of row r sits at chunk position c ^ (r & 7)
-        const uint32_t off = static_cast<uint32_t>(row) * 128u + ((((lane >> 2) ^ (row & 7)) << 4) | ((lane & 3) << 2));
-        sts32(sx + 0 * FU_BLOCK_R * 128 + off, l0);
-        sts32(sx + 1 * FU_BLOCK_R * 128 + off, l1);
-        sts32(sx + 2 * FU_BLOCK_R * 128 + off, l2);
-        sts32(sx + 3 * FU_BLOCK_R * 128 + off, l3);
+        for (int i = 0; i < FU_ROWS_PER_WARP; ++i)
+          byte_transpose4(r[i].x, r[i].y, r[i].z, r[i].w, lw[i][0], lw[i][1], lw[i][2], lw[i][3]);
+        store(lw);
+      };
+      uint4 ra[FU_ROWS_PER_WARP], rb[FU_ROWS_PER_WARP];
+      if (n_it > 0) load(0, ra);
+      if (n_it > 1) load(1, rb);
+      for (int64_t it = 0; it < n_it; it += 2) {
+        convert_store(ra);
+        if (it + 2 < n_it) load(it + 2, ra);
+        if (it + 1 < n_it) {
+          convert_store(rb);
+          if (it + 3 < n_it) load(it + 3, rb);
+        }
       }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(full_bar(stage));
-      if (++stage == STAGES) { stage = 0; phase ^= 1; }
-    };
-    uint4 ra[FU_ROWS_PER_WARP], rb[FU_ROWS_PER_WARP];
-    if (n_it > 0) load(0, ra);
-    if (n_it > 1) load(1, rb);
-    for (int64_t it = 0; it < n_it; it += 2) {
-      store(ra);
-      if (it + 2 < n_it) load(it + 2, ra);
-      if (it + 1 < n_it) {
-        store(rb);
-        if (it + 3 < n_it) load(it + 3, rb);
-      }
-    }
     }
   }
 

@@ -153,7 +153,7 @@ SKINNY = [
 ]
 
 
-@pytest.mark.parametrize("load", ["tma", "regs"])
+@pytest.mark.parametrize("load", ["tma", "regs", "hybrid"])
 @pytest.mark.parametrize("shape", SKINNY, ids=lambda s: "f%d_N%d_k%d_d2%d_d3%d_L%d" % s)
 def test_skinny_fused(shape, load, monkeypatch):
     """Both ways of feeding the fused kernel's converters: raw X tiles by TMA, or register loads
@@ -216,7 +216,7 @@ def test_mv_column_shard_and_entry_point(monkeypatch):
             assert np.array_equal(AUn[l], wa) and np.array_equal(BUn[l], wb), (c0, c1, l)
 
 
-@pytest.mark.parametrize("load", ["tma", "regs"])
+@pytest.mark.parametrize("load", ["tma", "regs", "hybrid"])
 def test_skinny_long_k_ring_wraparound(load, monkeypatch):
     """Long K (33–65 k-blocks per tile) wraps the raw-X and limb rings many times; a premature
     release of a raw tile once corrupted whole output rows intermittently — run it repeatedly."""

@@ -76,7 +76,8 @@ def main():
         for path in args.paths.split(","):
             # fused (TMA raw ring), fused-regs (register loads), fused-regs-pf<N> / fused-pf<N>
             # (L2 prefetch N iterations ahead)
-            os.environ["CTPT_FUSED_LOAD"] = "regs" if path.startswith("fused-regs") else "tma"
+            os.environ["CTPT_FUSED_LOAD"] = ("regs" if path.startswith("fused-regs") else
+                                             "hybrid" if path.startswith("fused-hybrid") else "tma")
             if "-pf" in path:
                 os.environ["CTPT_FUSED_PF"] = path.split("-pf")[1]
             else:
