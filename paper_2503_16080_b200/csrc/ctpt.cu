@@ -32,6 +32,12 @@ ctpt_status fail(ctpt_status s, const char* fmt, ...) {
   return s;
 }
 
+#define CUDA_TRY_L(label, expr)                                                                 \
+  do {                                                                                          \
+    cudaError_t e_ = (expr);                                                                    \
+    if (e_ != cudaSuccess) return fail(CTPT_ERR_CUDA, "%s: %s", label, cudaGetErrorString(e_)); \
+  } while (0)
+
 #define CUDA_TRY(expr)                                                                          \
   do {                                                                                          \
     cudaError_t e_ = (expr);                                                                    \
@@ -244,6 +250,10 @@ ctpt_status tc_setup() {
     CTPT_FU_ATTR(1, FU_HYBRID)
     CTPT_FU_ATTR(2, FU_HYBRID)
 #undef CTPT_FU_ATTR
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
   });
   if (e != cudaSuccess) return fail(CTPT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
   return CTPT_OK;
@@ -696,7 +706,7 @@ ctpt_status launch_mv(const GemmArgs& g, const uint32_t* x, void* mv_ws, cudaStr
   const int d3p = mp.nc / 4;
   dim3 eg(static_cast<unsigned>(std::min<int64_t>((d.d2p + 255) / 256, 1024)), static_cast<unsigned>(mp.nc));
   k_expand_u<<<eg, 256, 0, st>>>(plane, d.d2p, static_cast<int32_t>(d.j0), static_cast<int32_t>(d.d3_loc), d3p, ue);
-  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY_L("k_expand_u launch", cudaGetLastError());
   if (mp.splits > 1) CUDA_TRY(cudaMemsetAsync(w + mp.ticket_off, 0, static_cast<size_t>(mp.tiles) * 4, st));
   CUtensorMap tmX, tmUe;
   const uint64_t kbytes = static_cast<uint64_t>(4) * d.d2p;
@@ -723,7 +733,7 @@ ctpt_status launch_mv(const GemmArgs& g, const uint32_t* x, void* mv_ws, cudaStr
     case 64: k_gemm_mv<64><<<grid, MV_THREADS, MV_SMEM_BYTES, st>>>(tmX, tmUe, P); break;
     default: k_gemm_mv<128><<<grid, MV_THREADS, MV_SMEM_BYTES, st>>>(tmX, tmUe, P); break;
   }
-  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY_L("k_gemm_mv launch", cudaGetLastError());
   return CTPT_OK;
 }
 
