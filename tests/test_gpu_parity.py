@@ -548,6 +548,7 @@ RESCALE = [
     (R, 128, 1, 96, 40, 4, "int"),      # kU = 1 → fused skinny kernel + Rescale epilogue
     (SA, 16, 3, 77, 300, 3, "int"),     # structured-A (Algorithm 7 step 2), split + GEMM path
     (A, 8, 3, 50, 33, 2, "real"),       # R = 32: one partial tile
+    (S, 32, 2, 100, 20, 3, "int"),      # d3 <= 32: raw-byte kernel + Rescale (K-split partials)
 ]
 
 
