@@ -194,6 +194,15 @@ ctpt_status ctpt_gemm(const ctpt_problem* prob, int32_t l, const void* d_ws, siz
 ctpt_status ctpt_gemm_fused(const ctpt_problem* prob, int32_t l, const void* d_ctmat, const void* d_plain,
                             uint32_t* d_AU_l, uint32_t* d_BU_l, void* stream);
 
+/* RNS Rescale of residue arrays by the last prime: d_in uint32 [L][n] canonical
+ * residues of elements x ∈ Z_q → d_out uint32 [L−1][n] with ⌊x / primes[L−1]⌉ mod primes[l].
+ * Algorithm 7 step 2 rescales BOTH output parts: ctpt_matmul with rescale = 1
+ * does B', and this call does Ã (its d1/N polynomials, O(d1) work — "Rescale should be performed
+ * on this polynomial representation of Ã"), e.g. d_in = the a_polys of a structured-A
+ * ciphertext.  Never synchronises. */
+ctpt_status ctpt_rescale(int32_t L, const uint32_t* primes, int64_t n, const uint32_t* d_in, uint32_t* d_out,
+                         void* stream);
+
 /* Mod-PP-MM_{q; M, K, Nc} in RNS — the paper's plaintext modular product (notation P:1685,
  * "Mod-PP-MM_{q; d1,d2,d3}"), which CC-MM (Alg. 8: "≈ 12 fp-PP-MM calls",
  * P:1599) and the RGSW product (Alg. 9) reduce to, with operands that are full

@@ -824,6 +824,34 @@ ctpt_status ctpt_matmul(const ctpt_problem* pb, const void* d_ctmat, const void*
   return matmul_impl(pb, d, X0, d_plain, d_AU, d_BU, d_ws, ws_bytes, stream);
 }
 
+ctpt_status ctpt_rescale(int32_t L, const uint32_t* primes, int64_t n, const uint32_t* d_in, uint32_t* d_out,
+                         void* stream) {
+  if (L < 2 || L > kMaxPrimes) return fail(CTPT_ERR_ARG, "Rescale needs 2 <= L <= %d", kMaxPrimes);
+  if (!primes || (n > 0 && (!d_in || !d_out))) return fail(CTPT_ERR_ARG, "null pointer");
+  if (n < 0) return fail(CTPT_ERR_SHAPE, "n < 0");
+  for (int i = 0; i < L; ++i) {
+    const uint32_t p = primes[i];
+    if (p < 3 || !(p & 1u) || p >= (1u << 31) || !is_prime_u32(p)) return fail(CTPT_ERR_MODULUS, "bad prime %u", p);
+    for (int j = 0; j < i; ++j)
+      if (primes[j] == p) return fail(CTPT_ERR_MODULUS, "prime %u repeated", p);
+  }
+  if (n == 0) return CTPT_OK;
+  RescaleParams P{};
+  P.in = d_in;
+  P.out = d_out;
+  P.n = n;
+  P.L = L;
+  P.p_last = primes[L - 1];
+  for (int l = 0; l < L - 1; ++l) {
+    P.m[l] = make_modp(primes[l]);
+    P.inv[l] = powmod_u32(P.p_last % primes[l], primes[l] - 2, primes[l]);
+  }
+  dim3 grid(static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 4096)), static_cast<unsigned>(L - 1));
+  k_rescale<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(P);
+  CUDA_TRY(cudaGetLastError());
+  return CTPT_OK;
+}
+
 // Mod-PP-MM_{q; M, K, Nc} in RNS as the degenerate problem "structured-A with N = 1": rows_A = 0,
 // d1 = M, d2 = K, d3 = Nc, general per-prime Y planes (k_U = 4).
 static ctpt_problem modmm_problem(int32_t L, const uint32_t* primes, int64_t M, int64_t K, int64_t Nc) {

@@ -265,6 +265,29 @@ __device__ __forceinline__ uint32_t rescale_last(uint32_t v, uint32_t xl, const 
 
 __device__ __forceinline__ uint32_t sub_mod(uint32_t a, uint32_t b, uint32_t p) { return a >= b ? a - b : a + (p - b); }
 
+// Standalone RNS Rescale of residue arrays (Alg. 7 step 2 on Ã's polynomials):
+// in [L][n] canonical residues → out [L−1][n] = ⌊x / p_{L−1}⌉ mod p_l.
+struct RescaleParams {
+  const uint32_t* in;
+  uint32_t* out;
+  int64_t n;
+  int32_t L;
+  uint32_t p_last;
+  ModP m[64];
+  uint32_t inv[64];  // p_last^{-1} mod p_l
+};
+
+__global__ void __launch_bounds__(256) k_rescale(const __grid_constant__ RescaleParams P) {
+  const int l = blockIdx.y;
+  OutParams o{};
+  o.p_last = P.p_last;
+  o.p_last_inv = P.inv[l];
+  const uint32_t* xl = P.in + static_cast<int64_t>(P.L - 1) * P.n;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < P.n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    P.out[static_cast<int64_t>(l) * P.n + i] = rescale_last(P.in[static_cast<int64_t>(l) * P.n + i], xl[i], o, P.m[l]);
+}
+
 __device__ __forceinline__ void store_out(const OutParams& o, const ModP& m, int64_t j, int64_t r, uint32_t v) {
   uint32_t* q = out_ptr(o, j, r);
   if (o.rowcorr) v = sub_mod(v, o.rowcorr[r], m.p);

@@ -65,6 +65,7 @@ _sig = {
     "ctpt_gemm_simt": (ctypes.c_int, [_PP, ctypes.c_int32, _P, ctypes.c_size_t, _P, _P, _P, _P]),
     "ctpt_gemm_fused": (ctypes.c_int, [_PP, ctypes.c_int32, _P, _P, _P, _P, _P]),
     "ctpt_gemm_mv": (ctypes.c_int, [_PP, ctypes.c_int32, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
+    "ctpt_rescale": (ctypes.c_int, [ctypes.c_int32, _P, ctypes.c_int64, _P, _P, _P]),
     "ctpt_modmatmul_sizes": (ctypes.c_int, [ctypes.c_int32, _P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                             ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_size_t),
                                             ctypes.POINTER(ctypes.c_size_t)]),
@@ -211,6 +212,12 @@ def gemm_mv(spec: Spec, l: int, ctmat, plain, AU_l, BU_l, ws, stream=None):
 
 def _primes_arr(primes):
     return (ctypes.c_uint32 * len(primes))(*[int(p) for p in primes])
+
+
+def rescale(primes, n: int, x_in, x_out, stream=None):
+    """x_out [L-1][n] = round(x / primes[-1]) mod primes[l] for x_in [L][n] residues (device tensors)."""
+    arr = _primes_arr(primes)
+    _check(_lib.ctpt_rescale(len(primes), ctypes.cast(arr, _P), n, _ptr(x_in), _ptr(x_out), _stream(stream)))
 
 
 def modmatmul_sizes(primes, M: int, K: int, Nc: int):

@@ -661,3 +661,58 @@ def test_matmul_is_graph_capturable(shape, monkeypatch):
         for l, p in enumerate(ps):
             wa, wb = oracle_outputs(fmt, N, d1, ct.a_polys[l], ct.b_polys[l], U, p)
             assert np.array_equal(AUn[l], wa) and np.array_equal(BUn[l], wb), (seed, l)
+
+
+def test_rescale_standalone_matches_oracle():
+    """ctpt_rescale on residue arrays (incl. the values around ±q_1/2 and 0) == the oracle's
+    plain ⌊x/q_1⌉ (CRT, exact division)."""
+    import torch
+
+    from paper_2503_16080_b200 import ctpt
+
+    ps = ctgen.primes(3)
+    q = ps[0] * ps[1] * ps[2]
+    rng = np.random.default_rng(8)
+    xs = [int.from_bytes(rng.bytes(16), "little") % q for _ in range(3000)]
+    h = (ps[2] - 1) // 2
+    xs += [0, 1, q - 1, h, h + 1, q - h, q - h - 1, 5 * ps[2] + h, 5 * ps[2] + h + 1]
+    res = np.array([[x % p for x in xs] for p in ps], dtype=np.uint32)
+    out = torch.empty((2, len(xs)), dtype=torch.int32, device="cuda")
+    ctpt.rescale(ps, len(xs), torch.from_numpy(res.view(np.int32)).cuda(), out)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), oracle.rescale_last(res, ps))
+
+
+def test_struct_a_algorithm7_with_rescale():
+    """Algorithm 7 with its step 2: B'' = Rescale(B·U) from ctpt_matmul(rescale=1) and
+    Ã'' = Rescale(Ã) from ctpt_rescale on the a-polynomials; (Ã'', B'') decrypts under (S·U)_j over
+    the remaining primes to (P·U)/q_1 within (‖(S·U)_j‖₁ + 1)/2 (exact rational check)."""
+    from fractions import Fraction
+
+    import torch
+
+    from paper_2503_16080_b200 import ctpt
+
+    fmt, N, k, d2, d3, L, seed = SA, 16, 3, 40, 6, 3, 14
+    d1 = N * k
+    ps = ctgen.primes(L)
+    q1 = ps[-1]
+    ct = ctgen.encrypt(fmt, N, d1, d2, seed, 20, ps)
+    U = ctgen.U_matrix(seed, d2, d3, 8)
+    (AU, BU), eng = run_gpu(fmt, N, d1, d2, d3, ps, ct.a_polys, ct.b_polys, U=U, rescale=1)
+    a_in = torch.from_numpy(ct.a_polys.reshape(L, -1).view(np.int32)).cuda()
+    a_out = torch.empty((L - 1, a_in.shape[1]), dtype=torch.int32, device="cuda")
+    ctpt.rescale(ps, a_in.shape[1], a_in, a_out)
+    torch.cuda.synchronize()
+    a2 = a_out.cpu().numpy().view(np.uint32).reshape(L - 1, k, N)
+    assert np.array_equal(a2.reshape(L - 1, -1), oracle.rescale_last(ct.a_polys.reshape(L, -1), ps))
+    sks = [ctgen.sk(seed, j, N) for j in range(d2)]
+    P = ctgen.plain_matrix(seed, N, d1, range(d1), range(d2), 20)
+    PU = P.astype(object).dot(U.astype(object))
+    for j in range(d3):
+        w = oracle.su_column(sks, U, j)
+        decs = np.stack([oracle.decrypt_col(fmt, N, d1, [w], a2[l], BU[l, j], ps[l]) for l in range(L - 1)])
+        cen = oracle.crt_centred_array(decs, ps[:2])
+        bound = Fraction(int(np.abs(w).sum()) + 1, 2)
+        for i in range(d1):
+            assert abs(Fraction(cen[i]) - Fraction(int(PU[i, j]), q1)) <= bound, (j, i)
