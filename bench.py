@@ -50,6 +50,8 @@ def parse():
                     help="experiment: run prime l+1's limb split on a side stream during prime l's GEMM "
                          "(measured slower; default off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                    help="replay each step as one CUDA graph (auto: launch-bound workloads, < 1e9 residue MACs)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target seconds of oracle work per sample")
     ap.add_argument("--rescale", action="store_true",
                     help="Algorithm 6 with step 2 (SURVEY.md §8(f) row 3): U real uniform[-1,1) encoded at "
@@ -277,8 +279,13 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     ev_split = [torch.cuda.Event() for _ in range(2)]
     ev_free = [torch.cuda.Event() for _ in range(2)]
     counter = [0]
+    # Launch-bound workloads (c1: one 64-row tile per prime, ~5 µs of kernel against ~40 µs of
+    # host-side argument checks + TMA descriptor encoding per call) replay the step as one CUDA
+    # graph (the descriptors are kernel parameters, baked in at capture; tools/bench_graph.py).
+    use_graph = args.graph == "on" or (args.graph == "auto" and c.residue_macs < 1e9)
+    use_graph = use_graph and not overlap
 
-    def step(ev_pairs=None):
+    def step(ev_pairs=None, stream=stream):
         if args.rescale:  # the whole ctpt_matmul: last prime first, Rescale in the others' epilogues
             if ev_pairs is not None:
                 ev_pairs[0][0].record(stream)
@@ -293,7 +300,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                 counter[0] += 1
                 if overlap:
                     side.wait_event(ev_free[b])  # the GEMM that last read ws2[b] has finished
-                ctpt.split(spec, l, eng.ctmat, ws2[b], stream=side)
+                ctpt.split(spec, l, eng.ctmat, ws2[b], stream=side if overlap else stream)
                 if overlap:
                     ev_split[b].record(side)
                     stream.wait_event(ev_split[b])
@@ -313,6 +320,15 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
+    graph = None
+    if use_graph:
+        cap = torch.cuda.Stream(dev)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=cap):
+            step(stream=cap)
+        for _ in range(args.warmup):
+            graph.replay()
+        torch.cuda.synchronize(dev)
 
     # ------------------------------------------------ timed region (device-resident inputs)
     gemm_ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_ev)]
@@ -329,7 +345,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     step_ev[0].record(stream)
     for s in range(args.steps):
-        step(gemm_ev[s])
+        if graph is not None:
+            graph.replay()
+        else:
+            step(gemm_ev[s])
         step_ev[s + 1].record(stream)
     t_end.record(stream)
     torch.cuda.synchronize(dev)
@@ -337,8 +356,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if world > 1:
         torch.distributed.barrier()
     elapsed_ms = t_start.elapsed_time(t_end)
-    gemm_ms = [a.elapsed_time(b) for row in gemm_ev for (a, b) in row]
     step_ms = [step_ev[i].elapsed_time(step_ev[i + 1]) for i in range(args.steps)]
+    if graph is not None:  # no events inside the graph: one replay = the step's n_ev launches
+        gemm_ms = [t / n_ev for t in step_ms for _ in range(n_ev)]
+    else:
+        gemm_ms = [a.elapsed_time(b) for row in gemm_ev for (a, b) in row]
     if world > 1:
         t = torch.tensor([elapsed_ms], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -365,8 +387,13 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     except OSError:
         pass
 
+    # ------------------------------------------------ the untimed stages, each timed on its own
+    setup = setup_stage_rates(c, eng, a_dev, b_dev, U, dev, stream) if not args.rescale else None
+    del a_dev, b_dev
+
     # ------------------------------------------------ end to end through the ABI (host buffers)
-    e2e = (run_e2e(args, c, ps, ct, eng, dev, stream) if not args.rescale else
+    e2e = ({"value": None, "note": "skipped (--e2e-steps 0)"} if args.e2e_steps <= 0 else
+           run_e2e(args, c, ps, ct, eng, dev, stream) if not args.rescale else
            {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
             "note": "ctpt_matmul_host does not Rescale; no host-buffer path for this workload"})
 
@@ -406,6 +433,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         # per prime: k_split[_rows] + kU x k_gemm_tc, or one k_gemm_fused / k_gemm_mv (+ k_expand_u)
         "gpu_launches": (2 if mv else 1 if fused else 1 + kU) * len(ps) * args.steps,
         "split_overlap": overlap,
+        "cuda_graph": graph is not None,
+        "setup_stages": setup,
         "clocks": clocks,
         "input_generation_s": gen_s,
     }
@@ -418,6 +447,43 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         result["cpu_baseline"] = cpu_oracle_rate(c, ct, U, args.cpu_seconds, gpu0)
     if rank == 0:
         print(json.dumps(result))
+
+
+def setup_stage_rates(c, eng, a_dev, b_dev, U, dev, stream, reps: int = 3) -> dict:
+    """ctpt_layout (a1) and ctpt_plain_precompute (a2) are not in `value`; time
+    each on its own (CUDA events, mean of `reps` calls, device-resident inputs) and report GB/s of
+    their algorithmic bytes: layout reads every ciphertext residue and writes X (4 + 4 B per
+    residue); precompute reads U as int64 and writes its digit plane(s) (8 + kU B per entry).
+    The precompute call synchronises its stream once (it reads max|U| back, include/ctpt.h)."""
+    import torch
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1) / reps / 1e3
+
+    sz = eng.sizes
+    n_in = (a_dev.numel() if sz.rows_A else 0) + b_dev.numel()
+    lay_bytes = 4 * n_in + 4 * c.L * c.R * sz.d2p
+    t_lay = timed(lambda: eng.layout(a_dev, b_dev, validate=False))
+    U_dev = torch.from_numpy(np.ascontiguousarray(U, dtype=np.int64)).to(dev)
+    mode = (eng.spec.kU, eng.spec.u_unsigned, eng.spec.u_offset)
+    pre_bytes = 8 * c.d2 * c.d3 + eng.spec.kU * c.d3 * sz.d2p
+    t_pre = timed(lambda: eng.precompute(U_dev))
+    assert (eng.spec.kU, eng.spec.u_unsigned, eng.spec.u_offset) == mode
+    mp, _ = peaks()
+    hbm = float(mp["hbm_gbs"])
+    return {"layout": {"ms": t_lay * 1e3, "bytes": lay_bytes, "gbs": lay_bytes / t_lay / 1e9,
+                       "frac_hbm": lay_bytes / t_lay / 1e9 / hbm, "kernel": "k_layout (all primes)"},
+            "plain_precompute": {"ms": t_pre * 1e3, "bytes": pre_bytes, "gbs": pre_bytes / t_pre / 1e9,
+                                 "frac_hbm": pre_bytes / t_pre / 1e9 / hbm,
+                                 "kernel": "k_minmax_i64 + read-back + k_plain"}}
 
 
 def cublaslt_ratio(limb_macs_per_s: float, elapsed_ms: float):

@@ -223,20 +223,24 @@ ctpt_status make_tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType d
 }
 
 int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+    n = 148;
   return n;
 }
 
+// cudaFuncSetAttribute applies to the CURRENT device only: run the set-up once per device (a
+// process may drive several GPUs from different threads).
+constexpr int kMaxDevices = 64;
 ctpt_status tc_setup() {
-  static cudaError_t e = cudaErrorNotReady;
-  static std::once_flag once;
-  std::call_once(once, [] {
+  static cudaError_t errs[kMaxDevices];
+  static std::once_flag onces[kMaxDevices];
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) return fail(CTPT_ERR_CUDA, "device ordinal %d out of range", dev);
+  cudaError_t& e = errs[dev];
+  std::call_once(onces[dev], [&e] {
     e = cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BYTES);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_gemm_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, T2_SMEM_BYTES);
