@@ -128,6 +128,14 @@ ctpt_status check_problem(const ctpt_problem* pb, Dims& d) {
 
 size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
+// The 16-byte layout kernel needs 4-row chunks that never straddle A and B (and aligned vectors):
+// rows_A and d1 multiples of 4.  CTPT_LAYOUT=scalar forces the 4-byte kernel (A/B measurements).
+bool layout_vec_ok(int64_t rows_A, int64_t d1) {
+  const char* e = getenv("CTPT_LAYOUT");
+  if (e && strcmp(e, "scalar") == 0) return false;
+  return rows_A % 4 == 0 && d1 % 4 == 0;
+}
+
 // d_ws of ctpt_matmul / ctpt_split / ctpt_gemm, in this order:
 //   limbs   [4][R][d2p] u8                      (one prime's byte-limb planes)
 //   rowcorr [R] u32        (unsigned-U mode with u_offset ≠ 0: u_offset·Σ_k X[r][k] mod p)
@@ -384,7 +392,10 @@ ctpt_status ctpt_layout(const ctpt_problem* pb, const uint32_t* d_a, const uint3
   if (validate) CUDA_TRY(cudaMemsetAsync(hdr, 0, 4, st));
   dim3 grid(static_cast<unsigned>((d.R + 63) / 64), static_cast<unsigned>((d.d2p + 63) / 64), d.L);
   if (grid.y > 65535) return fail(CTPT_ERR_SHAPE, "d2 too large for the layout grid");
-  k_layout<<<grid, 256, 0, st>>>(P);
+  if (layout_vec_ok(d.rows_A, d.d1))
+    k_layout_v4<<<grid, 256, 0, st>>>(P);
+  else
+    k_layout<<<grid, 256, 0, st>>>(P);
   CUDA_TRY(cudaGetLastError());
   if (validate) {
     uint32_t flag = 0;
@@ -1022,7 +1033,10 @@ ctpt_status launch_layout_cols(const uint32_t* a_colmajor, uint32_t* x, int64_t 
   P.d2 = d2;
   P.d2p = d2p;
   dim3 grid(static_cast<unsigned>((rows + 63) / 64), static_cast<unsigned>((d2p + 63) / 64), 1);
-  k_layout<<<grid, 256, 0, st>>>(P);
+  if (layout_vec_ok(rows, 0))
+    k_layout_v4<<<grid, 256, 0, st>>>(P);
+  else
+    k_layout<<<grid, 256, 0, st>>>(P);
   CUDA_TRY(cudaGetLastError());
   return CTPT_OK;
 }

@@ -81,6 +81,62 @@ __global__ void __launch_bounds__(256) k_layout(const __grid_constant__ LayoutPa
   if (P.validate && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(P.bad_flag, 1u);
 }
 
+// The same permutation with 16-byte accesses on both sides (rows_A and d1 multiples of 4, so a
+// 4-row chunk never straddles A and B and every vector is aligned).  One 64 (k) × 64 (r) tile
+// per block: 4 LDG.128 per thread (16 r-chunks × 64 k), stored into shared memory with the
+// 16-byte chunk c of row k at position c ^ ((k >> 2) & 7); then each thread owns a 4 (k) × 4 (r)
+// block — 4 LDS.128 (conflict-free under that swizzle), a register transpose, 4 STG.128 that
+// 16 lanes turn into one 256-byte row segment of X.
+__global__ void __launch_bounds__(256) k_layout_v4(const __grid_constant__ LayoutParams P) {
+  __shared__ __align__(16) uint32_t tile[64 * 64];
+  const int l = blockIdx.z;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 64;
+  const int64_t k0 = static_cast<int64_t>(blockIdx.y) * 64;
+  const uint32_t p = P.p_arr[l];
+  const uint32_t* a = P.a + static_cast<int64_t>(l) * P.d2 * P.rows_A;
+  const uint32_t* b = P.b + static_cast<int64_t>(l) * P.d2 * P.d1;
+  const int c = threadIdx.x & 15;  // 4-row chunk of the tile
+  const int kq0 = threadIdx.x >> 4;  // 0..15
+  const int64_t r = r0 + 4 * c;
+  bool bad = false;
+  uint4 v[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t k = k0 + kq0 + 16 * i;
+    v[i] = make_uint4(0u, 0u, 0u, 0u);
+    if (k < P.d2 && r < P.R)
+      v[i] = (r < P.rows_A) ? __ldcs(reinterpret_cast<const uint4*>(a + k * P.rows_A + r))
+                            : __ldcs(reinterpret_cast<const uint4*>(b + k * P.d1 + (r - P.rows_A)));
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int kk = kq0 + 16 * i;
+    bad |= (v[i].x >= p) | (v[i].y >= p) | (v[i].z >= p) | (v[i].w >= p);
+    *reinterpret_cast<uint4*>(&tile[kk * 64 + ((c ^ ((kk >> 2) & 7)) << 2)]) = v[i];
+  }
+  __syncthreads();
+  const int kq = threadIdx.x & 15;  // k = 4kq .. 4kq+3
+  const int rq = threadIdx.x >> 4;  // r = 4rq .. 4rq+3
+  uint4 w[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int kk = 4 * kq + i;
+    w[i] = *reinterpret_cast<const uint4*>(&tile[kk * 64 + ((rq ^ ((kk >> 2) & 7)) << 2)]);
+  }
+  uint32_t* x = P.x + static_cast<int64_t>(l) * P.R * P.d2p;
+  const int64_t k = k0 + 4 * kq;
+  if (k < P.d2p) {  // d2p is a multiple of 16: a 4-k quad is all in or all out
+    const uint4 o0 = make_uint4(w[0].x, w[1].x, w[2].x, w[3].x), o1 = make_uint4(w[0].y, w[1].y, w[2].y, w[3].y),
+                o2 = make_uint4(w[0].z, w[1].z, w[2].z, w[3].z), o3 = make_uint4(w[0].w, w[1].w, w[2].w, w[3].w);
+    const int64_t rr = r0 + 4 * rq;
+    if (rr + 0 < P.R) __stcs(reinterpret_cast<uint4*>(x + (rr + 0) * P.d2p + k), o0);
+    if (rr + 1 < P.R) __stcs(reinterpret_cast<uint4*>(x + (rr + 1) * P.d2p + k), o1);
+    if (rr + 2 < P.R) __stcs(reinterpret_cast<uint4*>(x + (rr + 2) * P.d2p + k), o2);
+    if (rr + 3 < P.R) __stcs(reinterpret_cast<uint4*>(x + (rr + 3) * P.d2p + k), o3);
+  }
+  if (P.validate && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(P.bad_flag, 1u);
+}
+
 // ------------------------------------------------------------------------------------------
 // Limb split (inside the timed ctpt_matmul): x = Σ_{ℓ<4} x_ℓ 2^{8ℓ},
 // x_ℓ ∈ [0,255] — the digits of Lemma le:strategy1's decomposition with

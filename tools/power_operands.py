@@ -48,14 +48,23 @@ def main():
             X.zero_()
         elif kind == "small":  # residues < 2^8: limbs 1..3 are zero
             X.copy_(torch.randint(0, 256, X.shape, device="cuda", generator=g, dtype=torch.int32))
+        elif kind == "bytes16":  # every limb byte uniform in [0, 16]: X carries U's entropy per byte
+            b = torch.randint(0, 17, X.shape + (4,), device="cuda", generator=g, dtype=torch.int32)
+            X.copy_(b[..., 0] | (b[..., 1] << 8) | (b[..., 2] << 16) | (b[..., 3] << 24))
+        elif kind == "bytes8":  # every limb byte uniform in [0, 8]
+            b = torch.randint(0, 9, X.shape + (4,), device="cuda", generator=g, dtype=torch.int32)
+            X.copy_(b[..., 0] | (b[..., 1] << 8) | (b[..., 2] << 16) | (b[..., 3] << 24))
 
     def setU(lo, hi):
         U = torch.randint(lo, hi + 1, (c.d2, c.d3), device="cuda", generator=g, dtype=torch.int64)
         kU = eng.precompute(U)
         assert kU == 1
 
+    # the last four swap the entropies of the two MMA operands (A = U^T tile, 4 KB per MMA; B = the
+    # four X limb tiles, 8 KB per MMA): what a kernel with X as the A operand would see
     cases = [("uniform", (-8, 8)), ("uniform", (0, 16)), ("uniform", (0, 0)), ("zero", (-8, 8)),
-             ("uniform", (-128, 127)), ("uniform", (-1, 1)), ("small", (-8, 8)), ("uniform", (-8, 8))]
+             ("uniform", (-128, 127)), ("uniform", (-1, 1)), ("small", (-8, 8)), ("uniform", (-8, 8)),
+             ("bytes16", (0, 255)), ("uniform", (0, 16)), ("bytes16", (0, 16)), ("bytes8", (0, 255))]
     if args.cases:
         keep = set(args.cases.split(";"))
         cases = [cs for cs in cases if f"{cs[0]}:{cs[1][0]},{cs[1][1]}" in keep]
