@@ -15,6 +15,7 @@
 #include "gemm_tc.cuh"
 #include "gemm_tc2.cuh"
 #include "gemm_fused.cuh"
+#include "gemm_fused2.cuh"
 #include "gemm_mv.cuh"
 #include "kernels.cuh"
 
@@ -262,6 +263,8 @@ ctpt_status tc_setup() {
     CTPT_FU_ATTR(1, FU_HYBRID)
     CTPT_FU_ATTR(2, FU_HYBRID)
 #undef CTPT_FU_ATTR
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_fused2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, F2_SMEM_BYTES);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_fused2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, F2_SMEM_BYTES);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
@@ -684,11 +687,28 @@ ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st) 
   // L2 prefetch distance for the raw X ring (iterations ahead of the TMA into shared memory)
   P.l2_prefetch = 0;  // measured: any L2 prefetch distance (2..16) lowered the fused kernel 5–35 %
   if (const char* e = getenv("CTPT_FUSED_PF")) P.l2_prefetch = std::max(0, atoi(e));
+  const int ng = d.d3_loc <= 128 ? 1 : 2;
+  // 128 < d3_loc <= 256: CTPT_FUSED2=pair runs one M = 256 MMA over a CTA pair (gemm_fused2.cuh)
+  // instead of two M = 128 groups reading the same limb tile.  Measured no faster than the
+  // single-CTA kernel on c4's ciphertexts (2.05–2.22 vs 2.02–2.14 ms per launch, d3 = 129..256,
+  // profiles/r01/fused2_pair/), so the single-CTA kernel stays the default.
+  bool pair = false;
+  if (const char* e = getenv("CTPT_FUSED2")) pair = ng == 2 && mode == FU_TMA && num_sms() >= 2 && strcmp(e, "pair") == 0;
   CUtensorMap tmX;
   s = make_tmap_2d(&tmX, x, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, d.d2p, g.R, FU_BLOCK_K,
-                   static_cast<uint32_t>(fu_raw_rows(mode)));
+                   static_cast<uint32_t>(pair ? F2_ROWS : fu_raw_rows(mode)));
   if (s != CTPT_OK) return s;
-  const int ng = d.d3_loc <= 128 ? 1 : 2;
+  if (pair) {
+    const unsigned grid2 = static_cast<unsigned>(2 * std::min<int64_t>(nt, num_sms() / 2));
+    int cg = 2;  // converter groups (K-blocks in flight per CTA); CTPT_F2_GROUPS=1 for A/B runs
+    if (const char* e = getenv("CTPT_F2_GROUPS")) cg = atoi(e) == 1 ? 1 : 2;
+    if (cg == 2)
+      k_gemm_fused2<2><<<grid2, F2_THREADS, F2_SMEM_BYTES, st>>>(tmU, tmX, P);
+    else
+      k_gemm_fused2<1><<<grid2, F2_THREADS, F2_SMEM_BYTES, st>>>(tmU, tmX, P);
+    CUDA_TRY(cudaGetLastError());
+    return CTPT_OK;
+  }
 #define CTPT_FU_LAUNCH(NG, MODE) \
   k_gemm_fused<NG, MODE><<<grid, FU_THREADS, fu_smem_bytes(NG, MODE), st>>>(tmU, tmX, P)
   if (ng == 1) {

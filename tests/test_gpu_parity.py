@@ -153,15 +153,40 @@ SKINNY = [
 ]
 
 
-@pytest.mark.parametrize("load", ["tma", "regs", "hybrid"])
+def _fused_load(monkeypatch, load):
+    """'tma' = the default (raw X ring, single CTA), 'tma2' = the raw X ring with d3_loc > 128 on
+    the CTA-pair kernel k_gemm_fused2 (CTPT_FUSED2=pair), 'regs' / 'hybrid' = the register-load
+    feeds (single CTA)."""
+    monkeypatch.setenv("CTPT_FUSED_LOAD", "tma" if load == "tma2" else load)
+    if load == "tma2":
+        monkeypatch.setenv("CTPT_FUSED2", "pair")
+    else:
+        monkeypatch.delenv("CTPT_FUSED2", raising=False)
+
+
+@pytest.mark.parametrize("load", ["tma", "tma2", "regs", "hybrid"])
 @pytest.mark.parametrize("shape", SKINNY, ids=lambda s: "f%d_N%d_k%d_d2%d_d3%d_L%d" % s)
 def test_skinny_fused(shape, load, monkeypatch):
-    """Both ways of feeding the fused kernel's converters: raw X tiles by TMA, or register loads
-    (CTPT_MV=off keeps d3 <= 32 on the converter kernel too)."""
+    """Every way of feeding the fused kernel's converters: raw X tiles by TMA (single CTA, or the
+    CTA pair for d3 > 128), or register loads (CTPT_MV=off keeps d3 <= 32 on the converter kernel too)."""
     monkeypatch.delenv("CTPT_SKINNY", raising=False)
     monkeypatch.setenv("CTPT_MV", "off")
-    monkeypatch.setenv("CTPT_FUSED_LOAD", load)
+    _fused_load(monkeypatch, load)
     _check(*shape)
+
+
+@pytest.mark.parametrize("groups", ["1", "2"])
+@pytest.mark.parametrize("cols", [(0, 129), (20, 220), (44, 300), (171, 300)])
+def test_skinny_pair_column_shards(cols, groups, monkeypatch):
+    """k_gemm_fused2 on column blocks [c0, c1) of a wider U (129..256 columns: the pair's second
+    CTA holds U^T rows j_off + 128.. — partly past the block and, for (171, 300), past d3), with
+    ragged R (not a multiple of the 64-row pair tile) and more pairs than tiles."""
+    monkeypatch.delenv("CTPT_SKINNY", raising=False)
+    monkeypatch.setenv("CTPT_FUSED2", "pair")
+    monkeypatch.setenv("CTPT_FUSED_LOAD", "tma")
+    monkeypatch.setenv("CTPT_F2_GROUPS", groups)  # converter groups: K-blocks in flight per CTA
+    _check(A, 64, 3, 333, 300, 2, col_begin=cols[0], col_end=cols[1], seed=5)
+    _check(S, 512, 9, 300, 300, 1, col_begin=cols[0], col_end=cols[1], seed=6)  # R = 9216: 144 tiles
 
 
 MV = [
@@ -216,16 +241,17 @@ def test_mv_column_shard_and_entry_point(monkeypatch):
             assert np.array_equal(AUn[l], wa) and np.array_equal(BUn[l], wb), (c0, c1, l)
 
 
-@pytest.mark.parametrize("load", ["tma", "regs", "hybrid"])
+@pytest.mark.parametrize("load", ["tma", "tma2", "regs", "hybrid"])
 def test_skinny_long_k_ring_wraparound(load, monkeypatch):
     """Long K (33–65 k-blocks per tile) wraps the raw-X and limb rings many times; a premature
     release of a raw tile once corrupted whole output rows intermittently — run it repeatedly."""
     monkeypatch.delenv("CTPT_SKINNY", raising=False)
-    monkeypatch.setenv("CTPT_FUSED_LOAD", load)
+    _fused_load(monkeypatch, load)
     for rep in range(3):
         _check(A, 256, 2, 4112, 64, 1, seed=rep)
         _check(S, 128, 3, 8200, 100, 1, seed=rep)
         _check(R, 512, 1, 4096, 256, 1, seed=rep)
+        _check(S, 256, 4, 8200, 200, 1, seed=rep)
 
 
 def test_skinny_fused_direct_entry_point():
