@@ -393,7 +393,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     # ------------------------------------------------ end to end through the ABI (host buffers)
     e2e = ({"value": None, "note": "skipped (--e2e-steps 0)"} if args.e2e_steps <= 0 else
-           run_e2e(args, c, ps, ct, eng, dev, stream) if not args.rescale else
+           run_e2e(args, c, ps, ct, eng, dev, stream, world) if not args.rescale else
            {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
             "note": "ctpt_matmul_host does not Rescale; no host-buffer path for this workload"})
 
@@ -557,10 +557,11 @@ def pcie_bandwidth(dev, nbytes: int = 1 << 30) -> dict:
             "h2d_concurrent_gbs": nbytes / th_c / 1e9, "d2h_concurrent_gbs": nbytes / td_c / 1e9}
 
 
-def run_e2e(args, c, ps, ct, eng, dev, stream):
+def run_e2e(args, c, ps, ct, eng, dev, stream, world: int = 1):
     """Same metric through the public ABI with HOST buffers: every step is one ctpt_matmul_host
     call, which copies the ciphertexts from pinned host memory chunk by chunk, lays them out,
-    splits, multiplies and copies the outputs back, with copies and compute overlapped."""
+    splits, multiplies and copies the outputs back, with copies and compute overlapped.  With
+    N ranks: barrier, every rank's own problem, max over ranks; value = N problems ÷ that time."""
     import torch
 
     from paper_2503_16080_b200 import ctpt
@@ -580,6 +581,8 @@ def run_e2e(args, c, ps, ct, eng, dev, stream):
 
     step()
     torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     for _ in range(args.e2e_steps):
@@ -587,11 +590,16 @@ def run_e2e(args, c, ps, ct, eng, dev, stream):
     t1.record(stream)
     torch.cuda.synchronize(dev)
     ms = t0.elapsed_time(t1) / args.e2e_steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
     h2d = (a_h.numel() * 4 if eng.sizes.rows_A else 0) + b_h.numel() * 4  # structured-A: Ã is not read
     d2h = eng.sizes.out_AU_bytes + eng.sizes.out_BU_bytes
     bw = pcie_bandwidth(dev)
     floor_ms = max(h2d / bw["h2d_concurrent_gbs"], d2h / bw["d2h_concurrent_gbs"]) / 1e6
-    return {"value": c.residue_macs / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+    return {"value": world * c.residue_macs / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d * world,
+            "d2h_bytes_per_step": d2h * world,
             "ms_per_step": ms, "steps": args.e2e_steps,
             "pcie": dict(bw, floor_ms=floor_ms, frac_of_floor=floor_ms / ms),
             "path": "ctpt_matmul_host: pinned host ciphertexts -> chunked H2D || layout+split+GEMM || D2H "
