@@ -49,9 +49,11 @@
  *  - Kernel-choice knobs for A/B measurements only (environment, read at every call; the
  *    defaults are the measured best): CTPT_GEMM=2cta (CTA-pair GEMM instead of single-CTA),
  *    CTPT_SKINNY=off (no fused skinny kernels), CTPT_MV=off (no raw-byte kernel for d3 ≤ 32),
- *    CTPT_FUSED_LOAD=regs (converter register loads instead of the TMA raw ring),
- *    CTPT_FUSED_PF=n (L2 prefetch distance in the fused kernel), CTPT_GROUP_J=n (GEMM raster
- *    group).  None of them changes a result.
+ *    CTPT_FUSED_LOAD=regs|hybrid (converter register loads instead of the TMA raw ring),
+ *    CTPT_FUSED2=pair (CTA-pair fused kernel for 128 < d3_loc ≤ 256; CTPT_F2_GROUPS=1|2 its
+ *    converter groups), CTPT_FUSED_PF=n (L2 prefetch distance in the fused kernel),
+ *    CTPT_GROUP_J=n (GEMM raster group), CTPT_GEMM_PF=n (GEMM L2 prefetch distance),
+ *    CTPT_LAYOUT=scalar (4-byte layout kernel).  None of them changes a result.
  */
 #ifndef CTPT_H_
 #define CTPT_H_
