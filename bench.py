@@ -50,6 +50,9 @@ def parse():
                     help="experiment: run prime l+1's limb split on a side stream during prime l's GEMM "
                          "(measured slower; default off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--split-overlap", default="on", choices=["on", "off"],
+                    help="split + GEMM path: split prime l+1 inside prime l's GEMM kernel (ctpt_gemm_next); "
+                         "measured +0.3 %% (c3), +2.2 %% (c4), +1.6 %% (c2) per step (profiles/r01/split_in_gemm)")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay each step as one CUDA graph (auto: launch-bound workloads, < 1e9 residue MACs)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target seconds of oracle work per sample")
@@ -248,7 +251,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     seed = c.seed + rank
     ps, ct, U, gen_s = make_inputs(c, seed, max(1, cores // world))
 
-    eng = CpmmEngine(ctpt.Spec(c.fmt, c.N, c.d1, c.d2, c.d3, ps, rescale=int(args.rescale)), dev)
+    inkernel_split = args.split_overlap == "on" and not args.rescale and len(ps) >= 2 and not args.overlap
+    eng = CpmmEngine(ctpt.Spec(c.fmt, c.N, c.d1, c.d2, c.d3, ps, rescale=int(args.rescale),
+                               split_overlap=int(inkernel_split)), dev)
     a_dev = torch.from_numpy(ct.a_polys.view(np.int32)).to(dev)
     b_dev = torch.from_numpy(ct.b_polys.view(np.int32)).to(dev)
     eng.layout(a_dev, b_dev, validate=True)
@@ -295,6 +300,15 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             return
         for l in range(len(ps)):
             au, bu = AU[l * d3l * ra:], BU[l * d3l * c.d1:]
+            if not fused and inkernel_split:  # prime l+1's split rides inside prime l's GEMM
+                if l == 0:
+                    ctpt.split(spec, 0, eng.ctmat, eng.ws, stream=stream)
+                if ev_pairs is not None:
+                    ev_pairs[l][0].record(stream)
+                ctpt.gemm_next(spec, l, eng.ctmat, eng.ws, eng.plain, au, bu, stream=stream)
+                if ev_pairs is not None:
+                    ev_pairs[l][1].record(stream)
+                continue
             if not fused:
                 b = counter[0] % len(ws2)
                 counter[0] += 1
@@ -431,8 +445,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                      "avg_launch_ms": gemm_avg_s * 1e3, "share_of_step": gemm_share},
         "e2e": e2e,
         # per prime: k_split[_rows] + kU x k_gemm_tc, or one k_gemm_fused / k_gemm_mv (+ k_expand_u)
-        "gpu_launches": (2 if mv else 1 if fused else 1 + kU) * len(ps) * args.steps,
+        "gpu_launches": ((1 + kU * len(ps)) if inkernel_split else
+                         (2 if mv else 1 if fused else 1 + kU) * len(ps)) * args.steps,
         "split_overlap": overlap,
+        "split_in_gemm": inkernel_split,
         "cuda_graph": graph is not None,
         "setup_stages": setup,
         "clocks": clocks,

@@ -104,6 +104,12 @@ typedef struct {
                                (ctpt_plain_precompute_unsigned; kU = 1, shared plane, d2 ≤ 33025)
                                and the limb MMAs run u8 × u8; 0: balanced s8 digits.          */
   int32_t u_offset;         /* the offset ctpt_plain_precompute_unsigned returned (≥ 0)        */
+  int32_t split_overlap;    /* 1: ctpt_matmul splits prime l+1's residues into limbs INSIDE
+                               prime l's GEMM kernel (two otherwise idle warps per CTA), into a
+                               second limb workspace — only the first prime's split runs on its
+                               own.  Applies to the split + GEMM path (d3_loc > 256, no
+                               rescale, kU = 1); the workspace doubles its limb planes.
+                               0: split, GEMM, split, GEMM …                                   */
 } ctpt_problem;
 
 typedef struct {
@@ -251,6 +257,15 @@ ctpt_status ctpt_host_workspace_bytes(const ctpt_problem* prob, int64_t chunk_ro
 ctpt_status ctpt_matmul_host(const ctpt_problem* prob, const uint32_t* h_a_polys, const uint32_t* h_b_polys,
                              const void* d_plain, uint32_t* h_AU, uint32_t* h_BU, void* d_ws, size_t ws_bytes,
                              int64_t chunk_rows, void* stream);
+
+/* ctpt_gemm for prime l with the limb split of prime l+1 fused in (prob->split_overlap = 1,
+ * no rescale, L ≥ 2): while prime l's MMAs run, two otherwise idle warps of every CTA split
+ * prime l+1's residues of d_ctmat into the OTHER limb buffer of d_ws (prime l uses buffer l & 1;
+ * ctpt_split(prob, l, …) fills buffer l & 1 too), so a step is ctpt_split(0), then
+ * ctpt_gemm_next(l) for l = 0 … L−1 (the last one splits nothing).  Outputs, errors and
+ * synchronisation as for ctpt_gemm; CTPT_ERR_ARG without split_overlap. */
+ctpt_status ctpt_gemm_next(const ctpt_problem* prob, int32_t l, const void* d_ctmat, void* d_ws, size_t ws_bytes,
+                           const void* d_plain, uint32_t* d_AU_l, uint32_t* d_BU_l, void* stream);
 
 /* Bring-up / diagnostics only (not a product path): the same limb GEMM and epilogue on
  * CUDA cores, reading the same workspace and plain planes.  Used by the tests to tell a

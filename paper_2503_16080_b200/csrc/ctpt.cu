@@ -116,6 +116,7 @@ ctpt_status check_problem(const ctpt_problem* pb, Dims& d) {
   d.d2p = round_up(d.d2, 16);
   d.j0 = c0; d.j1 = c1; d.d3_loc = c1 - c0;
   if (pb->rescale != 0 && pb->rescale != 1) return fail(CTPT_ERR_ARG, "rescale must be 0 or 1");
+  if (pb->split_overlap != 0 && pb->split_overlap != 1) return fail(CTPT_ERR_ARG, "split_overlap must be 0 or 1");
   if (pb->rescale && pb->L < 2) return fail(CTPT_ERR_ARG, "Rescale by the last prime needs L >= 2 primes");
   d.L_out = pb->rescale ? pb->L - 1 : pb->L;
   if (pb->u_unsigned) {
@@ -155,10 +156,37 @@ size_t ws_base_bytes(const ctpt_problem* pb, const Dims& d) {
   return ws_limb_bytes(d);
 }
 // the very-skinny kernel's U_exp + split partials + tickets live after everything else
-size_t ws_mv_off(const ctpt_problem* pb, const Dims& d) { return align256(ws_base_bytes(pb, d)); }
+// split_overlap: a second limb + rowcorr buffer after the base region; prime l uses buffer l & 1
+bool overlap_on(const ctpt_problem* pb, const Dims& d) { return pb->split_overlap && !pb->rescale && d.L >= 2; }
+size_t ws_ovl_off(const ctpt_problem* pb, const Dims& d) { return align256(ws_base_bytes(pb, d)); }
+size_t ws_ovl_bytes(const ctpt_problem* pb, const Dims& d) {
+  return overlap_on(pb, d) ? align256(ws_limb_bytes(d)) + align256(static_cast<size_t>(4) * d.R) : 0;
+}
+void* ws_limbs(const ctpt_problem* pb, const Dims& d, void* ws, int l) {
+  return (overlap_on(pb, d) && (l & 1)) ? static_cast<uint8_t*>(ws) + ws_ovl_off(pb, d) : ws;
+}
+uint32_t* ws_corr(const ctpt_problem* pb, const Dims& d, void* ws, int l) {
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  return reinterpret_cast<uint32_t*>((overlap_on(pb, d) && (l & 1)) ? w + ws_ovl_off(pb, d) + align256(ws_limb_bytes(d))
+                                                                     : w + ws_corr_off(d));
+}
+size_t ws_mv_off(const ctpt_problem* pb, const Dims& d) { return align256(ws_base_bytes(pb, d)) + ws_ovl_bytes(pb, d); }
+// prime l's limb split as a job for the previous prime's GEMM kernel (warps 2–3, gemm_tc.cuh)
+SplitJob make_split_job(const ctpt_problem* pb, const Dims& d, const uint32_t* X0, void* ws, int l) {
+  SplitJob J{};
+  const uint32_t p = pb->primes[l];
+  J.x = reinterpret_cast<const uint4*>(X0 + static_cast<int64_t>(l) * d.R * d.d2p);
+  J.limbs = static_cast<uint4*>(ws_limbs(pb, d, ws, l));
+  J.rowcorr = needs_rowcorr(pb) ? ws_corr(pb, d, ws, l) : nullptr;
+  J.R = d.R;
+  J.d2p16 = d.d2p / 16;
+  J.p = p;
+  J.off_mod = static_cast<uint32_t>(((static_cast<int64_t>(pb->u_offset) % p) + p) % p);
+  return J;
+}
 size_t ws_bytes_needed(const ctpt_problem* pb, const Dims& d) {
   if (d.d3_loc <= 32) return ws_mv_off(pb, d) + mv_ws_bytes(d);
-  return ws_base_bytes(pb, d);
+  return overlap_on(pb, d) ? ws_ovl_off(pb, d) + ws_ovl_bytes(pb, d) : ws_base_bytes(pb, d);
 }
 
 ModP make_modp(uint32_t p) {
@@ -289,12 +317,14 @@ struct GemmArgs {
   int u_unsigned;        // U plane is u8 (U + u_offset)
   uint32_t p;
   OutParams o;           // accumulate / w are set per pass
+  SplitJob sj;           // the next prime's limb split, run inside the first pass (sj.x = nullptr: none)
 };
 ctpt_status launch_split(const uint32_t* x, int64_t n, void* limbs, cudaStream_t st);
 // the limb split of `rows` rows of X for prime p; in the unsigned-U mode it also writes rowcorr
 ctpt_status launch_split_prime(const ctpt_problem* pb, const uint32_t* x, int64_t rows, int64_t d2p, uint32_t p,
                                void* limbs, uint32_t* rowcorr, cudaStream_t st);
 ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt);
+ctpt_status launch_split_job(const SplitJob& J, cudaStream_t st);
 ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st);
 
 // The skinny regime: d3_loc ≤ 256 columns and one U digit plane.  There
@@ -512,12 +542,13 @@ ctpt_status ctpt_split(const ctpt_problem* pb, int32_t l, const void* d_ctmat, v
   if (ws_bytes < ws_bytes_needed(pb, d)) return fail(CTPT_ERR_ARG, "workspace too small");
   const int64_t n = d.R * d.d2p;  // multiple of 16
   const uint32_t* x = reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(d_ctmat) + kHeader) + l * n;
-  uint32_t* corr = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(d_ws) + ws_corr_off(d));
-  return launch_split_prime(pb, x, d.R, d.d2p, pb->primes[l], d_ws, corr, static_cast<cudaStream_t>(stream));
+  return launch_split_prime(pb, x, d.R, d.d2p, pb->primes[l], ws_limbs(pb, d, d_ws, l), ws_corr(pb, d, d_ws, l),
+                            static_cast<cudaStream_t>(stream));
 }
 
 static ctpt_status gemm_common(const ctpt_problem* pb, int32_t l, const void* d_ws, size_t ws_bytes,
-                               const void* d_plain, uint32_t* d_AU_l, uint32_t* d_BU_l, void* stream, bool simt) {
+                               const void* d_plain, uint32_t* d_AU_l, uint32_t* d_BU_l, void* stream, bool simt,
+                               const void* d_ctmat_next = nullptr) {
   Dims d;
   ctpt_status s = check_problem(pb, d);
   if (s != CTPT_OK) return s;
@@ -526,9 +557,9 @@ static ctpt_status gemm_common(const ctpt_problem* pb, int32_t l, const void* d_
   if (!d_ws || !d_plain || (!d_AU_l && d.rows_A > 0) || !d_BU_l) return fail(CTPT_ERR_ARG, "null device pointer");
   if (ws_bytes < ws_bytes_needed(pb, d)) return fail(CTPT_ERR_ARG, "workspace too small");
   GemmArgs g{};
-  g.limbs = d_ws;
+  g.limbs = ws_limbs(pb, d, const_cast<void*>(d_ws), l);
   g.u_unsigned = pb->u_unsigned;
-  if (needs_rowcorr(pb)) g.o.rowcorr = reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(d_ws) + ws_corr_off(d));
+  if (needs_rowcorr(pb)) g.o.rowcorr = ws_corr(pb, d, const_cast<void*>(d_ws), l);
   g.R = d.R;
   g.d = d;
   g.kU = pb->kU <= 0 ? 1 : pb->kU;
@@ -542,6 +573,9 @@ static ctpt_status gemm_common(const ctpt_problem* pb, int32_t l, const void* d_
   g.o.d1 = d.d1;
   g.o.R = d.R;
   g.o.d3_loc = d.d3_loc;
+  if (d_ctmat_next && l + 1 < d.L)
+    g.sj = make_split_job(pb, d, reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(d_ctmat_next) + kHeader),
+                          const_cast<void*>(d_ws), l + 1);
   return launch_gemm(g, static_cast<cudaStream_t>(stream), simt);
 }
 
@@ -560,6 +594,14 @@ ctpt_status launch_split_prime(const ctpt_problem* pb, const uint32_t* x, int64_
   const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(rows, INT32_MAX)));
   k_split_rows<<<blocks, 256, 0, st>>>(reinterpret_cast<const uint4*>(x), static_cast<uint4*>(limbs), rowcorr, rows,
                                         d2p / 16, p, off_mod);
+  CUDA_TRY(cudaGetLastError());
+  return CTPT_OK;
+}
+
+ctpt_status launch_split_job(const SplitJob& J, cudaStream_t st) {
+  if (!J.rowcorr) return launch_split(reinterpret_cast<const uint32_t*>(J.x), J.R * J.d2p16 * 16, J.limbs, st);
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(J.R, INT32_MAX)));
+  k_split_rows<<<blocks, 256, 0, st>>>(J.x, J.limbs, J.rowcorr, J.R, J.d2p16, J.p, J.off_mod);
   CUDA_TRY(cudaGetLastError());
   return CTPT_OK;
 }
@@ -594,7 +636,7 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
       k_gemm_simt<<<grid, 256, 0, st>>>(S);
       CUDA_TRY(cudaGetLastError());
     }
-    return CTPT_OK;
+    return g.sj.x ? launch_split_job(g.sj, st) : CTPT_OK;
   }
   ctpt_status s = tc_setup();
   if (s != CTPT_OK) return s;
@@ -644,12 +686,14 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
     P.o.accumulate = i > 0;
     P.o.w = pow2mod(8 * i, g.p);
     if (i < g.kU - 1) P.o.xlast = nullptr;  // Rescale on the final pass only
+    P.sj = (i == 0 && !pair) ? g.sj : SplitJob{};  // the next prime's split rides on the first pass
     if (pair)
       k_gemm_tc2<<<grid, T2_THREADS, T2_SMEM_BYTES, st>>>(tmU, tmX, P);
     else
       k_gemm_tc<<<grid, TC_THREADS, TC_SMEM_BYTES, st>>>(tmU, tmX, P);
     CUDA_TRY(cudaGetLastError());
   }
+  if (pair && g.sj.x) return launch_split_job(g.sj, st);  // the pair kernel has no side split
   return CTPT_OK;
 }
 
@@ -841,6 +885,16 @@ ctpt_status ctpt_gemm(const ctpt_problem* pb, int32_t l, const void* d_ws, size_
   return gemm_common(pb, l, d_ws, ws_bytes, d_plain, d_AU_l, d_BU_l, stream, false);
 }
 
+ctpt_status ctpt_gemm_next(const ctpt_problem* pb, int32_t l, const void* d_ctmat, void* d_ws, size_t ws_bytes,
+                           const void* d_plain, uint32_t* d_AU_l, uint32_t* d_BU_l, void* stream) {
+  Dims d;
+  ctpt_status s = check_problem(pb, d);
+  if (s != CTPT_OK) return s;
+  if (!overlap_on(pb, d)) return fail(CTPT_ERR_ARG, "ctpt_gemm_next needs split_overlap = 1, no rescale and L >= 2");
+  if (!d_ctmat) return fail(CTPT_ERR_ARG, "null device pointer");
+  return gemm_common(pb, l, d_ws, ws_bytes, d_plain, d_AU_l, d_BU_l, stream, false, d_ctmat);
+}
+
 ctpt_status ctpt_gemm_simt(const ctpt_problem* pb, int32_t l, const void* d_ws, size_t ws_bytes, const void* d_plain,
                            uint32_t* d_AU_l, uint32_t* d_BU_l, void* stream) {
   return gemm_common(pb, l, d_ws, ws_bytes, d_plain, d_AU_l, d_BU_l, stream, true);
@@ -946,6 +1000,7 @@ static ctpt_status matmul_impl(const ctpt_problem* pb, const Dims& d, const uint
     if (ws_bytes < need) return fail(CTPT_ERR_ARG, "workspace too small (%zu < %zu)", ws_bytes, need);
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool ovl = overlap_on(pb, d) && !fused && !mv;  // primes run in order 0..L−1 (no rescale)
   uint32_t* xlast = pb->rescale
                         ? reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(d_ws) + ws_xlast_off(pb, d))
                         : nullptr;
@@ -964,11 +1019,14 @@ static ctpt_status matmul_impl(const ctpt_problem* pb, const Dims& d, const uint
     const uint32_t* x = X0 + static_cast<int64_t>(l) * d.R * d.d2p;
     if (mv) return launch_mv(g, x, static_cast<uint8_t*>(d_ws) + ws_mv_off(pb, d), st);
     if (fused) return launch_fused(g, x, st);
-    uint32_t* corr = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(d_ws) + ws_corr_off(d));
-    ctpt_status s2 = launch_split_prime(pb, x, d.R, d.d2p, g.p, d_ws, corr, st);
-    if (s2 != CTPT_OK) return s2;
-    g.limbs = d_ws;
+    uint32_t* corr = ws_corr(pb, d, d_ws, l);
+    if (!ovl || l == 0) {  // with split_overlap only the first prime is split on its own
+      ctpt_status s2 = launch_split_prime(pb, x, d.R, d.d2p, g.p, ws_limbs(pb, d, d_ws, l), corr, st);
+      if (s2 != CTPT_OK) return s2;
+    }
+    g.limbs = ws_limbs(pb, d, d_ws, l);
     if (needs_rowcorr(pb)) g.o.rowcorr = corr;
+    if (ovl && l + 1 < d.L) g.sj = make_split_job(pb, d, X0, d_ws, l + 1);
     return launch_gemm(g, st, false);
   };
   if (pb->rescale) {

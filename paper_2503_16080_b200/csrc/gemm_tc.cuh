@@ -37,6 +37,44 @@ constexpr int TC_THREADS = 256;
 constexpr int TC_SMEM_BYTES = TC_STAGES * TC_STAGE_BYTES + 256 + 1024;
 constexpr int TC_GROUP_J_DEFAULT = 16;  // measured best of {8,16,32,64,128} on c3 (profiles/r01)
 
+// The limb split of the NEXT prime, run by the GEMM's two otherwise idle warps (2 and 3) while
+// this prime's MMAs run (ctpt_problem.split_overlap): x = Σ_{ℓ<4} x_ℓ 2^{8ℓ} byte transpose as in
+// k_split / k_split_rows (+ the unsigned-U row correction), streaming loads and stores
+// (evict-first) so the GEMM's L2-resident operand panels stay put.
+struct SplitJob {
+  const uint4* x;      // next prime's X, [R][d2p] int32 as uint4 (nullptr: no side split)
+  uint4* limbs;        // its four byte-limb planes [4][R][d2p]
+  uint32_t* rowcorr;   // u_offset·Σ_k X[r][k] mod p per row (unsigned-U mode), or nullptr
+  int64_t R, d2p16;    // rows; 16-residue groups per row
+  uint32_t p, off_mod; // next prime; u_offset mod p
+};
+
+__device__ __forceinline__ void side_split_rows(const SplitJob& J, int64_t worker, int64_t nworkers, int lane) {
+  const int64_t n16 = J.R * J.d2p16;
+  for (int64_t r = worker; r < J.R; r += nworkers) {
+    uint64_t sum = 0;
+    for (int64_t c = lane; c < J.d2p16; c += 32) {
+      const int64_t g = r * J.d2p16 + c;
+      uint4 w[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) w[i] = __ldcs(J.x + 4 * g + i);
+      uint32_t o[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        sum += static_cast<uint64_t>(w[i].x) + w[i].y + w[i].z + w[i].w;
+        byte_transpose4(w[i].x, w[i].y, w[i].z, w[i].w, o[0][i], o[1][i], o[2][i], o[3][i]);
+      }
+#pragma unroll
+      for (int l = 0; l < 4; ++l) __stcs(J.limbs + l * n16 + g, make_uint4(o[l][0], o[l][1], o[l][2], o[l][3]));
+    }
+    if (J.rowcorr) {
+#pragma unroll
+      for (int s = 16; s; s >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, s);
+      if (lane == 0) J.rowcorr[r] = static_cast<uint32_t>((sum % J.p) * J.off_mod % J.p);
+    }
+  }
+}
+
 struct TcParams {
   int64_t R, d2;
   int32_t j_off;      // first U column (col_begin)
@@ -49,6 +87,7 @@ struct TcParams {
   int32_t l2_pf;      // prefetch the operands of the iteration this far ahead into L2 (0: off)
   ModP m;
   OutParams o;
+  SplitJob sj;        // the next prime's limb split (warps 2–3), or sj.x = nullptr
 };
 
 __device__ __forceinline__ void tc_tile_coords(int32_t tile, const TcParams& P, int32_t& tj, int32_t& tr) {
@@ -159,6 +198,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
+  } else if (warp == 2 || warp == 3) {
+    // ---------------------------------------------------------------- next prime's limb split
+    if (P.sj.x) side_split_rows(P.sj, 2 * static_cast<int64_t>(blockIdx.x) + (warp - 2), 2 * static_cast<int64_t>(gridDim.x), lane);
   } else if (warp >= 4) {
     // ---------------------------------------------------------------- epilogue (128 threads)
     const int quad = warp & 3;  // TMEM lanes [32·quad, 32·quad + 32)

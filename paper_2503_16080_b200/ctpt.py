@@ -39,7 +39,7 @@ class Problem(ctypes.Structure):
                 ("d2", ctypes.c_int64), ("d3", ctypes.c_int64), ("primes", ctypes.POINTER(ctypes.c_uint32)),
                 ("col_begin", ctypes.c_int64), ("col_end", ctypes.c_int64), ("kU", ctypes.c_int32),
                 ("plain_per_prime", ctypes.c_int32), ("rescale", ctypes.c_int32),
-                ("u_unsigned", ctypes.c_int32), ("u_offset", ctypes.c_int32)]
+                ("u_unsigned", ctypes.c_int32), ("u_offset", ctypes.c_int32), ("split_overlap", ctypes.c_int32)]
 
 
 class Sizes(ctypes.Structure):
@@ -63,6 +63,7 @@ _sig = {
     "ctpt_split": (ctypes.c_int, [_PP, ctypes.c_int32, _P, _P, ctypes.c_size_t, _P]),
     "ctpt_gemm": (ctypes.c_int, [_PP, ctypes.c_int32, _P, ctypes.c_size_t, _P, _P, _P, _P]),
     "ctpt_gemm_simt": (ctypes.c_int, [_PP, ctypes.c_int32, _P, ctypes.c_size_t, _P, _P, _P, _P]),
+    "ctpt_gemm_next": (ctypes.c_int, [_PP, ctypes.c_int32, _P, _P, ctypes.c_size_t, _P, _P, _P, _P]),
     "ctpt_gemm_fused": (ctypes.c_int, [_PP, ctypes.c_int32, _P, _P, _P, _P, _P]),
     "ctpt_gemm_mv": (ctypes.c_int, [_PP, ctypes.c_int32, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
     "ctpt_rescale": (ctypes.c_int, [ctypes.c_int32, _P, ctypes.c_int64, _P, _P, _P]),
@@ -113,12 +114,13 @@ class Spec:
     rescale: int = 0
     u_unsigned: int = 0
     u_offset: int = 0
+    split_overlap: int = 0
 
     def cstruct(self) -> Problem:
         arr = (ctypes.c_uint32 * len(self.primes))(*[int(p) for p in self.primes])
         pb = Problem(self.fmt, len(self.primes), self.N, self.d1, self.d2, self.d3, arr, self.col_begin,
                      self.col_end, self.kU, self.plain_per_prime, self.rescale, self.u_unsigned,
-                     self.u_offset)
+                     self.u_offset, self.split_overlap)
         pb._keep = arr  # keep the host prime array alive with the struct
         return pb
 
@@ -194,6 +196,13 @@ def gemm(spec: Spec, l: int, ws, plain, AU_l, BU_l, stream=None, simt: bool = Fa
     f = _lib.ctpt_gemm_simt if simt else _lib.ctpt_gemm
     _check(f(ctypes.byref(pb), l, _ptr(ws), ws.numel() * ws.element_size(), _ptr(plain), _ptr(AU_l), _ptr(BU_l),
              _stream(stream)))
+
+
+def gemm_next(spec: Spec, l: int, ctmat, ws, plain, AU_l, BU_l, stream=None):
+    """ctpt_gemm of prime l with prime l+1's limb split inside the same kernel (spec.split_overlap = 1)."""
+    pb = spec.cstruct()
+    _check(_lib.ctpt_gemm_next(ctypes.byref(pb), l, _ptr(ctmat), _ptr(ws), ws.numel() * ws.element_size(), _ptr(plain),
+                               _ptr(AU_l), _ptr(BU_l), _stream(stream)))
 
 
 def gemm_fused(spec: Spec, l: int, ctmat, plain, AU_l, BU_l, stream=None):

@@ -742,3 +742,69 @@ def test_struct_a_algorithm7_with_rescale():
         bound = Fraction(int(np.abs(w).sum()) + 1, 2)
         for i in range(d1):
             assert abs(Fraction(cen[i]) - Fraction(int(PU[i, j]), q1)) <= bound, (j, i)
+
+
+# ------------------------------------------------------------------ split of prime l+1 inside GEMM l
+@pytest.mark.parametrize("kernel", ["1cta", "2cta"])
+@pytest.mark.parametrize("unsigned", ["never", "always"])
+def test_split_overlap_matmul(kernel, unsigned, monkeypatch):
+    """ctpt_problem.split_overlap = 1: ctpt_matmul splits prime 0 on its own and every further
+    prime inside the previous prime's GEMM (warps 2–3 of k_gemm_tc; the CTA-pair kernel falls back
+    to a standalone split after its GEMM), alternating two limb buffers — L = 3 and 4 primes, the
+    u8 plane with its row correction and the s8 plane, multi-digit U (side split in pass 0 only)."""
+    import torch
+
+    from paper_2503_16080_b200 import ctpt
+    from paper_2503_16080_b200.engine import CpmmEngine
+
+    monkeypatch.setenv("CTPT_SKINNY", "off")
+    monkeypatch.setenv("CTPT_GEMM", kernel)
+    for (fmt, N, k, d2, d3, L, ub) in [(A, 64, 3, 300, 260, 3, 8), (S, 32, 4, 129, 300, 4, 8),
+                                        (R, 256, 1, 200, 140, 2, 300)]:
+        d1 = N * k
+        ps = ctgen.primes(L)
+        ct = ctgen.encrypt(fmt, N, d1, d2, 21, 20, ps)
+        U = ctgen.U_matrix(21, d2, d3, ub)
+        eng = CpmmEngine(ctpt.Spec(fmt, N, d1, d2, d3, ps, split_overlap=1), "cuda")
+        eng.layout(ct.a_polys, ct.b_polys)
+        eng.precompute(U, unsigned=unsigned if ub <= 127 else "never")
+        AU, BU = eng.matmul()
+        torch.cuda.synchronize()
+        AUn, BUn = eng.outputs_numpy(AU, BU)
+        for l, p in enumerate(ps):
+            wa, wb = oracle_outputs(fmt, N, d1, ct.a_polys[l], ct.b_polys[l], U, p)
+            assert np.array_equal(AUn[l], wa) and np.array_equal(BUn[l], wb), (fmt, l)
+
+
+def test_split_overlap_stage_entry_points(monkeypatch):
+    """The per-stage form a benchmark times: ctpt_split(0), then ctpt_gemm_next(l) per prime;
+    ctpt_gemm_next refuses a problem without split_overlap."""
+    import torch
+
+    from paper_2503_16080_b200 import ctpt
+    from paper_2503_16080_b200.engine import CpmmEngine
+
+    monkeypatch.delenv("CTPT_GEMM", raising=False)
+    fmt, N, k, d2, d3, L = A, 128, 2, 520, 400, 3
+    d1 = N * k
+    ps = ctgen.primes(L)
+    ct = ctgen.encrypt(fmt, N, d1, d2, 22, 20, ps)
+    U = ctgen.U_matrix(22, d2, d3, 8)
+    eng = CpmmEngine(ctpt.Spec(fmt, N, d1, d2, d3, ps, split_overlap=1), "cuda")
+    eng.layout(ct.a_polys, ct.b_polys)
+    eng.precompute(U)
+    AU, BU = eng.alloc_outputs()
+    ra = eng.sizes.rows_A
+    for rep in range(2):  # the second step reuses both limb buffers
+        ctpt.split(eng.spec, 0, eng.ctmat, eng.ws)
+        for l in range(L):
+            ctpt.gemm_next(eng.spec, l, eng.ctmat, eng.ws, eng.plain, AU[l * d3 * ra:], BU[l * d3 * d1:])
+    torch.cuda.synchronize()
+    AUn, BUn = eng.outputs_numpy(AU, BU)
+    for l, p in enumerate(ps):
+        wa, wb = oracle_outputs(fmt, N, d1, ct.a_polys[l], ct.b_polys[l], U, p)
+        assert np.array_equal(AUn[l], wa) and np.array_equal(BUn[l], wb), l
+    plain = ctpt.Spec(fmt, N, d1, d2, d3, ps, kU=eng.spec.kU, u_unsigned=eng.spec.u_unsigned,
+                      u_offset=eng.spec.u_offset)
+    with pytest.raises(ctpt.CtptError, match="ERR_ARG"):
+        ctpt.gemm_next(plain, 0, eng.ctmat, eng.ws, eng.plain, AU, BU)
