@@ -165,7 +165,12 @@ def cpu_oracle_rate(c, ct, U, target_s: float, gpu_out=None):
     wb = oracle.modmatmul(Bc, U, p, cols=np.arange(ncols2), nthreads=cores)
     dt = time.perf_counter() - t0
     macs = c.R * c.d2 * ncols2
-    out = {"value": macs / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+    # single-thread rate (the paper's setting) on a slab: one output column of B·U
+    t1 = time.perf_counter()
+    oracle.modmatmul(Bc, U, p, cols=np.arange(1), nthreads=1)
+    st_rate = c.d1 * c.d2 / (time.perf_counter() - t1)
+    out = {"value": macs / dt, "unit": UNIT, "cores": cores, "kind": "oracle", "host": host_description(),
+           "single_thread_value": st_rate,
            "sample": f"prime 0, {ncols2} of {c.d3} output columns x all {c.R} stacked rows x d2={c.d2} "
                      f"({macs:.3e} residue-MACs, {dt:.1f} s, schoolbook __int128, OpenMP {cores} threads)"}
     if gpu_out is not None:
@@ -176,6 +181,53 @@ def cpu_oracle_rate(c, ct, U, target_s: float, gpu_out=None):
         out["parity_on_sample"] = {"entries": int(ncols2 * c.R), "mismatches": bad,
                                    "verdict": "bit-exact" if bad == 0 else "MISMATCH"}
     return out
+
+
+def host_description() -> str:
+    """lscpu model, sockets × cores × threads per core."""
+    try:
+        txt = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+    except (OSError, subprocess.SubprocessError):
+        return f"{os.cpu_count()} logical CPUs"
+    kv = {}
+    for line in txt.splitlines():
+        if ":" in line:
+            k, v = line.split(":", 1)
+            kv[k.strip()] = v.strip()
+    return (f"{kv.get('Model name', '?')}; {kv.get('Socket(s)', '?')} socket(s) x {kv.get('Core(s) per socket', '?')} "
+            f"cores x {kv.get('Thread(s) per core', '?')} threads = {os.cpu_count()} logical CPUs")
+
+
+def precision_on_sample(c, ps, AU, BU, U, cols, nthreads: int):
+    """Decrypt and decode sampled output columns of the timed run (all primes) and compare with
+    M·U in float64 — the paper's precision metric prec = log2‖M·U‖∞ − log2‖dec − M·U‖∞
+     and the relative error the north star bounds by 1e-6 (reading Q15).  Oracle
+    code only (decryption, exact CRT); AU / BU: device outputs [L][d3][rows_A], [L][d3][d1]."""
+    import ctgen
+    import oracle
+
+    nk = c.k if c.fmt == ctgen.SHARED_A else 1
+    sks = [ctgen.sk(c.seed, t, c.N) for t in range(nk)]
+    ra = c.rows_A
+    mu = np.zeros((c.d1, len(cols)), dtype=np.float64)
+    Uc = U[:, cols].astype(np.float64)
+    kb = 2048
+    for k0 in range(0, c.d2, kb):
+        n = min(kb, c.d2 - k0)
+        mu += ctgen.msg_block(c.seed, c.d1, 0, c.d1, k0, n, nthreads=nthreads).dot(Uc[k0:k0 + n])
+    worst_prec, worst_rel = float("inf"), 0.0
+    for ci, j in enumerate(cols):
+        decs = []
+        for l, p in enumerate(ps):
+            a_col = AU[l, j].cpu().numpy().view(np.uint32) if ra else None
+            b_col = BU[l, j].cpu().numpy().view(np.uint32)
+            decs.append(oracle.decrypt_col(c.fmt, c.N, c.d1, sks, a_col, b_col, p, nthreads=nthreads))
+        cen = oracle.crt_centred_array(np.stack(decs), ps)
+        dec = np.array([float(v) for v in cen]) / 2.0 ** c.log_delta
+        worst_prec = min(worst_prec, oracle.precision_bits(mu[:, ci], dec))
+        worst_rel = max(worst_rel, float(np.abs(dec - mu[:, ci]).max() / np.abs(mu[:, ci]).max()))
+    return {"columns": [int(j) for j in cols], "precision_bits": worst_prec, "rel_err_inf": worst_rel,
+            "bound": 1e-6, "verdict": "ok" if worst_rel <= 1e-6 else "ABOVE 1e-6"}
 
 
 # ------------------------------------------------------------------------------------ inputs
@@ -461,6 +513,13 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             gpu0 = (AU[:n0].cpu().numpy().view(np.uint32).reshape(d3l, ra),
                     BU[:d3l * c.d1].cpu().numpy().view(np.uint32).reshape(d3l, c.d1))
         result["cpu_baseline"] = cpu_oracle_rate(c, ct, U, args.cpu_seconds, gpu0)
+        if not args.rescale and c.fmt != ctgen.STRUCT_A:  # decode a few columns of the timed run
+            t0 = time.perf_counter()
+            AUv = AU.view(len(ps), d3l, ra) if ra else None
+            BUv = BU.view(len(ps), d3l, c.d1)
+            pr = precision_on_sample(c, ps, AUv, BUv, U, [0, d3l - 1], cores)
+            pr["seconds"] = time.perf_counter() - t0
+            result["cpu_baseline"]["decoded_on_sample"] = pr
     if rank == 0:
         print(json.dumps(result))
 
