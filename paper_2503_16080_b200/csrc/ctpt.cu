@@ -14,6 +14,7 @@
 #include "../../include/ctpt.h"
 #include "gemm_tc.cuh"
 #include "gemm_tc2.cuh"
+#include "gemm_tc_mc.cuh"
 #include "gemm_fused.cuh"
 #include "gemm_fused2.cuh"
 #include "gemm_mv.cuh"
@@ -281,6 +282,8 @@ ctpt_status tc_setup() {
     e = cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BYTES);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_gemm_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, T2_SMEM_BYTES);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_gemm_tc_mc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BYTES);
 #define CTPT_FU_ATTR(NG, MODE) \
     if (e == cudaSuccess)      \
       e = cudaFuncSetAttribute(k_gemm_fused<NG, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(NG, MODE));
@@ -645,13 +648,16 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
   // more efficient per clock — 95 % vs 84 % of 8192 MAC/clk/SM — but draws more power per
   // clock; profiles/r01/power_1cta_vs_2cta.txt), so it is the default; CTPT_GEMM=2cta selects
   // the pair kernel (tests exercise both).
-  bool pair = false;
-  if (const char* g = getenv("CTPT_GEMM")) pair = (strcmp(g, "2cta") == 0);
+  bool pair = false, mc = false;
+  if (const char* g = getenv("CTPT_GEMM")) {
+    pair = (strcmp(g, "2cta") == 0);
+    mc = (strcmp(g, "mc") == 0) && num_sms() >= 2;  // 2-CTA clusters sharing X by TMA multicast
+  }
   const int block_j = pair ? T2_BLOCK_J : TC_BLOCK_J;
   CUtensorMap tmU, tmX;
   s = make_tmap_u8(&tmU, g.planes, d.d2, d.d3, g.nplanes, d.d2p, d.d3 * d.d2p, TC_BLOCK_K, 128, 1);
   if (s != CTPT_OK) return s;
-  s = make_tmap_u8(&tmX, g.limbs, d.d2, g.R, 4, d.d2p, g.R * d.d2p, TC_BLOCK_K, TC_BLOCK_R, pair ? 2 : 4);
+  s = make_tmap_u8(&tmX, g.limbs, d.d2, g.R, 4, d.d2p, g.R * d.d2p, TC_BLOCK_K, TC_BLOCK_R, (pair || mc) ? 2 : 4);
   if (s != CTPT_OK) return s;
   TcParams P;
   P.R = g.R;
@@ -678,7 +684,10 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
   if (const char* g = getenv("CTPT_GEMM_PF")) P.l2_pf = std::max(0, atoi(g));     // tuning knob
   P.m = m;
   const int sms = num_sms();
+  if (mc) P.group_j = std::max(1, P.group_j / 2);  // raster groups of j-tile PAIRS, same U footprint
+  const int64_t nt_mc = static_cast<int64_t>((P.tiles_j + 1) / 2) * P.tiles_r;
   const unsigned grid = pair ? static_cast<unsigned>(2 * std::min<int64_t>(nt, sms / 2))
+                        : mc ? static_cast<unsigned>(2 * std::min<int64_t>(nt_mc, sms / 2))
                              : static_cast<unsigned>(std::min<int64_t>(nt, sms));
   for (int i = 0; i < g.kU; ++i) {
     P.plane = g.plane0 + i;
@@ -689,6 +698,8 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
     P.sj = (i == 0 && !pair) ? g.sj : SplitJob{};  // the next prime's split rides on the first pass
     if (pair)
       k_gemm_tc2<<<grid, T2_THREADS, T2_SMEM_BYTES, st>>>(tmU, tmX, P);
+    else if (mc)
+      k_gemm_tc_mc<<<grid, TC_THREADS, TC_SMEM_BYTES, st>>>(tmU, tmX, P);
     else
       k_gemm_tc<<<grid, TC_THREADS, TC_SMEM_BYTES, st>>>(tmU, tmX, P);
     CUDA_TRY(cudaGetLastError());

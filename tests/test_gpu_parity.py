@@ -56,11 +56,11 @@ def _check(fmt, N, k, d2, d3, L, seed=0, u_bound=8, simt=False, col_begin=0, col
         assert np.array_equal(BU[l], wb), f"B·U mismatch prime {l}: {np.argwhere(BU[l] != wb)[:5]}"
 
 
-@pytest.fixture(params=["1cta", "2cta", "fused"])
+@pytest.fixture(params=["1cta", "2cta", "mc", "fused"])
 def gemm_kernel(request, monkeypatch):
-    """Force the single-CTA (k_gemm_tc) or CTA-pair (k_gemm_tc2) tensor-core kernel after a
-    separate split (CTPT_SKINNY=off), or leave ctpt_matmul's default, which takes the fused
-    skinny kernel (k_gemm_fused) whenever d3_loc <= 256 and kU = 1."""
+    """Force the single-CTA (k_gemm_tc), CTA-pair (k_gemm_tc2) or multicast-cluster (k_gemm_tc_mc)
+    tensor-core kernel after a separate split (CTPT_SKINNY=off), or leave ctpt_matmul's default,
+    which takes the fused skinny kernel (k_gemm_fused) whenever d3_loc <= 256 and kU = 1."""
     if request.param == "fused":
         monkeypatch.delenv("CTPT_SKINNY", raising=False)
     else:
@@ -745,7 +745,7 @@ def test_struct_a_algorithm7_with_rescale():
 
 
 # ------------------------------------------------------------------ split of prime l+1 inside GEMM l
-@pytest.mark.parametrize("kernel", ["1cta", "2cta"])
+@pytest.mark.parametrize("kernel", ["1cta", "2cta", "mc"])
 @pytest.mark.parametrize("unsigned", ["never", "always"])
 def test_split_overlap_matmul(kernel, unsigned, monkeypatch):
     """ctpt_problem.split_overlap = 1: ctpt_matmul splits prime 0 on its own and every further
