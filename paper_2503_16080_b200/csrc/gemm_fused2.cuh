@@ -26,9 +26,9 @@
 // Status: opt-in (CTPT_FUSED2=pair).  Bit-exact in every test, but not faster than the
 // single-CTA NG = 2 kernel on c4's ciphertexts (2.05–2.22 vs 2.02–2.14 ms per launch for
 // d3 = 129..256; profiles/r01/fused2_pair/): its time does not follow d3, i.e. the MMA is not the
-// bound — the converters' per-K-block latency chain and the pair's lock-step stages are.  One
-// run of ~1700 launches ended in an unexplained launch failure that 12 stress runs did not
-// reproduce (fused2_pair/stress.log); a reason more to keep it off the default path.
+// bound — the converters' per-K-block latency chain and the pair's lock-step stages are.  (One
+// early run ended in a launch failure: an mbarrier parity alias with two converter groups on an
+// odd-length raw ring, fixed below.)
 // Warp roles (512 threads per CTA): w0 U^T TMA, w1 MMA issuer (leader), w2 TMEM allocator,
 // w3 raw X TMA, w4–7 epilogue, w8–15 converters (4 rows each).
 #pragma once
@@ -47,7 +47,13 @@ constexpr int F2_X_BYTES = 4 * F2_ROWS * F2_BLOCK_K;         // this CTA's 4 lim
 constexpr int F2_STAGE_BYTES = F2_U_BYTES + F2_X_BYTES;      // 32 KB
 constexpr int F2_STAGES = 4;
 constexpr int F2_RAW_BYTES = F2_ROWS * F2_BLOCK_K * 4;       // 16 KB raw int32 tile
-constexpr int F2_RAW_STAGES = 5;                             // 80 KB of X in flight per SM
+constexpr int F2_RAW_STAGES = 6;                             // 96 KB of X in flight per SM
+// Both rings' lengths must be multiples of the converter-group count CG (≤ 2): group g then
+// always meets the same stages, so its previous use of a stage is its own and an mbarrier parity
+// wait can never match a phase two behind.  (With 5 raw stages the groups alternated over a
+// stage: a group could pass raw_full(s) while the OTHER group's earlier fill of s was still in
+// flight — a TMA landing out of order — and read a stale tile: the one unexplained launch
+// failure of the first measurements.)
 constexpr int F2_ACC_COLS = 256;
 constexpr int F2_THREADS = 512;
 constexpr int F2_CONV_WARPS = 8;
@@ -209,7 +215,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2_THREADS, 1)
     // in flight at once and each warp amortises its per-iteration latency chain (barrier waits,
     // two proxy fences) over 4·CG rows.  Warp w of a group owns rows w + (8/CG)·i of this CTA's
     // 32-row half; lane owns residues 4·lane .. 4·lane+3 (one 512-B row segment per instruction).
-    constexpr int WPG = F2_CONV_WARPS / CG;       // warps per group
+    static_assert(F2_RAW_STAGES % CG == 0 && F2_STAGES % CG == 0, "ring lengths must be multiples of CG");
+  constexpr int WPG = F2_CONV_WARPS / CG;       // warps per group
     constexpr int RPW = F2_ROWS / WPG;            // rows per warp
     const int cw = warp - 8;
     const int grp = cw / WPG, w = cw % WPG;
