@@ -293,6 +293,8 @@ ctpt_status tc_setup() {
     CTPT_FU_ATTR(2, FU_TMA)
     CTPT_FU_ATTR(1, FU_HYBRID)
     CTPT_FU_ATTR(2, FU_HYBRID)
+    CTPT_FU_ATTR(1, FU_TMA2)
+    CTPT_FU_ATTR(2, FU_TMA2)
 #undef CTPT_FU_ATTR
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_fused2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, F2_SMEM_BYTES);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_fused2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, F2_SMEM_BYTES);
@@ -738,6 +740,7 @@ ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st) 
   if (const char* e = getenv("CTPT_FUSED_LOAD")) {
     if (strcmp(e, "regs") == 0) mode = FU_REGS;
     if (strcmp(e, "hybrid") == 0) mode = FU_HYBRID;
+    if (strcmp(e, "tma2") == 0) mode = FU_TMA2;
   }
   // L2 prefetch distance for the raw X ring (iterations ahead of the TMA into shared memory)
   P.l2_prefetch = 0;  // measured: any L2 prefetch distance (2..16) lowered the fused kernel 5–35 %
@@ -768,10 +771,12 @@ ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st) 
   k_gemm_fused<NG, MODE><<<grid, FU_THREADS, fu_smem_bytes(NG, MODE), st>>>(tmU, tmX, P)
   if (ng == 1) {
     if (mode == FU_TMA) CTPT_FU_LAUNCH(1, FU_TMA);
+    else if (mode == FU_TMA2) CTPT_FU_LAUNCH(1, FU_TMA2);
     else if (mode == FU_HYBRID) CTPT_FU_LAUNCH(1, FU_HYBRID);
     else CTPT_FU_LAUNCH(1, FU_REGS);
   } else {
     if (mode == FU_TMA) CTPT_FU_LAUNCH(2, FU_TMA);
+    else if (mode == FU_TMA2) CTPT_FU_LAUNCH(2, FU_TMA2);
     else if (mode == FU_HYBRID) CTPT_FU_LAUNCH(2, FU_HYBRID);
     else CTPT_FU_LAUNCH(2, FU_REGS);
   }

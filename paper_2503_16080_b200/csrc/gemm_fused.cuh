@@ -41,12 +41,16 @@ constexpr int FU_ROWS_PER_WARP = FU_BLOCK_R / FU_CONV_WARPS; // 8
 //   FU_HYBRID: rows 0–31 of every tile through the TMA ring (32-row raw tiles, twice as many
 //              stages in the same bytes), rows 32–63 by register loads — half the raw
 //              shared-memory round trip (the kernel is bound by shared-memory bandwidth).
-constexpr int FU_REGS = 0, FU_TMA = 1, FU_HYBRID = 2;
+//   FU_TMA2:   the TMA raw ring with TWO converter groups of 4 warps (16 rows each) taking
+//              alternate K-blocks, so two K-blocks are in conversion at once and each warp's
+//              per-iteration latency chain (barrier waits, two proxy fences) covers twice the rows;
+//              both ring lengths are even so a group always meets the same stages (parity safety).
+constexpr int FU_REGS = 0, FU_TMA = 1, FU_HYBRID = 2, FU_TMA2 = 3;
 __host__ __device__ constexpr int fu_raw_rows(int mode) { return mode == FU_HYBRID ? 32 : FU_BLOCK_R; }
 __host__ __device__ constexpr int fu_raw_bytes(int mode) { return fu_raw_rows(mode) * FU_BLOCK_K * 4; }
 __host__ __device__ constexpr int fu_stages(int ng, int mode) { return mode != FU_REGS ? 2 : (ng == 1 ? 4 : 3); }
 __host__ __device__ constexpr int fu_raw_stages(int ng, int mode) {
-  return mode == FU_REGS ? 0 : ((ng == 1 ? 128 : 96) * 1024) / fu_raw_bytes(mode);
+  return mode == FU_REGS ? 0 : mode == FU_TMA2 ? (ng == 1 ? 4 : 2) : ((ng == 1 ? 128 : 96) * 1024) / fu_raw_bytes(mode);
 }
 __host__ __device__ constexpr int fu_stage_bytes(int ng) { return ng * FU_U_BYTES + FU_X_BYTES; }
 __host__ __device__ constexpr int fu_smem_bytes(int ng, int mode) {
@@ -81,7 +85,9 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
   constexpr int STAGES = fu_stages(NG, MODE);
   constexpr int RAW = fu_raw_stages(NG, MODE);
   constexpr int RAW_BYTES = fu_raw_bytes(MODE);
-  constexpr int RAW_WARPS = MODE == FU_HYBRID ? 4 : (MODE == FU_TMA ? FU_CONV_WARPS : 0);
+  constexpr int RAW_WARPS = MODE == FU_HYBRID ? 4 : ((MODE == FU_TMA || MODE == FU_TMA2) ? FU_CONV_WARPS : 0);
+  constexpr int CG = MODE == FU_TMA2 ? 2 : 1;  // converter groups (alternate K-blocks)
+  static_assert(STAGES % CG == 0 && (RAW == 0 || RAW % CG == 0), "ring lengths must be multiples of CG");
   constexpr int STAGE_BYTES = fu_stage_bytes(NG);
   constexpr int NBUF = (NG == 1) ? 2 : 1;  // accumulator buffers (NBUF·NG·256 ≤ 512 columns)
   extern __shared__ uint8_t smem_raw[];
@@ -109,7 +115,7 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmU);
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full_bar(s), 1 + FU_CONV_WARPS);
+      mbar_init(full_bar(s), 1 + FU_CONV_WARPS / CG);
       mbar_init(empty_bar(s), 1);
     }
     for (int b = 0; b < NBUF; ++b) {
@@ -118,7 +124,7 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
     }
     for (int s = 0; s < RAW; ++s) {
       mbar_init(raw_full(s), 1);
-      mbar_init(raw_empty(s), RAW_WARPS);
+      mbar_init(raw_empty(s), RAW_WARPS / CG);
     }
     if (TMA_X) tma_prefetch(&tmX);
     fence_mbar_init();
@@ -256,7 +262,44 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
       mbar_arrive(tempty_bar(acc));
       if (++acc == NBUF) { acc = 0; acc_phase ^= 1; }
     }
-  } else if (warp >= FU_CONV_WARP0) {
+  } else if (MODE == FU_TMA2 && warp >= FU_CONV_WARP0) {
+    // ---------------------------------------------------------------- converters, two groups
+    // group g = cw / 4 converts the K-blocks it ≡ g (mod 2); warp w = cw % 4 of a group owns
+    // rows w + 4·i (i < 16) of the 64-row tile; lane owns residues 4·lane .. 4·lane+3.
+    constexpr int WPG = FU_CONV_WARPS / 2, RPW = FU_BLOCK_R / WPG;
+    const int cw = warp - FU_CONV_WARP0;
+    const int grp = cw / WPG, w = cw % WPG;
+    for (int64_t it = grp; it < n_it; it += 2) {
+      const int rs = static_cast<int>(it % RAW);
+      const int stage = static_cast<int>(it % STAGES);
+      mbar_wait(raw_full(rs), static_cast<uint32_t>((it / RAW) & 1));
+      const uint32_t sraw = raw_base + rs * RAW_BYTES;
+      uint32_t lw[RPW][4];
+#pragma unroll
+      for (int i = 0; i < RPW; ++i) {
+        const uint4 v = lds128(sraw + (w + WPG * i) * 512 + lane * 16);
+        byte_transpose4(v.x, v.y, v.z, v.w, lw[i][0], lw[i][1], lw[i][2], lw[i][3]);
+      }
+      fence_proxy_async_smem();  // release the raw tile after its values are consumed
+      __syncwarp();
+      if (lane == 0) mbar_arrive(raw_empty(rs));
+      mbar_wait(empty_bar(stage), static_cast<uint32_t>(((it / STAGES) & 1) ^ 1));
+      const uint32_t sx = sbase + stage * STAGE_BYTES + NG * FU_U_BYTES;
+#pragma unroll
+      for (int i = 0; i < RPW; ++i) {
+        const int row = w + WPG * i;
+        const uint32_t off =
+            static_cast<uint32_t>(row) * 128u + ((((lane >> 2) ^ (row & 7)) << 4) | ((lane & 3) << 2));
+        sts32(sx + 0 * FU_BLOCK_R * 128 + off, lw[i][0]);
+        sts32(sx + 1 * FU_BLOCK_R * 128 + off, lw[i][1]);
+        sts32(sx + 2 * FU_BLOCK_R * 128 + off, lw[i][2]);
+        sts32(sx + 3 * FU_BLOCK_R * 128 + off, lw[i][3]);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(full_bar(stage));
+    }
+  } else if (MODE != FU_TMA2 && warp >= FU_CONV_WARP0) {
     // ---------------------------------------------------------------- converters (256 threads)
     // Warp cw owns rows cw + 8·i (i < 8) of every 64-row tile; lane owns residues 4·lane..4·lane+3
     // of the K-block (one coalesced 512-B row segment per warp instruction).  Loads run two

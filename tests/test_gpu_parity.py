@@ -154,17 +154,17 @@ SKINNY = [
 
 
 def _fused_load(monkeypatch, load):
-    """'tma' = the default (raw X ring, single CTA), 'tma2' = the raw X ring with d3_loc > 128 on
-    the CTA-pair kernel k_gemm_fused2 (CTPT_FUSED2=pair), 'regs' / 'hybrid' = the register-load
-    feeds (single CTA)."""
-    monkeypatch.setenv("CTPT_FUSED_LOAD", "tma" if load == "tma2" else load)
-    if load == "tma2":
+    """'tma' = the default (raw X ring, single CTA), 'tma2' = the raw X ring with two converter
+    groups on alternate K-blocks (single CTA), 'pair' = the raw X ring with d3_loc > 128 on the
+    CTA-pair kernel k_gemm_fused2 (CTPT_FUSED2=pair), 'regs' / 'hybrid' = the register-load feeds."""
+    monkeypatch.setenv("CTPT_FUSED_LOAD", "tma" if load == "pair" else load)
+    if load == "pair":
         monkeypatch.setenv("CTPT_FUSED2", "pair")
     else:
         monkeypatch.delenv("CTPT_FUSED2", raising=False)
 
 
-@pytest.mark.parametrize("load", ["tma", "tma2", "regs", "hybrid"])
+@pytest.mark.parametrize("load", ["tma", "tma2", "pair", "regs", "hybrid"])
 @pytest.mark.parametrize("shape", SKINNY, ids=lambda s: "f%d_N%d_k%d_d2%d_d3%d_L%d" % s)
 def test_skinny_fused(shape, load, monkeypatch):
     """Every way of feeding the fused kernel's converters: raw X tiles by TMA (single CTA, or the
@@ -241,7 +241,7 @@ def test_mv_column_shard_and_entry_point(monkeypatch):
             assert np.array_equal(AUn[l], wa) and np.array_equal(BUn[l], wb), (c0, c1, l)
 
 
-@pytest.mark.parametrize("load", ["tma", "tma2", "regs", "hybrid"])
+@pytest.mark.parametrize("load", ["tma", "tma2", "pair", "regs", "hybrid"])
 def test_skinny_long_k_ring_wraparound(load, monkeypatch):
     """Long K (33–65 k-blocks per tile) wraps the raw-X and limb rings many times; a premature
     release of a raw tile once corrupted whole output rows intermittently — run it repeatedly."""
