@@ -503,7 +503,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                                     f"{elapsed_ms / 1e3:.2f} s)",
                      "per_launch": (f"{limb_macs_launch:.4e} limb MACs (4·kU·R·d2·d3 · L, whole step)" if args.rescale
                                     else f"{limb_macs_launch:.4e} limb MACs (4·kU·R·d2·d3, one prime)"),
-                     "avg_launch_ms": gemm_avg_s * 1e3, "share_of_step": gemm_share},
+                     "avg_launch_ms": gemm_avg_s * 1e3, "share_of_step": gemm_share,
+                     # achieved DRAM GB/s of that kernel (ncu bytes per launch ÷ the
+                     # live per-launch time) against the measured copy bandwidth
+                     "dram_gbs": (traffic / gemm_avg_s / 1e9) if traffic and not args.rescale else None,
+                     "dram_frac": (traffic / gemm_avg_s / 1e9 / float(mp["hbm_gbs"]))
+                     if traffic and not args.rescale else None},
         "e2e": e2e,
         # per prime: k_split[_rows] + kU x k_gemm_tc, or one k_gemm_fused / k_gemm_mv (+ k_expand_u)
         "gpu_launches": ((1 + kU * len(ps)) if inkernel_split else
