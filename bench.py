@@ -458,7 +458,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "gemm_dram_bytes.json")) as f:
-            traffic = json.load(f).get(c.name)
+            traffic = json.load(f).get(c.name + ("_side_split" if inkernel_split else ""))
     except OSError:
         pass
 
