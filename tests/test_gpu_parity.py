@@ -40,14 +40,14 @@ SHAPES = [
 
 
 def _check(fmt, N, k, d2, d3, L, seed=0, u_bound=8, simt=False, col_begin=0, col_end=0, unsigned="auto",
-           U=None):
+           U=None, split_overlap=0):
     d1 = N * k
     ps = ctgen.primes(L)
     ct = ctgen.encrypt(fmt, N, d1, d2, seed, 20, ps, nthreads=NTHREADS)
     if U is None:
         U = ctgen.U_matrix(seed, d2, d3, u_bound)
     (AU, BU), eng = run_gpu(fmt, N, d1, d2, d3, ps, ct.a_polys, ct.b_polys, U=U, simt=simt, col_begin=col_begin,
-                            col_end=col_end, unsigned=unsigned)
+                            col_end=col_end, unsigned=unsigned, split_overlap=split_overlap)
     c1 = col_end or d3
     cols = np.arange(col_begin, c1)
     for l, p in enumerate(ps):
@@ -808,3 +808,33 @@ def test_split_overlap_stage_entry_points(monkeypatch):
                       u_offset=eng.spec.u_offset)
     with pytest.raises(ctpt.CtptError, match="ERR_ARG"):
         ctpt.gemm_next(plain, 0, eng.ctmat, eng.ws, eng.plain, AU, BU)
+
+
+# ------------------------------------------------------------------ seeded random shapes (fuzz)
+def _fuzz_cases(n=48, seed=2025):
+    rng = np.random.default_rng(seed)
+    cases = []
+    for i in range(n):
+        fmt = int(rng.choice([R, S, A, SA]))
+        N = int(rng.choice([2, 4, 8, 16, 32, 64, 128, 256]))
+        k = 1 if fmt == R else int(rng.integers(1, 5))
+        d2 = int(rng.integers(1, 700))
+        d3 = int(rng.choice([1, 2, 5, 16, 31, 33, 64, 100, 128, 129, 200, 256, 257, 300, 520]))
+        L = int(rng.integers(1, 4))
+        ub = int(rng.choice([1, 8, 127, 128, 300, 40000]))
+        c0 = int(rng.integers(0, d3)) if rng.random() < 0.3 else 0
+        c1 = int(rng.integers(c0 + 1, d3 + 1)) if c0 or rng.random() < 0.2 else 0
+        cases.append((fmt, N, k, d2, d3, L, ub, c0, c1, i))
+    return cases
+
+
+@pytest.mark.parametrize("case", _fuzz_cases(), ids=lambda c: "f%d_N%d_k%d_d2%d_d3%d_L%d_u%d_c%d-%d_%d" % c)
+def test_fuzz_shapes_against_oracle(case, monkeypatch):
+    """Seeded random problems across every dimension regime the library dispatches on (d3_loc ≤ 32
+    raw-byte kernel, ≤ 256 fused kernel, else split + GEMM; k_U = 1..3 digits; s8 or u8 U
+    planes; column shards; d2 from 1; N from 2; every other case with split_overlap = 1) — each
+    output entry against the oracle."""
+    for var in ("CTPT_SKINNY", "CTPT_MV", "CTPT_GEMM", "CTPT_FUSED_LOAD", "CTPT_FUSED2", "CTPT_LAYOUT"):
+        monkeypatch.delenv(var, raising=False)
+    fmt, N, k, d2, d3, L, ub, c0, c1, i = case
+    _check(fmt, N, k, d2, d3, L, seed=100 + i, u_bound=ub, col_begin=c0, col_end=c1, split_overlap=i % 2)
