@@ -684,6 +684,8 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
   if (const char* g = getenv("CTPT_GROUP_J")) P.group_j = std::max(1, atoi(g));  // tuning knob
   P.l2_pf = 0;
   if (const char* g = getenv("CTPT_GEMM_PF")) P.l2_pf = std::max(0, atoi(g));     // tuning knob
+  P.l2_hint = 0;
+  if (const char* g = getenv("CTPT_GEMM_L2HINT")) P.l2_hint = std::max(0, atoi(g));  // tuning knob (measuring)
   P.m = m;
   const int sms = num_sms();
   if (mc) P.group_j = std::max(1, P.group_j / 2);  // raster groups of j-tile PAIRS, same U footprint

@@ -85,6 +85,7 @@ struct TcParams {
   int32_t group_j;    // tiles visited in groups of group_j j-tiles (L2 reuse of U panels)
   int32_t u_unsigned; // U plane is u8 (U + u_offset) instead of balanced s8 digits
   int32_t l2_pf;      // prefetch the operands of the iteration this far ahead into L2 (0: off)
+  int32_t l2_hint;    // U^T loads evict_last (reused by a whole raster pass); 1: X loads evict_first too
   ModP m;
   OutParams o;
   SplitJob sj;        // the next prime's limb split (warps 2–3), or sj.x = nullptr
@@ -140,6 +141,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      const uint64_t pol_u = l2_policy_evict_last(), pol_x = l2_policy_evict_first();
       // L2 prefetch of the (tile, k-block) iteration l2_pf ahead of the TMA loads: covers the
       // DRAM latency of first-touch X / U panels that a 4-stage shared-memory ring cannot
       int32_t pf_tile = blockIdx.x, pf_kb = 0;
@@ -163,8 +165,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t su = sbase + stage * TC_STAGE_BYTES;
           mbar_arrive_expect_tx(full_bar(stage), TC_STAGE_BYTES);
-          tma_load_3d(su, &tmU, full_bar(stage), kb * TC_BLOCK_K, P.j_off + tj * TC_BLOCK_J, P.plane);
-          tma_load_3d(su + TC_U_BYTES, &tmX, full_bar(stage), kb * TC_BLOCK_K, tr * TC_BLOCK_R, 0);
+          if (P.l2_hint) {
+            tma_load_3d_hint(su, &tmU, full_bar(stage), kb * TC_BLOCK_K, P.j_off + tj * TC_BLOCK_J, P.plane, pol_u);
+            if (P.l2_hint == 1)
+              tma_load_3d_hint(su + TC_U_BYTES, &tmX, full_bar(stage), kb * TC_BLOCK_K, tr * TC_BLOCK_R, 0, pol_x);
+            else
+              tma_load_3d(su + TC_U_BYTES, &tmX, full_bar(stage), kb * TC_BLOCK_K, tr * TC_BLOCK_R, 0);
+          } else {
+            tma_load_3d(su, &tmU, full_bar(stage), kb * TC_BLOCK_K, P.j_off + tj * TC_BLOCK_J, P.plane);
+            tma_load_3d(su + TC_U_BYTES, &tmX, full_bar(stage), kb * TC_BLOCK_K, tr * TC_BLOCK_R, 0);
+          }
           if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
         }
       }
