@@ -104,3 +104,19 @@ def test_modmatmul_sizes_and_ldx_check_without_gpu(ctpt):
                               1 << 20, None) == 2  # ERR_SHAPE: ldx must be 80
     with pytest.raises(ctpt.CtptError, match="ERR_OVERFLOW"):
         ctpt.modmatmul_sizes(ps, 10, 70000, 10)
+
+
+def test_split_overlap_workspace_and_validation(ctpt):
+    """split_overlap = 1 adds a second limb buffer (+ row-sum buffer) to the workspace when the
+    problem has ≥ 2 primes and no Rescale; any other value than 0 / 1 is refused."""
+    ps = [2147352577, 2146959361]
+    base = ctpt.query_sizes(_spec(ctpt, d3=300, primes=ps))
+    ovl = ctpt.query_sizes(_spec(ctpt, d3=300, primes=ps, split_overlap=1))
+    limbs = 4 * base.R * base.d2p
+    assert ovl.workspace_bytes >= base.workspace_bytes + limbs
+    one = ctpt.query_sizes(_spec(ctpt, d3=300, primes=ps[:1], split_overlap=1))  # one prime: nothing to overlap
+    assert one.workspace_bytes == ctpt.query_sizes(_spec(ctpt, d3=300, primes=ps[:1])).workspace_bytes
+    resc = ctpt.query_sizes(_spec(ctpt, d3=300, primes=ps, split_overlap=1, rescale=1))
+    assert resc.workspace_bytes == ctpt.query_sizes(_spec(ctpt, d3=300, primes=ps, rescale=1)).workspace_bytes
+    with pytest.raises(ctpt.CtptError, match="ERR_ARG"):
+        ctpt.query_sizes(_spec(ctpt, primes=ps, split_overlap=2))
