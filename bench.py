@@ -506,6 +506,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                      "avg_launch_ms": gemm_avg_s * 1e3, "share_of_step": gemm_share,
                      # achieved DRAM GB/s of that kernel (ncu bytes per launch ÷ the
                      # live per-launch time) against the measured copy bandwidth
+                     "vs_int8_mma_ceiling": mma_ceiling_ratio(achieved_tops) if not args.rescale else None,
                      "dram_gbs": (traffic / gemm_avg_s / 1e9) if traffic and not args.rescale else None,
                      "dram_frac": (traffic / gemm_avg_s / 1e9 / float(mp["hbm_gbs"]))
                      if traffic and not args.rescale else None},
@@ -573,6 +574,19 @@ def setup_stage_rates(c, eng, a_dev, b_dev, U, dev, stream, reps: int = 3) -> di
             "plain_precompute": {"ms": t_pre * 1e3, "bytes": pre_bytes, "gbs": pre_bytes / t_pre / 1e9,
                                  "frac_hbm": pre_bytes / t_pre / 1e9 / hbm,
                                  "kernel": "k_minmax_i64 + read-back + k_plain"}}
+
+
+def mma_ceiling_ratio(achieved_tops: float):
+    """Achieved per-launch TOP/s ÷ the measured power-limited INT8 tensor ceiling for k_gemm_tc's
+    MMA shape and operand statistics (tools/mma_ceiling.py: MMAs only, operands resident in shared
+    memory; profiles/r01/int8_mma_ceiling.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "int8_mma_ceiling.json")) as f:
+            mc = json.load(f)
+    except OSError:
+        return None
+    return {"frac": achieved_tops / float(mc["gemm_like_tops"]), "ceiling_tops": mc["gemm_like_tops"],
+            "ceiling_sm_mhz": mc["gemm_like_sm_mhz"], "source": "profiles/r01/int8_mma_ceiling.json"}
 
 
 def cublaslt_ratio(limb_macs_per_s: float, elapsed_ms: float):

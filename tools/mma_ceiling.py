@@ -40,6 +40,11 @@ def build(force: bool = False) -> str:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=4.0)
+    ap.add_argument("--mainloop", action="store_true",
+                    help="also run k_gemm_tc's TMA + MMA main loop without its epilogue on c3-shaped operands: "
+                         "real coordinates (mode 0, DRAM + L2 traffic) and always the same L2-resident "
+                         "k-block (mode 1, no DRAM)")
+    ap.add_argument("--launches", type=int, default=250)
     args = ap.parse_args()
     import torch
 
@@ -73,6 +78,44 @@ def main():
                           "tops": tops, "pct_of_4500": 100 * tops / 4500.0, "sm_mhz": cl.get("sm_mhz"),
                           "power_w_max": cl.get("power_w_max"), "reasons": cl.get("reasons"),
                           "per_clock_pct": (100 * tops * 1e12 / (2 * blocks * 8192 * cl["sm_mhz"] * 1e6)
+                                            if cl.get("sm_mhz") else None)}), flush=True)
+        time.sleep(2.0)
+    if args.mainloop:
+        mainloop(lib, args.launches)
+
+
+def mainloop(lib, launches: int):
+    import torch
+
+    from bench import ClockSampler
+
+    lib.mainloop_probe_run.restype = ctypes.c_int
+    lib.mainloop_probe_run.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_longlong,
+                                       ctypes.c_longlong, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                       ctypes.POINTER(ctypes.c_float), ctypes.c_void_p]
+    R, K, d3 = 20480, 16384, 16384  # c3: one prime's stacked rows, d2, d3
+    g = torch.Generator(device="cuda").manual_seed(0)
+    u = torch.randint(0, 17, (d3, K), dtype=torch.uint8, device="cuda", generator=g)
+    x = torch.randint(0, 256, (4, R, K), dtype=torch.uint8, device="cuda", generator=g)
+    x[3] >>= 1  # the top limb of a 31-bit residue has 7 bits
+    ms = ctypes.c_float()
+    stream = torch.cuda.current_stream().cuda_stream
+    macs = 4 * R * K * d3
+    for mode, name in [(0, "main loop, real coordinates (DRAM + L2), no epilogue"),
+                       (1, "main loop, one L2-resident k-block (no DRAM), no epilogue"),
+                       (0, "main loop, real coordinates (repeat)")]:
+        rc = lib.mainloop_probe_run(u.data_ptr(), x.data_ptr(), R, K, d3, 16, mode, 3, ctypes.byref(ms), stream)
+        assert rc == 0, rc
+        clk = ClockSampler(0)
+        time.sleep(0.3)
+        rc = lib.mainloop_probe_run(u.data_ptr(), x.data_ptr(), R, K, d3, 16, mode, launches, ctypes.byref(ms), stream)
+        cl = clk.stop()
+        assert rc == 0, rc
+        tops = 2 * macs / (ms.value / 1e3) / 1e12
+        print(json.dumps({"case": name, "mode": mode, "launches": launches, "ms_per_launch": ms.value, "tops": tops,
+                          "sm_mhz": cl.get("sm_mhz"), "power_w_max": cl.get("power_w_max"),
+                          "reasons": cl.get("reasons"),
+                          "per_clock_pct": (100 * tops * 1e12 / (2 * 148 * 8192 * cl["sm_mhz"] * 1e6)
                                             if cl.get("sm_mhz") else None)}), flush=True)
         time.sleep(2.0)
 

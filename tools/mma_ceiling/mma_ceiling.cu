@@ -100,3 +100,175 @@ extern "C" int mma_ceiling_run(int blocks, long long iters, int a_max, int b_max
   cudaEventDestroy(e1);
   return 0;
 }
+
+// ---------------------------------------------------------------------------------------------
+// Main-loop probe: k_gemm_tc's TMA → SMEM ring → tcgen05.mma pipeline WITHOUT its epilogue
+// (accumulators are never read), to split the gap between the pure-MMA ceiling above and the
+// real GEMM into data movement and epilogue.  mode 0: the real (tile, k-block) coordinates over
+// the caller's U^T plane and X limbs (DRAM + L2 traffic as in the GEMM); mode 1: every load
+// re-reads the SAME (tile 0, k-block 0) operands (L2-resident: L2 → SMEM traffic, no DRAM).
+// Same tile order, raster group and ring as gemm_tc.cuh.
+// ---------------------------------------------------------------------------------------------
+namespace {
+
+constexpr int PB_BLOCK_J = 128, PB_BLOCK_R = 64, PB_BLOCK_K = 128, PB_STAGES = 4;
+constexpr int PB_U = PB_BLOCK_J * PB_BLOCK_K, PB_X = 4 * PB_BLOCK_R * PB_BLOCK_K, PB_STAGE = PB_U + PB_X;
+
+struct ProbeParams {
+  int32_t num_kb, tiles_j, tiles_r, num_tiles, group_j, mode;
+};
+
+__global__ void __launch_bounds__(256, 1) k_mainloop_probe(const __grid_constant__ CUtensorMap tmU,
+                                                           const __grid_constant__ CUtensorMap tmX,
+                                                           const __grid_constant__ ProbeParams P) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar_base = sbase + PB_STAGES * PB_STAGE;
+  auto full_bar = [&](int s) { return bar_base + 8u * s; };
+  auto empty_bar = [&](int s) { return bar_base + 8u * (PB_STAGES + s); };
+  auto tfull_bar = [&](int b) { return bar_base + 8u * (2 * PB_STAGES + b); };
+  auto tempty_bar = [&](int b) { return bar_base + 8u * (2 * PB_STAGES + 2 + b); };
+  const uint32_t tmem_slot = bar_base + 8u * (2 * PB_STAGES + 4);
+  uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(smem + PB_STAGES * PB_STAGE + 8 * (2 * PB_STAGES + 4));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < PB_STAGES; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull_bar(b), 1);
+      mbar_init(tempty_bar(b), 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot_ptr;
+  auto coords = [&](int32_t tile, int32_t& tj, int32_t& tr) {
+    const int32_t per_group = P.group_j * P.tiles_r;
+    const int32_t g = tile / per_group, rem = tile - g * per_group;
+    const int32_t gj = min(P.group_j, P.tiles_j - g * P.group_j);
+    tj = g * P.group_j + rem % gj;
+    tr = rem / gj;
+  };
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int32_t tile = blockIdx.x; tile < P.num_tiles; tile += gridDim.x) {
+        int32_t tj, tr;
+        coords(tile, tj, tr);
+        if (P.mode == 1) tj = tr = 0;
+        for (int32_t kb = 0; kb < P.num_kb; ++kb) {
+          mbar_wait(empty_bar(stage), phase ^ 1);
+          const uint32_t su = sbase + stage * PB_STAGE;
+          const int32_t k = P.mode == 1 ? 0 : kb;
+          mbar_arrive_expect_tx(full_bar(stage), PB_STAGE);
+          tma_load_3d(su, &tmU, full_bar(stage), k * PB_BLOCK_K, tj * PB_BLOCK_J, 0);
+          tma_load_3d(su + PB_U, &tmX, full_bar(stage), k * PB_BLOCK_K, tr * PB_BLOCK_R, 0);
+          if (++stage == PB_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = idesc_i8(128, 256, false, false);
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      for (int32_t tile = blockIdx.x; tile < P.num_tiles; tile += gridDim.x) {
+        mbar_wait(tempty_bar(acc), acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * 256;
+        for (int32_t kb = 0; kb < P.num_kb; ++kb) {
+          mbar_wait(full_bar(stage), phase);
+          tc_fence_after();
+          const uint32_t su = sbase + stage * PB_STAGE;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_i8(d, umma_desc_sw128(su + kk * 32), umma_desc_sw128(su + PB_U + kk * 32), idesc, (kb | kk) != 0);
+          mma_commit(empty_bar(stage));
+          if (++stage == PB_STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(tfull_bar(acc));
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int32_t tile = blockIdx.x; tile < P.num_tiles; tile += gridDim.x) {  // no epilogue: hand back
+      mbar_wait(tfull_bar(acc), acc_phase);
+      tc_fence_after();
+      tc_fence_before();
+      mbar_arrive(tempty_bar(acc));
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem_base);
+  }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int tmap3(EncodeFn enc, CUtensorMap* m, void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1,
+          uint32_t b2) {
+  cuuint64_t dims[3] = {d0, d1, d2}, strides[2] = {d0, d0 * d1};
+  cuuint32_t box[3] = {b0, b1, b2}, es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+                 CUDA_SUCCESS
+             ? 0
+             : 1;
+}
+
+}  // namespace
+
+// u_plane: [d3][K] u8 (U^T), limbs: [4][R][K] u8, K a multiple of 128.  Runs `launches` launches
+// back to back; *ms_out = mean ms per launch.
+extern "C" int mainloop_probe_run(const void* u_plane, const void* limbs, long long R, long long K, long long d3,
+                                  int group_j, int mode, int launches, float* ms_out, void* stream) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) return 1;
+  EncodeFn enc = reinterpret_cast<EncodeFn>(fn);
+  CUtensorMap tmU, tmX;
+  if (tmap3(enc, &tmU, const_cast<void*>(u_plane), K, d3, 1, PB_BLOCK_K, PB_BLOCK_J, 1)) return 2;
+  if (tmap3(enc, &tmX, const_cast<void*>(limbs), K, R, 4, PB_BLOCK_K, PB_BLOCK_R, 4)) return 3;
+  ProbeParams P;
+  P.num_kb = static_cast<int32_t>(K / PB_BLOCK_K);
+  P.tiles_j = static_cast<int32_t>((d3 + PB_BLOCK_J - 1) / PB_BLOCK_J);
+  P.tiles_r = static_cast<int32_t>((R + PB_BLOCK_R - 1) / PB_BLOCK_R);
+  P.num_tiles = P.tiles_j * P.tiles_r;
+  P.group_j = group_j;
+  P.mode = mode;
+  const int smem = PB_STAGES * PB_STAGE + 256 + 1024;
+  if (cudaFuncSetAttribute(k_mainloop_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return 4;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, st);
+  for (int i = 0; i < launches; ++i)
+    k_mainloop_probe<<<sms < P.num_tiles ? sms : P.num_tiles, 256, smem, st>>>(tmU, tmX, P);
+  cudaEventRecord(e1, st);
+  if (cudaGetLastError() != cudaSuccess) return 5;
+  if (cudaEventSynchronize(e1) != cudaSuccess) return 6;
+  cudaEventElapsedTime(ms_out, e0, e1);
+  *ms_out /= launches;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return 0;
+}
