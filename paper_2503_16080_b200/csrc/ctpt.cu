@@ -684,6 +684,8 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
   if (const char* g = getenv("CTPT_GROUP_J")) P.group_j = std::max(1, atoi(g));  // tuning knob
   P.l2_pf = 0;
   if (const char* g = getenv("CTPT_GEMM_PF")) P.l2_pf = std::max(0, atoi(g));     // tuning knob
+  P.pf_x = 0;
+  if (const char* g = getenv("CTPT_GEMM_PFX")) P.pf_x = std::max(0, atoi(g));        // tuning knob (measuring)
   P.l2_hint = 0;
   if (const char* g = getenv("CTPT_GEMM_L2HINT")) P.l2_hint = std::max(0, atoi(g));  // tuning knob (measuring)
   P.m = m;

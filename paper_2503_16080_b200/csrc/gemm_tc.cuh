@@ -86,6 +86,8 @@ struct TcParams {
   int32_t u_unsigned; // U plane is u8 (U + u_offset) instead of balanced s8 digits
   int32_t l2_pf;      // prefetch the operands of the iteration this far ahead into L2 (0: off)
   int32_t l2_hint;    // U^T loads evict_last (reused by a whole raster pass); 1: X loads evict_first too
+  int32_t pf_x;       // X-panel L2 prefetch distance in k-blocks, issued only by the first CTA of the
+                      // group_j CTAs that share the panel (0: off)
   ModP m;
   OutParams o;
   SplitJob sj;        // the next prime's limb split (warps 2–3), or sj.x = nullptr
@@ -160,8 +162,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int32_t tile = blockIdx.x; tile < P.num_tiles; tile += gridDim.x) {
         int32_t tj, tr;
         tc_tile_coords(tile, P, tj, tr);
+        // the X panel of row tile tr is shared by the group's j-tiles, which run concurrently on
+        // neighbouring CTAs; the one holding the group's first j-tile streams it into L2 ahead
+        const bool pf_lead = P.pf_x > 0 && (tj % P.group_j) == 0;
+        if (pf_lead)
+          for (int32_t kb = 0; kb < P.pf_x && kb < P.num_kb; ++kb) tma_prefetch_l2_3d(&tmX, kb * TC_BLOCK_K, tr * TC_BLOCK_R, 0);
         for (int32_t kb = 0; kb < P.num_kb; ++kb) {
           if (P.l2_pf > 0) { pf_issue(); pf_advance(); }
+          if (pf_lead && kb + P.pf_x < P.num_kb)
+            tma_prefetch_l2_3d(&tmX, (kb + P.pf_x) * TC_BLOCK_K, tr * TC_BLOCK_R, 0);
           mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t su = sbase + stage * TC_STAGE_BYTES;
           mbar_arrive_expect_tx(full_bar(stage), TC_STAGE_BYTES);
