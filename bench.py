@@ -586,7 +586,8 @@ def mma_ceiling_ratio(achieved_tops: float):
     except OSError:
         return None
     return {"frac": achieved_tops / float(mc["gemm_like_tops"]), "ceiling_tops": mc["gemm_like_tops"],
-            "ceiling_sm_mhz": mc["gemm_like_sm_mhz"], "source": "profiles/r01/int8_mma_ceiling.json"}
+            "ceiling_sm_mhz": mc["gemm_like_sm_mhz"], "ceiling_kind": "sustained (~3 s at the power cap)",
+            "source": "profiles/r01/int8_mma_ceiling.json"}
 
 
 def cublaslt_ratio(limb_macs_per_s: float, elapsed_ms: float):
