@@ -900,6 +900,13 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # Test hook for the multi-rank code path on a one-GPU box: CTPT_BENCH_ONE_DEVICE=1 puts every
+    # rank on cuda:0 (independent problems; no kernel waits on another rank's) and
+    # CTPT_DIST_BACKEND=gloo replaces NCCL (which refuses two ranks on one device).  Never set by
+    # the driver; the numbers of such a run are not a scaling measurement.
+    if os.environ.get("CTPT_BENCH_ONE_DEVICE") == "1":
+        local_rank = 0
+    backend = os.environ.get("CTPT_DIST_BACKEND", "nccl")
     if args.impl == "reference":
         run_reference(args, rank)
         return
@@ -907,7 +914,10 @@ def main():
         import torch
 
         torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            torch.distributed.init_process_group(backend)
     try:
         if args.shard and args.gather == "ipc":
             run_sharded_ipc(args, rank, world, local_rank)
