@@ -354,9 +354,13 @@ MvPlan mv_plan(const Dims& d) {
   m.nc = mv_nc(d);
   m.tiles = static_cast<int32_t>((d.R + MV_BLOCK_R - 1) / MV_BLOCK_R);
   m.num_kb = static_cast<int32_t>(4 * d.d2p / MV_BLOCK_K + ((4 * d.d2p) % MV_BLOCK_K ? 1 : 0));
+  // K-split units: ≈ 12 per SM for balance, but never shorter than 32 k-blocks (512 KB of X per
+  // 128-row unit) — shorter units were dominated by their fixed cost (pipeline fill, the exact
+  // int32 partials and the ticket): at R = 8192, d2 = 4096, 8-k-block units ran at 0.29 of HBM
+  // and half the fused kernel's speed (tools/table4.py rows 1, 4)
   const int target = 12 * num_sms();
   int s = static_cast<int>((target + m.tiles - 1) / m.tiles);
-  s = std::max(1, std::min(s, std::max(1, m.num_kb / 8)));
+  s = std::max(1, std::min(s, std::max(1, m.num_kb / 32)));
   m.splits = s;
   m.ue_off = 0;
   m.part_off = align256(static_cast<size_t>(m.nc) * 4 * d.d2p);
