@@ -741,7 +741,13 @@ ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st) 
   P.o = g.o;
   P.o.accumulate = 0;
   P.o.w = 1;
-  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(nt, num_sms()));
+  // balanced persistent grid: the same number of rounds as min(nt, SMs) CTAs would take, spread
+  // over as few CTAs as that needs, so no round ends with most SMs idle behind a few stragglers
+  // (an HBM-bound CTA can pull more than 1/148 of the bandwidth).  CTPT_FUSED_GRID=sms: the old grid.
+  const int64_t rounds = (nt + num_sms() - 1) / num_sms();
+  int64_t grid64 = (nt + rounds - 1) / rounds;
+  if (const char* e = getenv("CTPT_FUSED_GRID")) if (strcmp(e, "sms") == 0) grid64 = std::min<int64_t>(nt, num_sms());
+  const unsigned grid = static_cast<unsigned>(grid64);
   // how the converters get X: TMA raw ring (default), half TMA / half register loads
   // (CTPT_FUSED_LOAD=hybrid) or register loads only (=regs) — for A/B runs
   int mode = FU_TMA;
