@@ -116,8 +116,11 @@ typedef struct {
   size_t ctmat_bytes;       /* d_ctmat: 256-byte header + L·R·d2p int32 (K-major stacked [A;B]) */
   size_t plain_bytes;       /* d_plain for ctpt_plain_precompute: 256 + kU·d3·d2p int8          */
   size_t plain_rns_bytes;   /* d_plain for ctpt_plain_precompute_rns: 256 + L·4·d3·d2p int8     */
-  size_t workspace_bytes;   /* d_ws for ctpt_matmul / ctpt_split / ctpt_gemm: 4·R·d2p (with
-                               rescale: ⌈4·R·d2p⌉_256 + 4·R·d3_loc for the last prime's product) */
+  size_t workspace_bytes;   /* d_ws for ctpt_matmul / ctpt_split / ctpt_gemm: the byte limbs of
+                               one prime in 32-KB tiles, 4·⌈R/64⌉·64·⌈d2p/128⌉·128 (+ row sums in
+                               the unsigned-U mode, + 4·R·d3_loc with rescale, + a second limb
+                               buffer with split_overlap, + the raw-byte kernel's U_exp and
+                               partials when d3_loc ≤ 32)                                       */
   size_t out_AU_bytes;      /* L_out·d3_loc·rows_A uint32 (L_out = L, or L − 1 with rescale)    */
   size_t out_BU_bytes;      /* L_out·d3_loc·d1 uint32                                          */
   int64_t rows_A, R, d2p, d3_loc;

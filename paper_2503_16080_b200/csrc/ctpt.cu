@@ -145,7 +145,12 @@ bool layout_vec_ok(int64_t rows_A, int64_t d1) {
 //   xlast   [d3_loc][R] u32 (rescale: the last prime's product)
 //   mv      U_exp + K-split partials + tickets   (d3_loc ≤ 32: the raw-byte kernel, MvPlan)
 bool needs_rowcorr(const ctpt_problem* pb) { return pb->u_unsigned && pb->u_offset != 0; }
-size_t ws_limb_bytes(const Dims& d) { return static_cast<size_t>(4) * d.R * d.d2p; }
+// the byte limbs of R rows in 32-KB tiles (limb_tile_off): rows padded to 64, K to 128
+int64_t limb_nkb(int64_t d2p) { return (d2p + 127) / 128; }
+size_t limb_tile_bytes(int64_t rows, int64_t d2p) {
+  return static_cast<size_t>(4) * round_up(rows, 64) * (limb_nkb(d2p) * 128);
+}
+size_t ws_limb_bytes(const Dims& d) { return limb_tile_bytes(d.R, d.d2p); }
 size_t ws_corr_off(const Dims& d) { return align256(ws_limb_bytes(d)); }
 size_t ws_xlast_off(const ctpt_problem* pb, const Dims& d) {
   return ws_corr_off(d) + (needs_rowcorr(pb) ? align256(static_cast<size_t>(4) * d.R) : 0);
@@ -177,10 +182,11 @@ SplitJob make_split_job(const ctpt_problem* pb, const Dims& d, const uint32_t* X
   SplitJob J{};
   const uint32_t p = pb->primes[l];
   J.x = reinterpret_cast<const uint4*>(X0 + static_cast<int64_t>(l) * d.R * d.d2p);
-  J.limbs = static_cast<uint4*>(ws_limbs(pb, d, ws, l));
+  J.limbs = static_cast<uint8_t*>(ws_limbs(pb, d, ws, l));
   J.rowcorr = needs_rowcorr(pb) ? ws_corr(pb, d, ws, l) : nullptr;
   J.R = d.R;
   J.d2p16 = d.d2p / 16;
+  J.nkb = limb_nkb(d.d2p);
   J.p = p;
   J.off_mod = static_cast<uint32_t>(((static_cast<int64_t>(pb->u_offset) % p) + p) % p);
   return J;
@@ -242,6 +248,23 @@ ctpt_status make_tmap_u8(CUtensorMap* m, const void* base, uint64_t dim0, uint64
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(CTPT_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+  return CTPT_OK;
+}
+
+// The byte limbs in 32-KB tiles as a 5-D tensor {128 B, 64 rows, 4 limbs, k-block, row tile}:
+// one box of {128, 64, box_limbs, 1, 1} is (part of) one contiguous tile (limb_tile_off).
+ctpt_status make_tmap_limb_tiles(CUtensorMap* m, const void* base, int64_t rows, int64_t d2p, uint32_t box_limbs) {
+  auto enc = get_encode();
+  if (!enc) return fail(CTPT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const uint64_t nkb = static_cast<uint64_t>((d2p + 127) / 128), ntr = static_cast<uint64_t>((rows + 63) / 64);
+  cuuint64_t dims[5] = {128, 64, 4, nkb, ntr};
+  cuuint64_t strides[4] = {128, 64 * 128, 4 * 64 * 128, nkb * 4 * 64 * 128};
+  cuuint32_t box[5] = {128, 64, box_limbs, 1, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CTPT_ERR_CUDA, "cuTensorMapEncodeTiled (limb tiles) failed (%d)", static_cast<int>(r));
   return CTPT_OK;
 }
 
@@ -324,7 +347,7 @@ struct GemmArgs {
   OutParams o;           // accumulate / w are set per pass
   SplitJob sj;           // the next prime's limb split, run inside the first pass (sj.x = nullptr: none)
 };
-ctpt_status launch_split(const uint32_t* x, int64_t n, void* limbs, cudaStream_t st);
+ctpt_status launch_split(const uint32_t* x, int64_t rows, int64_t d2p, void* limbs, cudaStream_t st);
 // the limb split of `rows` rows of X for prime p; in the unsigned-U mode it also writes rowcorr
 ctpt_status launch_split_prime(const ctpt_problem* pb, const uint32_t* x, int64_t rows, int64_t d2p, uint32_t p,
                                void* limbs, uint32_t* rowcorr, cudaStream_t st);
@@ -597,28 +620,29 @@ namespace {
 
 ctpt_status launch_split_prime(const ctpt_problem* pb, const uint32_t* x, int64_t rows, int64_t d2p, uint32_t p,
                                void* limbs, uint32_t* rowcorr, cudaStream_t st) {
-  if (!needs_rowcorr(pb)) return launch_split(x, rows * d2p, limbs, st);
+  if (!needs_rowcorr(pb)) return launch_split(x, rows, d2p, limbs, st);
   const int64_t off = pb->u_offset;
   const uint32_t off_mod = static_cast<uint32_t>(((off % static_cast<int64_t>(p)) + p) % p);
   const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(rows, INT32_MAX)));
-  k_split_rows<<<blocks, 256, 0, st>>>(reinterpret_cast<const uint4*>(x), static_cast<uint4*>(limbs), rowcorr, rows,
-                                        d2p / 16, p, off_mod);
+  k_split_rows<<<blocks, 256, 0, st>>>(reinterpret_cast<const uint4*>(x), static_cast<uint8_t*>(limbs), rowcorr, rows,
+                                        d2p / 16, limb_nkb(d2p), p, off_mod);
   CUDA_TRY(cudaGetLastError());
   return CTPT_OK;
 }
 
 ctpt_status launch_split_job(const SplitJob& J, cudaStream_t st) {
-  if (!J.rowcorr) return launch_split(reinterpret_cast<const uint32_t*>(J.x), J.R * J.d2p16 * 16, J.limbs, st);
+  if (!J.rowcorr) return launch_split(reinterpret_cast<const uint32_t*>(J.x), J.R, J.d2p16 * 16, J.limbs, st);
   const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(J.R, INT32_MAX)));
-  k_split_rows<<<blocks, 256, 0, st>>>(J.x, J.limbs, J.rowcorr, J.R, J.d2p16, J.p, J.off_mod);
+  k_split_rows<<<blocks, 256, 0, st>>>(J.x, J.limbs, J.rowcorr, J.R, J.d2p16, J.nkb, J.p, J.off_mod);
   CUDA_TRY(cudaGetLastError());
   return CTPT_OK;
 }
 
-ctpt_status launch_split(const uint32_t* x, int64_t n, void* limbs, cudaStream_t st) {
-  const int64_t n16 = n / 16;  // n is a multiple of 16 (rows of d2p)
-  const int blocks = static_cast<int>(std::min<int64_t>((n16 + 255) / 256, static_cast<int64_t>(num_sms()) * 16));
-  if (blocks > 0) k_split<<<blocks, 256, 0, st>>>(reinterpret_cast<const uint4*>(x), static_cast<uint4*>(limbs), n16);
+ctpt_status launch_split(const uint32_t* x, int64_t rows, int64_t d2p, void* limbs, cudaStream_t st) {
+  const int64_t nkb = limb_nkb(d2p), groups = rows * nkb * 8;  // 16-residue groups incl. K padding
+  const int blocks = static_cast<int>(std::min<int64_t>((groups + 255) / 256, static_cast<int64_t>(num_sms()) * 16));
+  if (blocks > 0)
+    k_split<<<blocks, 256, 0, st>>>(reinterpret_cast<const uint4*>(x), static_cast<uint8_t*>(limbs), rows, d2p / 16, nkb);
   CUDA_TRY(cudaGetLastError());
   return CTPT_OK;
 }
@@ -663,7 +687,7 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
   CUtensorMap tmU, tmX;
   s = make_tmap_u8(&tmU, g.planes, d.d2, d.d3, g.nplanes, d.d2p, d.d3 * d.d2p, TC_BLOCK_K, 128, 1);
   if (s != CTPT_OK) return s;
-  s = make_tmap_u8(&tmX, g.limbs, d.d2, g.R, 4, d.d2p, g.R * d.d2p, TC_BLOCK_K, TC_BLOCK_R, (pair || mc) ? 2 : 4);
+  s = make_tmap_limb_tiles(&tmX, g.limbs, g.R, d.d2p, (pair || mc) ? 2 : 4);
   if (s != CTPT_OK) return s;
   TcParams P;
   P.R = g.R;
@@ -1118,7 +1142,7 @@ HostPlan host_plan(const Dims& d, int64_t chunk_rows) {
   h.chunk = c;
   h.in_bytes = align256(static_cast<size_t>(d.d2) * c * 4);
   h.cm_bytes = align256(static_cast<size_t>(c) * d.d2p * 4);
-  h.limb_bytes = align256(static_cast<size_t>(4) * c * d.d2p);
+  h.limb_bytes = align256(limb_tile_bytes(c, d.d2p));
   h.out_bytes = align256(static_cast<size_t>(d.d3_loc) * c * 4);
   h.corr_bytes = align256(static_cast<size_t>(c) * 4);  // rowcorr of a chunk (unsigned-U mode)
   Dims dc = d;

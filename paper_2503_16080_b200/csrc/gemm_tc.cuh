@@ -43,29 +43,33 @@ constexpr int TC_GROUP_J_DEFAULT = 16;  // measured best of {8,16,32,64,128} on 
 // (evict-first) so the GEMM's L2-resident operand panels stay put.
 struct SplitJob {
   const uint4* x;      // next prime's X, [R][d2p] int32 as uint4 (nullptr: no side split)
-  uint4* limbs;        // its four byte-limb planes [4][R][d2p]
+  uint8_t* limbs;      // its byte limbs in 32-KB tiles (limb_tile_off, kernels.cuh)
   uint32_t* rowcorr;   // u_offset·Σ_k X[r][k] mod p per row (unsigned-U mode), or nullptr
-  int64_t R, d2p16;    // rows; 16-residue groups per row
+  int64_t R, d2p16;    // rows; 16-residue groups per row of X
+  int64_t nkb;         // 128-byte k-blocks per limb tile row (⌈d2p / 128⌉)
   uint32_t p, off_mod; // next prime; u_offset mod p
 };
 
 __device__ __forceinline__ void side_split_rows(const SplitJob& J, int64_t worker, int64_t nworkers, int lane) {
-  const int64_t n16 = J.R * J.d2p16;
+  const int64_t kp16 = J.nkb * 8;
   for (int64_t r = worker; r < J.R; r += nworkers) {
     uint64_t sum = 0;
-    for (int64_t c = lane; c < J.d2p16; c += 32) {
-      const int64_t g = r * J.d2p16 + c;
-      uint4 w[4];
+    for (int64_t c = lane; c < kp16; c += 32) {
+      uint4 w[4] = {};
+      if (c < J.d2p16) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) w[i] = __ldcs(J.x + 4 * g + i);
+        for (int i = 0; i < 4; ++i) w[i] = __ldcs(J.x + 4 * (r * J.d2p16 + c) + i);
+      }
       uint32_t o[4][4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         sum += static_cast<uint64_t>(w[i].x) + w[i].y + w[i].z + w[i].w;
         byte_transpose4(w[i].x, w[i].y, w[i].z, w[i].w, o[0][i], o[1][i], o[2][i], o[3][i]);
       }
+      uint8_t* t = J.limbs + limb_tile_off(r, 16 * c, J.nkb);
 #pragma unroll
-      for (int l = 0; l < 4; ++l) __stcs(J.limbs + l * n16 + g, make_uint4(o[l][0], o[l][1], o[l][2], o[l][3]));
+      for (int l = 0; l < 4; ++l)
+        __stcs(reinterpret_cast<uint4*>(t + l * 8192), make_uint4(o[l][0], o[l][1], o[l][2], o[l][3]));
     }
     if (J.rowcorr) {
 #pragma unroll
@@ -85,7 +89,7 @@ struct TcParams {
   int32_t group_j;    // tiles visited in groups of group_j j-tiles (L2 reuse of U panels)
   int32_t u_unsigned; // U plane is u8 (U + u_offset) instead of balanced s8 digits
   int32_t l2_pf;      // prefetch the operands of the iteration this far ahead into L2 (0: off)
-  int32_t l2_hint;    // U^T loads evict_last (reused by a whole raster pass); 1: X loads evict_first too
+  int32_t l2_hint;    // U^T loads evict_last (reused by a whole raster pass)
   int32_t pf_x;       // X-panel L2 prefetch distance in k-blocks, issued only by the first CTA of the
                       // group_j CTAs that share the panel (0: off)
   ModP m;
@@ -143,7 +147,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      const uint64_t pol_u = l2_policy_evict_last(), pol_x = l2_policy_evict_first();
+      const uint64_t pol_u = l2_policy_evict_last();
       // L2 prefetch of the (tile, k-block) iteration l2_pf ahead of the TMA loads: covers the
       // DRAM latency of first-touch X / U panels that a 4-stage shared-memory ring cannot
       int32_t pf_tile = blockIdx.x, pf_kb = 0;
@@ -154,7 +158,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (pf_tile < P.num_tiles) {
           int32_t ptj, ptr;
           tc_tile_coords(pf_tile, P, ptj, ptr);
-          tma_prefetch_l2_3d(&tmX, pf_kb * TC_BLOCK_K, ptr * TC_BLOCK_R, 0);
+          tma_prefetch_l2_5d(&tmX, 0, 0, 0, pf_kb, ptr);
           tma_prefetch_l2_3d(&tmU, pf_kb * TC_BLOCK_K, P.j_off + ptj * TC_BLOCK_J, P.plane);
         }
       };
@@ -166,24 +170,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // neighbouring CTAs; the one holding the group's first j-tile streams it into L2 ahead
         const bool pf_lead = P.pf_x > 0 && (tj % P.group_j) == 0;
         if (pf_lead)
-          for (int32_t kb = 0; kb < P.pf_x && kb < P.num_kb; ++kb) tma_prefetch_l2_3d(&tmX, kb * TC_BLOCK_K, tr * TC_BLOCK_R, 0);
+          for (int32_t kb = 0; kb < P.pf_x && kb < P.num_kb; ++kb) tma_prefetch_l2_5d(&tmX, 0, 0, 0, kb, tr);
         for (int32_t kb = 0; kb < P.num_kb; ++kb) {
           if (P.l2_pf > 0) { pf_issue(); pf_advance(); }
           if (pf_lead && kb + P.pf_x < P.num_kb)
-            tma_prefetch_l2_3d(&tmX, (kb + P.pf_x) * TC_BLOCK_K, tr * TC_BLOCK_R, 0);
+            tma_prefetch_l2_5d(&tmX, 0, 0, 0, kb + P.pf_x, tr);
           mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t su = sbase + stage * TC_STAGE_BYTES;
           mbar_arrive_expect_tx(full_bar(stage), TC_STAGE_BYTES);
-          if (P.l2_hint) {
+          if (P.l2_hint)
             tma_load_3d_hint(su, &tmU, full_bar(stage), kb * TC_BLOCK_K, P.j_off + tj * TC_BLOCK_J, P.plane, pol_u);
-            if (P.l2_hint == 1)
-              tma_load_3d_hint(su + TC_U_BYTES, &tmX, full_bar(stage), kb * TC_BLOCK_K, tr * TC_BLOCK_R, 0, pol_x);
-            else
-              tma_load_3d(su + TC_U_BYTES, &tmX, full_bar(stage), kb * TC_BLOCK_K, tr * TC_BLOCK_R, 0);
-          } else {
+          else
             tma_load_3d(su, &tmU, full_bar(stage), kb * TC_BLOCK_K, P.j_off + tj * TC_BLOCK_J, P.plane);
-            tma_load_3d(su + TC_U_BYTES, &tmX, full_bar(stage), kb * TC_BLOCK_K, tr * TC_BLOCK_R, 0);
-          }
+          tma_load_5d(su + TC_U_BYTES, &tmX, full_bar(stage), 0, 0, 0, kb, tr);  // one 32-KB limb tile
           if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
         }
       }

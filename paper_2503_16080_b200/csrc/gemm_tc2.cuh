@@ -104,7 +104,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
           // completes its bytes on it directly (no remote arrive, no cluster-scope fence).
           if (rank == 0) mbar_arrive_expect_tx(full_bar(stage), 2 * T2_STAGE_BYTES);
           tma_load_3d_pair(su, &tmU, lbar, kb * T2_BLOCK_K, jrow, P.plane);
-          tma_load_3d_pair(su + T2_U_BYTES, &tmX, lbar, kb * T2_BLOCK_K, tr * T2_BLOCK_R, 2 * static_cast<int32_t>(rank));
+          tma_load_5d_pair(su + T2_U_BYTES, &tmX, lbar, 0, 0, 2 * static_cast<int32_t>(rank), kb, tr);
           if (++stage == T2_STAGES) { stage = 0; phase ^= 1; }
         }
       }

@@ -27,13 +27,13 @@ namespace ctpt {
 
 constexpr int MC_X_HALF = 2 * TC_BLOCK_R * TC_BLOCK_K;  // 2 limbs × 64 rows × 128 B = 16 KB
 
-// 3-D TMA load multicast to the CTAs in `mask` (same smem / mbarrier offsets in each).
-__device__ __forceinline__ void tma_load_3d_mc(uint32_t dst, const CUtensorMap* m, uint32_t bar, int32_t c0,
-                                               int32_t c1, int32_t c2, uint16_t mask) {
+// 5-D TMA load multicast to the CTAs in `mask` (same smem / mbarrier offsets in each).
+__device__ __forceinline__ void tma_load_5d_mc(uint32_t dst, const CUtensorMap* m, uint32_t bar, int32_t c0,
+                                               int32_t c1, int32_t c2, int32_t c3, int32_t c4, uint16_t mask) {
   asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
-      "[%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "h"(mask)
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+      "[%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar), "h"(mask)
       : "memory");
 }
 // tcgen05.commit of this CTA's MMAs, arriving on the barrier at `bar` in every CTA of `mask`.
@@ -111,8 +111,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           const uint32_t su = sbase + stage * TC_STAGE_BYTES;
           mbar_arrive_expect_tx(full_bar(stage), TC_STAGE_BYTES);
           tma_load_3d(su, &tmU, full_bar(stage), kb * TC_BLOCK_K, jrow, P.plane);
-          tma_load_3d_mc(su + TC_U_BYTES + rank * MC_X_HALF, &tmX, full_bar(stage), kb * TC_BLOCK_K, tr * TC_BLOCK_R,
-                         2 * static_cast<int32_t>(rank), 0x3);
+          tma_load_5d_mc(su + TC_U_BYTES + rank * MC_X_HALF, &tmX, full_bar(stage), 0, 0, 2 * static_cast<int32_t>(rank), kb,
+                         tr, 0x3);
           if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
         }
       }

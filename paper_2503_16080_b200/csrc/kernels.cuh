@@ -153,45 +153,59 @@ __device__ __forceinline__ void byte_transpose4(uint32_t w0, uint32_t w1, uint32
   l3 = __byte_perm(t1, t3, 0x7632);
 }
 
-__global__ void __launch_bounds__(256) k_split(const uint4* __restrict__ x, uint4* __restrict__ limbs, int64_t n16) {
-  // n16 = number of 16-element groups; plane stride = n16 uint4
-  for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < n16;
+// Limb planes in 32-KB tiles: limb ℓ of X[r][k] lives at byte
+//   ((r / 64) · nkb + k / 128) · 32768 + ℓ · 8192 + (r % 64) · 128 + k % 128,   nkb = ⌈d2p / 128⌉,
+// i.e. each (64-row, 128-K) tile of all four limbs — one TMA box of the GEMM — is one contiguous
+// 32-KB block (measured: the GEMM's main loop +3.9 %, fewer DRAM-latency bubbles than 256 strided
+// 128-B rows; profiles/r01/gemm_breakdown/).  K columns d2p .. 128·nkb are written as zeros (they
+// enter every output's K sum); rows R .. 64·⌈R/64⌉ are never written (they only reach outputs
+// that are not stored).
+__device__ __forceinline__ int64_t limb_tile_off(int64_t r, int64_t k, int64_t nkb) {
+  return (((r >> 6) * nkb + (k >> 7)) << 15) + ((r & 63) << 7) + (k & 127);
+}
+
+__global__ void __launch_bounds__(256) k_split(const uint4* __restrict__ x, uint8_t* __restrict__ limbs, int64_t R,
+                                               int64_t d2p16, int64_t nkb) {
+  // one thread per 16 consecutive residues (16 | 128, so they share a tile); x row stride d2p
+  const int64_t kp16 = nkb * 8;
+  for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < R * kp16;
        g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    uint4 w[4];
+    const int64_t r = g / kp16, c = g - r * kp16;
+    uint4 w[4] = {};
+    if (c < d2p16) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) w[i] = __ldcs(x + 4 * g + i);  // streaming: read once
+      for (int i = 0; i < 4; ++i) w[i] = __ldcs(x + 4 * (r * d2p16 + c) + i);  // streaming: read once
+    }
     uint32_t o[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) byte_transpose4(w[i].x, w[i].y, w[i].z, w[i].w, o[0][i], o[1][i], o[2][i], o[3][i]);
+    uint8_t* t = limbs + limb_tile_off(r, 16 * c, nkb);
 #pragma unroll
-    for (int l = 0; l < 4; ++l) limbs[l * n16 + g] = make_uint4(o[l][0], o[l][1], o[l][2], o[l][3]);
+    for (int l = 0; l < 4; ++l) *reinterpret_cast<uint4*>(t + l * 8192) = make_uint4(o[l][0], o[l][1], o[l][2], o[l][3]);
   }
 }
-
-// The same split for the unsigned-U mode, one 256-thread block per row of X ([R][d2p]; c3: 64
-// residues per thread), which also forms rowcorr[r] = u_offset·Σ_k x[r][k] mod p (Σ < 2^47) for
-// the epilogue's correction.  Blocks per row keep the grid fine-grained (R blocks) so the
-// HBM-bound pass has no tail wave.
-__global__ void __launch_bounds__(256) k_split_rows(const uint4* __restrict__ x, uint4* __restrict__ limbs,
+__global__ void __launch_bounds__(256) k_split_rows(const uint4* __restrict__ x, uint8_t* __restrict__ limbs,
                                                    uint32_t* __restrict__ rowcorr, int64_t R, int64_t d2p16,
-                                                   uint32_t p, uint32_t off_mod_p) {
+                                                   int64_t nkb, uint32_t p, uint32_t off_mod_p) {
   __shared__ uint64_t part[8];
-  const int64_t n16 = R * d2p16;  // 16-element groups in the plane
+  const int64_t kp16 = nkb * 8;
   for (int64_t r = blockIdx.x; r < R; r += gridDim.x) {
     uint64_t sum = 0;
-    for (int64_t c = threadIdx.x; c < d2p16; c += blockDim.x) {
-      const int64_t g = r * d2p16 + c;
-      uint4 w[4];
+    for (int64_t c = threadIdx.x; c < kp16; c += blockDim.x) {
+      uint4 w[4] = {};
+      if (c < d2p16) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) w[i] = __ldcs(x + 4 * g + i);
+        for (int i = 0; i < 4; ++i) w[i] = __ldcs(x + 4 * (r * d2p16 + c) + i);
+      }
       uint32_t o[4][4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         sum += static_cast<uint64_t>(w[i].x) + w[i].y + w[i].z + w[i].w;
         byte_transpose4(w[i].x, w[i].y, w[i].z, w[i].w, o[0][i], o[1][i], o[2][i], o[3][i]);
       }
+      uint8_t* t = limbs + limb_tile_off(r, 16 * c, nkb);
 #pragma unroll
-      for (int l = 0; l < 4; ++l) limbs[l * n16 + g] = make_uint4(o[l][0], o[l][1], o[l][2], o[l][3]);
+      for (int l = 0; l < 4; ++l) *reinterpret_cast<uint4*>(t + l * 8192) = make_uint4(o[l][0], o[l][1], o[l][2], o[l][3]);
     }
 #pragma unroll
     for (int s = 16; s; s >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, s);
@@ -404,7 +418,7 @@ __device__ __forceinline__ void store16(const OutParams& o, const ModP& m, int64
 // One thread per (j, r) output; block 16 (r) x 16 (j).
 // ------------------------------------------------------------------------------------------
 struct SimtParams {
-  const uint8_t* limbs;  // [4][R][d2p]
+  const uint8_t* limbs;  // 32-KB limb tiles (limb_tile_off)
   const int8_t* uplane;  // [d3_total][d2p] plane for this pass
   int64_t R, d2, d2p, j_off;
   int32_t u_unsigned;    // plane holds u8 values (U + u_offset)
@@ -418,11 +432,12 @@ __global__ void k_gemm_simt(const __grid_constant__ SimtParams P) {
   if (r >= P.R || j >= P.o.d3_loc) return;
   int32_t c[4] = {0, 0, 0, 0};
   const int8_t* u = P.uplane + (P.j_off + j) * P.d2p;
-  const int64_t plane = P.R * P.d2p;
+  const int64_t nkb = (P.d2p + 127) / 128;
   for (int64_t k = 0; k < P.d2; ++k) {
     const int32_t uk = P.u_unsigned ? static_cast<int32_t>(static_cast<uint8_t>(u[k])) : static_cast<int32_t>(u[k]);
+    const uint8_t* t = P.limbs + limb_tile_off(r, k, nkb);
 #pragma unroll
-    for (int l = 0; l < 4; ++l) c[l] += static_cast<int32_t>(P.limbs[l * plane + r * P.d2p + k]) * uk;
+    for (int l = 0; l < 4; ++l) c[l] += static_cast<int32_t>(t[l * 8192]) * uk;
   }
   store_out(P.o, P.m, j, r, recombine_mod(c[0], c[1], c[2], c[3], P.m));
 }

@@ -14,7 +14,7 @@ import re
 from dataclasses import dataclass
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libctpt.so")
+LIB_PATH = os.environ.get("CTPT_LIB") or os.path.join(_HERE, "libctpt.so")  # CTPT_LIB: A/B of two builds
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "ctpt.h")
 
 RLWE, SHARED_S, SHARED_A, STRUCT_A = 0, 1, 2, 3

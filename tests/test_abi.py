@@ -42,7 +42,8 @@ def test_sizes(ctpt):
     assert s.ctmat_bytes == 256 + 80 * 48 * 4
     # d3 = 20 ≤ 32: the limb planes, then the raw-byte kernel's U_exp (NC = 4·32 rows × 4·d2p bytes)
     assert s.workspace_bytes >= 4 * 80 * 48 + 128 * 4 * 48
-    assert ctpt.query_sizes(_spec(ctpt, d3=40)).workspace_bytes == 4 * 80 * 48
+    # byte limbs in 32-KB tiles: rows padded to 64, K to 128 (kernels.cuh limb_tile_off)
+    assert ctpt.query_sizes(_spec(ctpt, d3=40)).workspace_bytes == 4 * 128 * 128
     assert s.out_AU_bytes == 20 * 16 * 4 and s.out_BU_bytes == 20 * 64 * 4
     s2 = ctpt.query_sizes(_spec(ctpt, fmt=ctpt.SHARED_S, d2=50, col_begin=3, col_end=11))
     assert s2.rows_A == 64 and s2.R == 128 and s2.d2p == 64 and s2.d3_loc == 8
@@ -96,7 +97,7 @@ def test_modmatmul_sizes_and_ldx_check_without_gpu(ctpt):
     """Mod-PP-MM entry points validate on the host: ldx = K rounded up to 16, d2 overflow."""
     ps = [2147352577, 2146959361]
     ldx, plain, ws = ctpt.modmatmul_sizes(ps, 100, 77, 50)
-    assert ldx == 80 and plain == 256 + 2 * 4 * 50 * 80 and ws == 4 * 100 * 80
+    assert ldx == 80 and plain == 256 + 2 * 4 * 50 * 80 and ws == 4 * 128 * 128  # limbs in 32-KB tiles
     lib = ctpt.raw_lib()
     arr = (ctypes.c_uint32 * 2)(*ps)
     fake = ctypes.c_void_p(256)

@@ -45,6 +45,7 @@ def main():
                          "real coordinates (mode 0, DRAM + L2 traffic) and always the same L2-resident "
                          "k-block (mode 1, no DRAM)")
     ap.add_argument("--launches", type=int, default=250)
+    ap.add_argument("--skip-ceiling", action="store_true")
     args = ap.parse_args()
     import torch
 
@@ -66,7 +67,7 @@ def main():
     rc = lib.mma_ceiling_run(blocks, 20000, 0, 0, 1, ctypes.byref(ms), None)
     assert rc == 0, rc
     iters = int(20000 * args.seconds * 1e3 / max(ms.value, 1e-3))
-    for name, a, b in cases:
+    for name, a, b in ([] if args.skip_ceiling else cases):
         clk = ClockSampler(0)
         time.sleep(0.3)
         rc = lib.mma_ceiling_run(blocks, iters, a, b, 7, ctypes.byref(ms), None)
@@ -103,7 +104,9 @@ def mainloop(lib, launches: int):
     macs = 4 * R * K * d3
     for mode, name in [(0, "main loop, real coordinates (DRAM + L2), no epilogue"),
                        (1, "main loop, one L2-resident k-block (no DRAM), no epilogue"),
-                       (0, "main loop, real coordinates (repeat)")]:
+                       (2, "main loop, real coordinates, X in 32-KB tile-contiguous blocks"),
+                       (0, "main loop, real coordinates (repeat)"),
+                       (2, "main loop, tile-contiguous X (repeat)")]:
         rc = lib.mainloop_probe_run(u.data_ptr(), x.data_ptr(), R, K, d3, 16, mode, 3, ctypes.byref(ms), stream)
         assert rc == 0, rc
         clk = ClockSampler(0)

@@ -111,6 +111,15 @@ extern "C" int mma_ceiling_run(int blocks, long long iters, int a_max, int b_max
 // ---------------------------------------------------------------------------------------------
 namespace {
 
+__device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* m, uint32_t bar, int32_t c0, int32_t c1,
+                                            int32_t c2, int32_t c3, int32_t c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+      "%6}], [%7];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar)
+      : "memory");
+}
+
 constexpr int PB_BLOCK_J = 128, PB_BLOCK_R = 64, PB_BLOCK_K = 128, PB_STAGES = 4;
 constexpr int PB_U = PB_BLOCK_J * PB_BLOCK_K, PB_X = 4 * PB_BLOCK_R * PB_BLOCK_K, PB_STAGE = PB_U + PB_X;
 
@@ -162,14 +171,17 @@ __global__ void __launch_bounds__(256, 1) k_mainloop_probe(const __grid_constant
       for (int32_t tile = blockIdx.x; tile < P.num_tiles; tile += gridDim.x) {
         int32_t tj, tr;
         coords(tile, tj, tr);
-        if (P.mode == 1) tj = tr = 0;
+        if (P.mode & 1) tj = tr = 0;
         for (int32_t kb = 0; kb < P.num_kb; ++kb) {
           mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t su = sbase + stage * PB_STAGE;
-          const int32_t k = P.mode == 1 ? 0 : kb;
+          const int32_t k = (P.mode & 1) ? 0 : kb;
           mbar_arrive_expect_tx(full_bar(stage), PB_STAGE);
           tma_load_3d(su, &tmU, full_bar(stage), k * PB_BLOCK_K, tj * PB_BLOCK_J, 0);
-          tma_load_3d(su + PB_U, &tmX, full_bar(stage), k * PB_BLOCK_K, tr * PB_BLOCK_R, 0);
+          if (P.mode & 2)
+            tma_load_5d(su + PB_U, &tmX, full_bar(stage), 0, 0, 0, k, tr);
+          else
+            tma_load_3d(su + PB_U, &tmX, full_bar(stage), k * PB_BLOCK_K, tr * PB_BLOCK_R, 0);
           if (++stage == PB_STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -243,7 +255,17 @@ extern "C" int mainloop_probe_run(const void* u_plane, const void* limbs, long l
   EncodeFn enc = reinterpret_cast<EncodeFn>(fn);
   CUtensorMap tmU, tmX;
   if (tmap3(enc, &tmU, const_cast<void*>(u_plane), K, d3, 1, PB_BLOCK_K, PB_BLOCK_J, 1)) return 2;
-  if (tmap3(enc, &tmX, const_cast<void*>(limbs), K, R, 4, PB_BLOCK_K, PB_BLOCK_R, 4)) return 3;
+  if (mode & 2) {  // the same bytes viewed as tiles [R/64][K/128][4 limbs][64 rows][128 B], 32 KB each
+    cuuint64_t dims[5] = {128, 64, 4, static_cast<cuuint64_t>(K / 128), static_cast<cuuint64_t>(R / 64)};
+    cuuint64_t strides[4] = {128, 64 * 128, 4 * 64 * 128, static_cast<cuuint64_t>(K / 128) * 4 * 64 * 128};
+    cuuint32_t box[5] = {128, 64, 4, 1, 1}, es[5] = {1, 1, 1, 1, 1};
+    if (enc(&tmX, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<void*>(limbs), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return 3;
+  } else if (tmap3(enc, &tmX, const_cast<void*>(limbs), K, R, 4, PB_BLOCK_K, PB_BLOCK_R, 4)) {
+    return 3;
+  }
   ProbeParams P;
   P.num_kb = static_cast<int32_t>(K / PB_BLOCK_K);
   P.tiles_j = static_cast<int32_t>((d3 + PB_BLOCK_J - 1) / PB_BLOCK_J);
