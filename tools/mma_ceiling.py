@@ -105,8 +105,9 @@ def mainloop(lib, launches: int):
     for mode, name in [(0, "main loop, real coordinates (DRAM + L2), no epilogue"),
                        (1, "main loop, one L2-resident k-block (no DRAM), no epilogue"),
                        (2, "main loop, real coordinates, X in 32-KB tile-contiguous blocks"),
-                       (0, "main loop, real coordinates (repeat)"),
-                       (2, "main loop, tile-contiguous X (repeat)")]:
+                       (6, "main loop, X and U^T both tile-contiguous"),
+                       (2, "main loop, tile-contiguous X (repeat)"),
+                       (6, "main loop, X and U^T tile-contiguous (repeat)")]:
         rc = lib.mainloop_probe_run(u.data_ptr(), x.data_ptr(), R, K, d3, 16, mode, 3, ctypes.byref(ms), stream)
         assert rc == 0, rc
         clk = ClockSampler(0)

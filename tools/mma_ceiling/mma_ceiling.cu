@@ -177,7 +177,10 @@ __global__ void __launch_bounds__(256, 1) k_mainloop_probe(const __grid_constant
           const uint32_t su = sbase + stage * PB_STAGE;
           const int32_t k = (P.mode & 1) ? 0 : kb;
           mbar_arrive_expect_tx(full_bar(stage), PB_STAGE);
-          tma_load_3d(su, &tmU, full_bar(stage), k * PB_BLOCK_K, tj * PB_BLOCK_J, 0);
+          if (P.mode & 4)
+            tma_load_5d(su, &tmU, full_bar(stage), 0, 0, 0, k, tj);
+          else
+            tma_load_3d(su, &tmU, full_bar(stage), k * PB_BLOCK_K, tj * PB_BLOCK_J, 0);
           if (P.mode & 2)
             tma_load_5d(su + PB_U, &tmX, full_bar(stage), 0, 0, 0, k, tr);
           else
@@ -254,7 +257,17 @@ extern "C" int mainloop_probe_run(const void* u_plane, const void* limbs, long l
   if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) return 1;
   EncodeFn enc = reinterpret_cast<EncodeFn>(fn);
   CUtensorMap tmU, tmX;
-  if (tmap3(enc, &tmU, const_cast<void*>(u_plane), K, d3, 1, PB_BLOCK_K, PB_BLOCK_J, 1)) return 2;
+  if (mode & 4) {  // U^T viewed as tiles [d3/128][K/128][1][128 j][128 B], 16 KB each
+    cuuint64_t dims[5] = {128, 128, 1, static_cast<cuuint64_t>(K / 128), static_cast<cuuint64_t>(d3 / 128)};
+    cuuint64_t strides[4] = {128, 128 * 128, 128 * 128, static_cast<cuuint64_t>(K / 128) * 128 * 128};
+    cuuint32_t box[5] = {128, 128, 1, 1, 1}, es[5] = {1, 1, 1, 1, 1};
+    if (enc(&tmU, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<void*>(u_plane), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return 2;
+  } else if (tmap3(enc, &tmU, const_cast<void*>(u_plane), K, d3, 1, PB_BLOCK_K, PB_BLOCK_J, 1)) {
+    return 2;
+  }
   if (mode & 2) {  // the same bytes viewed as tiles [R/64][K/128][4 limbs][64 rows][128 B], 32 KB each
     cuuint64_t dims[5] = {128, 64, 4, static_cast<cuuint64_t>(K / 128), static_cast<cuuint64_t>(R / 64)};
     cuuint64_t strides[4] = {128, 64 * 128, 4 * 64 * 128, static_cast<cuuint64_t>(K / 128) * 4 * 64 * 128};
