@@ -693,7 +693,15 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
   P.R = g.R;
   P.d2 = d.d2;
   P.j_off = static_cast<int32_t>(d.j0);
-  P.num_kb = static_cast<int32_t>((d.d2 + TC_BLOCK_K - 1) / TC_BLOCK_K);
+  const int32_t num_kb_all = static_cast<int32_t>((d.d2 + TC_BLOCK_K - 1) / TC_BLOCK_K);
+  // K split (single-CTA kernel): the K loop in nks consecutive launches whose epilogues accumulate
+  // mod p, so a raster group's U^T panels cover nks× more columns in the same L2 and X is re-read
+  // from DRAM nks× less often, for one extra output read + write per chunk.  CTPT_GEMM_KSPLIT=n.
+  int nks = 1;
+  if (const char* e = getenv("CTPT_GEMM_KSPLIT")) nks = std::max(1, std::min(atoi(e), num_kb_all));
+  if (pair || mc) nks = 1;
+  P.kb_off = 0;
+  P.num_kb = num_kb_all;
   P.tiles_j = static_cast<int32_t>((d.d3_loc + block_j - 1) / block_j);
   P.tiles_r = static_cast<int32_t>((g.R + TC_BLOCK_R - 1) / TC_BLOCK_R);
   const int64_t nt = static_cast<int64_t>(P.tiles_j) * P.tiles_r;
@@ -704,7 +712,7 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
     // keep a raster group's U^T panels within ≈ 32 MB of L2 but never below the measured best
     // of 16 j-tiles: short-K problems (c2: 0.5 MB per panel) take every j-tile in one group, so
     // each X panel is read from DRAM once (c2: +2.4 %; c3, c4: 16 measured best)
-    const int64_t per_panel = static_cast<int64_t>(TC_BLOCK_J) * d.d2p;
+    const int64_t per_panel = static_cast<int64_t>(TC_BLOCK_J) * ((num_kb_all + nks - 1) / nks) * TC_BLOCK_K;
     const int64_t fit = (32LL << 20) / std::max<int64_t>(per_panel, 1);
     P.group_j = static_cast<int32_t>(std::min<int64_t>(std::max<int64_t>(fit, TC_GROUP_J_DEFAULT), P.tiles_j));
   }
@@ -724,19 +732,25 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
                         : mc ? static_cast<unsigned>(2 * std::min<int64_t>(nt_mc, sms / 2))
                              : static_cast<unsigned>(std::min<int64_t>(nt, sms));
   for (int i = 0; i < g.kU; ++i) {
-    P.plane = g.plane0 + i;
-    P.o = g.o;
-    P.o.accumulate = i > 0;
-    P.o.w = pow2mod(8 * i, g.p);
-    if (i < g.kU - 1) P.o.xlast = nullptr;  // Rescale on the final pass only
-    P.sj = (i == 0 && !pair) ? g.sj : SplitJob{};  // the next prime's split rides on the first pass
-    if (pair)
-      k_gemm_tc2<<<grid, T2_THREADS, T2_SMEM_BYTES, st>>>(tmU, tmX, P);
-    else if (mc)
-      k_gemm_tc_mc<<<grid, TC_THREADS, TC_SMEM_BYTES, st>>>(tmU, tmX, P);
-    else
-      k_gemm_tc<<<grid, TC_THREADS, TC_SMEM_BYTES, st>>>(tmU, tmX, P);
-    CUDA_TRY(cudaGetLastError());
+    for (int kc = 0; kc < nks; ++kc) {
+      const bool first = (i == 0 && kc == 0), last = (i == g.kU - 1 && kc == nks - 1);
+      P.plane = g.plane0 + i;
+      P.kb_off = static_cast<int32_t>(static_cast<int64_t>(num_kb_all) * kc / nks);
+      P.num_kb = static_cast<int32_t>(static_cast<int64_t>(num_kb_all) * (kc + 1) / nks) - P.kb_off;
+      P.o = g.o;
+      P.o.accumulate = !first;
+      P.o.w = pow2mod(8 * i, g.p);
+      if (!last) P.o.xlast = nullptr;     // Rescale on the final pass only
+      if (!first) P.o.rowcorr = nullptr;  // the unsigned-U row correction exactly once
+      P.sj = (first && !pair) ? g.sj : SplitJob{};  // the next prime's split rides on the first pass
+      if (pair)
+        k_gemm_tc2<<<grid, T2_THREADS, T2_SMEM_BYTES, st>>>(tmU, tmX, P);
+      else if (mc)
+        k_gemm_tc_mc<<<grid, TC_THREADS, TC_SMEM_BYTES, st>>>(tmU, tmX, P);
+      else
+        k_gemm_tc<<<grid, TC_THREADS, TC_SMEM_BYTES, st>>>(tmU, tmX, P);
+      CUDA_TRY(cudaGetLastError());
+    }
   }
   if (pair && g.sj.x) return launch_split_job(g.sj, st);  // the pair kernel has no side split
   return CTPT_OK;

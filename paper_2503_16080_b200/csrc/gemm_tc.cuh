@@ -83,7 +83,8 @@ struct TcParams {
   int64_t R, d2;
   int32_t j_off;      // first U column (col_begin)
   int32_t plane;      // U digit plane index (3rd TMA coordinate)
-  int32_t num_kb;     // ceil(d2 / 128)
+  int32_t num_kb;     // k-blocks of 128 B this launch covers (ceil(d2 / 128) without a K split)
+  int32_t kb_off;     // first k-block of this launch (K split: the epilogue accumulates the chunks)
   int32_t tiles_j, tiles_r;
   int32_t num_tiles;
   int32_t group_j;    // tiles visited in groups of group_j j-tiles (L2 reuse of U panels)
@@ -158,8 +159,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (pf_tile < P.num_tiles) {
           int32_t ptj, ptr;
           tc_tile_coords(pf_tile, P, ptj, ptr);
-          tma_prefetch_l2_5d(&tmX, 0, 0, 0, pf_kb, ptr);
-          tma_prefetch_l2_3d(&tmU, pf_kb * TC_BLOCK_K, P.j_off + ptj * TC_BLOCK_J, P.plane);
+          tma_prefetch_l2_5d(&tmX, 0, 0, 0, pf_kb + P.kb_off, ptr);
+          tma_prefetch_l2_3d(&tmU, (pf_kb + P.kb_off) * TC_BLOCK_K, P.j_off + ptj * TC_BLOCK_J, P.plane);
         }
       };
       for (int32_t i = 0; i < P.l2_pf; ++i) { pf_issue(); pf_advance(); }
@@ -170,19 +171,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // neighbouring CTAs; the one holding the group's first j-tile streams it into L2 ahead
         const bool pf_lead = P.pf_x > 0 && (tj % P.group_j) == 0;
         if (pf_lead)
-          for (int32_t kb = 0; kb < P.pf_x && kb < P.num_kb; ++kb) tma_prefetch_l2_5d(&tmX, 0, 0, 0, kb, tr);
+          for (int32_t kb = 0; kb < P.pf_x && kb < P.num_kb; ++kb) tma_prefetch_l2_5d(&tmX, 0, 0, 0, kb + P.kb_off, tr);
         for (int32_t kb = 0; kb < P.num_kb; ++kb) {
           if (P.l2_pf > 0) { pf_issue(); pf_advance(); }
           if (pf_lead && kb + P.pf_x < P.num_kb)
-            tma_prefetch_l2_5d(&tmX, 0, 0, 0, kb + P.pf_x, tr);
+            tma_prefetch_l2_5d(&tmX, 0, 0, 0, kb + P.pf_x + P.kb_off, tr);
           mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t su = sbase + stage * TC_STAGE_BYTES;
           mbar_arrive_expect_tx(full_bar(stage), TC_STAGE_BYTES);
+          const int32_t kg = kb + P.kb_off;
           if (P.l2_hint)
-            tma_load_3d_hint(su, &tmU, full_bar(stage), kb * TC_BLOCK_K, P.j_off + tj * TC_BLOCK_J, P.plane, pol_u);
+            tma_load_3d_hint(su, &tmU, full_bar(stage), kg * TC_BLOCK_K, P.j_off + tj * TC_BLOCK_J, P.plane, pol_u);
           else
-            tma_load_3d(su, &tmU, full_bar(stage), kb * TC_BLOCK_K, P.j_off + tj * TC_BLOCK_J, P.plane);
-          tma_load_5d(su + TC_U_BYTES, &tmX, full_bar(stage), 0, 0, 0, kb, tr);  // one 32-KB limb tile
+            tma_load_3d(su, &tmU, full_bar(stage), kg * TC_BLOCK_K, P.j_off + tj * TC_BLOCK_J, P.plane);
+          tma_load_5d(su + TC_U_BYTES, &tmX, full_bar(stage), 0, 0, 0, kg, tr);  // one 32-KB limb tile
           if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
         }
       }
