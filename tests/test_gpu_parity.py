@@ -838,3 +838,16 @@ def test_fuzz_shapes_against_oracle(case, monkeypatch):
         monkeypatch.delenv(var, raising=False)
     fmt, N, k, d2, d3, L, ub, c0, c1, i = case
     _check(fmt, N, k, d2, d3, L, seed=100 + i, u_bound=ub, col_begin=c0, col_end=c1, split_overlap=i % 2)
+
+
+@pytest.mark.parametrize("ksplit", ["2", "3"])
+def test_gemm_k_split_accumulates(ksplit, monkeypatch):
+    """CTPT_GEMM_KSPLIT: the limb GEMM's K loop in consecutive launches whose epilogues accumulate
+    mod p — with the unsigned-U row correction (applied once), multi-digit U (k_U passes × K
+    chunks), the in-kernel split of the next prime, and Rescale on the last pass only."""
+    monkeypatch.setenv("CTPT_GEMM_KSPLIT", ksplit)
+    monkeypatch.setenv("CTPT_SKINNY", "off")
+    monkeypatch.delenv("CTPT_GEMM", raising=False)
+    _check(A, 64, 3, 700, 300, 2, unsigned="always", seed=41)
+    _check(S, 32, 2, 1000, 260, 3, u_bound=300, seed=42, split_overlap=1)
+    _check(R, 256, 1, 129, 300, 1, seed=43)  # fewer k-blocks than chunks on some launches
