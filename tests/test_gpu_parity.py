@@ -851,3 +851,17 @@ def test_gemm_k_split_accumulates(ksplit, monkeypatch):
     _check(A, 64, 3, 700, 300, 2, unsigned="always", seed=41)
     _check(S, 32, 2, 1000, 260, 3, u_bound=300, seed=42, split_overlap=1)
     _check(R, 256, 1, 129, 300, 1, seed=43)  # fewer k-blocks than chunks on some launches
+
+
+@pytest.mark.parametrize("knob", ["CTPT_GEMM_PF=4", "CTPT_GEMM_PFX=4", "CTPT_GEMM_L2HINT=2", "CTPT_GROUP_J=3",
+                                  "CTPT_GEMM=mc", "CTPT_LAYOUT=scalar", "CTPT_FUSED_LOAD=hybrid"])
+def test_measurement_knobs_keep_results_exact(knob, monkeypatch):
+    """Every A/B knob the measurements used (include/ctpt.h) leaves the residues bit-exact: L2
+    prefetch of the GEMM's operands or of the X tiles, U^T eviction hints, another raster group,
+    the multicast-cluster GEMM, the 4-byte layout kernel, the hybrid converter feed."""
+    name, val = knob.split("=")
+    monkeypatch.setenv(name, val)
+    for var in ("CTPT_SKINNY", "CTPT_MV"):
+        monkeypatch.delenv(var, raising=False)
+    _check(A, 64, 3, 700, 300, 2, seed=51)  # split + GEMM regime
+    _check(S, 32, 4, 520, 100, 1, seed=52)  # fused skinny regime
