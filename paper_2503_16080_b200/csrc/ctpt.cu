@@ -302,7 +302,9 @@ ctpt_status tc_setup() {
   if (dev < 0 || dev >= kMaxDevices) return fail(CTPT_ERR_CUDA, "device ordinal %d out of range", dev);
   cudaError_t& e = errs[dev];
   std::call_once(onces[dev], [&e] {
-    e = cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BYTES);
+    e = cudaFuncSetAttribute(k_gemm_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BYTES);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_gemm_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BYTES);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_gemm_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, T2_SMEM_BYTES);
     if (e == cudaSuccess)
@@ -731,6 +733,29 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
   const unsigned grid = pair ? static_cast<unsigned>(2 * std::min<int64_t>(nt, sms / 2))
                         : mc ? static_cast<unsigned>(2 * std::min<int64_t>(nt_mc, sms / 2))
                              : static_cast<unsigned>(std::min<int64_t>(nt, sms));
+  // k_U > 1: every digit in one launch (MULTI kernel, CTPT_GEMM_MULTI=on) instead of k_U launches
+  // that accumulate through the outputs.  Measured slower on the Rescale workload (7.9 vs 8.3e13
+  // residue-MAC/s: the tile's four digit passes keep four U^T panels per j-tile live in L2 and the
+  // extra DRAM traffic lowers the clock; with the raster group divided by k_U, 7.1e13), so the
+  // per-digit launches stay the default (profiles/r01/gemm_multi_digit/).
+  bool multi = false;
+  if (const char* e = getenv("CTPT_GEMM_MULTI"))
+    multi = strcmp(e, "on") == 0 && g.kU > 1 && g.kU <= 4 && !pair && !mc && nks == 1;
+  if (multi) {
+    P.plane = g.plane0;
+    P.ndig = g.kU;
+    for (int i = 0; i < 4; ++i) P.wdig[i] = pow2mod(8 * i, g.p);
+    P.kb_off = 0;
+    P.num_kb = num_kb_all;
+    P.o = g.o;
+    P.o.accumulate = 0;
+    P.o.w = 1;
+    P.sj = g.sj;
+    k_gemm_tc<true><<<grid, TC_THREADS, TC_SMEM_BYTES, st>>>(tmU, tmX, P);
+    CUDA_TRY(cudaGetLastError());
+    return CTPT_OK;
+  }
+  P.ndig = 1;
   for (int i = 0; i < g.kU; ++i) {
     for (int kc = 0; kc < nks; ++kc) {
       const bool first = (i == 0 && kc == 0), last = (i == g.kU - 1 && kc == nks - 1);
@@ -748,7 +773,7 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
       else if (mc)
         k_gemm_tc_mc<<<grid, TC_THREADS, TC_SMEM_BYTES, st>>>(tmU, tmX, P);
       else
-        k_gemm_tc<<<grid, TC_THREADS, TC_SMEM_BYTES, st>>>(tmU, tmX, P);
+        k_gemm_tc<false><<<grid, TC_THREADS, TC_SMEM_BYTES, st>>>(tmU, tmX, P);
       CUDA_TRY(cudaGetLastError());
     }
   }

@@ -96,6 +96,8 @@ struct TcParams {
   ModP m;
   OutParams o;
   SplitJob sj;        // the next prime's limb split (warps 2–3), or sj.x = nullptr
+  int32_t ndig;       // MULTI kernel: U digit planes plane .. plane + ndig − 1, all in this launch
+  uint32_t wdig[4];   // 2^{8i} mod p for digit i
 };
 
 __device__ __forceinline__ void tc_tile_coords(int32_t tile, const TcParams& P, int32_t& tj, int32_t& tr) {
@@ -107,6 +109,11 @@ __device__ __forceinline__ void tc_tile_coords(int32_t tile, const TcParams& P, 
   tr = rem / gj;
 }
 
+// MULTI = true (k_U > 1 digit planes: Rescale's real U, general Mod-PP-MM): every tile runs its K
+// loop once per digit plane into alternating TMEM buffers, and the epilogue accumulates
+// Σ_i 2^{8i}·(digit i's product mod p) in registers, storing once — instead of k_U launches that
+// each re-read the outputs.  MULTI = false is the k_U = 1 kernel, unchanged.
+template <bool MULTI>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmX,
               const __grid_constant__ TcParams P) {
@@ -172,6 +179,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const bool pf_lead = P.pf_x > 0 && (tj % P.group_j) == 0;
         if (pf_lead)
           for (int32_t kb = 0; kb < P.pf_x && kb < P.num_kb; ++kb) tma_prefetch_l2_5d(&tmX, 0, 0, 0, kb + P.kb_off, tr);
+        for (int32_t dg = 0; dg < (MULTI ? P.ndig : 1); ++dg)
         for (int32_t kb = 0; kb < P.num_kb; ++kb) {
           if (P.l2_pf > 0) { pf_issue(); pf_advance(); }
           if (pf_lead && kb + P.pf_x < P.num_kb)
@@ -180,10 +188,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const uint32_t su = sbase + stage * TC_STAGE_BYTES;
           mbar_arrive_expect_tx(full_bar(stage), TC_STAGE_BYTES);
           const int32_t kg = kb + P.kb_off;
+          const int32_t plane = P.plane + (MULTI ? dg : 0);
           if (P.l2_hint)
-            tma_load_3d_hint(su, &tmU, full_bar(stage), kg * TC_BLOCK_K, P.j_off + tj * TC_BLOCK_J, P.plane, pol_u);
+            tma_load_3d_hint(su, &tmU, full_bar(stage), kg * TC_BLOCK_K, P.j_off + tj * TC_BLOCK_J, plane, pol_u);
           else
-            tma_load_3d(su, &tmU, full_bar(stage), kg * TC_BLOCK_K, P.j_off + tj * TC_BLOCK_J, P.plane);
+            tma_load_3d(su, &tmU, full_bar(stage), kg * TC_BLOCK_K, P.j_off + tj * TC_BLOCK_J, plane);
           tma_load_5d(su + TC_U_BYTES, &tmX, full_bar(stage), 0, 0, 0, kg, tr);  // one 32-KB limb tile
           if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
         }
@@ -197,7 +206,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int32_t tile = blockIdx.x; tile < P.num_tiles; tile += gridDim.x) {
+      for (int32_t tile = blockIdx.x; tile < P.num_tiles; tile += gridDim.x)
+      for (int32_t dg = 0; dg < (MULTI ? P.ndig : 1); ++dg) {
         mbar_wait(tempty_bar(acc), acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * TC_ACC_COLS;
@@ -221,7 +231,51 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else if (warp == 2 || warp == 3) {
     // ---------------------------------------------------------------- next prime's limb split
     if (P.sj.x) side_split_rows(P.sj, 2 * static_cast<int64_t>(blockIdx.x) + (warp - 2), 2 * static_cast<int64_t>(gridDim.x), lane);
-  } else if (warp >= 4) {
+  } else if (MULTI && warp >= 4) {
+    // ---------------------------------------------------------------- epilogue, k_U digits
+    const int quad = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int32_t tile = blockIdx.x; tile < P.num_tiles; tile += gridDim.x) {
+      int32_t tj, tr;
+      tc_tile_coords(tile, P, tj, tr);
+      const int64_t j = static_cast<int64_t>(tj) * TC_BLOCK_J + quad * 32 + lane;
+      uint32_t sum[TC_BLOCK_R];  // Σ_i w_i·(digit i's product mod p), this thread's 64 outputs
+      for (int32_t dg = 0; dg < P.ndig; ++dg) {
+        mbar_wait(tfull_bar(acc), acc_phase);
+        tc_fence_after();
+        const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * TC_ACC_COLS;
+        const uint32_t w = P.wdig[dg];
+#pragma unroll
+        for (int c = 0; c < TC_BLOCK_R / 16; ++c) {
+          uint32_t v0[16], v1[16], v2[16], v3[16];
+          tmem_ld16(t_row + 0 * TC_BLOCK_R + c * 16, v0);
+          tmem_ld16(t_row + 1 * TC_BLOCK_R + c * 16, v1);
+          tmem_ld16(t_row + 2 * TC_BLOCK_R + c * 16, v2);
+          tmem_ld16(t_row + 3 * TC_BLOCK_R + c * 16, v3);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const uint32_t r = recombine_mod(static_cast<int32_t>(v0[i]), static_cast<int32_t>(v1[i]),
+                                             static_cast<int32_t>(v2[i]), static_cast<int32_t>(v3[i]), P.m);
+            sum[c * 16 + i] = dg == 0 ? r : accum_mod(sum[c * 16 + i], r, w, P.m);
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(tempty_bar(acc));  // the buffer is free as soon as it is read
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+      if (j < P.o.d3_loc) {
+#pragma unroll
+        for (int c = 0; c < TC_BLOCK_R / 16; ++c) {
+          uint32_t res[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) res[i] = sum[c * 16 + i];
+          store16(P.o, P.m, j, static_cast<int64_t>(tr) * TC_BLOCK_R + c * 16, res);
+        }
+      }
+    }
+  } else if (!MULTI && warp >= 4) {
     // ---------------------------------------------------------------- epilogue (128 threads)
     const int quad = warp & 3;  // TMEM lanes [32·quad, 32·quad + 32)
     int acc = 0;

@@ -865,3 +865,14 @@ def test_measurement_knobs_keep_results_exact(knob, monkeypatch):
         monkeypatch.delenv(var, raising=False)
     _check(A, 64, 3, 700, 300, 2, seed=51)  # split + GEMM regime
     _check(S, 32, 4, 520, 100, 1, seed=52)  # fused skinny regime
+
+
+def test_multi_digit_single_launch_knob(monkeypatch):
+    """CTPT_GEMM_MULTI=on: all k_U digit planes in one k_gemm_tc<true> launch, the epilogue
+    accumulating Σ 2^{8i}·(digit i's product) in registers — k_U = 2 and 3, with the in-kernel
+    split of the next prime."""
+    monkeypatch.setenv("CTPT_GEMM_MULTI", "on")
+    monkeypatch.setenv("CTPT_SKINNY", "off")
+    monkeypatch.delenv("CTPT_GEMM", raising=False)
+    _check(A, 64, 3, 400, 300, 2, u_bound=300, seed=61, split_overlap=1)   # k_U = 2
+    _check(S, 32, 2, 300, 260, 1, u_bound=40000, seed=62)                 # k_U = 3
