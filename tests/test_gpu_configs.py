@@ -35,6 +35,16 @@ def _boundary(n, tile):
     return sorted(i for i in idx if 0 <= i < n)
 
 
+def _dec_cols(d3, n=16, seed=7):
+    """the decryption identity and the decoded value on 16 sampled output
+    columns — the tile boundaries (0, 127, 128, 255, 256, last) plus seeded random columns."""
+    cols = {0, 127, 128, 255, 256, d3 - 1}
+    rng = np.random.default_rng(seed)
+    while len(cols) < n:
+        cols.add(int(rng.integers(0, d3)))
+    return sorted(c for c in cols if 0 <= c < d3)
+
+
 def _check_matrix(Xc, U, C, p, rng, name, n_random):
     """Xc: col-major [d2][rows] ciphertext matrix; C: [d3][rows] GPU output."""
     d2, rows = Xc.shape
@@ -131,23 +141,23 @@ def _run_config(name, primes_per_call, n_random, dec_cols):
 
 def test_config3_full_size():
     c = ctgen.CONFIGS["c3"]
-    _run_config("c3", primes_per_call=3, n_random=65536, dec_cols=[0, 127, 128, 8191, c.d3 - 1])
+    _run_config("c3", primes_per_call=3, n_random=65536, dec_cols=_dec_cols(c.d3))
 
 
 def test_config4_full_size():
     c = ctgen.CONFIGS["c4"]
-    _run_config("c4", primes_per_call=4, n_random=32768, dec_cols=[0, 128, c.d3 - 1])
+    _run_config("c4", primes_per_call=4, n_random=65536, dec_cols=_dec_cols(c.d3))
 
 
 def test_config3a_struct_a_full_size():
     """SURVEY.md §8(f) row 2 at c3's sizes: Algorithm 7 in structured-A shared-a (R = d1 = 16384)."""
     c = ctgen.CONFIGS["c3a"]
-    _run_config("c3a", primes_per_call=3, n_random=32768, dec_cols=[0, 128, c.d3 - 1])
+    _run_config("c3a", primes_per_call=3, n_random=65536, dec_cols=_dec_cols(c.d3))
 
 
 def test_config5_full_size():
     c = ctgen.CONFIGS["c5"]
-    _run_config("c5", primes_per_call=1, n_random=8192, dec_cols=[0, c.d3 - 1])
+    _run_config("c5", primes_per_call=1, n_random=65536, dec_cols=_dec_cols(c.d3))
 
 
 def test_config4_skinny_sweep_full_size(monkeypatch):
