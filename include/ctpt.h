@@ -52,8 +52,12 @@
  *    CTPT_FUSED_LOAD=regs|hybrid (converter register loads instead of the TMA raw ring),
  *    CTPT_FUSED2=pair (CTA-pair fused kernel for 128 < d3_loc ≤ 256; CTPT_F2_GROUPS=1|2 its
  *    converter groups), CTPT_FUSED_PF=n (L2 prefetch distance in the fused kernel),
- *    CTPT_GROUP_J=n (GEMM raster group), CTPT_GEMM_PF=n (GEMM L2 prefetch distance),
- *    CTPT_LAYOUT=scalar (4-byte layout kernel).  None of them changes a result.
+ *    CTPT_GROUP_J=n (GEMM raster group), CTPT_GEMM_PF=n / CTPT_GEMM_PFX=n (GEMM L2 prefetch of
+ *    the operands / of the X tiles), CTPT_GEMM_L2HINT=2 (U^T loads evict_last), CTPT_GEMM=mc
+ *    (multicast-cluster GEMM), CTPT_GEMM_KSPLIT=n (K loop in n accumulating launches),
+ *    CTPT_GEMM_MULTI=on (all k_U digits in one launch), CTPT_FUSED_LOAD=tma2 (two converter
+ *    groups), CTPT_LAYOUT=scalar (4-byte layout kernel).  None of them changes a result
+ *    (tests/test_gpu_parity.py runs each); DESIGN.md §6 has what each measured.
  */
 #ifndef CTPT_H_
 #define CTPT_H_
