@@ -895,6 +895,102 @@ def run_sharded_ipc(args, rank: int, world: int, local_rank: int):
             "clocks": clocks, "input_generation_s": gen_s}))
 
 
+def run_modmm(args, rank: int, world: int, local_rank: int):
+    """SURVEY.md §8(f) row 4 under the bench contract: the Mod-PP-MM stage that CC-MM (Alg. 8,
+    P:1843–1845) and the RGSW product (Alg. 9) reduce to — Z = X·Y mod p for 3 primes
+    with FULL residues on both sides (16384³), through ctpt_modmatmul: Y's 4 balanced digit
+    planes precomputed once (outside the timed region, as for a reused operand), then per prime
+    the limb split of X and 4 GEMM passes (16 limb MACs per residue MAC) accumulating in the
+    epilogue.  Inputs: seeded uniform residues (ctgen), device-resident; weak scaling."""
+    import torch
+
+    import ctgen
+    from paper_2503_16080_b200 import ctpt
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    M = K = Nc = 16384
+    L = 3
+    ps = ctgen.primes(L)
+    cores = os.cpu_count() or 1
+    seed = 9 + rank
+    ldx, plain_bytes, ws_bytes = ctpt.modmatmul_sizes(ps, M, K, Nc)
+    t0 = time.perf_counter()
+    Xh = np.zeros((L, M, ldx), np.uint32)
+    Yh = np.empty((L, K, Nc), np.uint32)
+    for l, p in enumerate(ps):
+        Xh[l, :, :K] = ctgen.uniform_residues(seed * 1000 + 2 * l, p, M * K, nthreads=max(1, cores // world)).reshape(M, K)
+        Yh[l] = ctgen.uniform_residues(seed * 1000 + 2 * l + 1, p, K * Nc, nthreads=max(1, cores // world)).reshape(K, Nc)
+    gen_s = time.perf_counter() - t0
+    X = torch.from_numpy(Xh.view(np.int32)).to(dev)
+    Y = torch.from_numpy(Yh.view(np.int32)).to(dev)
+    plain = torch.empty(plain_bytes, dtype=torch.uint8, device=dev)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    ZT = torch.empty((L, Nc, M), dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    ctpt.modmatmul_precompute(ps, M, K, Nc, Y, plain, stream=stream)
+    del Y
+    for _ in range(args.warmup):
+        ctpt.modmatmul(ps, M, K, Nc, X, ldx, plain, ZT, ws, stream=stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    clk = ClockSampler(local_rank)
+    time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        ctpt.modmatmul(ps, M, K, Nc, X, ldx, plain, ZT, ws, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    macs = L * M * K * Nc
+    value = world * macs / (ms / 1e3)
+    mp, which = peaks()
+    tops = 2 * 16 * macs / (ms / 1e3) / 1e12
+    peak_key = "bf16_tflops" if ms * args.steps < 2000.0 else "bf16_tflops_sustained"
+    result = {
+        "metric": "Mod-PP-MM residue-MACs/s (full residues both sides, 16384^3 x 3 primes)", "value": value,
+        "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+        "config": {"workload": "modmm: Z = X.Y mod p, X 16384x16384, Y 16384x16384 uniform residues, 3 primes < 2^31 "
+                               "(SURVEY.md §8(f) row 4)", "M": M, "K": K, "N": Nc, "L": L,
+                   "limb_macs_per_residue_mac": 16, "l2": "inputs 3 GiB per step > L2"},
+        "pct_int8_datasheet": 100.0 * 16 * macs / (ms / 1e3) / INT8_DATASHEET_MACS,
+        "roofline": {"bound": "tensor", "achieved": tops, "peak": 2 * float(mp[peak_key]), "unit": "TOP/s",
+                     "frac": tops / (2 * float(mp[peak_key])), "traffic": None,
+                     "kernel": "k_split + 4 passes of k_gemm_tc per prime (whole step)",
+                     "vs_int8_mma_ceiling": mma_ceiling_ratio(tops)},
+        "e2e": {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                "note": "device-resident workload (no host-buffer entry point for Mod-PP-MM)"},
+        "gpu_launches": (1 + 4) * L * args.steps, "clocks": clocks, "input_generation_s": gen_s,
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        import oracle
+
+        p = ps[0]
+        Xc = np.ascontiguousarray(Xh[0, :, :K].T)  # col-major [K][M] view of X for the oracle
+        Yi = Yh[0].astype(np.int64)
+        ncols = max(1, cores)
+        t0 = time.perf_counter()
+        want = oracle.modmatmul(Xc, Yi, p, cols=np.arange(ncols), nthreads=cores)
+        dt = time.perf_counter() - t0
+        got = ZT[0, :ncols].cpu().numpy().view(np.uint32)
+        bad = int(np.count_nonzero(got != want))
+        result["cpu_baseline"] = {"value": M * K * ncols / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+                                  "host": host_description(),
+                                  "sample": f"prime 0, {ncols} output columns x {M} rows x K={K} (schoolbook __int128)",
+                                  "parity_on_sample": {"entries": int(got.size), "mismatches": bad,
+                                                       "verdict": "bit-exact" if bad == 0 else "MISMATCH"}}
+    if rank == 0:
+        print(json.dumps(result))
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -919,7 +1015,9 @@ def main():
         else:
             torch.distributed.init_process_group(backend)
     try:
-        if args.shard and args.gather == "ipc":
+        if args.config == "modmm":
+            run_modmm(args, rank, world, local_rank)
+        elif args.shard and args.gather == "ipc":
             run_sharded_ipc(args, rank, world, local_rank)
         elif args.shard:
             run_sharded(args, rank, world, local_rank)
