@@ -722,6 +722,10 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
   if (const char* g = getenv("CTPT_GROUP_J")) P.group_j = std::max(1, atoi(g));  // tuning knob
   P.l2_pf = 0;
   if (const char* g = getenv("CTPT_GEMM_PF")) P.l2_pf = std::max(0, atoi(g));     // tuning knob
+  // epilogue with 32-column TMEM loads and the accumulator handed back before the last stores:
+  // c3 3.709 vs 3.694e14, 3 interleaved reps each (profiles/r01/gemm_epilogue_ld32/)
+  P.ep32 = 1;
+  if (const char* g = getenv("CTPT_GEMM_EP32")) P.ep32 = atoi(g) != 0;
   P.pf_x = 0;
   if (const char* g = getenv("CTPT_GEMM_PFX")) P.pf_x = std::max(0, atoi(g));        // tuning knob (measuring)
   P.l2_hint = 0;

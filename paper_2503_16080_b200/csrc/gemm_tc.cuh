@@ -96,6 +96,7 @@ struct TcParams {
   ModP m;
   OutParams o;
   SplitJob sj;        // the next prime's limb split (warps 2–3), or sj.x = nullptr
+  int32_t ep32;       // epilogue with 32-column TMEM loads, buffer released before the last stores
   int32_t ndig;       // MULTI kernel: U digit planes plane .. plane + ndig − 1, all in this launch
   uint32_t wdig[4];   // 2^{8i} mod p for digit i
 };
@@ -287,6 +288,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tc_fence_after();
       const int64_t j = static_cast<int64_t>(tj) * TC_BLOCK_J + quad * 32 + lane;
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * TC_ACC_COLS;
+      if (P.ep32) {  // two halves of 32 rows: 4 × 32-column TMEM loads each (default; CTPT_GEMM_EP32=0: the 16-column loop)
+#pragma unroll 1
+        for (int h = 0; h < TC_BLOCK_R / 32; ++h) {
+          uint32_t v0[32], v1[32], v2[32], v3[32];
+          tmem_ld32(t_row + 0 * TC_BLOCK_R + h * 32, v0);
+          tmem_ld32(t_row + 1 * TC_BLOCK_R + h * 32, v1);
+          tmem_ld32(t_row + 2 * TC_BLOCK_R + h * 32, v2);
+          tmem_ld32(t_row + 3 * TC_BLOCK_R + h * 32, v3);
+          tmem_ld_wait();
+          if (h == TC_BLOCK_R / 32 - 1) {  // every column read: hand the buffer back before storing
+            tc_fence_before();
+            mbar_arrive(tempty_bar(acc));
+          }
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            uint32_t res[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              res[i] = recombine_mod(static_cast<int32_t>(v0[q * 16 + i]), static_cast<int32_t>(v1[q * 16 + i]),
+                                     static_cast<int32_t>(v2[q * 16 + i]), static_cast<int32_t>(v3[q * 16 + i]), P.m);
+            if (j < P.o.d3_loc) store16(P.o, P.m, j, static_cast<int64_t>(tr) * TC_BLOCK_R + h * 32 + q * 16, res);
+          }
+        }
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        continue;
+      }
 #pragma unroll 1
       for (int c = 0; c < TC_BLOCK_R / 16; ++c) {
         uint32_t v0[16], v1[16], v2[16], v3[16];
