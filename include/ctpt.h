@@ -56,7 +56,7 @@
  *    the operands / of the X tiles), CTPT_GEMM_L2HINT=2 (U^T loads evict_last), CTPT_GEMM=mc
  *    (multicast-cluster GEMM), CTPT_GEMM_KSPLIT=n (K loop in n accumulating launches),
  *    CTPT_GEMM_MULTI=on (all k_U digits in one launch), CTPT_GEMM_EP32=0 (16-column epilogue
- *    loads), CTPT_FUSED_LOAD=tma2 (two converter
+ *    loads), CTPT_GEMM_CS=1 (evict-first output stores), CTPT_FUSED_LOAD=tma2 (two converter
  *    groups), CTPT_LAYOUT=scalar (4-byte layout kernel).  None of them changes a result
  *    (tests/test_gpu_parity.py runs each); DESIGN.md §6 has what each measured.
  */

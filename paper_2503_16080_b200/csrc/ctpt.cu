@@ -726,6 +726,8 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
   // c3 3.709 vs 3.694e14, 3 interleaved reps each (profiles/r01/gemm_epilogue_ld32/)
   P.ep32 = 1;
   if (const char* g = getenv("CTPT_GEMM_EP32")) P.ep32 = atoi(g) != 0;
+  int stream_stores = 0;
+  if (const char* g = getenv("CTPT_GEMM_CS")) stream_stores = atoi(g) != 0;       // tuning knob (measuring)
   P.pf_x = 0;
   if (const char* g = getenv("CTPT_GEMM_PFX")) P.pf_x = std::max(0, atoi(g));        // tuning knob (measuring)
   P.l2_hint = 0;
@@ -767,6 +769,7 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
       P.kb_off = static_cast<int32_t>(static_cast<int64_t>(num_kb_all) * kc / nks);
       P.num_kb = static_cast<int32_t>(static_cast<int64_t>(num_kb_all) * (kc + 1) / nks) - P.kb_off;
       P.o = g.o;
+      P.o.stream_stores = stream_stores;
       P.o.accumulate = !first;
       P.o.w = pow2mod(8 * i, g.p);
       if (!last) P.o.xlast = nullptr;     // Rescale on the final pass only

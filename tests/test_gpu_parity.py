@@ -853,7 +853,7 @@ def test_gemm_k_split_accumulates(ksplit, monkeypatch):
     _check(R, 256, 1, 129, 300, 1, seed=43)  # fewer k-blocks than chunks on some launches
 
 
-@pytest.mark.parametrize("knob", ["CTPT_GEMM_PF=4", "CTPT_GEMM_PFX=4", "CTPT_GEMM_L2HINT=2", "CTPT_GROUP_J=3", "CTPT_GEMM_EP32=0",
+@pytest.mark.parametrize("knob", ["CTPT_GEMM_PF=4", "CTPT_GEMM_PFX=4", "CTPT_GEMM_L2HINT=2", "CTPT_GROUP_J=3", "CTPT_GEMM_EP32=0", "CTPT_GEMM_CS=1",
                                   "CTPT_GEMM=mc", "CTPT_LAYOUT=scalar", "CTPT_FUSED_LOAD=hybrid"])
 def test_measurement_knobs_keep_results_exact(knob, monkeypatch):
     """Every A/B knob the measurements used (include/ctpt.h) leaves the residues bit-exact: L2
