@@ -255,6 +255,31 @@ def run_reference(args, rank: int):
 
     if rank != 0:
         return
+    if args.config == "modmm":  # the oracle's schoolbook on a bounded sample of the Mod-PP-MM workload
+        import oracle
+
+        cores = os.cpu_count() or 1
+        p = ctgen.primes(1)[0]
+        K = M = 16384
+        X = ctgen.uniform_residues(9000, p, K * M, nthreads=cores).reshape(K, M)  # col-major [K][M]
+        Y = ctgen.uniform_residues(9001, p, K * cores, nthreads=cores).reshape(K, cores).astype(np.int64)
+        times = []
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            oracle.modmatmul(X, Y, p, nthreads=cores)
+            if i >= args.warmup:
+                times.append(time.perf_counter() - t0)
+        t = statistics.mean(times)
+        v = M * K * cores / t
+        print(json.dumps({
+            "impl": "reference", "metric": "Mod-PP-MM residue-MACs/s (full residues both sides, 16384^3 x 3 primes)",
+            "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u128 (schoolbook residues)", "data": "synthetic", "config": {"workload": "modmm"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"per step: one prime, {cores} output columns x {M} rows x K={K}"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
     c = ctgen.CONFIGS[args.config]
     cores = os.cpu_count() or 1
     ps, ct, U, _ = make_inputs(c, c.seed, cores)
