@@ -46,6 +46,7 @@ def main():
                          "k-block (mode 1, no DRAM)")
     ap.add_argument("--launches", type=int, default=250)
     ap.add_argument("--skip-ceiling", action="store_true")
+    ap.add_argument("--reuse", action="store_true", help="A-operand collector reuse probe")
     args = ap.parse_args()
     import torch
 
@@ -83,6 +84,31 @@ def main():
         time.sleep(2.0)
     if args.mainloop:
         mainloop(lib, args.launches)
+    if args.reuse:
+        reuse_probe(lib, blocks, iters // 2)
+
+
+def reuse_probe(lib, blocks: int, iters: int):
+    """Two MMAs per K slice sharing A, with / without .collector::a::fill / ::lastuse."""
+    from bench import ClockSampler
+
+    lib.mma_reuse_run.restype = ctypes.c_int
+    lib.mma_reuse_run.argtypes = [ctypes.c_int, ctypes.c_longlong, ctypes.c_int, ctypes.c_int, ctypes.c_uint,
+                                  ctypes.c_int, ctypes.POINTER(ctypes.c_float), ctypes.c_void_p]
+    ms = ctypes.c_float()
+    macs = 8 * 128 * 256 * 32
+    for reuse in (0, 1, 0, 1):
+        clk = ClockSampler(0)
+        time.sleep(0.3)
+        rc = lib.mma_reuse_run(blocks, iters, 16, 255, 7, reuse, ctypes.byref(ms), None)
+        cl = clk.stop()
+        assert rc == 0, rc
+        tops = 2 * blocks * iters * macs / (ms.value / 1e3) / 1e12
+        print(json.dumps({"case": "A shared by 2 MMAs, collector reuse" if reuse else "A shared by 2 MMAs, no hint",
+                          "tops": tops, "sm_mhz": cl.get("sm_mhz"), "power_w_max": cl.get("power_w_max"),
+                          "per_clock_pct": (100 * tops * 1e12 / (2 * blocks * 8192 * cl["sm_mhz"] * 1e6)
+                                            if cl.get("sm_mhz") else None)}), flush=True)
+        time.sleep(2.0)
 
 
 def mainloop(lib, launches: int):

@@ -80,6 +80,93 @@ __global__ void __launch_bounds__(128, 1) k_mma_ceiling(long long iters, int a_m
   }
 }
 
+// A-operand reuse probe: per K slice two MMAs share A (M = 128) against two different B tiles
+// (N = 256 each) into two accumulators; with `reuse` the first is issued with
+// .collector::a::fill and the second with .collector::a::lastuse, so the second MMA need not
+// read A from shared memory again.  Same MACs and operand statistics either way.
+__device__ __forceinline__ void mma_i8_col(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc, int mode) {
+  if (mode == 1)
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::i8.collector::a::fill [%0], %1, %2, %3, p;\n}" ::"r"(d),
+                 "l"(a), "l"(b), "r"(idesc), "r"(acc) : "memory");
+  else if (mode == 2)
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::i8.collector::a::lastuse [%0], %1, %2, %3, p;\n}" ::"r"(d),
+                 "l"(a), "l"(b), "r"(idesc), "r"(acc) : "memory");
+  else
+    mma_i8(d, a, b, idesc, acc);
+}
+
+__global__ void __launch_bounds__(128, 1) k_mma_reuse(long long iters, int a_max, int b_max, unsigned seed, int reuse) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar = sbase + kA + 2 * kB;
+  const uint32_t tmem_slot = bar + 8;
+  uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(smem + kA + 2 * kB + 8);
+  for (int i = threadIdx.x; i < (kA + 2 * kB) / 4; i += blockDim.x) {
+    const int lim = (4 * i < kA) ? a_max : b_max;
+    uint32_t w = 0;
+    for (int b = 0; b < 4; ++b) {
+      const uint32_t h = hash32(seed ^ (blockIdx.x * 0x9E3779B9u) ^ static_cast<uint32_t>(4 * i + b) * 0x85EBCA6Bu);
+      w |= (lim > 0 ? (h % static_cast<uint32_t>(lim + 1)) : 0u) << (8 * b);
+    }
+    reinterpret_cast<uint32_t*>(smem)[i] = w;
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  if (threadIdx.x < 32) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot_ptr;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = idesc_i8(128, 256, false, false);
+    for (long long it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint64_t a = umma_desc_sw128(sbase + kk * 32);
+        const uint32_t acc = (it >= 1) || kk;
+        mma_i8_col(tmem_base, a, umma_desc_sw128(sbase + kA + kk * 32), idesc, acc, reuse ? 1 : 0);
+        mma_i8_col(tmem_base + 256, a, umma_desc_sw128(sbase + kA + kB + kk * 32), idesc, acc, reuse ? 2 : 0);
+      }
+    }
+    mma_commit(bar);
+    mbar_wait(bar, 0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem_base);
+  }
+}
+
+}  // namespace
+
+extern "C" int mma_reuse_run(int blocks, long long iters, int a_max, int b_max, unsigned seed, int reuse, float* ms_out,
+                             void* stream) {
+  const int smem = kA + 2 * kB + 64 + 1024;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (cudaFuncSetAttribute(k_mma_reuse, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return 1;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, st);
+  k_mma_reuse<<<blocks, 128, smem, st>>>(iters, a_max, b_max, seed, reuse);
+  cudaEventRecord(e1, st);
+  if (cudaGetLastError() != cudaSuccess) return 2;
+  if (cudaEventSynchronize(e1) != cudaSuccess) return 3;
+  cudaEventElapsedTime(ms_out, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return 0;
+}
+
+namespace {
 }  // namespace
 
 extern "C" int mma_ceiling_run(int blocks, long long iters, int a_max, int b_max, unsigned seed, float* ms_out,
