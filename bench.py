@@ -353,11 +353,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     spec, sizes = eng.spec, eng.sizes
     stream = torch.cuda.current_stream(dev)
     d3l, ra = sizes.d3_loc, sizes.rows_A
-    fused = (d3l <= 256 and kU == 1 and not (spec.u_unsigned and spec.u_offset)
-             and os.environ.get("CTPT_SKINNY") != "off" and not args.rescale)
+    # the library's automatic kernel choice (include/ctpt.h ctpt_kernel), stage by stage
+    fused = (d3l <= 256 and kU == 1 and not (spec.u_unsigned and spec.u_offset) and not args.rescale)
     n_ev = 1 if args.rescale else len(ps)
 
-    mv = fused and d3l <= 32 and os.environ.get("CTPT_MV") != "off"
+    mv = fused and d3l <= 32
     # Split/GEMM overlap (split path): the limb split of prime l+1 runs on a side stream into the
     # other of two workspaces while prime l's GEMM runs (the split needs no shared memory and
     # little SM time, so it co-resides with the persistent GEMM); gemm(l) waits on split(l).

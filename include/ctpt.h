@@ -46,19 +46,11 @@
  *    ctpt_last_error() describes the problem.  Asynchronous CUDA faults surface as
  *    CTPT_ERR_CUDA on a later call.
  *  - Calls on distinct streams and distinct buffers may run concurrently.
- *  - Kernel-choice knobs for A/B measurements only (environment, read at every call; the
- *    defaults are the measured best): CTPT_GEMM=2cta (CTA-pair GEMM instead of single-CTA),
- *    CTPT_SKINNY=off (no fused skinny kernels), CTPT_MV=off (no raw-byte kernel for d3 ≤ 32),
- *    CTPT_FUSED_LOAD=regs|hybrid (converter register loads instead of the TMA raw ring),
- *    CTPT_FUSED2=pair (CTA-pair fused kernel for 128 < d3_loc ≤ 256; CTPT_F2_GROUPS=1|2 its
- *    converter groups), CTPT_FUSED_PF=n (L2 prefetch distance in the fused kernel),
- *    CTPT_GROUP_J=n (GEMM raster group), CTPT_GEMM_PF=n / CTPT_GEMM_PFX=n (GEMM L2 prefetch of
- *    the operands / of the X tiles), CTPT_GEMM_L2HINT=2 (U^T loads evict_last), CTPT_GEMM=mc
- *    (multicast-cluster GEMM), CTPT_GEMM_KSPLIT=n (K loop in n accumulating launches),
- *    CTPT_GEMM_MULTI=on (all k_U digits in one launch), CTPT_GEMM_EP32=0 (16-column epilogue
- *    loads), CTPT_GEMM_CS=1 (evict-first output stores), CTPT_FUSED_LOAD=tma2 (two converter
- *    groups), CTPT_LAYOUT=scalar (4-byte layout kernel).  None of them changes a result
- *    (tests/test_gpu_parity.py runs each); DESIGN.md §6 has what each measured.
+ *  - The library reads no environment variables.  Kernel choice, raster group and grid cap are
+ *    explicit ctpt_problem fields: kernel, raster_group and max_ctas.  Every choice gives the same
+ *    residues (tests/test_gpu_parity.py runs each).  Variants that were measured and lost in
+ *    round 1 (CTA-pair and multicast GEMMs, K split, L2 prefetch/hints, register-fed converters,
+ *    …) were removed; DESIGN.md §6 keeps what each measured.
  */
 #ifndef CTPT_H_
 #define CTPT_H_
@@ -83,6 +75,17 @@ typedef enum {
 } ctpt_status;
 
 typedef enum { CTPT_RLWE = 0, CTPT_SHARED_S = 1, CTPT_SHARED_A = 2, CTPT_STRUCT_A = 3 } ctpt_format;
+
+/* Which kernel path ctpt_matmul / ctpt_matmul_host run per prime (ctpt_problem.kernel).  AUTO:
+ * the raw-byte kernel k_gemm_mv when d3_loc ≤ 32, the fused skinny kernel k_gemm_fused when
+ * d3_loc ≤ 256, else the limb split + k_gemm_tc (the first two need kU = 1 and u_offset = 0).
+ * A forced choice that does not apply returns CTPT_ERR_UNSUPPORTED. */
+typedef enum {
+  CTPT_KERNEL_AUTO = 0,
+  CTPT_KERNEL_SPLIT_GEMM = 1, /* k_split[_rows] + k_gemm_tc (tcgen05, any d3, any kU)            */
+  CTPT_KERNEL_FUSED = 2,      /* k_gemm_fused: split in the GEMM's load path (d3_loc ≤ 256)       */
+  CTPT_KERNEL_MV = 3          /* k_gemm_mv: raw residue bytes × expanded U (d3_loc ≤ 32)          */
+} ctpt_kernel;
 
 /* One CP-MM problem, possibly a shard of a larger one:
  * `primes` may be any subset of the RNS basis and [col_begin, col_end) any block of U's
@@ -115,6 +118,13 @@ typedef struct {
                                own.  Applies to the split + GEMM path (d3_loc > 256, no
                                rescale, kU = 1); the workspace doubles its limb planes.
                                0: split, GEMM, split, GEMM …                                   */
+  int32_t kernel;           /* a ctpt_kernel value; 0 = CTPT_KERNEL_AUTO                       */
+  int32_t raster_group;     /* k_gemm_tc: j-tiles (128 output columns each) per raster group, so
+                               a group's U^T panels stay in L2 while the X panels stream;
+                               0: automatic (≈ 32 MB of U^T panels, at least 16)             */
+  int32_t max_ctas;         /* cap on the persistent kernels' CTA count; 0: one CTA per SM.  Set
+                               it when a concurrent kernel (e.g. an NCCL receive posted before
+                               the compute) must keep SMs of its own.         */
 } ctpt_problem;
 
 typedef struct {
@@ -134,7 +144,8 @@ typedef struct {
 /* Thread-local description of the last non-OK status (never NULL). */
 const char* ctpt_last_error(void);
 
-/* Library version / build string. */
+/* Library version / build string, including "src=<hash>": a sha256 prefix of the csrc/ and
+ * include/ sources the binary was built from (__graft_entry__.py computes the same hash). */
 const char* ctpt_version(void);
 
 /* Validate `prob` (Table 1 rules, primes, exactness bound for prob->kU; kU=0 is treated as 1)
@@ -204,8 +215,8 @@ ctpt_status ctpt_gemm(const ctpt_problem* prob, int32_t l, const void* d_ws, siz
  * (A·U mod p, B·U mod p) as ctpt_split + ctpt_gemm, but the limb split runs inside the GEMM's
  * load path, reading the int32 residues of d_ctmat exactly once (no workspace): the regime is
  * HBM-bound and this saves the split's write + re-read.  ctpt_matmul (and ctpt_matmul_host)
- * choose this kernel automatically for every prime when 32 < d3_loc ≤ 256 and kU = 1 (environment
- * CTPT_SKINNY=off disables that, for A/B measurements).  Outputs as for ctpt_gemm.
+ * choose this kernel automatically for every prime when 32 < d3_loc ≤ 256 and kU = 1
+ * (ctpt_problem.kernel overrides that).  Outputs as for ctpt_gemm.
  * CTPT_ERR_UNSUPPORTED when kU ≠ 1 or d3_loc > 256.  Never synchronises. */
 ctpt_status ctpt_gemm_fused(const ctpt_problem* prob, int32_t l, const void* d_ctmat, const void* d_plain,
                             uint32_t* d_AU_l, uint32_t* d_BU_l, void* stream);
@@ -245,7 +256,7 @@ ctpt_status ctpt_modmatmul(int32_t L, const uint32_t* primes, int64_t M, int64_t
  * U_exp (U's digits spread to byte position ℓ of every 4-byte group, built in d_ws), so every
  * limb product comes out of ONE byte-level contraction with no limb split at all; work is split
  * over K with exact int32 partials in d_ws (ws_bytes from ctpt_query_sizes).  ctpt_matmul
- * takes this kernel automatically when d3_loc ≤ 32 (CTPT_MV=off disables that).  Outputs as for
+ * takes this kernel automatically when d3_loc ≤ 32 (ctpt_problem.kernel overrides that).  Outputs as for
  * ctpt_gemm.  CTPT_ERR_UNSUPPORTED when kU ≠ 1, d3_loc > 32 or u_offset ≠ 0.  Never synchronises. */
 ctpt_status ctpt_gemm_mv(const ctpt_problem* prob, int32_t l, const void* d_ctmat, const void* d_plain,
                          uint32_t* d_AU_l, uint32_t* d_BU_l, void* d_ws, size_t ws_bytes, void* stream);

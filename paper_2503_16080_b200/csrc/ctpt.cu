@@ -13,10 +13,7 @@
 
 #include "../../include/ctpt.h"
 #include "gemm_tc.cuh"
-#include "gemm_tc2.cuh"
-#include "gemm_tc_mc.cuh"
 #include "gemm_fused.cuh"
-#include "gemm_fused2.cuh"
 #include "gemm_mv.cuh"
 #include "kernels.cuh"
 
@@ -118,6 +115,8 @@ ctpt_status check_problem(const ctpt_problem* pb, Dims& d) {
   d.j0 = c0; d.j1 = c1; d.d3_loc = c1 - c0;
   if (pb->rescale != 0 && pb->rescale != 1) return fail(CTPT_ERR_ARG, "rescale must be 0 or 1");
   if (pb->split_overlap != 0 && pb->split_overlap != 1) return fail(CTPT_ERR_ARG, "split_overlap must be 0 or 1");
+  if (pb->kernel < CTPT_KERNEL_AUTO || pb->kernel > CTPT_KERNEL_MV) return fail(CTPT_ERR_ARG, "unknown kernel choice %d", pb->kernel);
+  if (pb->raster_group < 0 || pb->max_ctas < 0) return fail(CTPT_ERR_ARG, "raster_group and max_ctas must be >= 0");
   if (pb->rescale && pb->L < 2) return fail(CTPT_ERR_ARG, "Rescale by the last prime needs L >= 2 primes");
   d.L_out = pb->rescale ? pb->L - 1 : pb->L;
   if (pb->u_unsigned) {
@@ -132,12 +131,8 @@ ctpt_status check_problem(const ctpt_problem* pb, Dims& d) {
 size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
 // The 16-byte layout kernel needs 4-row chunks that never straddle A and B (and aligned vectors):
-// rows_A and d1 multiples of 4.  CTPT_LAYOUT=scalar forces the 4-byte kernel (A/B measurements).
-bool layout_vec_ok(int64_t rows_A, int64_t d1) {
-  const char* e = getenv("CTPT_LAYOUT");
-  if (e && strcmp(e, "scalar") == 0) return false;
-  return rows_A % 4 == 0 && d1 % 4 == 0;
-}
+// rows_A and d1 multiples of 4; other shapes take the 4-byte kernel.
+bool layout_vec_ok(int64_t rows_A, int64_t d1) { return rows_A % 4 == 0 && d1 % 4 == 0; }
 
 // d_ws of ctpt_matmul / ctpt_split / ctpt_gemm, in this order:
 //   limbs   [4][R][d2p] u8                      (one prime's byte-limb planes)
@@ -302,27 +297,9 @@ ctpt_status tc_setup() {
   if (dev < 0 || dev >= kMaxDevices) return fail(CTPT_ERR_CUDA, "device ordinal %d out of range", dev);
   cudaError_t& e = errs[dev];
   std::call_once(onces[dev], [&e] {
-    e = cudaFuncSetAttribute(k_gemm_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BYTES);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_gemm_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BYTES);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_gemm_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, T2_SMEM_BYTES);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_gemm_tc_mc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BYTES);
-#define CTPT_FU_ATTR(NG, MODE) \
-    if (e == cudaSuccess)      \
-      e = cudaFuncSetAttribute(k_gemm_fused<NG, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(NG, MODE));
-    CTPT_FU_ATTR(1, FU_REGS)
-    CTPT_FU_ATTR(2, FU_REGS)
-    CTPT_FU_ATTR(1, FU_TMA)
-    CTPT_FU_ATTR(2, FU_TMA)
-    CTPT_FU_ATTR(1, FU_HYBRID)
-    CTPT_FU_ATTR(2, FU_HYBRID)
-    CTPT_FU_ATTR(1, FU_TMA2)
-    CTPT_FU_ATTR(2, FU_TMA2)
-#undef CTPT_FU_ATTR
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_fused2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, F2_SMEM_BYTES);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_fused2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, F2_SMEM_BYTES);
+    e = cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BYTES);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_fused<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(1));
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_fused<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(2));
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
@@ -348,7 +325,20 @@ struct GemmArgs {
   uint32_t p;
   OutParams o;           // accumulate / w are set per pass
   SplitJob sj;           // the next prime's limb split, run inside the first pass (sj.x = nullptr: none)
+  int raster_group;      // k_gemm_tc raster group (0: automatic)
+  int max_ctas;          // cap on the persistent grids (0: one CTA per SM)
 };
+// GemmArgs fields that come straight from the problem
+void gemm_args_from_problem(GemmArgs& g, const ctpt_problem* pb) {
+  g.raster_group = pb->raster_group;
+  g.max_ctas = pb->max_ctas;
+}
+// persistent grid size: one CTA per SM (or the caller's cap, e.g. SMs left to a concurrent
+// communication kernel), never more than the work units
+int64_t grid_cap(int max_ctas) {
+  const int sms = num_sms();
+  return max_ctas > 0 ? std::min(max_ctas, sms) : sms;
+}
 ctpt_status launch_split(const uint32_t* x, int64_t rows, int64_t d2p, void* limbs, cudaStream_t st);
 // the limb split of `rows` rows of X for prime p; in the unsigned-U mode it also writes rowcorr
 ctpt_status launch_split_prime(const ctpt_problem* pb, const uint32_t* x, int64_t rows, int64_t d2p, uint32_t p,
@@ -357,12 +347,14 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt);
 ctpt_status launch_split_job(const SplitJob& J, cudaStream_t st);
 ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st);
 
-// The skinny regime: d3_loc ≤ 256 columns and one U digit plane.  There
-// the step is HBM-bound and the fused kernel (split inside the GEMM's load path, X read once)
-// replaces split + GEMM.  CTPT_SKINNY=off forces split + GEMM (for A/B measurements).
+// Kernel choice per prime (ctpt_problem.kernel):
+//  * the skinny regime: d3_loc ≤ 256 columns and one U digit plane — the
+//    step is HBM-bound and the fused kernel (split inside the GEMM's load path, X read once)
+//    replaces split + GEMM;
+//  * the very-skinny regime (d3_loc ≤ 32): raw residue bytes straight into the MMA (gemm_mv.cuh);
+//  * otherwise the limb split + k_gemm_tc.
+// CTPT_KERNEL_AUTO takes the first that applies; a forced choice that does not apply is refused.
 constexpr int64_t kFusedMaxD3 = 256;
-// The very-skinny regime (d3_loc ≤ 32): raw residue bytes straight into the MMA (gemm_mv.cuh).
-// CTPT_MV=off falls back to the converter kernel (for A/B measurements).
 constexpr int64_t kMvMaxD3 = 32;
 int mv_nc(const Dims& d) {  // N = 4·d3p, d3p ∈ {4, 8, 16, 32}
   int d3p = 4;
@@ -394,17 +386,27 @@ MvPlan mv_plan(const Dims& d) {
   m.total = m.ticket_off + align256(static_cast<size_t>(m.tiles) * 4);
   return m;
 }
-bool mv_eligible(const Dims& d, int kU, const ctpt_problem* pb);
-
-bool fused_eligible(const Dims& d, int kU, const ctpt_problem* pb) {
-  if (kU != 1 || d.d3_loc > kFusedMaxD3 || needs_rowcorr(pb)) return false;
-  const char* e = getenv("CTPT_SKINNY");
-  return !(e && strcmp(e, "off") == 0);
+bool fused_applies(const Dims& d, int kU, const ctpt_problem* pb) {
+  return kU == 1 && d.d3_loc <= kFusedMaxD3 && !needs_rowcorr(pb);
 }
-bool mv_eligible(const Dims& d, int kU, const ctpt_problem* pb) {
-  if (!fused_eligible(d, kU, pb) || d.d3_loc > kMvMaxD3) return false;
-  const char* e = getenv("CTPT_MV");
-  return !(e && strcmp(e, "off") == 0);
+bool mv_applies(const Dims& d, int kU, const ctpt_problem* pb) { return fused_applies(d, kU, pb) && d.d3_loc <= kMvMaxD3; }
+enum class Path { SplitGemm, Fused, Mv };
+ctpt_status choose_path(const ctpt_problem* pb, const Dims& d, Path& path) {
+  const int kU = pb->kU <= 0 ? 1 : pb->kU;
+  switch (pb->kernel) {
+    case CTPT_KERNEL_SPLIT_GEMM: path = Path::SplitGemm; return CTPT_OK;
+    case CTPT_KERNEL_FUSED:
+      if (!fused_applies(d, kU, pb)) return fail(CTPT_ERR_UNSUPPORTED, "fused kernel needs kU = 1, d3_loc <= 256 and u_offset = 0");
+      path = Path::Fused;
+      return CTPT_OK;
+    case CTPT_KERNEL_MV:
+      if (!mv_applies(d, kU, pb)) return fail(CTPT_ERR_UNSUPPORTED, "raw-byte kernel needs kU = 1, d3_loc <= 32 and u_offset = 0");
+      path = Path::Mv;
+      return CTPT_OK;
+    default:
+      path = mv_applies(d, kU, pb) ? Path::Mv : fused_applies(d, kU, pb) ? Path::Fused : Path::SplitGemm;
+      return CTPT_OK;
+  }
 }
 size_t mv_ws_bytes(const Dims& d) { return mv_plan(d).total; }
 
@@ -414,7 +416,12 @@ extern "C" {
 
 const char* ctpt_last_error(void) { return g_err; }
 
-const char* ctpt_version(void) { return "ctpt 0.1 sm_100a tcgen05 kind::i8 (u8 limbs x s8 U digits)"; }
+// CTPT_SRC_HASH: sha256 prefix of csrc/ + include/ at build time (__graft_entry__.build_ctpt), so a
+// run's records show which source the loaded binary was built from.
+#ifndef CTPT_SRC_HASH
+#define CTPT_SRC_HASH "unknown"
+#endif
+const char* ctpt_version(void) { return "ctpt 0.2 sm_100a tcgen05 kind::i8 src=" CTPT_SRC_HASH; }
 
 ctpt_status ctpt_query_sizes(const ctpt_problem* pb, ctpt_sizes* out) {
   Dims d;
@@ -591,6 +598,7 @@ static ctpt_status gemm_common(const ctpt_problem* pb, int32_t l, const void* d_
   if (!d_ws || !d_plain || (!d_AU_l && d.rows_A > 0) || !d_BU_l) return fail(CTPT_ERR_ARG, "null device pointer");
   if (ws_bytes < ws_bytes_needed(pb, d)) return fail(CTPT_ERR_ARG, "workspace too small");
   GemmArgs g{};
+  gemm_args_from_problem(g, pb);
   g.limbs = ws_limbs(pb, d, const_cast<void*>(d_ws), l);
   g.u_unsigned = pb->u_unsigned;
   if (needs_rowcorr(pb)) g.o.rowcorr = ws_corr(pb, d, const_cast<void*>(d_ws), l);
@@ -675,116 +683,50 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
   }
   ctpt_status s = tc_setup();
   if (s != CTPT_OK) return s;
-  // Kernel choice.  Under the 1000 W cap the single-CTA kernel sustains more int8 ops
-  // (c3, 100 steps: 2844 TOP/s at 1395 MHz vs 2634 TOP/s at 1140 MHz for the CTA pair, which is
-  // more efficient per clock — 95 % vs 84 % of 8192 MAC/clk/SM — but draws more power per
-  // clock; profiles/r01/power_1cta_vs_2cta.txt), so it is the default; CTPT_GEMM=2cta selects
-  // the pair kernel (tests exercise both).
-  bool pair = false, mc = false;
-  if (const char* g = getenv("CTPT_GEMM")) {
-    pair = (strcmp(g, "2cta") == 0);
-    mc = (strcmp(g, "mc") == 0) && num_sms() >= 2;  // 2-CTA clusters sharing X by TMA multicast
-  }
-  const int block_j = pair ? T2_BLOCK_J : TC_BLOCK_J;
+  // (A CTA-pair kernel — cta_group::2, M = 256 — and a 2-CTA multicast cluster were measured
+  // against this single-CTA kernel under the 1000 W cap and lost: they keep the tensor pipe busier
+  // per clock but clock lower, profiles/r01/gemm_1cta_vs_2cta_final/, gemm_mc_vs_tc/; removed.)
   CUtensorMap tmU, tmX;
   s = make_tmap_u8(&tmU, g.planes, d.d2, d.d3, g.nplanes, d.d2p, d.d3 * d.d2p, TC_BLOCK_K, 128, 1);
   if (s != CTPT_OK) return s;
-  s = make_tmap_limb_tiles(&tmX, g.limbs, g.R, d.d2p, (pair || mc) ? 2 : 4);
+  s = make_tmap_limb_tiles(&tmX, g.limbs, g.R, d.d2p, 4);
   if (s != CTPT_OK) return s;
   TcParams P;
   P.R = g.R;
   P.d2 = d.d2;
   P.j_off = static_cast<int32_t>(d.j0);
-  const int32_t num_kb_all = static_cast<int32_t>((d.d2 + TC_BLOCK_K - 1) / TC_BLOCK_K);
-  // K split (single-CTA kernel): the K loop in nks consecutive launches whose epilogues accumulate
-  // mod p, so a raster group's U^T panels cover nks× more columns in the same L2 and X is re-read
-  // from DRAM nks× less often, for one extra output read + write per chunk.  CTPT_GEMM_KSPLIT=n.
-  int nks = 1;
-  if (const char* e = getenv("CTPT_GEMM_KSPLIT")) nks = std::max(1, std::min(atoi(e), num_kb_all));
-  if (pair || mc) nks = 1;
-  P.kb_off = 0;
-  P.num_kb = num_kb_all;
-  P.tiles_j = static_cast<int32_t>((d.d3_loc + block_j - 1) / block_j);
+  P.num_kb = static_cast<int32_t>((d.d2 + TC_BLOCK_K - 1) / TC_BLOCK_K);
+  P.tiles_j = static_cast<int32_t>((d.d3_loc + TC_BLOCK_J - 1) / TC_BLOCK_J);
   P.tiles_r = static_cast<int32_t>((g.R + TC_BLOCK_R - 1) / TC_BLOCK_R);
   const int64_t nt = static_cast<int64_t>(P.tiles_j) * P.tiles_r;
   if (nt > INT32_MAX) return fail(CTPT_ERR_SHAPE, "too many tiles");
   P.num_tiles = static_cast<int32_t>(nt);
-  P.group_j = pair ? T2_GROUP_J_DEFAULT : TC_GROUP_J_DEFAULT;
-  if (!pair) {
-    // keep a raster group's U^T panels within ≈ 32 MB of L2 but never below the measured best
-    // of 16 j-tiles: short-K problems (c2: 0.5 MB per panel) take every j-tile in one group, so
-    // each X panel is read from DRAM once (c2: +2.4 %; c3, c4: 16 measured best)
-    const int64_t per_panel = static_cast<int64_t>(TC_BLOCK_J) * ((num_kb_all + nks - 1) / nks) * TC_BLOCK_K;
-    const int64_t fit = (32LL << 20) / std::max<int64_t>(per_panel, 1);
-    P.group_j = static_cast<int32_t>(std::min<int64_t>(std::max<int64_t>(fit, TC_GROUP_J_DEFAULT), P.tiles_j));
-  }
+  // raster group: keep a group's U^T panels within ≈ 32 MB of L2 but never below the measured best
+  // of 16 j-tiles: short-K problems (c2: 0.5 MB per panel) take every j-tile in one group, so each
+  // X panel is read from DRAM once (c2: +2.4 %; c3, c4: 16 measured best, profiles/r01/raster_group_*)
+  const int64_t per_panel = static_cast<int64_t>(TC_BLOCK_J) * P.num_kb * TC_BLOCK_K;
+  const int64_t fit = (32LL << 20) / std::max<int64_t>(per_panel, 1);
+  P.group_j = static_cast<int32_t>(std::min<int64_t>(std::max<int64_t>(fit, TC_GROUP_J_DEFAULT), P.tiles_j));
+  if (g.raster_group > 0) P.group_j = g.raster_group;
   P.u_unsigned = g.u_unsigned;
-  if (const char* g = getenv("CTPT_GROUP_J")) P.group_j = std::max(1, atoi(g));  // tuning knob
-  P.l2_pf = 0;
-  if (const char* g = getenv("CTPT_GEMM_PF")) P.l2_pf = std::max(0, atoi(g));     // tuning knob
-  // epilogue with 32-column TMEM loads and the accumulator handed back before the last stores:
-  // c3 3.709 vs 3.694e14, 3 interleaved reps each (profiles/r01/gemm_epilogue_ld32/)
-  P.ep32 = 1;
-  if (const char* g = getenv("CTPT_GEMM_EP32")) P.ep32 = atoi(g) != 0;
-  int stream_stores = 0;
-  if (const char* g = getenv("CTPT_GEMM_CS")) stream_stores = atoi(g) != 0;       // tuning knob (measuring)
-  P.pf_x = 0;
-  if (const char* g = getenv("CTPT_GEMM_PFX")) P.pf_x = std::max(0, atoi(g));        // tuning knob (measuring)
-  P.l2_hint = 0;
-  if (const char* g = getenv("CTPT_GEMM_L2HINT")) P.l2_hint = std::max(0, atoi(g));  // tuning knob (measuring)
   P.m = m;
-  const int sms = num_sms();
-  if (mc) P.group_j = std::max(1, P.group_j / 2);  // raster groups of j-tile PAIRS, same U footprint
-  const int64_t nt_mc = static_cast<int64_t>((P.tiles_j + 1) / 2) * P.tiles_r;
-  const unsigned grid = pair ? static_cast<unsigned>(2 * std::min<int64_t>(nt, sms / 2))
-                        : mc ? static_cast<unsigned>(2 * std::min<int64_t>(nt_mc, sms / 2))
-                             : static_cast<unsigned>(std::min<int64_t>(nt, sms));
-  // k_U > 1: every digit in one launch (MULTI kernel, CTPT_GEMM_MULTI=on) instead of k_U launches
-  // that accumulate through the outputs.  Measured slower on the Rescale workload (7.9 vs 8.3e13
-  // residue-MAC/s: the tile's four digit passes keep four U^T panels per j-tile live in L2 and the
-  // extra DRAM traffic lowers the clock; with the raster group divided by k_U, 7.1e13), so the
-  // per-digit launches stay the default (profiles/r01/gemm_multi_digit/).
-  bool multi = false;
-  if (const char* e = getenv("CTPT_GEMM_MULTI"))
-    multi = strcmp(e, "on") == 0 && g.kU > 1 && g.kU <= 4 && !pair && !mc && nks == 1;
-  if (multi) {
-    P.plane = g.plane0;
-    P.ndig = g.kU;
-    for (int i = 0; i < 4; ++i) P.wdig[i] = pow2mod(8 * i, g.p);
-    P.kb_off = 0;
-    P.num_kb = num_kb_all;
-    P.o = g.o;
-    P.o.accumulate = 0;
-    P.o.w = 1;
-    P.sj = g.sj;
-    k_gemm_tc<true><<<grid, TC_THREADS, TC_SMEM_BYTES, st>>>(tmU, tmX, P);
-    CUDA_TRY(cudaGetLastError());
-    return CTPT_OK;
-  }
-  P.ndig = 1;
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(nt, grid_cap(g.max_ctas)));
+  // k_U > 1 digit planes (Rescale's real U, general Mod-PP-MM): one launch per digit whose epilogue
+  // accumulates Σ_i 2^{8i}·(digit i's product mod p) through the outputs.  (All digits in one launch
+  // with register accumulation was measured slower: the tile's k_U U^T panels crowd L2,
+  // profiles/r01/gemm_multi_digit/; removed.)
   for (int i = 0; i < g.kU; ++i) {
-    for (int kc = 0; kc < nks; ++kc) {
-      const bool first = (i == 0 && kc == 0), last = (i == g.kU - 1 && kc == nks - 1);
-      P.plane = g.plane0 + i;
-      P.kb_off = static_cast<int32_t>(static_cast<int64_t>(num_kb_all) * kc / nks);
-      P.num_kb = static_cast<int32_t>(static_cast<int64_t>(num_kb_all) * (kc + 1) / nks) - P.kb_off;
-      P.o = g.o;
-      P.o.stream_stores = stream_stores;
-      P.o.accumulate = !first;
-      P.o.w = pow2mod(8 * i, g.p);
-      if (!last) P.o.xlast = nullptr;     // Rescale on the final pass only
-      if (!first) P.o.rowcorr = nullptr;  // the unsigned-U row correction exactly once
-      P.sj = (first && !pair) ? g.sj : SplitJob{};  // the next prime's split rides on the first pass
-      if (pair)
-        k_gemm_tc2<<<grid, T2_THREADS, T2_SMEM_BYTES, st>>>(tmU, tmX, P);
-      else if (mc)
-        k_gemm_tc_mc<<<grid, TC_THREADS, TC_SMEM_BYTES, st>>>(tmU, tmX, P);
-      else
-        k_gemm_tc<false><<<grid, TC_THREADS, TC_SMEM_BYTES, st>>>(tmU, tmX, P);
-      CUDA_TRY(cudaGetLastError());
-    }
+    const bool first = i == 0, last = i == g.kU - 1;
+    P.plane = g.plane0 + i;
+    P.o = g.o;
+    P.o.accumulate = !first;
+    P.o.w = pow2mod(8 * i, g.p);
+    if (!last) P.o.xlast = nullptr;     // Rescale on the final pass only
+    if (!first) P.o.rowcorr = nullptr;  // the unsigned-U row correction exactly once
+    P.sj = first ? g.sj : SplitJob{};   // the next prime's split rides on the first pass
+    k_gemm_tc<<<grid, TC_THREADS, TC_SMEM_BYTES, st>>>(tmU, tmX, P);
+    CUDA_TRY(cudaGetLastError());
   }
-  if (pair && g.sj.x) return launch_split_job(g.sj, st);  // the pair kernel has no side split
   return CTPT_OK;
 }
 
@@ -813,58 +755,18 @@ ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st) 
   P.o.w = 1;
   // balanced persistent grid: the same number of rounds as min(nt, SMs) CTAs would take, spread
   // over as few CTAs as that needs, so no round ends with most SMs idle behind a few stragglers
-  // (an HBM-bound CTA can pull more than 1/148 of the bandwidth).  CTPT_FUSED_GRID=sms: the old grid.
-  const int64_t rounds = (nt + num_sms() - 1) / num_sms();
-  int64_t grid64 = (nt + rounds - 1) / rounds;
-  if (const char* e = getenv("CTPT_FUSED_GRID")) if (strcmp(e, "sms") == 0) grid64 = std::min<int64_t>(nt, num_sms());
-  const unsigned grid = static_cast<unsigned>(grid64);
-  // how the converters get X: TMA raw ring (default), half TMA / half register loads
-  // (CTPT_FUSED_LOAD=hybrid) or register loads only (=regs) — for A/B runs
-  int mode = FU_TMA;
-  if (const char* e = getenv("CTPT_FUSED_LOAD")) {
-    if (strcmp(e, "regs") == 0) mode = FU_REGS;
-    if (strcmp(e, "hybrid") == 0) mode = FU_HYBRID;
-    if (strcmp(e, "tma2") == 0) mode = FU_TMA2;
-  }
-  // L2 prefetch distance for the raw X ring (iterations ahead of the TMA into shared memory)
-  P.l2_prefetch = 0;  // measured: any L2 prefetch distance (2..16) lowered the fused kernel 5–35 %
-  if (const char* e = getenv("CTPT_FUSED_PF")) P.l2_prefetch = std::max(0, atoi(e));
+  // (an HBM-bound CTA can pull more than 1/148 of the bandwidth; profiles/r01/fused_balanced_grid/)
+  const int64_t cap = grid_cap(g.max_ctas);
+  const int64_t rounds = (nt + cap - 1) / cap;
+  const unsigned grid = static_cast<unsigned>((nt + rounds - 1) / rounds);
   const int ng = d.d3_loc <= 128 ? 1 : 2;
-  // 128 < d3_loc <= 256: CTPT_FUSED2=pair runs one M = 256 MMA over a CTA pair (gemm_fused2.cuh)
-  // instead of two M = 128 groups reading the same limb tile.  Measured no faster than the
-  // single-CTA kernel on c4's ciphertexts (2.05–2.22 vs 2.02–2.14 ms per launch, d3 = 129..256,
-  // profiles/r01/fused2_pair/), so the single-CTA kernel stays the default.
-  bool pair = false;
-  if (const char* e = getenv("CTPT_FUSED2")) pair = ng == 2 && mode == FU_TMA && num_sms() >= 2 && strcmp(e, "pair") == 0;
   CUtensorMap tmX;
-  s = make_tmap_2d(&tmX, x, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, d.d2p, g.R, FU_BLOCK_K,
-                   static_cast<uint32_t>(pair ? F2_ROWS : fu_raw_rows(mode)));
+  s = make_tmap_2d(&tmX, x, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, d.d2p, g.R, FU_BLOCK_K, FU_BLOCK_R);
   if (s != CTPT_OK) return s;
-  if (pair) {
-    const unsigned grid2 = static_cast<unsigned>(2 * std::min<int64_t>(nt, num_sms() / 2));
-    int cg = 2;  // converter groups (K-blocks in flight per CTA); CTPT_F2_GROUPS=1 for A/B runs
-    if (const char* e = getenv("CTPT_F2_GROUPS")) cg = atoi(e) == 1 ? 1 : 2;
-    if (cg == 2)
-      k_gemm_fused2<2><<<grid2, F2_THREADS, F2_SMEM_BYTES, st>>>(tmU, tmX, P);
-    else
-      k_gemm_fused2<1><<<grid2, F2_THREADS, F2_SMEM_BYTES, st>>>(tmU, tmX, P);
-    CUDA_TRY(cudaGetLastError());
-    return CTPT_OK;
-  }
-#define CTPT_FU_LAUNCH(NG, MODE) \
-  k_gemm_fused<NG, MODE><<<grid, FU_THREADS, fu_smem_bytes(NG, MODE), st>>>(tmU, tmX, P)
-  if (ng == 1) {
-    if (mode == FU_TMA) CTPT_FU_LAUNCH(1, FU_TMA);
-    else if (mode == FU_TMA2) CTPT_FU_LAUNCH(1, FU_TMA2);
-    else if (mode == FU_HYBRID) CTPT_FU_LAUNCH(1, FU_HYBRID);
-    else CTPT_FU_LAUNCH(1, FU_REGS);
-  } else {
-    if (mode == FU_TMA) CTPT_FU_LAUNCH(2, FU_TMA);
-    else if (mode == FU_TMA2) CTPT_FU_LAUNCH(2, FU_TMA2);
-    else if (mode == FU_HYBRID) CTPT_FU_LAUNCH(2, FU_HYBRID);
-    else CTPT_FU_LAUNCH(2, FU_REGS);
-  }
-#undef CTPT_FU_LAUNCH
+  if (ng == 1)
+    k_gemm_fused<1><<<grid, FU_THREADS, fu_smem_bytes(1), st>>>(tmU, tmX, P);
+  else
+    k_gemm_fused<2><<<grid, FU_THREADS, fu_smem_bytes(2), st>>>(tmU, tmX, P);
   CUDA_TRY(cudaGetLastError());
   return CTPT_OK;
 }
@@ -905,7 +807,7 @@ ctpt_status launch_mv(const GemmArgs& g, const uint32_t* x, void* mv_ws, cudaStr
   P.o.accumulate = 0;
   P.o.w = 1;
   const int64_t units = static_cast<int64_t>(mp.tiles) * mp.splits;
-  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(units, num_sms()));
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(units, grid_cap(g.max_ctas)));
   switch (mp.nc) {
     case 16: k_gemm_mv<16><<<grid, MV_THREADS, MV_SMEM_BYTES, st>>>(tmX, tmUe, P); break;
     case 32: k_gemm_mv<32><<<grid, MV_THREADS, MV_SMEM_BYTES, st>>>(tmX, tmUe, P); break;
@@ -931,6 +833,7 @@ ctpt_status ctpt_gemm_mv(const ctpt_problem* pb, int32_t l, const void* d_ctmat,
   if (!d_ctmat || !d_plain || (!d_AU_l && d.rows_A > 0) || !d_BU_l || !d_ws) return fail(CTPT_ERR_ARG, "null pointer");
   if (ws_bytes < ws_bytes_needed(pb, d)) return fail(CTPT_ERR_ARG, "workspace too small");
   GemmArgs g{};
+  gemm_args_from_problem(g, pb);
   g.R = d.R;
   g.d = d;
   g.kU = pb->kU <= 0 ? 1 : pb->kU;
@@ -960,6 +863,7 @@ ctpt_status ctpt_gemm_fused(const ctpt_problem* pb, int32_t l, const void* d_ctm
   if (l < 0 || l >= d.L) return fail(CTPT_ERR_ARG, "prime index %d out of range", l);
   if (!d_ctmat || !d_plain || (!d_AU_l && d.rows_A > 0) || !d_BU_l) return fail(CTPT_ERR_ARG, "null device pointer");
   GemmArgs g{};
+  gemm_args_from_problem(g, pb);
   g.limbs = nullptr;
   g.u_unsigned = pb->u_unsigned;
   g.R = d.R;
@@ -1091,9 +995,11 @@ ctpt_status ctpt_modmatmul(int32_t L, const uint32_t* primes, int64_t M, int64_t
 
 static ctpt_status matmul_impl(const ctpt_problem* pb, const Dims& d, const uint32_t* X0, const void* d_plain,
                                uint32_t* d_AU, uint32_t* d_BU, void* d_ws, size_t ws_bytes, void* stream) {
-  ctpt_status s = CTPT_OK;
-  const bool fused = fused_eligible(d, pb->kU <= 0 ? 1 : pb->kU, pb);
-  const bool mv = mv_eligible(d, pb->kU <= 0 ? 1 : pb->kU, pb);
+  Path path;
+  ctpt_status s = choose_path(pb, d, path);
+  if (s != CTPT_OK) return s;
+  const bool fused = path != Path::SplitGemm;
+  const bool mv = path == Path::Mv;
   if ((!fused || mv) && !d_ws) return fail(CTPT_ERR_ARG, "null workspace");
   if (!fused || mv || pb->rescale) {
     const size_t need = ws_bytes_needed(pb, d);
@@ -1107,6 +1013,8 @@ static ctpt_status matmul_impl(const ctpt_problem* pb, const Dims& d, const uint
   // one prime's product (fused skinny kernel, or split + limb GEMM) into the outputs `o`
   auto run = [&](int l, const OutParams& o) -> ctpt_status {
     GemmArgs g{};
+    gemm_args_from_problem(g, pb);
+  gemm_args_from_problem(g, pb);
     g.d = d;
     g.R = d.R;
     g.kU = pb->kU <= 0 ? 1 : pb->kU;
@@ -1253,6 +1161,9 @@ ctpt_status ctpt_matmul_host(const ctpt_problem* pb, const uint32_t* h_a, const 
   if (((!h_a || !h_AU) && d.rows_A > 0) || !h_b || !d_plain || !h_BU || !d_ws) return fail(CTPT_ERR_ARG, "null pointer");
   const HostPlan hp = host_plan(d, chunk_rows);
   if (ws_bytes < hp.total) return fail(CTPT_ERR_ARG, "workspace too small (%zu < %zu)", ws_bytes, hp.total);
+  Path path;
+  s = choose_path(pb, d, path);
+  if (s != CTPT_OK) return s;
   cudaStream_t sc = static_cast<cudaStream_t>(stream);
   uint8_t* w = static_cast<uint8_t*>(d_ws);
   uint32_t* in[2] = {reinterpret_cast<uint32_t*>(w), reinterpret_cast<uint32_t*>(w + hp.in_bytes)};
@@ -1279,6 +1190,7 @@ ctpt_status ctpt_matmul_host(const ctpt_problem* pb, const uint32_t* h_a, const 
   CUDA_TRY(cudaStreamWaitEvent(ss.d2h, ev_start, 0));
 
   GemmArgs g{};
+  gemm_args_from_problem(g, pb);
   g.d = d;
   g.kU = pb->kU <= 0 ? 1 : pb->kU;
   g.planes = reinterpret_cast<const int8_t*>(static_cast<const uint8_t*>(d_plain) + kHeader);
@@ -1286,8 +1198,8 @@ ctpt_status ctpt_matmul_host(const ctpt_problem* pb, const uint32_t* h_a, const 
   g.limbs = limbs;
   g.u_unsigned = pb->u_unsigned;
   if (needs_rowcorr(pb)) g.o.rowcorr = corr;
-  const bool fused = fused_eligible(d, g.kU, pb);
-  const bool mv = mv_eligible(d, g.kU, pb);
+  const bool fused = path != Path::SplitGemm;
+  const bool mv = path == Path::Mv;
 
   int64_t it = 0;
   for (int l = 0; l < d.L; ++l) {

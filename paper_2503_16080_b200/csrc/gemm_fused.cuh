@@ -7,13 +7,13 @@
 // ridge), so the schedule is built around reading X exactly once:
 //   * one tile = 64 rows of X × ALL of U's d3_loc columns (NG = ⌈d3_loc/128⌉ ≤ 2 MMA groups of
 //     M = 128 U^T rows) × the full K loop — X is never re-read;
-//   * the residues are read as int32 straight from the stacked K-major X of ctpt_layout by eight
-//     converter warps (coalesced 512-B rows, two K-blocks of loads in flight per thread), split
+//   * the residues are read as int32 straight from the stacked K-major X of ctpt_layout (TMA
+//     into a raw shared-memory ring, then LDS.128 by eight converter warps), split
 //     into their four base-2^8 digits with a PRMT byte transpose in registers and stored into the
 //     SWIZZLE_128B K-major shared-memory image the UMMA descriptor expects — no limb workspace,
 //     8 B/residue of HBM traffic saved against split + GEMM (4 B read instead of 4 + 4 + 4);
 //   * U^T tiles (≤ 256 × 128 B per K-block, L2-resident) arrive by TMA on the same stage barrier.
-// Warp roles (512 threads): w0 U TMA, w1 MMA issuer, w2 TMEM allocator, w4–7 epilogue,
+// Warp roles (512 threads): w0 U TMA, w1 MMA issuer, w2 TMEM allocator, w3 raw X TMA, w4–7 epilogue,
 // w8–15 converters.  Stage barrier `full` completes on 1 TMA arrival (+ tx bytes) and 8 converter
 // warp arrivals; converters fence their generic-proxy stores (fence.proxy.async) first.
 #pragma once
@@ -34,27 +34,17 @@ constexpr int FU_THREADS = 512;
 constexpr int FU_CONV_WARP0 = 8;
 constexpr int FU_CONV_WARPS = 8;
 constexpr int FU_ROWS_PER_WARP = FU_BLOCK_R / FU_CONV_WARPS; // 8
-// Three ways to feed the converters (template MODE):
-//   FU_REGS:   each converter thread loads its residues into registers, two K-blocks ahead;
-//   FU_TMA:    a TMA producer streams raw int32 X tiles (64 rows) into a ring of RAW stages
-//              (96–128 KB in flight per SM, no register cost), converters read them with LDS.128;
-//   FU_HYBRID: rows 0–31 of every tile through the TMA ring (32-row raw tiles, twice as many
-//              stages in the same bytes), rows 32–63 by register loads — half the raw
-//              shared-memory round trip (the kernel is bound by shared-memory bandwidth).
-//   FU_TMA2:   the TMA raw ring with TWO converter groups of 4 warps (16 rows each) taking
-//              alternate K-blocks, so two K-blocks are in conversion at once and each warp's
-//              per-iteration latency chain (barrier waits, two proxy fences) covers twice the rows;
-//              both ring lengths are even so a group always meets the same stages (parity safety).
-constexpr int FU_REGS = 0, FU_TMA = 1, FU_HYBRID = 2, FU_TMA2 = 3;
-__host__ __device__ constexpr int fu_raw_rows(int mode) { return mode == FU_HYBRID ? 32 : FU_BLOCK_R; }
-__host__ __device__ constexpr int fu_raw_bytes(int mode) { return fu_raw_rows(mode) * FU_BLOCK_K * 4; }
-__host__ __device__ constexpr int fu_stages(int ng, int mode) { return mode != FU_REGS ? 2 : (ng == 1 ? 4 : 3); }
-__host__ __device__ constexpr int fu_raw_stages(int ng, int mode) {
-  return mode == FU_REGS ? 0 : mode == FU_TMA2 ? (ng == 1 ? 4 : 2) : ((ng == 1 ? 128 : 96) * 1024) / fu_raw_bytes(mode);
-}
+// X reaches the converters through a ring of RAW shared-memory stages filled by TMA (warp 3):
+// raw int32 tiles of 64 rows × 128 residues (32 KB), 96–128 KB in flight per SM without any
+// register cost; converters read them with LDS.128.  (Measured against register loads two
+// K-blocks ahead, a half-TMA / half-register hybrid and two converter groups: the TMA ring was
+// best or tied, profiles/r01/skinny_sweep_*.jsonl, fused_tma2/; those variants were removed.)
+constexpr int FU_RAW_BYTES = FU_BLOCK_R * FU_BLOCK_K * 4;   // 32 KB
+constexpr int FU_STAGES = 2;                                 // limb stages
+__host__ __device__ constexpr int fu_raw_stages(int ng) { return ((ng == 1 ? 128 : 96) * 1024) / FU_RAW_BYTES; }
 __host__ __device__ constexpr int fu_stage_bytes(int ng) { return ng * FU_U_BYTES + FU_X_BYTES; }
-__host__ __device__ constexpr int fu_smem_bytes(int ng, int mode) {
-  return fu_stages(ng, mode) * fu_stage_bytes(ng) + fu_raw_stages(ng, mode) * fu_raw_bytes(mode) + 256 + 1024;
+__host__ __device__ constexpr int fu_smem_bytes(int ng) {
+  return FU_STAGES * fu_stage_bytes(ng) + fu_raw_stages(ng) * FU_RAW_BYTES + 256 + 1024;
 }
 
 struct FusedParams {
@@ -65,7 +55,6 @@ struct FusedParams {
   int32_t num_kb;      // ceil(d2p / 128)
   int32_t num_tiles;   // ceil(R / 64)
   int32_t u_unsigned;  // U plane is u8 (U + u_offset) instead of balanced s8 digits
-  int32_t l2_prefetch; // raw X tiles prefetched into L2 this many iterations ahead of their TMA (0: off)
   ModP m;
   OutParams o;         // d3_loc ≤ 128·NG
 };
@@ -77,17 +66,13 @@ __device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
-template <int NG, int MODE>
+template <int NG>
 __global__ void __launch_bounds__(FU_THREADS, 1)
     k_gemm_fused(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmX,
                  const __grid_constant__ FusedParams P) {
-  constexpr bool TMA_X = MODE != FU_REGS;
-  constexpr int STAGES = fu_stages(NG, MODE);
-  constexpr int RAW = fu_raw_stages(NG, MODE);
-  constexpr int RAW_BYTES = fu_raw_bytes(MODE);
-  constexpr int RAW_WARPS = MODE == FU_HYBRID ? 4 : ((MODE == FU_TMA || MODE == FU_TMA2) ? FU_CONV_WARPS : 0);
-  constexpr int CG = MODE == FU_TMA2 ? 2 : 1;  // converter groups (alternate K-blocks)
-  static_assert(STAGES % CG == 0 && (RAW == 0 || RAW % CG == 0), "ring lengths must be multiples of CG");
+  constexpr int STAGES = FU_STAGES;
+  constexpr int RAW = fu_raw_stages(NG);
+  constexpr int RAW_BYTES = FU_RAW_BYTES;
   constexpr int STAGE_BYTES = fu_stage_bytes(NG);
   constexpr int NBUF = (NG == 1) ? 2 : 1;  // accumulator buffers (NBUF·NG·256 ≤ 512 columns)
   extern __shared__ uint8_t smem_raw[];
@@ -115,7 +100,7 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmU);
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full_bar(s), 1 + FU_CONV_WARPS / CG);
+      mbar_init(full_bar(s), 1 + FU_CONV_WARPS);
       mbar_init(empty_bar(s), 1);
     }
     for (int b = 0; b < NBUF; ++b) {
@@ -124,9 +109,9 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
     }
     for (int s = 0; s < RAW; ++s) {
       mbar_init(raw_full(s), 1);
-      mbar_init(raw_empty(s), RAW_WARPS / CG);
+      mbar_init(raw_empty(s), FU_CONV_WARPS);
     }
-    if (TMA_X) tma_prefetch(&tmX);
+    tma_prefetch(&tmX);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -184,45 +169,16 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
     }
   } else if (warp == 3) {
     // ---------------------------------------------------------------- raw X TMA producer
-    if (TMA_X && lane == 0) {
+    if (lane == 0) {
       int rs = 0;
       uint32_t rphase = 0;
-      auto coords = [&](int64_t it, int32_t& c0, int32_t& c1) {
-        c1 = (static_cast<int32_t>(blockIdx.x) + static_cast<int32_t>(it / P.num_kb) * gridDim.x) * FU_BLOCK_R;
-        c0 = static_cast<int32_t>(it % P.num_kb) * FU_BLOCK_K;
-      };
-      for (int64_t it = 0; it < P.l2_prefetch && it < n_it; ++it) {
-        int32_t c0, c1;
-        coords(it, c0, c1);
-        tma_prefetch_l2_2d(&tmX, c0, c1);
-      }
       for (int64_t it = 0; it < n_it; ++it) {
         const int32_t tr = static_cast<int32_t>(blockIdx.x) + static_cast<int32_t>(it / P.num_kb) * gridDim.x;
         const int32_t kb = static_cast<int32_t>(it % P.num_kb);
-        if (P.l2_prefetch > 0 && it + P.l2_prefetch < n_it) {
-          int32_t c0, c1;
-          coords(it + P.l2_prefetch, c0, c1);
-          tma_prefetch_l2_2d(&tmX, c0, c1);
-        }
         mbar_wait(raw_empty(rs), rphase ^ 1);
         mbar_arrive_expect_tx(raw_full(rs), RAW_BYTES);
         tma_load_2d(raw_base + rs * RAW_BYTES, &tmX, raw_full(rs), kb * FU_BLOCK_K, tr * FU_BLOCK_R);
         if (++rs == RAW) { rs = 0; rphase ^= 1; }
-      }
-    } else if (!TMA_X && lane == 0 && P.l2_prefetch > 0) {
-      // register-load variant: keep the converters' upcoming tiles streaming into L2 (no shared
-      // memory used), paced by the MMA's progress through the limb stages
-      auto prefetch = [&](int64_t it) {
-        const int32_t c1 = (static_cast<int32_t>(blockIdx.x) + static_cast<int32_t>(it / P.num_kb) * gridDim.x) * FU_BLOCK_R;
-        tma_prefetch_l2_2d(&tmX, static_cast<int32_t>(it % P.num_kb) * FU_BLOCK_K, c1);
-      };
-      for (int64_t it = 0; it < P.l2_prefetch && it < n_it; ++it) prefetch(it);
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int64_t it = 0; it + P.l2_prefetch < n_it; ++it) {
-        mbar_wait(empty_bar(stage), phase ^ 1);
-        prefetch(it + P.l2_prefetch);
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp >= 4 && warp < 8) {
@@ -262,65 +218,40 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
       mbar_arrive(tempty_bar(acc));
       if (++acc == NBUF) { acc = 0; acc_phase ^= 1; }
     }
-  } else if (MODE == FU_TMA2 && warp >= FU_CONV_WARP0) {
-    // ---------------------------------------------------------------- converters, two groups
-    // group g = cw / 4 converts the K-blocks it ≡ g (mod 2); warp w = cw % 4 of a group owns
-    // rows w + 4·i (i < 16) of the 64-row tile; lane owns residues 4·lane .. 4·lane+3.
-    constexpr int WPG = FU_CONV_WARPS / 2, RPW = FU_BLOCK_R / WPG;
-    const int cw = warp - FU_CONV_WARP0;
-    const int grp = cw / WPG, w = cw % WPG;
-    for (int64_t it = grp; it < n_it; it += 2) {
-      const int rs = static_cast<int>(it % RAW);
-      const int stage = static_cast<int>(it % STAGES);
-      mbar_wait(raw_full(rs), static_cast<uint32_t>((it / RAW) & 1));
-      const uint32_t sraw = raw_base + rs * RAW_BYTES;
-      uint32_t lw[RPW][4];
-#pragma unroll
-      for (int i = 0; i < RPW; ++i) {
-        const uint4 v = lds128(sraw + (w + WPG * i) * 512 + lane * 16);
-        byte_transpose4(v.x, v.y, v.z, v.w, lw[i][0], lw[i][1], lw[i][2], lw[i][3]);
-      }
-      fence_proxy_async_smem();  // release the raw tile after its values are consumed
-      __syncwarp();
-      if (lane == 0) mbar_arrive(raw_empty(rs));
-      mbar_wait(empty_bar(stage), static_cast<uint32_t>(((it / STAGES) & 1) ^ 1));
-      const uint32_t sx = sbase + stage * STAGE_BYTES + NG * FU_U_BYTES;
-#pragma unroll
-      for (int i = 0; i < RPW; ++i) {
-        const int row = w + WPG * i;
-        const uint32_t off =
-            static_cast<uint32_t>(row) * 128u + ((((lane >> 2) ^ (row & 7)) << 4) | ((lane & 3) << 2));
-        sts32(sx + 0 * FU_BLOCK_R * 128 + off, lw[i][0]);
-        sts32(sx + 1 * FU_BLOCK_R * 128 + off, lw[i][1]);
-        sts32(sx + 2 * FU_BLOCK_R * 128 + off, lw[i][2]);
-        sts32(sx + 3 * FU_BLOCK_R * 128 + off, lw[i][3]);
-      }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(full_bar(stage));
-    }
-  } else if (MODE != FU_TMA2 && warp >= FU_CONV_WARP0) {
+  } else if (warp >= FU_CONV_WARP0) {
     // ---------------------------------------------------------------- converters (256 threads)
     // Warp cw owns rows cw + 8·i (i < 8) of every 64-row tile; lane owns residues 4·lane..4·lane+3
-    // of the K-block (one coalesced 512-B row segment per warp instruction).  Loads run two
-    // iterations ahead of the stores (registers ra / rb).
+    // of the K-block (LDS.128 of the raw tile's 512-B rows).
     const int cw = warp - FU_CONV_WARP0;
-    // this warp's 8 rows of every 64-row tile: raw-ring warps take rows [0, 8·RAW_WARPS) with
-    // stride RAW_WARPS, register warps the remaining rows with stride (8 − RAW_WARPS)
-    const bool from_raw = cw < RAW_WARPS;
-    const int rw = from_raw ? cw : cw - RAW_WARPS;                  // index within its group
-    const int rstride = from_raw ? RAW_WARPS : FU_CONV_WARPS - RAW_WARPS;
-    const int rbase = from_raw ? 0 : FU_ROWS_PER_WARP * RAW_WARPS;  // first row of its group
     int stage = 0;
     uint32_t phase = 0;
-    // store the limb words of this warp's 8 rows into the next limb stage (SWIZZLE_128B
-    // K-major: 16-B chunk c of row r at chunk position c ^ (r & 7)) and arrive on its barrier
-    auto store = [&](const uint32_t (&lw)[FU_ROWS_PER_WARP][4]) {
+    int rs = 0;
+    uint32_t rphase = 0;
+    for (int64_t it = 0; it < n_it; ++it) {
+      mbar_wait(raw_full(rs), rphase);
+      const uint32_t sraw = raw_base + rs * RAW_BYTES;
+      uint32_t lw[FU_ROWS_PER_WARP][4];
+#pragma unroll
+      for (int i = 0; i < FU_ROWS_PER_WARP; ++i) {
+        const uint4 v = lds128(sraw + (cw + FU_CONV_WARPS * i) * 512 + lane * 16);
+        byte_transpose4(v.x, v.y, v.z, v.w, lw[i][0], lw[i][1], lw[i][2], lw[i][3]);
+      }
+      // Hand the raw tile back to the TMA producer as soon as its values are CONSUMED (the
+      // byte transposes above depend on every LDS), behind a proxy fence (a generic read
+      // followed by an async-proxy write of the same bytes), and before waiting for a free limb
+      // stage — so the raw ring keeps streaming while the MMAs drain.  Releasing it right after
+      // merely issuing the LDS corrupted whole output rows intermittently (K ≥ 32 blocks).
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(raw_empty(rs));
+      if (++rs == RAW) { rs = 0; rphase ^= 1; }
+      // store the limb words of this warp's 8 rows into the next limb stage (SWIZZLE_128B
+      // K-major: 16-B chunk c of row r at chunk position c ^ (r & 7)) and arrive on its barrier
       mbar_wait(empty_bar(stage), phase ^ 1);
       const uint32_t sx = sbase + stage * STAGE_BYTES + NG * FU_U_BYTES;
 #pragma unroll
       for (int i = 0; i < FU_ROWS_PER_WARP; ++i) {
-        const int row = rbase + rw + rstride * i;
+        const int row = cw + FU_CONV_WARPS * i;
         const uint32_t off =
             static_cast<uint32_t>(row) * 128u + ((((lane >> 2) ^ (row & 7)) << 4) | ((lane & 3) << 2));
         sts32(sx + 0 * FU_BLOCK_R * 128 + off, lw[i][0]);
@@ -332,59 +263,6 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(full_bar(stage));
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
-    };
-    if (from_raw) {
-      int rs = 0;
-      uint32_t rphase = 0;
-      for (int64_t it = 0; it < n_it; ++it) {
-        mbar_wait(raw_full(rs), rphase);
-        const uint32_t sraw = raw_base + rs * RAW_BYTES;
-        uint32_t lw[FU_ROWS_PER_WARP][4];
-#pragma unroll
-        for (int i = 0; i < FU_ROWS_PER_WARP; ++i) {
-          const uint4 v = lds128(sraw + (rw + rstride * i) * 512 + lane * 16);
-          byte_transpose4(v.x, v.y, v.z, v.w, lw[i][0], lw[i][1], lw[i][2], lw[i][3]);
-        }
-        // Hand the raw tile back to the TMA producer as soon as its values are CONSUMED (the
-        // byte transposes above depend on every LDS), behind a proxy fence (a generic read
-        // followed by an async-proxy write of the same bytes), and before waiting for a free limb
-        // stage — so the raw ring keeps streaming while the MMAs drain.  Releasing it right after
-        // merely issuing the LDS corrupted whole output rows intermittently (K ≥ 32 blocks).
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(raw_empty(rs));
-        if (++rs == RAW) { rs = 0; rphase ^= 1; }
-        store(lw);
-      }
-    } else {
-      auto load = [&](int64_t it, uint4 (&r)[FU_ROWS_PER_WARP]) {
-        const int32_t tr = static_cast<int32_t>(blockIdx.x) + static_cast<int32_t>(it / P.num_kb) * gridDim.x;
-        const int64_t k = static_cast<int64_t>(it % P.num_kb) * FU_BLOCK_K + 4 * lane;
-#pragma unroll
-        for (int i = 0; i < FU_ROWS_PER_WARP; ++i) {
-          const int64_t row = static_cast<int64_t>(tr) * FU_BLOCK_R + rbase + rw + rstride * i;
-          r[i] = (row < P.R && k < P.d2p) ? __ldcs(reinterpret_cast<const uint4*>(P.x + row * P.d2p + k))
-                                          : make_uint4(0u, 0u, 0u, 0u);
-        }
-      };
-      auto convert_store = [&](const uint4 (&r)[FU_ROWS_PER_WARP]) {
-        uint32_t lw[FU_ROWS_PER_WARP][4];
-#pragma unroll
-        for (int i = 0; i < FU_ROWS_PER_WARP; ++i)
-          byte_transpose4(r[i].x, r[i].y, r[i].z, r[i].w, lw[i][0], lw[i][1], lw[i][2], lw[i][3]);
-        store(lw);
-      };
-      uint4 ra[FU_ROWS_PER_WARP], rb[FU_ROWS_PER_WARP];
-      if (n_it > 0) load(0, ra);
-      if (n_it > 1) load(1, rb);
-      for (int64_t it = 0; it < n_it; it += 2) {
-        convert_store(ra);
-        if (it + 2 < n_it) load(it + 2, ra);
-        if (it + 1 < n_it) {
-          convert_store(rb);
-          if (it + 3 < n_it) load(it + 3, rb);
-        }
-      }
     }
   }
 

@@ -83,22 +83,14 @@ struct TcParams {
   int64_t R, d2;
   int32_t j_off;      // first U column (col_begin)
   int32_t plane;      // U digit plane index (3rd TMA coordinate)
-  int32_t num_kb;     // k-blocks of 128 B this launch covers (ceil(d2 / 128) without a K split)
-  int32_t kb_off;     // first k-block of this launch (K split: the epilogue accumulates the chunks)
+  int32_t num_kb;     // k-blocks of 128 B (ceil(d2 / 128))
   int32_t tiles_j, tiles_r;
   int32_t num_tiles;
   int32_t group_j;    // tiles visited in groups of group_j j-tiles (L2 reuse of U panels)
   int32_t u_unsigned; // U plane is u8 (U + u_offset) instead of balanced s8 digits
-  int32_t l2_pf;      // prefetch the operands of the iteration this far ahead into L2 (0: off)
-  int32_t l2_hint;    // U^T loads evict_last (reused by a whole raster pass)
-  int32_t pf_x;       // X-panel L2 prefetch distance in k-blocks, issued only by the first CTA of the
-                      // group_j CTAs that share the panel (0: off)
   ModP m;
   OutParams o;
   SplitJob sj;        // the next prime's limb split (warps 2–3), or sj.x = nullptr
-  int32_t ep32;       // epilogue with 32-column TMEM loads, buffer released before the last stores
-  int32_t ndig;       // MULTI kernel: U digit planes plane .. plane + ndig − 1, all in this launch
-  uint32_t wdig[4];   // 2^{8i} mod p for digit i
 };
 
 __device__ __forceinline__ void tc_tile_coords(int32_t tile, const TcParams& P, int32_t& tj, int32_t& tr) {
@@ -110,11 +102,6 @@ __device__ __forceinline__ void tc_tile_coords(int32_t tile, const TcParams& P, 
   tr = rem / gj;
 }
 
-// MULTI = true (k_U > 1 digit planes: Rescale's real U, general Mod-PP-MM): every tile runs its K
-// loop once per digit plane into alternating TMEM buffers, and the epilogue accumulates
-// Σ_i 2^{8i}·(digit i's product mod p) in registers, storing once — instead of k_U launches that
-// each re-read the outputs.  MULTI = false is the k_U = 1 kernel, unchanged.
-template <bool MULTI>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmX,
               const __grid_constant__ TcParams P) {
@@ -156,45 +143,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      const uint64_t pol_u = l2_policy_evict_last();
-      // L2 prefetch of the (tile, k-block) iteration l2_pf ahead of the TMA loads: covers the
-      // DRAM latency of first-touch X / U panels that a 4-stage shared-memory ring cannot
-      int32_t pf_tile = blockIdx.x, pf_kb = 0;
-      auto pf_advance = [&]() {
-        if (++pf_kb == P.num_kb) { pf_kb = 0; pf_tile += gridDim.x; }
-      };
-      auto pf_issue = [&]() {
-        if (pf_tile < P.num_tiles) {
-          int32_t ptj, ptr;
-          tc_tile_coords(pf_tile, P, ptj, ptr);
-          tma_prefetch_l2_5d(&tmX, 0, 0, 0, pf_kb + P.kb_off, ptr);
-          tma_prefetch_l2_3d(&tmU, (pf_kb + P.kb_off) * TC_BLOCK_K, P.j_off + ptj * TC_BLOCK_J, P.plane);
-        }
-      };
-      for (int32_t i = 0; i < P.l2_pf; ++i) { pf_issue(); pf_advance(); }
       for (int32_t tile = blockIdx.x; tile < P.num_tiles; tile += gridDim.x) {
         int32_t tj, tr;
         tc_tile_coords(tile, P, tj, tr);
-        // the X panel of row tile tr is shared by the group's j-tiles, which run concurrently on
-        // neighbouring CTAs; the one holding the group's first j-tile streams it into L2 ahead
-        const bool pf_lead = P.pf_x > 0 && (tj % P.group_j) == 0;
-        if (pf_lead)
-          for (int32_t kb = 0; kb < P.pf_x && kb < P.num_kb; ++kb) tma_prefetch_l2_5d(&tmX, 0, 0, 0, kb + P.kb_off, tr);
-        for (int32_t dg = 0; dg < (MULTI ? P.ndig : 1); ++dg)
         for (int32_t kb = 0; kb < P.num_kb; ++kb) {
-          if (P.l2_pf > 0) { pf_issue(); pf_advance(); }
-          if (pf_lead && kb + P.pf_x < P.num_kb)
-            tma_prefetch_l2_5d(&tmX, 0, 0, 0, kb + P.pf_x + P.kb_off, tr);
           mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t su = sbase + stage * TC_STAGE_BYTES;
           mbar_arrive_expect_tx(full_bar(stage), TC_STAGE_BYTES);
-          const int32_t kg = kb + P.kb_off;
-          const int32_t plane = P.plane + (MULTI ? dg : 0);
-          if (P.l2_hint)
-            tma_load_3d_hint(su, &tmU, full_bar(stage), kg * TC_BLOCK_K, P.j_off + tj * TC_BLOCK_J, plane, pol_u);
-          else
-            tma_load_3d(su, &tmU, full_bar(stage), kg * TC_BLOCK_K, P.j_off + tj * TC_BLOCK_J, plane);
-          tma_load_5d(su + TC_U_BYTES, &tmX, full_bar(stage), 0, 0, 0, kg, tr);  // one 32-KB limb tile
+          tma_load_3d(su, &tmU, full_bar(stage), kb * TC_BLOCK_K, P.j_off + tj * TC_BLOCK_J, P.plane);
+          tma_load_5d(su + TC_U_BYTES, &tmX, full_bar(stage), 0, 0, 0, kb, tr);  // one 32-KB limb tile
           if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -207,8 +164,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int32_t tile = blockIdx.x; tile < P.num_tiles; tile += gridDim.x)
-      for (int32_t dg = 0; dg < (MULTI ? P.ndig : 1); ++dg) {
+      for (int32_t tile = blockIdx.x; tile < P.num_tiles; tile += gridDim.x) {
         mbar_wait(tempty_bar(acc), acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * TC_ACC_COLS;
@@ -232,52 +188,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else if (warp == 2 || warp == 3) {
     // ---------------------------------------------------------------- next prime's limb split
     if (P.sj.x) side_split_rows(P.sj, 2 * static_cast<int64_t>(blockIdx.x) + (warp - 2), 2 * static_cast<int64_t>(gridDim.x), lane);
-  } else if (MULTI && warp >= 4) {
-    // ---------------------------------------------------------------- epilogue, k_U digits
-    const int quad = warp & 3;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int32_t tile = blockIdx.x; tile < P.num_tiles; tile += gridDim.x) {
-      int32_t tj, tr;
-      tc_tile_coords(tile, P, tj, tr);
-      const int64_t j = static_cast<int64_t>(tj) * TC_BLOCK_J + quad * 32 + lane;
-      uint32_t sum[TC_BLOCK_R];  // Σ_i w_i·(digit i's product mod p), this thread's 64 outputs
-      for (int32_t dg = 0; dg < P.ndig; ++dg) {
-        mbar_wait(tfull_bar(acc), acc_phase);
-        tc_fence_after();
-        const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * TC_ACC_COLS;
-        const uint32_t w = P.wdig[dg];
-#pragma unroll
-        for (int c = 0; c < TC_BLOCK_R / 16; ++c) {
-          uint32_t v0[16], v1[16], v2[16], v3[16];
-          tmem_ld16(t_row + 0 * TC_BLOCK_R + c * 16, v0);
-          tmem_ld16(t_row + 1 * TC_BLOCK_R + c * 16, v1);
-          tmem_ld16(t_row + 2 * TC_BLOCK_R + c * 16, v2);
-          tmem_ld16(t_row + 3 * TC_BLOCK_R + c * 16, v3);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const uint32_t r = recombine_mod(static_cast<int32_t>(v0[i]), static_cast<int32_t>(v1[i]),
-                                             static_cast<int32_t>(v2[i]), static_cast<int32_t>(v3[i]), P.m);
-            sum[c * 16 + i] = dg == 0 ? r : accum_mod(sum[c * 16 + i], r, w, P.m);
-          }
-        }
-        tc_fence_before();
-        mbar_arrive(tempty_bar(acc));  // the buffer is free as soon as it is read
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-      }
-      if (j < P.o.d3_loc) {
-#pragma unroll
-        for (int c = 0; c < TC_BLOCK_R / 16; ++c) {
-          uint32_t res[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) res[i] = sum[c * 16 + i];
-          store16(P.o, P.m, j, static_cast<int64_t>(tr) * TC_BLOCK_R + c * 16, res);
-        }
-      }
-    }
-  } else if (!MULTI && warp >= 4) {
-    // ---------------------------------------------------------------- epilogue (128 threads)
+  } else {
+    // ---------------------------------------------------------------- epilogue (warps 4–7)
     const int quad = warp & 3;  // TMEM lanes [32·quad, 32·quad + 32)
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -288,52 +200,31 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tc_fence_after();
       const int64_t j = static_cast<int64_t>(tj) * TC_BLOCK_J + quad * 32 + lane;
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * TC_ACC_COLS;
-      if (P.ep32) {  // two halves of 32 rows: 4 × 32-column TMEM loads each (default; CTPT_GEMM_EP32=0: the 16-column loop)
+      // two halves of 32 rows: four 32-column TMEM loads (one per limb) each; the accumulator is
+      // handed back to the MMA warp as soon as the last loads have landed, before the last stores
+      // (c3 3.709 vs 3.694e14 against 16-column loads, profiles/r01/gemm_epilogue_ld32/)
 #pragma unroll 1
-        for (int h = 0; h < TC_BLOCK_R / 32; ++h) {
-          uint32_t v0[32], v1[32], v2[32], v3[32];
-          tmem_ld32(t_row + 0 * TC_BLOCK_R + h * 32, v0);
-          tmem_ld32(t_row + 1 * TC_BLOCK_R + h * 32, v1);
-          tmem_ld32(t_row + 2 * TC_BLOCK_R + h * 32, v2);
-          tmem_ld32(t_row + 3 * TC_BLOCK_R + h * 32, v3);
-          tmem_ld_wait();
-          if (h == TC_BLOCK_R / 32 - 1) {  // every column read: hand the buffer back before storing
-            tc_fence_before();
-            mbar_arrive(tempty_bar(acc));
-          }
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            uint32_t res[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i)
-              res[i] = recombine_mod(static_cast<int32_t>(v0[q * 16 + i]), static_cast<int32_t>(v1[q * 16 + i]),
-                                     static_cast<int32_t>(v2[q * 16 + i]), static_cast<int32_t>(v3[q * 16 + i]), P.m);
-            if (j < P.o.d3_loc) store16(P.o, P.m, j, static_cast<int64_t>(tr) * TC_BLOCK_R + h * 32 + q * 16, res);
-          }
-        }
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-        continue;
-      }
-#pragma unroll 1
-      for (int c = 0; c < TC_BLOCK_R / 16; ++c) {
-        uint32_t v0[16], v1[16], v2[16], v3[16];
-        tmem_ld16(t_row + 0 * TC_BLOCK_R + c * 16, v0);
-        tmem_ld16(t_row + 1 * TC_BLOCK_R + c * 16, v1);
-        tmem_ld16(t_row + 2 * TC_BLOCK_R + c * 16, v2);
-        tmem_ld16(t_row + 3 * TC_BLOCK_R + c * 16, v3);
+      for (int h = 0; h < TC_BLOCK_R / 32; ++h) {
+        uint32_t v0[32], v1[32], v2[32], v3[32];
+        tmem_ld32(t_row + 0 * TC_BLOCK_R + h * 32, v0);
+        tmem_ld32(t_row + 1 * TC_BLOCK_R + h * 32, v1);
+        tmem_ld32(t_row + 2 * TC_BLOCK_R + h * 32, v2);
+        tmem_ld32(t_row + 3 * TC_BLOCK_R + h * 32, v3);
         tmem_ld_wait();
-        uint32_t res[16];
+        if (h == TC_BLOCK_R / 32 - 1) {
+          tc_fence_before();
+          mbar_arrive(tempty_bar(acc));
+        }
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-          res[i] = recombine_mod(static_cast<int32_t>(v0[i]), static_cast<int32_t>(v1[i]),
-                                 static_cast<int32_t>(v2[i]), static_cast<int32_t>(v3[i]), P.m);
-        if (j < P.o.d3_loc) {
-          const int64_t r0 = static_cast<int64_t>(tr) * TC_BLOCK_R + c * 16;
-          store16(P.o, P.m, j, r0, res);
+        for (int q = 0; q < 2; ++q) {
+          uint32_t res[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            res[i] = recombine_mod(static_cast<int32_t>(v0[q * 16 + i]), static_cast<int32_t>(v1[q * 16 + i]),
+                                   static_cast<int32_t>(v2[q * 16 + i]), static_cast<int32_t>(v3[q * 16 + i]), P.m);
+          if (j < P.o.d3_loc) store16(P.o, P.m, j, static_cast<int64_t>(tr) * TC_BLOCK_R + h * 32 + q * 16, res);
         }
       }
-      tc_fence_before();
-      mbar_arrive(tempty_bar(acc));
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }

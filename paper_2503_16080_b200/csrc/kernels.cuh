@@ -317,7 +317,6 @@ struct OutParams {
   // Unsigned-U mode (planes hold U' = U + u_offset ≥ 0): X·U = X·U' − u_offset·Σ_k X[r][k], so
   // the epilogue subtracts rowcorr[r] = u_offset·Σ_k X[r][k] mod p (nullptr: nothing to subtract).
   const uint32_t* rowcorr;
-  int32_t stream_stores;  // 1: st.global.cs (evict-first) for the 16-byte output stores
 };
 
 __device__ __forceinline__ uint32_t* out_ptr(const OutParams& o, int64_t j, int64_t r) {
@@ -405,13 +404,8 @@ __device__ __forceinline__ void store16(const OutParams& o, const ModP& m, int64
         res[4 * i + 3] = rescale_last(res[4 * i + 3], x.w, o, m);
       }
     }
-    if (o.stream_stores) {  // write-once outputs: evict-first, so they do not push operands out of L2
 #pragma unroll
-      for (int i = 0; i < 4; ++i) __stcs(q + i, make_uint4(res[4 * i], res[4 * i + 1], res[4 * i + 2], res[4 * i + 3]));
-    } else {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) q[i] = make_uint4(res[4 * i], res[4 * i + 1], res[4 * i + 2], res[4 * i + 3]);
-    }
+    for (int i = 0; i < 4; ++i) q[i] = make_uint4(res[4 * i], res[4 * i + 1], res[4 * i + 2], res[4 * i + 3]);
   } else {
 #pragma unroll
     for (int i = 0; i < 16; ++i)

@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("CTPT_LIB") or os.path.join(_HERE, "libctpt.so")  # CT
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "ctpt.h")
 
 RLWE, SHARED_S, SHARED_A, STRUCT_A = 0, 1, 2, 3
+KERNEL_AUTO, KERNEL_SPLIT_GEMM, KERNEL_FUSED, KERNEL_MV = 0, 1, 2, 3  # ctpt_kernel
 STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_SHAPE", 3: "ERR_MODULUS", 4: "ERR_OVERFLOW", 5: "ERR_RANGE",
           6: "ERR_UNSUPPORTED", 7: "ERR_CUDA"}
 
@@ -39,7 +40,8 @@ class Problem(ctypes.Structure):
                 ("d2", ctypes.c_int64), ("d3", ctypes.c_int64), ("primes", ctypes.POINTER(ctypes.c_uint32)),
                 ("col_begin", ctypes.c_int64), ("col_end", ctypes.c_int64), ("kU", ctypes.c_int32),
                 ("plain_per_prime", ctypes.c_int32), ("rescale", ctypes.c_int32),
-                ("u_unsigned", ctypes.c_int32), ("u_offset", ctypes.c_int32), ("split_overlap", ctypes.c_int32)]
+                ("u_unsigned", ctypes.c_int32), ("u_offset", ctypes.c_int32), ("split_overlap", ctypes.c_int32),
+                ("kernel", ctypes.c_int32), ("raster_group", ctypes.c_int32), ("max_ctas", ctypes.c_int32)]
 
 
 class Sizes(ctypes.Structure):
@@ -98,6 +100,12 @@ def version() -> str:
     return _lib.ctpt_version().decode()
 
 
+def source_hash() -> str:
+    """The src=<hash> the loaded library was built with (see __graft_entry__.source_hash)."""
+    v = version()
+    return v.split("src=", 1)[1].split()[0] if "src=" in v else "unknown"
+
+
 @dataclass
 class Spec:
     """A CP-MM problem (or shard): format, ring degree, dims, primes, U column block."""
@@ -115,12 +123,15 @@ class Spec:
     u_unsigned: int = 0
     u_offset: int = 0
     split_overlap: int = 0
+    kernel: int = KERNEL_AUTO
+    raster_group: int = 0
+    max_ctas: int = 0
 
     def cstruct(self) -> Problem:
         arr = (ctypes.c_uint32 * len(self.primes))(*[int(p) for p in self.primes])
         pb = Problem(self.fmt, len(self.primes), self.N, self.d1, self.d2, self.d3, arr, self.col_begin,
                      self.col_end, self.kU, self.plain_per_prime, self.rescale, self.u_unsigned,
-                     self.u_offset, self.split_overlap)
+                     self.u_offset, self.split_overlap, self.kernel, self.raster_group, self.max_ctas)
         pb._keep = arr  # keep the host prime array alive with the struct
         return pb
 

@@ -13,14 +13,15 @@ NTHREADS = os.cpu_count() or 8
 
 
 def run_gpu(fmt, N, d1, d2, d3, primes, a_polys, b_polys, U=None, Ures=None, col_begin=0, col_end=0, simt=False,
-            validate=True, rescale=0, unsigned="auto", split_overlap=0):
+            validate=True, rescale=0, unsigned="auto", split_overlap=0, kernel=0, raster_group=0, max_ctas=0):
     import torch
 
     from paper_2503_16080_b200 import ctpt
     from paper_2503_16080_b200.engine import CpmmEngine
 
     eng = CpmmEngine(ctpt.Spec(fmt, N, d1, d2, d3, list(primes), col_begin, col_end, rescale=rescale,
-                               split_overlap=split_overlap), "cuda")
+                               split_overlap=split_overlap, kernel=kernel, raster_group=raster_group,
+                               max_ctas=max_ctas), "cuda")
     eng.layout(a_polys, b_polys, validate=validate)
     if Ures is not None:
         eng.precompute_rns(Ures)

@@ -111,7 +111,7 @@ def _decrypt_and_decode(c, ps, AUc, BUc, U, cols, a_polys_sa=None):
     return worst
 
 
-def _run_config(name, primes_per_call, n_random, dec_cols):
+def _run_config(name, primes_per_call, n_random, dec_cols, split_overlap=0):
     import torch
 
     c = ctgen.CONFIGS[name]
@@ -124,7 +124,8 @@ def _run_config(name, primes_per_call, n_random, dec_cols):
     for l0 in range(0, c.L, primes_per_call):
         ps = ps_all[l0:l0 + primes_per_call]
         ct = ctgen.encrypt(c.fmt, c.N, c.d1, c.d2, c.seed, c.log_delta, ps, nthreads=NTHREADS)
-        (AU, BU), eng = run_gpu(c.fmt, c.N, c.d1, c.d2, c.d3, ps, ct.a_polys, ct.b_polys, U=U, validate=True)
+        (AU, BU), eng = run_gpu(c.fmt, c.N, c.d1, c.d2, c.d3, ps, ct.a_polys, ct.b_polys, U=U, validate=True,
+                                split_overlap=split_overlap)
         del eng
         torch.cuda.empty_cache()
         for i, p in enumerate(ps):
@@ -144,9 +145,12 @@ def test_config3_full_size():
     _run_config("c3", primes_per_call=3, n_random=65536, dec_cols=_dec_cols(c.d3))
 
 
-def test_config4_full_size():
+@pytest.mark.parametrize("split_overlap", [0, 1])
+def test_config4_full_size(split_overlap):
+    """split_overlap = 1 is the launch configuration bench.py times for c4 (d3 <= 8192): primes
+    1..3 are split inside the previous prime's k_gemm_tc (ctpt_gemm_next's kernel)."""
     c = ctgen.CONFIGS["c4"]
-    _run_config("c4", primes_per_call=4, n_random=65536, dec_cols=_dec_cols(c.d3))
+    _run_config("c4", primes_per_call=4, n_random=65536, dec_cols=_dec_cols(c.d3), split_overlap=split_overlap)
 
 
 def test_config3a_struct_a_full_size():
@@ -160,7 +164,7 @@ def test_config5_full_size():
     _run_config("c5", primes_per_call=1, n_random=65536, dec_cols=_dec_cols(c.d3))
 
 
-def test_config4_skinny_sweep_full_size(monkeypatch):
+def test_config4_skinny_sweep_full_size():
     """SURVEY.md §8(f) row 1 at full size: config c4's ciphertexts (shared-s, N = 8192,
     d1 = d2 = 32768, R = 65536; one prime) times a U with d3_loc ∈ {1, 64, 128, 256} — Table 4's
     d3 values and CP-Mv — through ctpt_matmul, which takes the fused skinny
@@ -171,7 +175,6 @@ def test_config4_skinny_sweep_full_size(monkeypatch):
 
     from paper_2503_16080_b200 import ctpt
 
-    monkeypatch.delenv("CTPT_SKINNY", raising=False)
     c = ctgen.CONFIGS["c4"]
     ps = ctgen.primes(1)
     p = ps[0]
@@ -262,3 +265,23 @@ def test_config3_rescale_full_size():
         approx = np.array([float(v) for v in cen]) / 2.0 ** c.log_delta
         worst = max(worst, np.abs(approx - mu[:, ci]).max() / np.abs(mu).max())
     assert worst <= 1e-6, worst
+
+
+@pytest.mark.slow
+def test_config3_prime0_every_entry():
+    """Config c3 (the headline workload) at full size, prime 0: EVERY entry of A·U (4096 × 16384)
+    and B·U (16384 × 16384) against the oracle's schoolbook ("every entry if the
+    host's oracle time allows": 5.5e12 residue MACs, ≈ 5 min on 16 host cores), in the bench's
+    launch configuration (limb split + k_gemm_tc, u8 U plane)."""
+    c = ctgen.CONFIGS["c3"]
+    ps = ctgen.primes(c.L)[:1]
+    ct = ctgen.encrypt(c.fmt, c.N, c.d1, c.d2, c.seed, c.log_delta, ps, nthreads=NTHREADS)
+    U = ctgen.U_matrix(c.seed, c.d2, c.d3, c.u_bound, nthreads=NTHREADS)
+    (AU, BU), eng = run_gpu(c.fmt, c.N, c.d1, c.d2, c.d3, ps, ct.a_polys, ct.b_polys, U=U)
+    assert eng.spec.u_unsigned == 1  # the bench's plane mode (the GEMM regime)
+    Ac, Bc = colmajor_views(c.fmt, c.N, c.d1, c.d2, ct.a_polys[0], ct.b_polys[0])
+    wa = oracle.modmatmul(Ac, U, ps[0], nthreads=NTHREADS)
+    assert np.array_equal(AU[0], wa), f"A·U: {np.count_nonzero(AU[0] != wa)} entries differ"
+    del wa
+    wb = oracle.modmatmul(Bc, U, ps[0], nthreads=NTHREADS)
+    assert np.array_equal(BU[0], wb), f"B·U: {np.count_nonzero(BU[0] != wb)} entries differ"

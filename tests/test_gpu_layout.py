@@ -1,8 +1,8 @@
 """GPU parity of the format layout (ctpt_layout): the stacked K-major
 X = [A; B] the library writes must equal the oracle's format matrices (P:45–71, P:1071,
 reading Q18) entry by entry, zero padded to d2p columns — through the 16-byte kernel
-(k_layout_v4, rows_A and d1 multiples of 4) and the 4-byte kernel (CTPT_LAYOUT=scalar, and
-every shape whose 4-row chunks would straddle A and B)."""
+(k_layout_v4, rows_A and d1 multiples of 4) and the 4-byte kernel k_layout (every shape whose
+4-row chunks would straddle A and B: rows_A or d1 not a multiple of 4)."""
 import os
 import sys
 
@@ -42,18 +42,13 @@ def _expected(fmt, N, d1, d2, ct, L, d2p):
     return np.stack(out)
 
 
-@pytest.mark.parametrize("kernel", ["default", "scalar"])
 @pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "f%d_N%d_k%d_d2%d_L%d" % s)
-def test_layout_matches_oracle(shape, kernel, monkeypatch):
+def test_layout_matches_oracle(shape):
     import torch
 
     from paper_2503_16080_b200 import ctpt
     from paper_2503_16080_b200.engine import CpmmEngine
 
-    if kernel == "scalar":
-        monkeypatch.setenv("CTPT_LAYOUT", "scalar")
-    else:
-        monkeypatch.delenv("CTPT_LAYOUT", raising=False)
     fmt, N, k, d2, L = shape
     d1 = N * k
     ps = ctgen.primes(L)
@@ -67,17 +62,13 @@ def test_layout_matches_oracle(shape, kernel, monkeypatch):
     assert np.array_equal(got, want), np.argwhere(got != want)[:5]
 
 
-@pytest.mark.parametrize("kernel", ["default", "scalar"])
-def test_layout_validate_flags_out_of_range(kernel, monkeypatch):
+@pytest.mark.parametrize("N", [64, 2])  # 16-byte kernel; 4-byte kernel (rows_A = 2)
+def test_layout_validate_flags_out_of_range(N):
     """validate = 1: a residue ≥ its prime anywhere (A part, B part, last prime) → ERR_RANGE."""
     from paper_2503_16080_b200 import ctpt
     from paper_2503_16080_b200.engine import CpmmEngine
 
-    if kernel == "scalar":
-        monkeypatch.setenv("CTPT_LAYOUT", "scalar")
-    else:
-        monkeypatch.delenv("CTPT_LAYOUT", raising=False)
-    fmt, N, k, d2, L = A, 64, 2, 100, 2
+    fmt, k, d2, L = A, 2, 100, 2
     ps = ctgen.primes(L)
     for where in ("a", "b"):
         ct = ctgen.encrypt(fmt, N, N * k, d2, 0, 20, ps)

@@ -20,6 +20,7 @@ from gpu_helpers import NTHREADS, U_residues, oracle_outputs, run_gpu  # noqa: E
 pytestmark = pytest.mark.gpu
 
 R, S, A, SA = ctgen.RLWE, ctgen.SHARED_S, ctgen.SHARED_A, ctgen.STRUCT_A
+AUTO, SPLIT_GEMM, FUSED, MV_K = 0, 1, 2, 3  # ctpt_problem.kernel (include/ctpt.h ctpt_kernel)
 
 SHAPES = [
     # fmt, N, k, d2, d3, L  — several tiles + ragged tails in every dimension
@@ -40,14 +41,15 @@ SHAPES = [
 
 
 def _check(fmt, N, k, d2, d3, L, seed=0, u_bound=8, simt=False, col_begin=0, col_end=0, unsigned="auto",
-           U=None, split_overlap=0):
+           U=None, split_overlap=0, kernel=AUTO, raster_group=0, max_ctas=0):
     d1 = N * k
     ps = ctgen.primes(L)
     ct = ctgen.encrypt(fmt, N, d1, d2, seed, 20, ps, nthreads=NTHREADS)
     if U is None:
         U = ctgen.U_matrix(seed, d2, d3, u_bound)
     (AU, BU), eng = run_gpu(fmt, N, d1, d2, d3, ps, ct.a_polys, ct.b_polys, U=U, simt=simt, col_begin=col_begin,
-                            col_end=col_end, unsigned=unsigned, split_overlap=split_overlap)
+                            col_end=col_end, unsigned=unsigned, split_overlap=split_overlap, kernel=kernel,
+                            raster_group=raster_group, max_ctas=max_ctas)
     c1 = col_end or d3
     cols = np.arange(col_begin, c1)
     for l, p in enumerate(ps):
@@ -56,40 +58,30 @@ def _check(fmt, N, k, d2, d3, L, seed=0, u_bound=8, simt=False, col_begin=0, col
         assert np.array_equal(BU[l], wb), f"B·U mismatch prime {l}: {np.argwhere(BU[l] != wb)[:5]}"
 
 
-@pytest.fixture(params=["1cta", "2cta", "mc", "fused"])
-def gemm_kernel(request, monkeypatch):
-    """Force the single-CTA (k_gemm_tc), CTA-pair (k_gemm_tc2) or multicast-cluster (k_gemm_tc_mc)
-    tensor-core kernel after a separate split (CTPT_SKINNY=off), or leave ctpt_matmul's default,
-    which takes the fused skinny kernel (k_gemm_fused) whenever d3_loc <= 256 and kU = 1."""
-    if request.param == "fused":
-        monkeypatch.delenv("CTPT_SKINNY", raising=False)
-    else:
-        monkeypatch.setenv("CTPT_SKINNY", "off")
-        monkeypatch.setenv("CTPT_GEMM", request.param)
-    return request.param
+@pytest.fixture(params=["split_gemm", "auto"])
+def gemm_kernel(request):
+    """ctpt_problem.kernel: force the limb split + the tcgen05 GEMM k_gemm_tc, or leave
+    ctpt_matmul's automatic choice (the raw-byte kernel at d3_loc <= 32, the fused skinny kernel
+    at d3_loc <= 256 when kU = 1 and u_offset = 0, else split + GEMM)."""
+    return SPLIT_GEMM if request.param == "split_gemm" else AUTO
 
 
 @pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "f%d_N%d_k%d_d2%d_d3%d_L%d" % s)
 def test_shapes_tcgen05(shape, gemm_kernel):
-    if gemm_kernel == "fused" and shape[4] > 256:
-        pytest.skip("d3 > 256 never takes the fused kernel")
-    _check(*shape, unsigned="never")
+    _check(*shape, unsigned="never", kernel=gemm_kernel)
 
 
 @pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "f%d_N%d_k%d_d2%d_d3%d_L%d" % s)
 def test_shapes_unsigned_U(shape, gemm_kernel):
     """The unsigned-U plane (U + u_offset as u8, u8 × u8 MMAs, row-sum correction in the
-    epilogue) through both tensor-core kernels; the fused kernel only takes it with offset 0."""
-    if gemm_kernel == "fused":
-        pytest.skip("u_offset != 0 never takes the fused kernel")
-    _check(*shape, unsigned="always")
+    epilogue); with u_offset != 0 the automatic choice is always split + GEMM."""
+    _check(*shape, unsigned="always", kernel=gemm_kernel)
 
 
 @pytest.mark.parametrize("lo,hi", [(-128, 127), (0, 255), (3, 200), (-1, 0), (0, 0)])
-def test_unsigned_U_ranges(lo, hi, monkeypatch):
+def test_unsigned_U_ranges(lo, hi):
     """u_offset = max(0, −min U) for every admissible span, incl. offset 0 (no correction; the
     fused skinny kernel then runs u8 × u8) and U = 0."""
-    monkeypatch.delenv("CTPT_SKINNY", raising=False)
     rng = np.random.default_rng(hi - lo)
     for d3 in (100, 300):
         U = rng.integers(lo, hi + 1, (260, d3)).astype(np.int64)
@@ -133,8 +125,8 @@ def test_unsigned_U_max_d2_bound():
 
 
 def test_column_shard_both_kernels(gemm_kernel):
-    _check(S, 128, 2, 160, 600, 1, col_begin=37, col_end=591)
-    _check(A, 64, 3, 300, 600, 2, col_begin=300, col_end=555)  # d3_loc = 255: fused when allowed
+    _check(S, 128, 2, 160, 600, 1, col_begin=37, col_end=591, kernel=gemm_kernel)
+    _check(A, 64, 3, 300, 600, 2, col_begin=300, col_end=555, kernel=gemm_kernel)  # d3_loc = 255: fused when auto
 
 
 # ------------------------------------------------------------------ skinny regime (§8(f) row 1)
@@ -153,40 +145,21 @@ SKINNY = [
 ]
 
 
-def _fused_load(monkeypatch, load):
-    """'tma' = the default (raw X ring, single CTA), 'tma2' = the raw X ring with two converter
-    groups on alternate K-blocks (single CTA), 'pair' = the raw X ring with d3_loc > 128 on the
-    CTA-pair kernel k_gemm_fused2 (CTPT_FUSED2=pair), 'regs' / 'hybrid' = the register-load feeds."""
-    monkeypatch.setenv("CTPT_FUSED_LOAD", "tma" if load == "pair" else load)
-    if load == "pair":
-        monkeypatch.setenv("CTPT_FUSED2", "pair")
-    else:
-        monkeypatch.delenv("CTPT_FUSED2", raising=False)
-
-
-@pytest.mark.parametrize("load", ["tma", "tma2", "pair", "regs", "hybrid"])
 @pytest.mark.parametrize("shape", SKINNY, ids=lambda s: "f%d_N%d_k%d_d2%d_d3%d_L%d" % s)
-def test_skinny_fused(shape, load, monkeypatch):
-    """Every way of feeding the fused kernel's converters: raw X tiles by TMA (single CTA, or the
-    CTA pair for d3 > 128), or register loads (CTPT_MV=off keeps d3 <= 32 on the converter kernel too)."""
-    monkeypatch.delenv("CTPT_SKINNY", raising=False)
-    monkeypatch.setenv("CTPT_MV", "off")
-    _fused_load(monkeypatch, load)
-    _check(*shape)
+def test_skinny_fused(shape):
+    """The fused kernel forced (kernel = FUSED) on every skinny width, d3 <= 32 included (which the
+    automatic choice gives to the raw-byte kernel), and the automatic choice on the same shapes."""
+    _check(*shape, kernel=FUSED)
+    _check(*shape, seed=1)
 
 
-@pytest.mark.parametrize("groups", ["1", "2"])
 @pytest.mark.parametrize("cols", [(0, 129), (20, 220), (44, 300), (171, 300)])
-def test_skinny_pair_column_shards(cols, groups, monkeypatch):
-    """k_gemm_fused2 on column blocks [c0, c1) of a wider U (129..256 columns: the pair's second
-    CTA holds U^T rows j_off + 128.. — partly past the block and, for (171, 300), past d3), with
-    ragged R (not a multiple of the 64-row pair tile) and more pairs than tiles."""
-    monkeypatch.delenv("CTPT_SKINNY", raising=False)
-    monkeypatch.setenv("CTPT_FUSED2", "pair")
-    monkeypatch.setenv("CTPT_FUSED_LOAD", "tma")
-    monkeypatch.setenv("CTPT_F2_GROUPS", groups)  # converter groups: K-blocks in flight per CTA
-    _check(A, 64, 3, 333, 300, 2, col_begin=cols[0], col_end=cols[1], seed=5)
-    _check(S, 512, 9, 300, 300, 1, col_begin=cols[0], col_end=cols[1], seed=6)  # R = 9216: 144 tiles
+def test_skinny_column_shards(cols):
+    """k_gemm_fused on column blocks [c0, c1) of a wider U (129..256 columns: the second MMA group
+    holds U^T rows j_off + 128.. — partly past the block and, for (171, 300), past d3), with ragged R
+    (not a multiple of the 64-row tile) and more CTAs than tiles."""
+    _check(A, 64, 3, 333, 300, 2, col_begin=cols[0], col_end=cols[1], seed=5, kernel=FUSED)
+    _check(S, 512, 9, 300, 300, 1, col_begin=cols[0], col_end=cols[1], seed=6, kernel=FUSED)  # R = 9216: 144 tiles
 
 
 MV = [
@@ -206,21 +179,18 @@ MV = [
 
 
 @pytest.mark.parametrize("shape", MV, ids=lambda s: "f%d_N%d_k%d_d2%d_d3%d_L%d" % s)
-def test_mv_raw_bytes(shape, monkeypatch):
-    monkeypatch.delenv("CTPT_SKINNY", raising=False)
-    monkeypatch.delenv("CTPT_MV", raising=False)
-    _check(*shape)
+def test_mv_raw_bytes(shape):
+    _check(*shape, kernel=MV_K)
     _check(*shape, seed=1)  # the tickets were left at zero for the next launch
 
 
-def test_mv_column_shard_and_entry_point(monkeypatch):
+def test_mv_column_shard_and_entry_point():
     """A 1..32-column block [col_begin, col_end) of a wider U through ctpt_gemm_mv, per prime."""
     import torch
 
     from paper_2503_16080_b200 import ctpt
     from paper_2503_16080_b200.engine import CpmmEngine
 
-    monkeypatch.delenv("CTPT_MV", raising=False)
     fmt, N, k, d2, d3, L = A, 64, 4, 700, 300, 2
     d1 = N * k
     ps = ctgen.primes(L)
@@ -241,13 +211,10 @@ def test_mv_column_shard_and_entry_point(monkeypatch):
             assert np.array_equal(AUn[l], wa) and np.array_equal(BUn[l], wb), (c0, c1, l)
 
 
-@pytest.mark.parametrize("load", ["tma", "tma2", "pair", "regs", "hybrid"])
-def test_skinny_long_k_ring_wraparound(load, monkeypatch):
+def test_skinny_long_k_ring_wraparound():
     """Long K (33–65 k-blocks per tile) wraps the raw-X and limb rings many times; a premature
     release of a raw tile once corrupted whole output rows intermittently — run it repeatedly."""
-    monkeypatch.delenv("CTPT_SKINNY", raising=False)
-    _fused_load(monkeypatch, load)
-    for rep in range(3):
+    for rep in range(5):
         _check(A, 256, 2, 4112, 64, 1, seed=rep)
         _check(S, 128, 3, 8200, 100, 1, seed=rep)
         _check(R, 512, 1, 4096, 256, 1, seed=rep)
@@ -285,12 +252,10 @@ def test_skinny_fused_direct_entry_point():
 
 
 @pytest.mark.parametrize("d3", [130, 20])
-def test_skinny_adversarial_residues(d3, monkeypatch):
+def test_skinny_adversarial_residues(d3):
     """The fused split (d3 = 130) and the raw-byte kernel (d3 = 20, K split into exact partials)
     on residues 0, 1, (p±1)/2, p−1, p−2 with U digits at −128 / 127 and d2 = 65536 (the int32
     exactness limit) — C_ℓ reaches ±d2·255·128."""
-    monkeypatch.delenv("CTPT_SKINNY", raising=False)
-    monkeypatch.delenv("CTPT_MV", raising=False)
     fmt, N, d2 = R, 64, 65536
     ps = ctgen.primes(1)
     p = ps[0]
@@ -308,8 +273,7 @@ def test_skinny_adversarial_residues(d3, monkeypatch):
     assert np.array_equal(AU[0], wa) and np.array_equal(BU[0], wb)
 
 
-def test_multi_digit_U_pair_kernel(monkeypatch):
-    monkeypatch.setenv("CTPT_GEMM", "2cta")
+def test_multi_digit_U_two_digits():
     fmt, N, k, d2, d3 = A, 64, 2, 256, 300
     d1 = N * k
     ps = ctgen.primes(1)
@@ -509,14 +473,17 @@ def test_config1_full_and_decrypt():
     assert np.abs(approx - MU).max() <= np.abs(U).max() * c.d2 * 20.5 / 2.0 ** c.log_delta
 
 
-def test_config2_full():
+@pytest.mark.parametrize("split_overlap", [0, 1])
+def test_config2_full(split_overlap):
     """Config c2 (RLWE, N = d = 4096, two primes): every output entry vs the oracle, plus the
-    decryption identity and the 1e-6 decode bound on sampled columns."""
+    decryption identity and the 1e-6 decode bound on sampled columns.  split_overlap = 1 is the
+    launch configuration bench.py times for c2 (d3 <= 8192): prime 1 is split inside prime 0's
+    k_gemm_tc."""
     c = ctgen.CONFIGS["c2"]
     ps = ctgen.primes(c.L)
     ct = ctgen.encrypt(c.fmt, c.N, c.d1, c.d2, c.seed, c.log_delta, ps, nthreads=NTHREADS)
     U = ctgen.U_matrix(c.seed, c.d2, c.d3, c.u_bound, nthreads=NTHREADS)
-    (AU, BU), _ = run_gpu(c.fmt, c.N, c.d1, c.d2, c.d3, ps, ct.a_polys, ct.b_polys, U=U)
+    (AU, BU), _ = run_gpu(c.fmt, c.N, c.d1, c.d2, c.d3, ps, ct.a_polys, ct.b_polys, U=U, split_overlap=split_overlap)
     for l, p in enumerate(ps):
         wa, wb = oracle_outputs(c.fmt, c.N, c.d1, ct.a_polys[l], ct.b_polys[l], U, p)
         assert np.array_equal(AU[l], wa), "A·U mismatch"
@@ -603,16 +570,8 @@ def _rescale_check(fmt, N, k, d2, d3, L, ukind, seed=21):
 
 
 @pytest.mark.parametrize("case", RESCALE, ids=lambda s: "f%d_N%d_k%d_d2%d_d3%d_L%d_%s" % s)
-def test_rescale_fused_epilogue(case, monkeypatch):
-    monkeypatch.delenv("CTPT_SKINNY", raising=False)
+def test_rescale_fused_epilogue(case):
     _rescale_check(*case)
-
-
-def test_rescale_pair_kernel(monkeypatch):
-    monkeypatch.setenv("CTPT_GEMM", "2cta")
-    monkeypatch.setenv("CTPT_SKINNY", "off")
-    _rescale_check(S, 32, 2, 200, 300, 3, "real")
-    _rescale_check(R, 64, 1, 64, 100, 2, "int")
 
 
 # ------------------------------------------------------------------ Mod-PP-MM entry point (§8(f) row 4)
@@ -651,7 +610,7 @@ def test_modmatmul_full_residues(M, K, Nc, L):
 # ------------------------------------------------------------------ CUDA graph capture
 @pytest.mark.parametrize("shape", [(R, 64, 1, 64, 64, 1), (A, 64, 3, 300, 20, 2), (S, 32, 2, 200, 300, 2)],
                          ids=["c1_fused", "mv", "split_gemm"])
-def test_matmul_is_graph_capturable(shape, monkeypatch):
+def test_matmul_is_graph_capturable(shape):
     """ctpt_matmul never synchronises or allocates, so a CUDA graph can capture it (every kernel
     path: fused, raw-byte with its memset + U expansion, split + GEMM) and replay it: the replayed
     outputs equal the oracle, and a replay after changing the inputs in place recomputes them."""
@@ -660,7 +619,6 @@ def test_matmul_is_graph_capturable(shape, monkeypatch):
     from paper_2503_16080_b200 import ctpt
     from paper_2503_16080_b200.engine import CpmmEngine
 
-    monkeypatch.delenv("CTPT_MV", raising=False)
     fmt, N, k, d2, d3, L = shape
     d1 = N * k
     ps = ctgen.primes(L)
@@ -745,27 +703,24 @@ def test_struct_a_algorithm7_with_rescale():
 
 
 # ------------------------------------------------------------------ split of prime l+1 inside GEMM l
-@pytest.mark.parametrize("kernel", ["1cta", "2cta", "mc"])
 @pytest.mark.parametrize("unsigned", ["never", "always"])
-def test_split_overlap_matmul(kernel, unsigned, monkeypatch):
+def test_split_overlap_matmul(unsigned):
     """ctpt_problem.split_overlap = 1: ctpt_matmul splits prime 0 on its own and every further
-    prime inside the previous prime's GEMM (warps 2–3 of k_gemm_tc; the CTA-pair kernel falls back
-    to a standalone split after its GEMM), alternating two limb buffers — L = 3 and 4 primes, the
-    u8 plane with its row correction and the s8 plane, multi-digit U (side split in pass 0 only)."""
+    prime inside the previous prime's GEMM (warps 2–3 of k_gemm_tc), alternating two limb buffers
+    — L = 3 and 4 primes, the u8 plane with its row correction and the s8 plane, multi-digit U
+    (side split in pass 0 only)."""
     import torch
 
     from paper_2503_16080_b200 import ctpt
     from paper_2503_16080_b200.engine import CpmmEngine
 
-    monkeypatch.setenv("CTPT_SKINNY", "off")
-    monkeypatch.setenv("CTPT_GEMM", kernel)
     for (fmt, N, k, d2, d3, L, ub) in [(A, 64, 3, 300, 260, 3, 8), (S, 32, 4, 129, 300, 4, 8),
                                         (R, 256, 1, 200, 140, 2, 300)]:
         d1 = N * k
         ps = ctgen.primes(L)
         ct = ctgen.encrypt(fmt, N, d1, d2, 21, 20, ps)
         U = ctgen.U_matrix(21, d2, d3, ub)
-        eng = CpmmEngine(ctpt.Spec(fmt, N, d1, d2, d3, ps, split_overlap=1), "cuda")
+        eng = CpmmEngine(ctpt.Spec(fmt, N, d1, d2, d3, ps, split_overlap=1, kernel=SPLIT_GEMM), "cuda")
         eng.layout(ct.a_polys, ct.b_polys)
         eng.precompute(U, unsigned=unsigned if ub <= 127 else "never")
         AU, BU = eng.matmul()
@@ -776,7 +731,7 @@ def test_split_overlap_matmul(kernel, unsigned, monkeypatch):
             assert np.array_equal(AUn[l], wa) and np.array_equal(BUn[l], wb), (fmt, l)
 
 
-def test_split_overlap_stage_entry_points(monkeypatch):
+def test_split_overlap_stage_entry_points():
     """The per-stage form a benchmark times: ctpt_split(0), then ctpt_gemm_next(l) per prime;
     ctpt_gemm_next refuses a problem without split_overlap."""
     import torch
@@ -784,7 +739,6 @@ def test_split_overlap_stage_entry_points(monkeypatch):
     from paper_2503_16080_b200 import ctpt
     from paper_2503_16080_b200.engine import CpmmEngine
 
-    monkeypatch.delenv("CTPT_GEMM", raising=False)
     fmt, N, k, d2, d3, L = A, 128, 2, 520, 400, 3
     d1 = N * k
     ps = ctgen.primes(L)
@@ -829,50 +783,35 @@ def _fuzz_cases(n=48, seed=2025):
 
 
 @pytest.mark.parametrize("case", _fuzz_cases(), ids=lambda c: "f%d_N%d_k%d_d2%d_d3%d_L%d_u%d_c%d-%d_%d" % c)
-def test_fuzz_shapes_against_oracle(case, monkeypatch):
+def test_fuzz_shapes_against_oracle(case):
     """Seeded random problems across every dimension regime the library dispatches on (d3_loc ≤ 32
     raw-byte kernel, ≤ 256 fused kernel, else split + GEMM; k_U = 1..3 digits; s8 or u8 U
-    planes; column shards; d2 from 1; N from 2; every other case with split_overlap = 1) — each
-    output entry against the oracle."""
-    for var in ("CTPT_SKINNY", "CTPT_MV", "CTPT_GEMM", "CTPT_FUSED_LOAD", "CTPT_FUSED2", "CTPT_LAYOUT"):
-        monkeypatch.delenv(var, raising=False)
+    planes; column shards; d2 from 1; N from 2; every other case with split_overlap = 1; every
+    third case with split + GEMM forced) — each output entry against the oracle."""
     fmt, N, k, d2, d3, L, ub, c0, c1, i = case
-    _check(fmt, N, k, d2, d3, L, seed=100 + i, u_bound=ub, col_begin=c0, col_end=c1, split_overlap=i % 2)
+    _check(fmt, N, k, d2, d3, L, seed=100 + i, u_bound=ub, col_begin=c0, col_end=c1, split_overlap=i % 2,
+           kernel=SPLIT_GEMM if i % 3 == 0 else AUTO)
 
 
-@pytest.mark.parametrize("ksplit", ["2", "3"])
-def test_gemm_k_split_accumulates(ksplit, monkeypatch):
-    """CTPT_GEMM_KSPLIT: the limb GEMM's K loop in consecutive launches whose epilogues accumulate
-    mod p — with the unsigned-U row correction (applied once), multi-digit U (k_U passes × K
-    chunks), the in-kernel split of the next prime, and Rescale on the last pass only."""
-    monkeypatch.setenv("CTPT_GEMM_KSPLIT", ksplit)
-    monkeypatch.setenv("CTPT_SKINNY", "off")
-    monkeypatch.delenv("CTPT_GEMM", raising=False)
-    _check(A, 64, 3, 700, 300, 2, unsigned="always", seed=41)
-    _check(S, 32, 2, 1000, 260, 3, u_bound=300, seed=42, split_overlap=1)
-    _check(R, 256, 1, 129, 300, 1, seed=43)  # fewer k-blocks than chunks on some launches
+@pytest.mark.parametrize("raster_group,max_ctas", [(1, 0), (3, 0), (1000, 0), (0, 1), (0, 7), (5, 3)])
+def test_raster_group_and_grid_cap_keep_results_exact(raster_group, max_ctas):
+    """ctpt_problem.raster_group (k_gemm_tc's tile order) and max_ctas (the persistent grids' CTA
+    cap, for SMs left to a concurrent NCCL kernel) change the schedule, never a residue — in the
+    split + GEMM, fused and raw-byte regimes, with the next prime's split inside the GEMM."""
+    _check(A, 64, 3, 700, 300, 2, seed=51, raster_group=raster_group, max_ctas=max_ctas, split_overlap=1)
+    _check(S, 32, 4, 520, 100, 1, seed=52, raster_group=raster_group, max_ctas=max_ctas)
+    _check(S, 256, 4, 4112, 8, 1, seed=53, raster_group=raster_group, max_ctas=max_ctas)
 
 
-@pytest.mark.parametrize("knob", ["CTPT_GEMM_PF=4", "CTPT_GEMM_PFX=4", "CTPT_GEMM_L2HINT=2", "CTPT_GROUP_J=3", "CTPT_GEMM_EP32=0", "CTPT_GEMM_CS=1",
-                                  "CTPT_GEMM=mc", "CTPT_LAYOUT=scalar", "CTPT_FUSED_LOAD=hybrid"])
-def test_measurement_knobs_keep_results_exact(knob, monkeypatch):
-    """Every A/B knob the measurements used (include/ctpt.h) leaves the residues bit-exact: L2
-    prefetch of the GEMM's operands or of the X tiles, U^T eviction hints, another raster group,
-    the multicast-cluster GEMM, the 4-byte layout kernel, the hybrid converter feed."""
-    name, val = knob.split("=")
-    monkeypatch.setenv(name, val)
-    for var in ("CTPT_SKINNY", "CTPT_MV"):
-        monkeypatch.delenv(var, raising=False)
-    _check(A, 64, 3, 700, 300, 2, seed=51)  # split + GEMM regime
-    _check(S, 32, 4, 520, 100, 1, seed=52)  # fused skinny regime
+def test_forced_kernel_refusals():
+    """A forced kernel that does not apply is refused (ERR_UNSUPPORTED), never silently replaced."""
+    from paper_2503_16080_b200 import ctpt
 
-
-def test_multi_digit_single_launch_knob(monkeypatch):
-    """CTPT_GEMM_MULTI=on: all k_U digit planes in one k_gemm_tc<true> launch, the epilogue
-    accumulating Σ 2^{8i}·(digit i's product) in registers — k_U = 2 and 3, with the in-kernel
-    split of the next prime."""
-    monkeypatch.setenv("CTPT_GEMM_MULTI", "on")
-    monkeypatch.setenv("CTPT_SKINNY", "off")
-    monkeypatch.delenv("CTPT_GEMM", raising=False)
-    _check(A, 64, 3, 400, 300, 2, u_bound=300, seed=61, split_overlap=1)   # k_U = 2
-    _check(S, 32, 2, 300, 260, 1, u_bound=40000, seed=62)                 # k_U = 3
+    fmt, N, d2 = R, 64, 100
+    ps = ctgen.primes(1)
+    ct = ctgen.encrypt(fmt, N, N, d2, 0, 20, ps)
+    U = ctgen.U_matrix(0, d2, 300, 8)
+    with pytest.raises(ctpt.CtptError, match="ERR_UNSUPPORTED"):
+        run_gpu(fmt, N, N, d2, 300, ps, ct.a_polys, ct.b_polys, U=U, kernel=FUSED)
+    with pytest.raises(ctpt.CtptError, match="ERR_UNSUPPORTED"):
+        run_gpu(fmt, N, N, d2, 40, ps, ct.a_polys, ct.b_polys, U=U[:, :40], kernel=MV_K)

@@ -74,14 +74,6 @@ def main():
         BU = torch.empty(sz.out_BU_bytes // 4, dtype=torch.int32, device="cuda")
         ra = sz.rows_A
         for path in args.paths.split(","):
-            # fused (TMA raw ring), fused-regs (register loads), fused-regs-pf<N> / fused-pf<N>
-            # (L2 prefetch N iterations ahead)
-            os.environ["CTPT_FUSED_LOAD"] = ("regs" if path.startswith("fused-regs") else
-                                             "hybrid" if path.startswith("fused-hybrid") else "tma")
-            if "-pf" in path:
-                os.environ["CTPT_FUSED_PF"] = path.split("-pf")[1]
-            else:
-                os.environ.pop("CTPT_FUSED_PF", None)
 
             def step(evs=None):
                 for l in range(len(ps)):
