@@ -27,6 +27,7 @@ import subprocess
 import sys
 import tempfile
 import time
+import types
 
 import numpy as np
 
@@ -36,6 +37,10 @@ sys.path.insert(0, ROOT)
 METRIC = "ct-pt matmul residue-MACs/s at d=16384 and % of B200 dense INT8 TC peak"
 UNIT = "residue-MAC/s"
 INT8_DATASHEET_MACS = 2.25e15  # dense INT8 4.5 POPS, in MAC/s
+# configs whose device-resident single-problem step does not fit one GPU (c5: 68.7 GB of laid-out
+# inputs + 68.7 GB of outputs + the raw ciphertexts during layout): even at N = 1 they run as
+# per-prime units with the primes streamed sequentially (BASELINE.json configs[4])
+STREAMED_CONFIGS = {"c5"}
 
 
 def parse():
@@ -62,13 +67,17 @@ def parse():
                     help="Algorithm 6 with step 2 (SURVEY.md §8(f) row 3): U real uniform[-1,1) encoded at "
                          "Δ_U = the last prime (per-prime residues, kU = 4), RNS Rescale by that prime "
                          "fused into the other primes' epilogues")
-    ap.add_argument("--shard", action="store_true",
-                    help="strong scaling: shard ONE problem's (prime, column) units over the ranks "
-                         "(shard.plan_units); host-resident inputs/outputs via ctpt_matmul_host")
-    ap.add_argument("--gather", default="host", choices=["host", "ipc"],
-                    help="with --shard: 'host' = host-resident streaming (ctpt_matmul_host); 'ipc' = "
-                         "device-resident units whose GEMM epilogues write straight into rank 0's "
-                         "gathered output through peer (IPC) mappings — the fused compute + gather")
+    ap.add_argument("--mode", default="auto", choices=["auto", "strong", "weak"],
+                    help="auto: ONE problem strong-scaled over the ranks (N > 1, or a config whose inputs and "
+                         "outputs do not fit one device-resident problem, i.e. c5: the primes stream through "
+                         "per-prime units); at N = 1 the device-resident single-problem step.  strong: always "
+                         "the per-unit sharded path.  weak: every rank runs its own independent problem "
+                         "(no data-path collective)")
+    ap.add_argument("--gather", default="auto", choices=["auto", "ipc", "nccl"],
+                    help="strong mode, N > 1: how the units' outputs reach rank 0 inside the timed region. "
+                         "ipc = the GEMM epilogues store into rank 0's buffers through CUDA IPC peer mappings "
+                         "(NVLink); nccl = point-to-point, rank 0 posts its receives before computing; auto = ipc "
+                         "when every rank's GPU has peer access to rank 0's, else nccl")
     return ap.parse_args()
 
 
@@ -80,6 +89,17 @@ def peaks():
         return mp, "measured"
     except OSError:
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def config_for(c, world: int, mode: str) -> dict:
+    """The `config` object of the JSON line — the same for our arm and the reference (oracle) arm:
+    the workload, its L2 footprint and the parallelism."""
+    l2 = c.L * c.R * ((c.d2 + 15) // 16 * 16) * 4
+    par = {"strong": f"strong: ONE problem's (prime, U-column) units sharded over {world} GPU(s) "
+                     f"(shard.plan_units), outputs gathered into rank 0 inside the timed region",
+           "weak": f"weak: {world} independent problem(s), one per GPU, no data-path collective"}[mode]
+    return dict(workload_desc(c), l2=f"inputs {l2 / 2**30:.2f} GiB per step > 126 MB L2 (no flush needed)",
+                parallelism=par)
 
 
 def workload_desc(c) -> dict:
@@ -97,11 +117,14 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu_index: int):
+    def __init__(self, dev):
+        """dev: the torch CUDA device whose clocks to sample — selected by UUID, since NVML's indices
+        need not follow CUDA's device order (CUDA_VISIBLE_DEVICES, PCI ordering)."""
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        gid = gpu_uuid_of(dev) or str(getattr(dev, "index", dev) or 0)
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                       "-lms", "100", "-i", str(gpu_index)], stdout=self.f, stderr=subprocess.DEVNULL)
+                                       "-lms", "100", "-i", gid], stdout=self.f, stderr=subprocess.DEVNULL)
         except OSError:
             self.p = None
 
@@ -250,7 +273,14 @@ def make_inputs(c, seed: int, nthreads: int):
 
 
 # ------------------------------------------------------------------------------------ reference arm
-def run_reference(args, rank: int):
+def arm_mode(args, world: int) -> str:
+    """'strong' or 'weak': the parallelism both arms report (main() dispatches on the same rule)."""
+    return "weak" if args.mode == "weak" else "strong"
+
+
+def run_reference(args, rank: int, world: int = 1):
+    """The reference arm: the CPU oracle as it stands on the host cores, rank 0 only (the other
+    ranks exit without work), on a bounded sample of the same workload and the same `config`."""
     import ctgen
 
     if rank != 0:
@@ -273,7 +303,7 @@ def run_reference(args, rank: int):
         v = M * K * cores / t
         print(json.dumps({
             "impl": "reference", "metric": "Mod-PP-MM residue-MACs/s (full residues both sides, 16384^3 x 3 primes)",
-            "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "u128 (schoolbook residues)", "data": "synthetic", "config": {"workload": "modmm"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
@@ -282,7 +312,10 @@ def run_reference(args, rank: int):
         return
     c = ctgen.CONFIGS[args.config]
     cores = os.cpu_count() or 1
-    ps, ct, U, _ = make_inputs(c, c.seed, cores)
+    ps = ctgen.primes(c.L)
+    # only prime 0's ciphertexts: the sample never touches the others (c5: 8.6 GB instead of 69 GB)
+    ct = ctgen.encrypt(c.fmt, c.N, c.d1, c.d2, c.seed, c.log_delta, ps[:1], nthreads=cores)
+    U = ctgen.U_matrix(c.seed, c.d2, c.d3, c.u_bound, nthreads=cores)
     import oracle
 
     p = ps[0]
@@ -312,17 +345,20 @@ def run_reference(args, rank: int):
     sample = (f"per step: prime 0, {ncols} of {c.d3} output columns x all {c.R} stacked rows x d2={c.d2} "
               f"({macs:.3e} residue-MACs)")
     print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": arm_mode(args, world),
         "vs_baseline": None, "dtype": "u128 (schoolbook residues)", "data": "synthetic",
-        "config": workload_desc(c),
+        "config": config_for(c, world, arm_mode(args, world)),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
 
 # ------------------------------------------------------------------------------------ our arm
-def run_ours(args, rank: int, world: int, local_rank: int):
+def run_ours(args, rank: int, world: int, local_rank: int, scaling: str = "strong"):
+    """The device-resident single-problem step (every prime in one ctpt_problem): at N = 1 the
+    default (the strong-scaling curve's N = 1 point); with --mode weak every rank runs its own
+    independent problem (seed = rank), no data-path collective."""
     import torch
 
     import ctgen
@@ -437,7 +473,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize(dev)
-    clk = ClockSampler(local_rank)
+    clk = ClockSampler(dev)
     time.sleep(0.3)  # let the sampler start
     t_start.record(stream)
     if overlap:
@@ -500,17 +536,15 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     gemm_share = sum(gemm_ms) / elapsed_ms
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "int8", "data": "synthetic",
         # per-step device times (the paper reports the mean of 10 runs)
         "step_ms_stats": {"mean": statistics.mean(step_ms), "median": statistics.median(step_ms),
                           "min": min(step_ms), "max": max(step_ms)},
-        "config": dict(workload_desc(c), **{
-            "l2": f"inputs {sizes.ctmat_bytes * 1.0 / 2**30:.2f} GiB per step > 126 MB L2 (no flush needed)",
-            "parallelism": f"weak: {world} independent problem(s), one per GPU, no data-path collective",
-            "kU": kU, "limb_macs_per_residue_mac": 4 * kU,
-            "u_plane": (f"u8: U+{eng.spec.u_offset} (ctpt_plain_precompute_unsigned)" if eng.spec.u_unsigned
-                        else "s8 balanced digits")}),
+        "config": config_for(c, world, scaling),
+        "kernel_config": {"kU": kU, "limb_macs_per_residue_mac": 4 * kU,
+                          "u_plane": (f"u8: U+{eng.spec.u_offset} (ctpt_plain_precompute_unsigned)" if eng.spec.u_unsigned
+                                      else "s8 balanced digits")},
         "pct_int8_datasheet": 100.0 * value * 4 * kU / world / INT8_DATASHEET_MACS,
         "rescale": bool(args.rescale),
         "vs_cublaslt_int8": cublaslt_ratio(value * 4 * kU / world, elapsed_ms),
@@ -639,16 +673,6 @@ def roofline_fused(c, d3l, launch_s, share, mp, which, kernel="k_gemm_fused"):
             "avg_launch_ms": launch_s * 1e3, "share_of_step": share}
 
 
-def host_launches(c, n_units: int, kU: int, spec_is_split: bool) -> int:
-    """Kernels ctpt_matmul_host launches per call for n_units one-prime units: per row chunk
-    (R/6 rounded up to 64, the library default) k_layout + (k_split[_rows] + kU × k_gemm_tc, or one
-    fused kernel)."""
-    chunk = ((c.R + 5) // 6 + 63) // 64 * 64
-    n_chunks = (c.R + chunk - 1) // chunk
-    per_chunk = 1 + ((1 + kU) if spec_is_split else 1)
-    return n_units * n_chunks * per_chunk
-
-
 def pcie_bandwidth(dev, nbytes: int = 1 << 30) -> dict:
     """Pinned host<->device copy bandwidth (GB/s): each direction alone and both at once on
     two streams — the floor of the e2e path, whose every step moves its inputs and outputs."""
@@ -735,189 +759,352 @@ def run_e2e(args, c, ps, ct, eng, dev, stream, world: int = 1):
                     "(3 streams) -> pinned host outputs"}
 
 
-def run_sharded(args, rank: int, world: int, local_rank: int):
-    """One problem (e.g. c5: 8 primes, 68.7 GB of ciphertexts) sharded over the ranks by
-    (prime, U-column) units; each rank streams its units from pinned host
-    memory through ctpt_matmul_host (a 1-GPU run streams the primes sequentially) and leaves
-    its output blocks in host memory (the sharded result; shard.run_and_gather is the NCCL
-    gather for device-resident outputs).  Device time, max over ranks; "scaling": "strong"."""
+def gpu_uuid_of(dev) -> str | None:
+    """nvidia-smi id of the CUDA device `dev` (its UUID: NVML indices need not follow CUDA's order)."""
     import torch
+
+    try:
+        return f"GPU-{torch.cuda.get_device_properties(dev).uuid}"
+    except (RuntimeError, AttributeError):
+        return None
+
+
+def kernel_path(d3_loc: int, kU: int, u_unsigned: int, u_offset: int) -> str:
+    """The library's automatic kernel choice for one prime (include/ctpt.h ctpt_kernel)."""
+    if kU == 1 and d3_loc <= 256 and not (u_unsigned and u_offset):
+        return "mv" if d3_loc <= 32 else "fused"
+    return "split_gemm"
+
+
+def launch_unit(spec_u, eng, au, bu, stream, ev=None):
+    """One (prime, column-block) unit through the stage entry points: the limb split + k_gemm_tc
+    (ev brackets the GEMM), or the fused / raw-byte kernel (ev brackets it).  Returns #launches."""
+    from paper_2503_16080_b200 import ctpt
+
+    sz = eng.unit_sizes[(spec_u.col_begin, spec_u.col_end)]
+    path = kernel_path(sz.d3_loc, spec_u.kU, spec_u.u_unsigned, spec_u.u_offset)
+    if path == "split_gemm":
+        ctpt.split(spec_u, 0, eng.ctmat, eng.ws, stream=stream)
+    if ev is not None:
+        ev[0].record(stream)
+    if path == "mv":
+        ctpt.gemm_mv(spec_u, 0, eng.ctmat, eng.plain, au, bu, eng.ws, stream=stream)
+    elif path == "fused":
+        ctpt.gemm_fused(spec_u, 0, eng.ctmat, eng.plain, au, bu, stream=stream)
+    else:
+        ctpt.gemm(spec_u, 0, eng.ws, eng.plain, au, bu, stream=stream)
+    if ev is not None:
+        ev[1].record(stream)
+    return (1 + spec_u.kU) if path == "split_gemm" else (2 if path == "mv" else 1)
+
+
+def run_strong(args, rank: int, world: int, local_rank: int):
+    """ONE problem strong-scaled over the ranks: the (prime, U-column) units of
+    shard.plan_units (whole primes when world | L, else prime-major column slices), each rank's
+    inputs device-resident (one laid-out X per prime it needs, prime by prime), and the GATHER of
+    every unit's (A·U, B·U) block into rank 0's [L][d3][rows] buffers INSIDE the timed region:
+    ipc = the GEMM epilogues store straight into rank 0's buffers through CUDA IPC mappings opened
+    on each rank's own device (NVLink / NVSwitch peer stores, overlapped tile by tile with the
+    MMAs); nccl = rank 0 posts every receive before computing its own units, senders isend each
+    unit as soon as it is computed.  One step = every rank's units + the gather; timed with CUDA
+    events on each rank from a barrier to its last kernel / receive, max over ranks; value = the
+    whole problem's residue MACs ÷ that time.  At N = 1 the primes stream through one GPU."""
+    import torch
+    import torch.distributed as dist
 
     import ctgen
     from paper_2503_16080_b200 import ctpt
     from paper_2503_16080_b200.engine import CpmmEngine
-    from paper_2503_16080_b200.shard import plan_units, primes_needed
+    from paper_2503_16080_b200.shard import (PeerGather, choose_gather, gathered_bytes, plan_units, primes_needed,
+                                             share_gather_buffers)
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     c = ctgen.CONFIGS[args.config]
     cores = os.cpu_count() or 1
+    nthreads = max(1, cores // world)
     ps = ctgen.primes(c.L)
     plan = plan_units(c.L, c.d3, world)
     mine = plan[rank]
-    t0 = time.perf_counter()
-    U = ctgen.U_matrix(c.seed, c.d2, c.d3, c.u_bound, nthreads=max(1, cores // world))
-    host_ct = {}
-    for l in primes_needed(mine):
-        ct = ctgen.encrypt(c.fmt, c.N, c.d1, c.d2, c.seed, c.log_delta, [ps[l]], nthreads=max(1, cores // world))
-        host_ct[l] = (torch.from_numpy(ct.a_polys.view(np.int32)).pin_memory(),
-                      torch.from_numpy(ct.b_polys.view(np.int32)).pin_memory())
-        del ct
-    gen_s = time.perf_counter() - t0
-    eng = CpmmEngine(ctpt.Spec(c.fmt, c.N, c.d1, c.d2, c.d3, [ps[mine[0].l]]), dev)
-    kU = eng.precompute(U)
-    specs, outs = [], []
-    ws_bytes = 0
-    for u in mine:
-        sp = dataclasses.replace(eng.spec, primes=[ps[u.l]], col_begin=u.c0, col_end=u.c1)
-        sz = ctpt.query_sizes(sp)
-        specs.append(sp)
-        outs.append((torch.empty(sz.out_AU_bytes // 4, dtype=torch.int32).pin_memory(),
-                     torch.empty(sz.out_BU_bytes // 4, dtype=torch.int32).pin_memory()))
-        ws_bytes = max(ws_bytes, ctpt.host_workspace_bytes(sp, 0))
-    hws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream(dev)
+    ra = c.rows_A
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
 
-    def step():
-        for u, sp, (au, bu) in zip(mine, specs, outs):
-            a_h, b_h = host_ct[u.l]
-            ctpt.matmul_host(sp, a_h, b_h, eng.plain, au, bu, hws, stream=stream)
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize(dev)
+    # ---------------------------------------------------------------- which gather
+    can_reach = True
     if world > 1:
-        torch.distributed.barrier()
-    clk = ClockSampler(local_rank)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    clocks = clk.stop()
-    ms = e0.elapsed_time(e1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-    h2d = sum(host_ct[u.l][0].numel() * 4 + host_ct[u.l][1].numel() * 4 for u in mine)
-    d2h = sum(au.numel() * 4 + bu.numel() * 4 for au, bu in outs)
-    if rank == 0:
-        print(json.dumps({
-            "metric": METRIC, "value": c.residue_macs / (ms / 1e3), "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "int8", "data": "synthetic",
-            "config": dict(workload_desc(c), parallelism=f"sharded over {world} rank(s): "
-                                                        f"{[[(u.l, u.c0, u.c1) for u in us] for us in plan]}",
-                           path="pinned host ciphertexts -> ctpt_matmul_host per unit -> pinned host outputs"),
-            "e2e": {"value": c.residue_macs / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
-            "gpu_launches": host_launches(c, len(mine), kU, spec_is_split=(c.d3 > 256)) * args.steps,
-            "clocks": clocks, "input_generation_s": gen_s}))
+        ids = [None] * world
+        dist.all_gather_object(ids, torch.cuda.get_device_properties(dev).pci_bus_id)
+        bus0 = ids[0]
+        idx0 = next((i for i in range(torch.cuda.device_count())
+                     if torch.cuda.get_device_properties(i).pci_bus_id == bus0), None)
+        can_reach = idx0 is not None and ctpt.peer_access(local_rank, idx0)
+    gather = choose_gather(args.gather, world, can_reach)
+    # the NCCL gather's kernels need SMs of their own while the persistent GEMMs run
+    max_ctas = sms - 8 if gather == "nccl" else 0
 
-
-def run_sharded_ipc(args, rank: int, world: int, local_rank: int):
-    """One problem sharded over the ranks by (prime, U-column) units with the
-    FUSED gather: every rank's inputs are device-resident (one laid-out X per prime it needs) and
-    its GEMM epilogues store the output residues directly into rank 0's gathered [L][d3][rows]
-    buffers, mapped into every rank by CUDA IPC (peer memory over NVLink on a multi-GPU node).
-    Timed: barrier → all units → device sync → barrier, max over ranks; "scaling": "strong"."""
-    import torch
-
-    import ctgen
-    from paper_2503_16080_b200 import ctpt
-    from paper_2503_16080_b200.engine import CpmmEngine
-    from paper_2503_16080_b200.shard import plan_units, primes_needed, share_gather_buffers
-
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    c = ctgen.CONFIGS[args.config]
-    cores = os.cpu_count() or 1
-    ps = ctgen.primes(c.L)
-    plan = plan_units(c.L, c.d3, world)
-    mine = plan[rank]
+    # ---------------------------------------------------------------- inputs, prime by prime
     t0 = time.perf_counter()
-    U = ctgen.U_matrix(c.seed, c.d2, c.d3, c.u_bound, nthreads=max(1, cores // world))
-    engines = {}
-    shared_ws = None  # one workspace for all of this rank's primes (units run one after another)
+    U = ctgen.U_matrix(c.seed, c.d2, c.d3, c.u_bound, nthreads=nthreads)
+    engines, host_ct = {}, {}
+    shared_ws = None
+    want_e2e = args.e2e_steps > 0
     for l in primes_needed(mine):
-        ct = ctgen.encrypt(c.fmt, c.N, c.d1, c.d2, c.seed, c.log_delta, [ps[l]], nthreads=max(1, cores // world))
-        eng = CpmmEngine(ctpt.Spec(c.fmt, c.N, c.d1, c.d2, c.d3, [ps[l]]), dev)
+        ct = ctgen.encrypt(c.fmt, c.N, c.d1, c.d2, c.seed, c.log_delta, [ps[l]], nthreads=nthreads)
+        eng = CpmmEngine(ctpt.Spec(c.fmt, c.N, c.d1, c.d2, c.d3, [ps[l]], max_ctas=max_ctas), dev,
+                         alloc_ws=shared_ws is None)
         if shared_ws is None:
             shared_ws = eng.ws
-        else:
-            eng.ws = shared_ws
-            torch.cuda.empty_cache()
-        eng.layout(ct.a_polys, ct.b_polys)
-        del ct
+        eng.ws = shared_ws
+        a_dev = torch.from_numpy(ct.a_polys.view(np.int32)).to(dev) if ra else None
+        b_dev = torch.from_numpy(ct.b_polys.view(np.int32)).to(dev)
+        eng.layout(a_dev, b_dev, validate=True)
+        del a_dev, b_dev
         if not engines:
             eng.precompute(U)
-        else:  # the same U for every prime: share the first engine's digit planes
+        else:  # the same U for every prime: share the first engine's digit plane(s)
             first = next(iter(engines.values()))
             eng.plain = first.plain
             eng.spec = dataclasses.replace(eng.spec, kU=first.spec.kU, u_unsigned=first.spec.u_unsigned,
                                            u_offset=first.spec.u_offset)
             eng.sizes = ctpt.query_sizes(eng.spec)
         engines[l] = eng
+        if want_e2e:  # the host-buffer leg reads the same per-column ciphertexts from pinned memory
+            host_ct[l] = (torch.from_numpy(ct.a_polys.view(np.int32)).pin_memory() if ra else None,
+                          torch.from_numpy(ct.b_polys.view(np.int32)).pin_memory())
+        del ct
+        torch.cuda.empty_cache()
     gen_s = time.perf_counter() - t0
-    ra = c.rows_A
-    out_AU = torch.empty((c.L, c.d3, ra), dtype=torch.int32, device=dev) if rank == 0 else None
-    out_BU = torch.empty((c.L, c.d3, c.d1), dtype=torch.int32, device=dev) if rank == 0 else None
-    peer_AU, peer_BU = share_gather_buffers(out_AU, out_BU, rank) if world > 1 else (out_AU, out_BU)
     specs = []
     for u in mine:
         eng = engines[u.l]
         sp = dataclasses.replace(eng.spec, col_begin=u.c0, col_end=u.c1)
-        need = ctpt.query_sizes(sp).workspace_bytes
-        if shared_ws.numel() < need:
-            shared_ws = torch.empty(need, dtype=torch.uint8, device=dev)
+        sz = ctpt.query_sizes(sp)
+        eng.unit_sizes = getattr(eng, "unit_sizes", {})
+        eng.unit_sizes[(u.c0, u.c1)] = sz
+        if shared_ws.numel() < sz.workspace_bytes:
+            shared_ws = torch.empty(sz.workspace_bytes, dtype=torch.uint8, device=dev)
         specs.append(sp)
     for eng in engines.values():
         eng.ws = shared_ws
+    kU = next(iter(engines.values())).spec.kU
     stream = torch.cuda.current_stream(dev)
 
-    def step():
-        for u, sp in zip(mine, specs):
-            eng = engines[u.l]
-            ctpt.matmul(sp, eng.ctmat, eng.plain, peer_AU[u.l, u.c0:u.c1], peer_BU[u.l, u.c0:u.c1], eng.ws,
-                        stream=stream)
+    # ---------------------------------------------------------------- outputs and the gather
+    out_AU = torch.empty((c.L, c.d3, max(ra, 1)), dtype=torch.int32, device=dev) if rank == 0 else None
+    out_BU = torch.empty((c.L, c.d3, c.d1), dtype=torch.int32, device=dev) if rank == 0 else None
+    if gather == "ipc":
+        peers = share_gather_buffers(out_AU, out_BU, rank, c.L, c.d3, ra, c.d1)
+    elif rank == 0:
+        peers = PeerGather(out_AU.data_ptr() if ra else 0, out_BU.data_ptr(), c.L, c.d3, ra, c.d1)
+    else:
+        peers = None
+    # per-unit local buffers: the NCCL senders' staging, and every rank's "no gather" pass
+    local = [(torch.empty((u.ncols, max(ra, 1)), dtype=torch.int32, device=dev),
+              torch.empty((u.ncols, c.d1), dtype=torch.int32, device=dev)) for u in mine] if world > 1 else []
+
+    def dst(i, u, to_local):
+        if to_local or (gather == "nccl" and rank != 0):
+            return local[i][0].data_ptr() if ra else 0, local[i][1].data_ptr()
+        return peers.block(u)
+
+    def step(evs=None, to_local=False):
+        n = 0
+        reqs = []
+        if gather == "nccl" and not to_local and rank == 0:
+            for src in range(1, world):  # every remote receive posted before rank 0 computes
+                for u in plan[src]:
+                    if ra:
+                        reqs.append(dist.irecv(out_AU[u.l, u.c0:u.c1], src=src))
+                    reqs.append(dist.irecv(out_BU[u.l, u.c0:u.c1], src=src))
+        for i, (u, sp) in enumerate(zip(mine, specs)):
+            au, bu = dst(i, u, to_local)
+            n += launch_unit(sp, engines[u.l], au, bu, stream, None if evs is None else evs[i])
+            if gather == "nccl" and not to_local and rank != 0:
+                if ra:
+                    reqs.append(dist.isend(local[i][0], dst=0))
+                reqs.append(dist.isend(local[i][1], dst=0))
+        for r in reqs:
+            r.wait()  # NCCL: the current stream waits for the transfer
+        return n
+
+    def timed(steps, to_local=False, with_events=False):
+        evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in mine]
+               for _ in range(steps)] if with_events else None
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        clk = ClockSampler(dev) if with_events else None
+        if clk:
+            time.sleep(0.3)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        launches = 0
+        for st_i in range(steps):
+            launches += step(None if evs is None else evs[st_i], to_local)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        clocks = clk.stop() if clk else None
+        if world > 1:
+            dist.barrier()  # every rank's stores into rank 0's buffers have landed
+        ms = e0.elapsed_time(e1) / steps
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        gemm = [a.elapsed_time(b) for row in evs for (a, b) in row] if evs else []
+        return ms, gemm, launches, clocks
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
-    if world > 1:
-        torch.distributed.barrier()
-    clk = ClockSampler(local_rank)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        torch.distributed.barrier()  # every rank's stores into rank 0's buffers have landed
-    clocks = clk.stop()
-    ms = e0.elapsed_time(e1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-    kU = engines[mine[0].l].spec.kU
+    ms, gemm_ms, launches, clocks = timed(args.steps, with_events=True)
+    ms_local, _, _, _ = timed(args.steps, to_local=True) if world > 1 else (ms, None, None, None)
+
+    # ---------------------------------------------------------------- roofline (rank-0 unit launches)
+    mp, which = peaks()
+    macs = c.residue_macs
+    value = macs / (ms / 1e3)
+    paths = {kernel_path(engines[u.l].unit_sizes[(u.c0, u.c1)].d3_loc, kU, engines[u.l].spec.u_unsigned,
+                         engines[u.l].spec.u_offset) for u in mine}
+    unit_limb_macs = [4 * kU * c.R * c.d2 * u.ncols for u in mine]
+    if paths == {"split_gemm"}:
+        tops = [2 * m / (t / 1e3) / 1e12 for m, t in zip(unit_limb_macs * args.steps, gemm_ms)]
+        peak_key = "bf16_tflops" if ms * args.steps < 2000.0 else "bf16_tflops_sustained"
+        ach = 2 * sum(unit_limb_macs) * args.steps / (sum(gemm_ms) / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": ach, "peak": 2 * float(mp[peak_key]), "unit": "TOP/s",
+                "frac": ach / (2 * float(mp[peak_key])), "traffic": None, "kernel": "k_gemm_tc",
+                "peak_source": f"{which}: 2 x {peak_key} (int8/bf16 nominal 2x)",
+                "per_launch": "4·kU·R·d2·ncols limb MACs per unit launch (rank 0's units)",
+                "avg_launch_ms": statistics.mean(gemm_ms), "min_unit_tops": min(tops),
+                "share_of_step": sum(gemm_ms) / args.steps / ms,
+                "vs_int8_mma_ceiling": mma_ceiling_ratio(ach)}
+    else:
+        alg = sum(4 * c.R * c.d2 + u.ncols * c.d2 + 4 * c.R * u.ncols for u in mine) * args.steps
+        gbs = alg / (sum(gemm_ms) / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": gbs, "peak": float(mp["hbm_gbs"]), "unit": "GB/s",
+                "frac": gbs / float(mp["hbm_gbs"]), "traffic": None, "kernel": "/".join(sorted(paths)),
+                "peak_source": f"{which}: hbm_gbs", "avg_launch_ms": statistics.mean(gemm_ms),
+                "share_of_step": sum(gemm_ms) / args.steps / ms}
+    gbytes = gathered_bytes(plan, ra, c.d1) if world > 1 else 0
+    link = 770.0  # measured NVLink peer copy, GB/s per direction (B200_PROFILING.md)
+    compute_floor_ms = 4 * kU * macs / world / (2 * float(mp["bf16_tflops"]) * 1e12 / 2) * 1e3
+    gather_info = {
+        "mode": gather, "bytes_into_rank0_per_step": gbytes,
+        "rank0_ingest_gbs": gbytes / (ms / 1e3) / 1e9 if gbytes else 0.0,
+        "link_gbs_measured_peer_copy": link,
+        "gather_floor_ms": gbytes / (link * 1e9) * 1e3,
+        "compute_floor_ms": compute_floor_ms,
+        "frac_of_max_floor": max(gbytes / (link * 1e9) * 1e3, compute_floor_ms) / ms,
+        "no_gather_ms": ms_local,
+        "max_ctas": max_ctas or sms,
+    }
+
+    # ---------------------------------------------------------------- end to end from host buffers
+    e2e = {"value": None, "note": "skipped (--e2e-steps 0)"}
+    if want_e2e:
+        for eng in engines.values():
+            eng.ctmat = None
+        torch.cuda.empty_cache()
+        outs, hws_bytes = [], 0
+        for u, sp in zip(mine, specs):
+            sz = engines[u.l].unit_sizes[(u.c0, u.c1)]
+            outs.append((torch.empty(max(1, sz.out_AU_bytes // 4), dtype=torch.int32).pin_memory(),
+                         torch.empty(sz.out_BU_bytes // 4, dtype=torch.int32).pin_memory()))
+            hws_bytes = max(hws_bytes, ctpt.host_workspace_bytes(sp, 0))
+        hws = torch.empty(hws_bytes, dtype=torch.uint8, device=dev)
+
+        def hstep():
+            for u, sp, (au, bu) in zip(mine, specs, outs):
+                a_h, b_h = host_ct[u.l]
+                ctpt.matmul_host(sp, a_h, b_h, engines[u.l].plain, au, bu, hws, stream=stream)
+
+        hstep()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.e2e_steps):
+            hstep()
+        f1.record(stream)
+        torch.cuda.synchronize(dev)
+        hms = f0.elapsed_time(f1) / args.e2e_steps
+        h2d = sum((host_ct[u.l][0].numel() * 4 if ra else 0) + host_ct[u.l][1].numel() * 4 for u in mine)
+        d2h = sum(au.numel() * 4 * (ra > 0) + bu.numel() * 4 for au, bu in outs)
+        vals = torch.tensor([hms, h2d, d2h], dtype=torch.float64, device=dev)
+        if world > 1:
+            mx = vals.clone()
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            dist.all_reduce(vals, op=dist.ReduceOp.SUM)
+            hms = float(mx[0].item())
+        h2d, d2h = int(vals[1].item()), int(vals[2].item())
+        e2e = {"value": macs / (hms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": hms, "steps": args.e2e_steps,
+               "path": "per rank: pinned host ciphertexts -> ctpt_matmul_host per unit (chunked H2D || layout + "
+                       "split + GEMM || D2H) -> pinned host outputs (the sharded result in host memory)"}
+
+    # ---------------------------------------------------------------- gather parity on sampled columns
+    sample = None
+    if rank == 0 and world > 1 and not args.no_cpu_baseline:
+        sample = gather_parity(c, ps, plan, U, out_AU, out_BU, cores)
+
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+        "config": config_for(c, world, "strong"),
+        "kernel_config": {"kU": kU, "limb_macs_per_residue_mac": 4 * kU,
+                          "u_plane": "u8 (U + u_offset)" if next(iter(engines.values())).spec.u_unsigned else "s8",
+                          "units_per_rank": [[(u.l, u.c0, u.c1) for u in us] for us in plan]},
+        "pct_int8_datasheet": 100.0 * value * 4 * kU / world / INT8_DATASHEET_MACS,
+        "roofline": roof, "gather": gather_info, "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks, "input_generation_s": gen_s,
+    }
+    if sample is not None:
+        result["gather_parity_on_sample"] = sample
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and 0 in host_ct:
+        ct0 = types.SimpleNamespace(primes=ps, a_polys=host_ct[0][0].numpy().view(np.uint32)[None] if ra else None,
+                                    b_polys=host_ct[0][1].numpy().view(np.uint32)[None])
+        gpu0 = None
+        if out_AU is not None:
+            gpu0 = (out_AU[0].cpu().numpy().view(np.uint32).reshape(c.d3, max(ra, 1)),
+                    out_BU[0].cpu().numpy().view(np.uint32).reshape(c.d3, c.d1))
+        result["cpu_baseline"] = cpu_oracle_rate(c, ct0, U, args.cpu_seconds, gpu0)
+    if gather == "ipc" and rank != 0:
+        peers.close()
     if rank == 0:
-        print(json.dumps({
-            "metric": METRIC, "value": c.residue_macs / (ms / 1e3), "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "int8", "data": "synthetic",
-            "config": dict(workload_desc(c), parallelism=f"sharded over {world} rank(s), fused gather (IPC peer "
-                                                        f"stores from the GEMM epilogues): "
-                                                        f"{[[(u.l, u.c0, u.c1) for u in us] for us in plan]}",
-                           path="device-resident laid-out X per prime -> ctpt_matmul per unit -> rank 0's "
-                                "gathered output"),
-            "e2e": {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
-                    "note": "device-resident inputs; see --gather host for the host-buffer path"},
-            "gpu_launches": (2 if c.d3 > 256 else 1) * len(mine) * args.steps if kU == 1 else None,
-            "clocks": clocks, "input_generation_s": gen_s}))
+        print(json.dumps(result))
+
+
+def gather_parity(c, ps, plan, U, out_AU, out_BU, cores):
+    """After the timed run: in rank 0's GATHERED buffers, one sampled output column of the first unit
+    of rank 1 and of the last rank (so at least one block that arrived through the gather) against
+    the oracle's schoolbook over all R rows and the full d2 (every entry of those columns)."""
+    import ctgen
+    import oracle
+
+    picks = []
+    for r in sorted({1, len(plan) - 1}):
+        u = plan[r][0]
+        picks.append((r, u.l, u.c0))
+    ra = c.rows_A
+    bad, n = 0, 0
+    for r, l, j in picks:
+        ct = ctgen.encrypt(c.fmt, c.N, c.d1, c.d2, c.seed, c.log_delta, [ps[l]], nthreads=cores)
+        cols = np.array([j])
+        wb = oracle.modmatmul(ct.b_polys[0].reshape(c.d2, c.d1), U, ps[l], cols=cols, nthreads=cores)
+        gb = out_BU[l, j].cpu().numpy().view(np.uint32)
+        bad += int(np.count_nonzero(gb != wb[0]))
+        n += gb.size
+        if ra:
+            wa = oracle.modmatmul(ct.a_polys[0].reshape(c.d2, ra), U, ps[l], cols=cols, nthreads=cores)
+            ga = out_AU[l, j].cpu().numpy().view(np.uint32)
+            bad += int(np.count_nonzero(ga != wa[0]))
+            n += ga.size
+        del ct
+    return {"columns": [{"from_rank": r, "prime": l, "column": j} for r, l, j in picks], "entries": n,
+            "mismatches": bad, "verdict": "bit-exact" if bad == 0 else "MISMATCH"}
 
 
 def run_modmm(args, rank: int, world: int, local_rank: int):
@@ -960,7 +1147,7 @@ def run_modmm(args, rank: int, world: int, local_rank: int):
     torch.cuda.synchronize(dev)
     if world > 1:
         torch.distributed.barrier()
-    clk = ClockSampler(local_rank)
+    clk = ClockSampler(dev)
     time.sleep(0.3)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -1016,20 +1203,39 @@ def run_modmm(args, rank: int, world: int, local_rank: int):
         print(json.dumps(result))
 
 
+def relaunch_under_torchrun(args) -> int:
+    """`python bench.py --gpus N` (N > 1) outside torchrun: re-run this command as N ranks under
+    torch.distributed.run on this node (rendezvous on 127.0.0.1)."""
+    import socket
+
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch_under_torchrun(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: refusing to run a different "
+                         f"number of ranks than asked\n")
+        sys.exit(2)
     # Test hook for the multi-rank code path on a one-GPU box: CTPT_BENCH_ONE_DEVICE=1 puts every
-    # rank on cuda:0 (independent problems; no kernel waits on another rank's) and
-    # CTPT_DIST_BACKEND=gloo replaces NCCL (which refuses two ranks on one device).  Never set by
-    # the driver; the numbers of such a run are not a scaling measurement.
+    # rank on cuda:0 (no kernel waits on another rank's) and CTPT_DIST_BACKEND=gloo replaces NCCL
+    # (which refuses two ranks on one device).  Never set by the driver; the numbers of such a run
+    # are not a scaling measurement.
     if os.environ.get("CTPT_BENCH_ONE_DEVICE") == "1":
         local_rank = 0
     backend = os.environ.get("CTPT_DIST_BACKEND", "nccl")
     if args.impl == "reference":
-        run_reference(args, rank)
+        run_reference(args, rank, world)
         return
     if world > 1:
         import torch
@@ -1042,12 +1248,12 @@ def main():
     try:
         if args.config == "modmm":
             run_modmm(args, rank, world, local_rank)
-        elif args.shard and args.gather == "ipc":
-            run_sharded_ipc(args, rank, world, local_rank)
-        elif args.shard:
-            run_sharded(args, rank, world, local_rank)
+        elif args.mode == "weak" or args.rescale:  # Rescale needs every prime of an element: no prime units
+            run_ours(args, rank, world, local_rank, scaling="weak" if world > 1 else "strong")
+        elif args.mode == "strong" or world > 1 or args.config in STREAMED_CONFIGS:
+            run_strong(args, rank, world, local_rank)
         else:
-            run_ours(args, rank, world, local_rank)
+            run_ours(args, rank, world, local_rank, scaling="strong")
     finally:
         if world > 1:
             import torch

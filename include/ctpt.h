@@ -286,6 +286,27 @@ ctpt_status ctpt_matmul_host(const ctpt_problem* prob, const uint32_t* h_a_polys
 ctpt_status ctpt_gemm_next(const ctpt_problem* prob, int32_t l, const void* d_ctmat, void* d_ws, size_t ws_bytes,
                            const void* d_plain, uint32_t* d_AU_l, uint32_t* d_BU_l, void* stream);
 
+/* ---- Multi-GPU gather over peer memory (output column j is ciphertext j,
+ * P:1688–1690, so a (prime, column-block) unit's outputs are one contiguous block of the gathered
+ * [L][d3][rows] layout and a remote rank's ctpt_matmul can store them there directly).
+ *
+ * ctpt_ipc_export: a CUDA IPC handle (CTPT_IPC_HANDLE_BYTES opaque bytes written to `handle`) for
+ *   the device allocation containing d_ptr, and d_ptr's byte offset in it (the allocation may be a
+ *   block of a caching allocator's larger segment).  Host only, no stream work.
+ * ctpt_ipc_open: map a handle exported by another process into the CALLING thread's current
+ *   device (the owner may be another GPU: peer access is enabled as needed,
+ *   cudaIpcMemLazyEnablePeerAccess), so the current device's kernels can store into it over
+ *   NVLink.  *d_base receives the mapping's base (for ctpt_ipc_close), *d_ptr = base + offset.
+ *   Errors: CTPT_ERR_CUDA (e.g. no peer access between the two devices: use an NCCL gather).
+ * ctpt_ipc_close: unmap a base returned by ctpt_ipc_open.
+ * ctpt_peer_access: *can = 1 if `device` can read and write `peer`'s memory (1 when device ==
+ *   peer).  Does not enable anything. */
+#define CTPT_IPC_HANDLE_BYTES 64
+ctpt_status ctpt_ipc_export(const void* d_ptr, void* handle, uint64_t* offset);
+ctpt_status ctpt_ipc_open(const void* handle, uint64_t offset, void** d_base, void** d_ptr);
+ctpt_status ctpt_ipc_close(void* d_base);
+ctpt_status ctpt_peer_access(int32_t device, int32_t peer, int32_t* can);
+
 /* Bring-up / diagnostics only (not a product path): the same limb GEMM and epilogue on
  * CUDA cores, reading the same workspace and plain planes.  Used by the tests to tell a
  * layout/split bug from a tensor-core descriptor bug. */

@@ -217,6 +217,19 @@ uint32_t pow2mod(int e, uint32_t p) {
 }
 
 // ---------------------------------------------------------------- TMA descriptors
+PFN_cuMemGetAddressRange_v3020 get_addr_range() {
+  static PFN_cuMemGetAddressRange_v3020 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(p);
+  });
+  return fn;
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -276,6 +289,35 @@ ctpt_status make_tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType d
                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(CTPT_ERR_CUDA, "cuTensorMapEncodeTiled (2d) failed (%d)", static_cast<int>(r));
   return CTPT_OK;
+}
+
+// 2-D uint32 output tensor [cols][rows] (an output matrix in per-column layout: column j contiguous)
+// for the TMA-store epilogue: box {32 rows, 32 columns}, SWIZZLE_128B.
+ctpt_status make_tmap_out(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols) {
+  auto enc = get_encode();
+  if (!enc) return fail(CTPT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {rows, cols};
+  cuuint64_t strides[1] = {rows * 4};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CTPT_ERR_CUDA, "cuTensorMapEncodeTiled (outputs) failed (%d)", static_cast<int>(r));
+  return CTPT_OK;
+}
+
+// Memory of the CURRENT device (not a peer / IPC mapping of another GPU's memory, nor host memory):
+// the TMA-store epilogue is used only there; stores into a peer's buffer (the fused multi-GPU
+// gather) keep the plain 16-byte STG path.
+bool on_current_device(const void* p) {
+  int dev = -1;
+  cudaPointerAttributes a;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();  // clear a sticky "invalid value" from an unregistered pointer
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice && a.device == dev;
 }
 
 int num_sms() {
@@ -710,6 +752,21 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
   if (g.raster_group > 0) P.group_j = g.raster_group;
   P.u_unsigned = g.u_unsigned;
   P.m = m;
+  // TMA-store epilogue: a tile's 64 rows must lie inside A' or inside B' (rows_A, d1 multiples of
+  // 64; then every row pitch is 16-B aligned) and the outputs must be this device's memory
+  const OutParams& o0 = g.o;
+  const bool has_a = o0.rows_A > 0, has_b = o0.d1 > 0;
+  P.tma_store = o0.rows_A % 64 == 0 && o0.d1 % 64 == 0 && (has_a || has_b) &&
+                (!has_a || (reinterpret_cast<uintptr_t>(o0.AU) % 16 == 0 && on_current_device(o0.AU))) &&
+                (!has_b || (reinterpret_cast<uintptr_t>(o0.BU) % 16 == 0 && on_current_device(o0.BU)));
+#ifdef CTPT_NO_TMA_STORE  // A/B measurement build only (tools/ab_build.py): the 16-byte STG epilogue
+  P.tma_store = 0;
+#endif
+  CUtensorMap tmAU = tmU, tmBU = tmU;  // unused placeholders unless tma_store
+  if (P.tma_store) {
+    if (has_a && (s = make_tmap_out(&tmAU, o0.AU, o0.rows_A, d.d3_loc)) != CTPT_OK) return s;
+    if (has_b && (s = make_tmap_out(&tmBU, o0.BU, o0.d1, d.d3_loc)) != CTPT_OK) return s;
+  }
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>(nt, grid_cap(g.max_ctas)));
   // k_U > 1 digit planes (Rescale's real U, general Mod-PP-MM): one launch per digit whose epilogue
   // accumulates Σ_i 2^{8i}·(digit i's product mod p) through the outputs.  (All digits in one launch
@@ -724,7 +781,7 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
     if (!last) P.o.xlast = nullptr;     // Rescale on the final pass only
     if (!first) P.o.rowcorr = nullptr;  // the unsigned-U row correction exactly once
     P.sj = first ? g.sj : SplitJob{};   // the next prime's split rides on the first pass
-    k_gemm_tc<<<grid, TC_THREADS, TC_SMEM_BYTES, st>>>(tmU, tmX, P);
+    k_gemm_tc<<<grid, TC_THREADS, TC_SMEM_BYTES, st>>>(tmU, tmX, tmAU, tmBU, P);
     CUDA_TRY(cudaGetLastError());
   }
   return CTPT_OK;
@@ -1257,6 +1314,61 @@ ctpt_status ctpt_matmul_host(const ctpt_problem* pb, const uint32_t* h_a, const 
   // join: the caller's stream completes only after the last device→host copy
   CUDA_TRY(cudaEventRecord(ev_end, ss.d2h));
   CUDA_TRY(cudaStreamWaitEvent(sc, ev_end, 0));
+  return CTPT_OK;
+}
+
+}  // extern "C"
+
+// =============================================================================================
+// Multi-GPU gather over peer memory: CUDA IPC plumbing so a rank's ctpt_matmul
+// can store its unit's outputs straight into rank 0's gathered [L][d3][rows] buffers.
+// =============================================================================================
+extern "C" {
+
+ctpt_status ctpt_ipc_export(const void* d_ptr, void* handle, uint64_t* offset) {
+  if (!d_ptr || !handle || !offset) return fail(CTPT_ERR_ARG, "null pointer");
+  static_assert(sizeof(cudaIpcMemHandle_t) == CTPT_IPC_HANDLE_BYTES, "IPC handle size");
+  auto range = get_addr_range();
+  if (!range) return fail(CTPT_ERR_CUDA, "cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  const CUresult r = range(&base, &size, reinterpret_cast<CUdeviceptr>(d_ptr));
+  if (r != CUDA_SUCCESS) return fail(CTPT_ERR_CUDA, "cuMemGetAddressRange failed (%d)", static_cast<int>(r));
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  memcpy(handle, &h, sizeof(h));
+  *offset = static_cast<uint64_t>(reinterpret_cast<CUdeviceptr>(d_ptr) - base);
+  return CTPT_OK;
+}
+
+ctpt_status ctpt_ipc_open(const void* handle, uint64_t offset, void** d_base, void** d_ptr) {
+  if (!handle || !d_base || !d_ptr) return fail(CTPT_ERR_ARG, "null pointer");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  void* base = nullptr;
+  // opened in the calling thread's CURRENT device context: the mapping is usable by that device's
+  // kernels, with peer access to the owning GPU enabled on demand
+  CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  *d_base = base;
+  *d_ptr = static_cast<uint8_t*>(base) + offset;
+  return CTPT_OK;
+}
+
+ctpt_status ctpt_ipc_close(void* d_base) {
+  if (!d_base) return fail(CTPT_ERR_ARG, "null pointer");
+  CUDA_TRY(cudaIpcCloseMemHandle(d_base));
+  return CTPT_OK;
+}
+
+ctpt_status ctpt_peer_access(int32_t device, int32_t peer, int32_t* can) {
+  if (!can) return fail(CTPT_ERR_ARG, "null pointer");
+  if (device == peer) {
+    *can = 1;
+    return CTPT_OK;
+  }
+  int c = 0;
+  CUDA_TRY(cudaDeviceCanAccessPeer(&c, device, peer));
+  *can = c;
   return CTPT_OK;
 }
 

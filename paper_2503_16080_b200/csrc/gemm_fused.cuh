@@ -59,13 +59,6 @@ struct FusedParams {
   OutParams o;         // d3_loc ≤ 128·NG
 };
 
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
-  asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
-}
-
 template <int NG>
 __global__ void __launch_bounds__(FU_THREADS, 1)
     k_gemm_fused(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmX,

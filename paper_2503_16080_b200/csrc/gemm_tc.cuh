@@ -34,7 +34,11 @@ constexpr int TC_X_BYTES = 4 * TC_BLOCK_R * TC_BLOCK_K;        // 32 KB
 constexpr int TC_STAGE_BYTES = TC_U_BYTES + TC_X_BYTES;        // 48 KB
 constexpr int TC_ACC_COLS = 4 * TC_BLOCK_R;                    // 256
 constexpr int TC_THREADS = 256;
-constexpr int TC_SMEM_BYTES = TC_STAGES * TC_STAGE_BYTES + 256 + 1024;
+// TMA-store epilogue: per epilogue warp two 4-KB staging halves ([32 columns j][32 rows r] uint32,
+// SWIZZLE_128B), one TMA store per half
+constexpr int TC_OUT_HALF_BYTES = 32 * 32 * 4;
+constexpr int TC_OUT_BYTES = 4 * 2 * TC_OUT_HALF_BYTES;         // 32 KB
+constexpr int TC_SMEM_BYTES = TC_STAGES * TC_STAGE_BYTES + TC_OUT_BYTES + 256 + 1024;
 constexpr int TC_GROUP_J_DEFAULT = 16;  // measured best of {8,16,32,64,128} on c3 (profiles/r01)
 
 // The limb split of the NEXT prime, run by the GEMM's two otherwise idle warps (2 and 3) while
@@ -88,6 +92,9 @@ struct TcParams {
   int32_t num_tiles;
   int32_t group_j;    // tiles visited in groups of group_j j-tiles (L2 reuse of U panels)
   int32_t u_unsigned; // U plane is u8 (U + u_offset) instead of balanced s8 digits
+  int32_t tma_store;  // epilogue stages each 32 × 32 output block in shared memory and writes it with
+                      // one TMA store (tmAU / tmBU); needs rows_A and d1 multiples of 64 (a tile's 64
+                      // rows lie inside A' or B') and device-local outputs; else 16-byte STG stores
   ModP m;
   OutParams o;
   SplitJob sj;        // the next prime's limb split (warps 2–3), or sj.x = nullptr
@@ -104,17 +111,20 @@ __device__ __forceinline__ void tc_tile_coords(int32_t tile, const TcParams& P, 
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmX,
+              const __grid_constant__ CUtensorMap tmAU, const __grid_constant__ CUtensorMap tmBU,
               const __grid_constant__ TcParams P) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
-  const uint32_t bar_base = sbase + TC_STAGES * TC_STAGE_BYTES;
+  const uint32_t out_base = sbase + TC_STAGES * TC_STAGE_BYTES;  // 1024-B aligned (SWIZZLE_128B atoms)
+  const uint32_t bar_base = out_base + TC_OUT_BYTES;
   auto full_bar = [&](int s) { return bar_base + 8u * s; };
   auto empty_bar = [&](int s) { return bar_base + 8u * (TC_STAGES + s); };
   auto tfull_bar = [&](int b) { return bar_base + 8u * (2 * TC_STAGES + b); };
   auto tempty_bar = [&](int b) { return bar_base + 8u * (2 * TC_STAGES + 2 + b); };
   const uint32_t tmem_slot = bar_base + 8u * (2 * TC_STAGES + 4);
-  uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(smem + TC_STAGES * TC_STAGE_BYTES + 8 * (2 * TC_STAGES + 4));
+  uint32_t* tmem_slot_ptr =
+      reinterpret_cast<uint32_t*>(smem + TC_STAGES * TC_STAGE_BYTES + TC_OUT_BYTES + 8 * (2 * TC_STAGES + 4));
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -122,6 +132,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmU);
     tma_prefetch(&tmX);
+    if (P.tma_store) {
+      tma_prefetch(&tmAU);
+      tma_prefetch(&tmBU);
+    }
     for (int s = 0; s < TC_STAGES; ++s) {
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), 1);
@@ -191,6 +205,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else {
     // ---------------------------------------------------------------- epilogue (warps 4–7)
     const int quad = warp & 3;  // TMEM lanes [32·quad, 32·quad + 32)
+    const uint32_t stg = out_base + quad * 2 * TC_OUT_HALF_BYTES;  // this warp's two staging halves
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int32_t tile = blockIdx.x; tile < P.num_tiles; tile += gridDim.x) {
@@ -200,6 +215,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tc_fence_after();
       const int64_t j = static_cast<int64_t>(tj) * TC_BLOCK_J + quad * 32 + lane;
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * TC_ACC_COLS;
+      const int64_t r_tile = static_cast<int64_t>(tr) * TC_BLOCK_R;
       // two halves of 32 rows: four 32-column TMEM loads (one per limb) each; the accumulator is
       // handed back to the MMA warp as soon as the last loads have landed, before the last stores
       // (c3 3.709 vs 3.694e14 against 16-column loads, profiles/r01/gemm_epilogue_ld32/)
@@ -215,6 +231,36 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           tc_fence_before();
           mbar_arrive(tempty_bar(acc));
         }
+        if (P.tma_store) {
+          // the 32 × 32 block (columns j of this warp, rows r_tile + 32h ..) through shared memory:
+          // lane = column j holds 32 consecutive rows = one 128-B row of the staging image, its 16-B
+          // chunk c at position c ^ (j & 7) (SWIZZLE_128B; conflict-free STS.128)
+          uint32_t res[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            res[i] = recombine_mod(static_cast<int32_t>(v0[i]), static_cast<int32_t>(v1[i]),
+                                   static_cast<int32_t>(v2[i]), static_cast<int32_t>(v3[i]), P.m);
+          const int64_t r0 = r_tile + h * 32;
+          finish_rows<32>(P.o, P.m, j, r0, res, j < P.o.d3_loc);
+          const uint32_t buf = stg + h * TC_OUT_HALF_BYTES;
+          if (lane == 0) bulk_wait_read<1>();  // this half's previous store has read its buffer
+          __syncwarp();
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            sts128(buf + lane * 128 + ((c ^ (lane & 7)) << 4), res[4 * c], res[4 * c + 1], res[4 * c + 2],
+                   res[4 * c + 3]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            const int32_t jc = static_cast<int32_t>(tj) * TC_BLOCK_J + quad * 32;
+            if (r0 < P.o.rows_A)
+              tma_store_2d(&tmAU, buf, static_cast<int32_t>(r0), jc);
+            else
+              tma_store_2d(&tmBU, buf, static_cast<int32_t>(r0 - P.o.rows_A), jc);
+            bulk_commit();
+          }
+          continue;
+        }
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           uint32_t res[16];
@@ -222,11 +268,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           for (int i = 0; i < 16; ++i)
             res[i] = recombine_mod(static_cast<int32_t>(v0[q * 16 + i]), static_cast<int32_t>(v1[q * 16 + i]),
                                    static_cast<int32_t>(v2[q * 16 + i]), static_cast<int32_t>(v3[q * 16 + i]), P.m);
-          if (j < P.o.d3_loc) store16(P.o, P.m, j, static_cast<int64_t>(tr) * TC_BLOCK_R + h * 32 + q * 16, res);
+          if (j < P.o.d3_loc) store16(P.o, P.m, j, r_tile + h * 32 + q * 16, res);
         }
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (P.tma_store && lane == 0) bulk_wait<0>();  // every store performed before the CTA exits
   }
 
   tc_fence_before();

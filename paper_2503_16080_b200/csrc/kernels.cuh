@@ -366,6 +366,51 @@ __device__ __forceinline__ void store_out(const OutParams& o, const ModP& m, int
   *q = v;
 }
 
+// The output transforms of store16 without the store, for NR consecutive rows r0.. of column j that
+// lie inside A' or inside B' with 4-aligned vectors (the TMA-store epilogue stages the results in
+// shared memory): the unsigned-U row correction, the k_U > 1 accumulation of the previous pass's
+// outputs and the Rescale.  j_ok = false (a column past d3_loc, clipped by the TMA store) skips the
+// reads of the previous outputs / xlast.
+template <int NR>
+__device__ __forceinline__ void finish_rows(const OutParams& o, const ModP& m, int64_t j, int64_t r0, uint32_t (&res)[NR],
+                                            bool j_ok) {
+  static_assert(NR % 4 == 0, "vector rows");
+  if (o.rowcorr) {
+    const uint4* rc = reinterpret_cast<const uint4*>(o.rowcorr + r0);
+#pragma unroll
+    for (int i = 0; i < NR / 4; ++i) {
+      const uint4 c = rc[i];
+      res[4 * i] = sub_mod(res[4 * i], c.x, m.p);
+      res[4 * i + 1] = sub_mod(res[4 * i + 1], c.y, m.p);
+      res[4 * i + 2] = sub_mod(res[4 * i + 2], c.z, m.p);
+      res[4 * i + 3] = sub_mod(res[4 * i + 3], c.w, m.p);
+    }
+  }
+  if (!j_ok) return;
+  if (o.accumulate) {
+    const uint4* q = reinterpret_cast<const uint4*>(out_ptr(o, j, r0));
+#pragma unroll
+    for (int i = 0; i < NR / 4; ++i) {
+      const uint4 pv = q[i];
+      res[4 * i] = accum_mod(pv.x, res[4 * i], o.w, m);
+      res[4 * i + 1] = accum_mod(pv.y, res[4 * i + 1], o.w, m);
+      res[4 * i + 2] = accum_mod(pv.z, res[4 * i + 2], o.w, m);
+      res[4 * i + 3] = accum_mod(pv.w, res[4 * i + 3], o.w, m);
+    }
+  }
+  if (o.xlast) {
+    const uint4* xl = reinterpret_cast<const uint4*>(o.xlast + j * o.R + r0);
+#pragma unroll
+    for (int i = 0; i < NR / 4; ++i) {
+      const uint4 x = xl[i];
+      res[4 * i] = rescale_last(res[4 * i], x.x, o, m);
+      res[4 * i + 1] = rescale_last(res[4 * i + 1], x.y, o, m);
+      res[4 * i + 2] = rescale_last(res[4 * i + 2], x.z, o, m);
+      res[4 * i + 3] = rescale_last(res[4 * i + 3], x.w, o, m);
+    }
+  }
+}
+
 // Store 16 consecutive rows r0..r0+15 of output column j (one epilogue thread's TMEM chunk):
 // 4 × 16-byte stores when the 16 rows lie inside A' or inside B' and both are 4-aligned.
 __device__ __forceinline__ void store16(const OutParams& o, const ModP& m, int64_t j, int64_t r0, uint32_t (&res)[16]) {

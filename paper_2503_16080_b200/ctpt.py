@@ -78,6 +78,10 @@ _sig = {
                                       ctypes.c_int64, _P, _P, _P, ctypes.c_size_t, _P]),
     "ctpt_host_workspace_bytes": (ctypes.c_int, [_PP, ctypes.c_int64, ctypes.POINTER(ctypes.c_size_t)]),
     "ctpt_matmul_host": (ctypes.c_int, [_PP, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, ctypes.c_int64, _P]),
+    "ctpt_ipc_export": (ctypes.c_int, [_P, _P, ctypes.POINTER(ctypes.c_uint64)]),
+    "ctpt_ipc_open": (ctypes.c_int, [_P, ctypes.c_uint64, ctypes.POINTER(_P), ctypes.POINTER(_P)]),
+    "ctpt_ipc_close": (ctypes.c_int, [_P]),
+    "ctpt_peer_access": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_lib, _name)
@@ -274,6 +278,36 @@ def matmul_host(spec: Spec, a_polys_h, b_polys_h, plain, AU_h, BU_h, ws, chunk_r
     pb = spec.cstruct()
     _check(_lib.ctpt_matmul_host(ctypes.byref(pb), _ptr(a_polys_h), _ptr(b_polys_h), _ptr(plain), _ptr(AU_h),
                                  _ptr(BU_h), _ptr(ws), ws.numel() * ws.element_size(), chunk_rows, _stream(stream)))
+
+
+IPC_HANDLE_BYTES = 64  # CTPT_IPC_HANDLE_BYTES
+
+
+def ipc_export(t) -> tuple[bytes, int]:
+    """(handle bytes, byte offset) of device tensor / address t's allocation (ctpt_ipc_export)."""
+    h = (ctypes.c_char * IPC_HANDLE_BYTES)()
+    off = ctypes.c_uint64(0)
+    _check(_lib.ctpt_ipc_export(_ptr(t), ctypes.cast(h, _P), ctypes.byref(off)))
+    return bytes(h.raw), off.value
+
+
+def ipc_open(handle: bytes, offset: int) -> tuple[int, int]:
+    """Map another process's allocation into the CURRENT device (peer access enabled as needed);
+    returns (base, address) — base for ipc_close, address = base + offset."""
+    h = (ctypes.c_char * IPC_HANDLE_BYTES).from_buffer_copy(handle)
+    base, ptr = _P(), _P()
+    _check(_lib.ctpt_ipc_open(ctypes.cast(h, _P), offset, ctypes.byref(base), ctypes.byref(ptr)))
+    return base.value, ptr.value
+
+
+def ipc_close(base: int):
+    _check(_lib.ctpt_ipc_close(_P(base)))
+
+
+def peer_access(device: int, peer: int) -> bool:
+    can = ctypes.c_int32(0)
+    _check(_lib.ctpt_peer_access(device, peer, ctypes.byref(can)))
+    return bool(can.value)
 
 
 def raw_lib():

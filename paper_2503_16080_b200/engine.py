@@ -24,11 +24,14 @@ def dev_to_u32(t: torch.Tensor) -> np.ndarray:
 
 
 class CpmmEngine:
-    def __init__(self, spec: ctpt.Spec, device: str | torch.device = "cuda"):
+    def __init__(self, spec: ctpt.Spec, device: str | torch.device = "cuda", alloc_ws: bool = True):
+        """alloc_ws=False: the caller provides self.ws (e.g. one workspace shared by several engines
+        whose problems run one after another)."""
         self.device = torch.device(device)
         self.spec = dataclasses.replace(spec)
         self.sizes = ctpt.query_sizes(self.spec)
-        self.ws = torch.empty(self.sizes.workspace_bytes, dtype=torch.uint8, device=self.device)
+        self.ws = (torch.empty(self.sizes.workspace_bytes, dtype=torch.uint8, device=self.device) if alloc_ws
+                   else torch.empty(0, dtype=torch.uint8, device=self.device))
         self.ctmat = None
         self.plain = None
 

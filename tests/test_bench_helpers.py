@@ -19,12 +19,44 @@ def test_roofline_fused_bytes_and_fraction():
     assert abs(r["frac"] - r["achieved"] / 6556.2) < 1e-12
 
 
-def test_host_launch_count_matches_library_chunking():
+def test_kernel_path_mirrors_the_library_choice():
+    """bench.kernel_path = ctpt.cu choose_path under CTPT_KERNEL_AUTO (launch counting, roofline)."""
+    assert bench.kernel_path(16384, 1, 1, 8) == "split_gemm"   # c3: u8 plane with offset
+    assert bench.kernel_path(256, 1, 0, 0) == "fused"
+    assert bench.kernel_path(256, 1, 1, 8) == "split_gemm"     # fused kernel has no row correction
+    assert bench.kernel_path(32, 1, 0, 0) == "mv"
+    assert bench.kernel_path(100, 2, 0, 0) == "split_gemm"     # kU > 1
+
+
+def test_both_arms_report_the_same_config():
+    """The reference (oracle) arm and our arm build `config` with the same function."""
+    import argparse
+
     c = ctgen.CONFIGS["c3"]
-    chunk = ((c.R + 5) // 6 + 63) // 64 * 64  # ctpt.cu host_plan default
-    n_chunks = -(-c.R // chunk)
-    assert bench.host_launches(c, 3, 1, True) == 3 * n_chunks * 3   # layout + split + GEMM per chunk
-    assert bench.host_launches(c, 2, 1, False) == 2 * n_chunks * 2  # layout + fused
+    for world in (1, 2, 8):
+        for mode in ("auto", "strong", "weak"):
+            args = argparse.Namespace(mode=mode)
+            m = bench.arm_mode(args, world)
+            assert bench.config_for(c, world, m) == bench.config_for(c, world, "weak" if mode == "weak" else "strong")
+    assert "strong" in bench.config_for(c, 8, "strong")["parallelism"]
+
+
+def test_gpus_flag_relaunches_under_torchrun_and_refuses_a_mismatch(tmp_path):
+    """`bench.py --gpus 2` outside torchrun re-runs itself as 2 ranks (here the reference arm on
+    c1, which needs no GPU: rank 0 prints one JSON line with n_gpus = 2, the other rank exits 0);
+    under a launcher whose WORLD_SIZE differs from --gpus it refuses to run (exit 2)."""
+    import subprocess
+
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--impl", "reference",
+                        "--config", "c1", "--steps", "1", "--warmup", "0"], capture_output=True, text=True, env=env,
+                       timeout=600, cwd=str(tmp_path))
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1 and lines[0]["n_gpus"] == 2 and lines[0]["impl"] == "reference", r.stdout
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--impl", "reference"],
+                       capture_output=True, text=True, env=dict(env, WORLD_SIZE="1"), timeout=120)
+    assert r.returncode == 2 and "refusing" in r.stderr
 
 
 def test_cublaslt_ratio_uses_burst_for_short_runs():

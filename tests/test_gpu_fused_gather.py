@@ -1,8 +1,9 @@
 """The fused compute + gather path (paper_2503_16080_b200/shard.py: share_gather_buffers,
 run_fused_gather) on one B200: two processes, both on cuda:0, gloo for the handle exchange and
 the barrier.  Rank 1's GEMM epilogues store its units' residues straight into rank 0's output
-buffer through a CUDA IPC mapping — the same code path that, on a multi-GPU node, writes over
-NVLink into rank 0's HBM.  No kernel waits on another process (only a host barrier after both
+buffer through a CUDA IPC mapping opened on rank 1's current device (ctpt_ipc_open, peer access
+enabled as needed) — the same code path that, on a multi-GPU node, writes over NVLink into rank
+0's HBM.  No kernel waits on another process (only a host barrier after both
 finished), so sharing one GPU is safe.  The gathered result must equal the oracle everywhere."""
 import os
 import socket
@@ -43,17 +44,17 @@ def _worker(rank, world, port, cfg, out_path):
     plan = plan_units(L, d3, world)
     out_AU = torch.full((L, d3, ra), -1, dtype=torch.int32, device="cuda") if rank == 0 else None
     out_BU = torch.full((L, d3, d1), -1, dtype=torch.int32, device="cuda") if rank == 0 else None
-    peer_AU, peer_BU = share_gather_buffers(out_AU, out_BU, rank)
+    peers = share_gather_buffers(out_AU, out_BU, rank, L, d3, ra, d1)
 
     def cts(l):
         ct = ctgen.encrypt(fmt, N, d1, d2, 5, 20, [ps[l]])
         return ct.a_polys[0], ct.b_polys[0]
 
     compute_into = gpu_compute_into_fn(fmt, N, d1, d2, d3, ps, cts, U, "cuda")
-    run_fused_gather(plan, rank, compute_into, peer_AU, peer_BU)
+    run_fused_gather(plan, rank, compute_into, peers)
     if rank == 0:
         np.savez(out_path, AU=out_AU.cpu().numpy().view(np.uint32), BU=out_BU.cpu().numpy().view(np.uint32))
-    del peer_AU, peer_BU
+    peers.close()
     dist.barrier()
     dist.destroy_process_group()
 
