@@ -14,6 +14,7 @@
 #include "../../include/ctpt.h"
 #include "gemm_tc.cuh"
 #include "gemm_fused.cuh"
+#include "gemm_fused_t.cuh"
 #include "gemm_mv.cuh"
 #include "kernels.cuh"
 
@@ -320,6 +321,22 @@ bool on_current_device(const void* p) {
   return a.type == cudaMemoryTypeDevice && a.device == dev;
 }
 
+// 2-D uint32 tensor [dim1][dim0] (the stacked int32 X of one prime) read in boxes of 32 rows × 32
+// residues (128 B) with SWIZZLE_128B: the raw tiles of the limbs-in-TMEM skinny kernel.
+ctpt_status make_tmap_u32_sw128(CUtensorMap* m, const void* base, uint64_t dim0, uint64_t dim1) {
+  auto enc = get_encode();
+  if (!enc) return fail(CTPT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {dim0, dim1};
+  cuuint64_t strides[1] = {dim0 * 4};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CTPT_ERR_CUDA, "cuTensorMapEncodeTiled (raw X) failed (%d)", static_cast<int>(r));
+  return CTPT_OK;
+}
+
 int num_sms() {
   int dev = 0, n = 0;
   if (cudaGetDevice(&dev) != cudaSuccess ||
@@ -342,6 +359,8 @@ ctpt_status tc_setup() {
     e = cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BYTES);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_fused<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(1));
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_fused<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(2));
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_fused_t<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, ft_smem_bytes(128));
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_fused_t<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, ft_smem_bytes(256));
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
@@ -810,6 +829,37 @@ ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st) 
   P.o = g.o;
   P.o.accumulate = 0;
   P.o.w = 1;
+#ifndef CTPT_FUSED_SMEM_LIMBS  // A/B build switch (tools/ab_build.py): the limbs-in-shared-memory kernel below
+  {
+    // limbs in tensor memory (gemm_fused_t.cuh): 32-row tiles, MMA N = d3_loc rounded up to 16
+    FusedTParams T;
+    T.R = g.R;
+    T.j_off = static_cast<int32_t>(d.j0);
+    T.plane = g.plane0;
+    T.num_kb = static_cast<int32_t>((d.d2p + FT_BK - 1) / FT_BK);
+    const int64_t ntt = (g.R + FT_ROWS - 1) / FT_ROWS;
+    if (ntt > INT32_MAX) return fail(CTPT_ERR_SHAPE, "too many tiles");
+    T.num_tiles = static_cast<int32_t>(ntt);
+    T.np = static_cast<int32_t>((d.d3_loc + 15) / 16 * 16);
+    T.u_unsigned = g.u_unsigned;
+    T.m = P.m;
+    T.o = P.o;
+    CUtensorMap tmUt, tmXt;
+    s = make_tmap_u8(&tmUt, g.planes, d.d2, d.d3, g.nplanes, d.d2p, d.d3 * d.d2p, FT_BK, static_cast<uint32_t>(T.np), 1);
+    if (s != CTPT_OK) return s;
+    s = make_tmap_u32_sw128(&tmXt, x, d.d2p, g.R);
+    if (s != CTPT_OK) return s;
+    const int64_t cap = grid_cap(g.max_ctas);
+    const int64_t rounds = (ntt + cap - 1) / cap;
+    const unsigned grid = static_cast<unsigned>((ntt + rounds - 1) / rounds);
+    if (T.np <= 128)
+      k_gemm_fused_t<128><<<grid, FT_THREADS, ft_smem_bytes(128), st>>>(tmUt, tmXt, T);
+    else
+      k_gemm_fused_t<256><<<grid, FT_THREADS, ft_smem_bytes(256), st>>>(tmUt, tmXt, T);
+    CUDA_TRY(cudaGetLastError());
+    return CTPT_OK;
+  }
+#endif
   // balanced persistent grid: the same number of rounds as min(nt, SMs) CTAs would take, spread
   // over as few CTAs as that needs, so no round ends with most SMs idle behind a few stragglers
   // (an HBM-bound CTA can pull more than 1/148 of the bandwidth; profiles/r01/fused_balanced_grid/)

@@ -1,0 +1,331 @@
+// gemm_fused_t.cuh — the skinny-U limb GEMM with the limb split fused into its load path and the
+// byte limbs kept in TENSOR MEMORY (32 < d3 ≤ 256; Table 4's d3 ∈ {2^6,
+// 2^7}).
+//
+// Same contraction and epilogue arithmetic as gemm_tc.cuh / gemm_fused.cuh (C_ℓ = X_ℓ·U over Z,
+// out = Σ 2^{8ℓ} C_ℓ mod p), same "read X exactly once" schedule as gemm_fused.cuh,
+// but the operands swap roles so that the limbs never touch shared memory:
+//   MMA A = the limb tile in TMEM (tcgen05.mma …, [a-tmem]): M = 128 lanes = 32 rows of X × 4
+//           limbs — lane 4r'+ℓ of quadrant q holds limb ℓ of row q + 4r' of the tile, its 32-bit
+//           columns 4 consecutive residues' bytes (K-major);
+//   MMA B = U^T (N = d3_loc rounded up to 16, ≤ 256 rows × 128 B per K-block, TMA, SWIZZLE_128B);
+//   D     = 128 lanes × N columns: lane (r', ℓ) holds C_ℓ[row][j] for every j.
+// So the converters store their PRMT byte transposes with tcgen05.st (STTM, 256 B/clk) instead
+// of STS into a swizzled shared-memory image that the MMA then re-reads, and N is d3 itself (no
+// second M = 128 group padded to 256 columns for 128 < d3 < 256).  The four limb sums of an output
+// sit in four neighbouring lanes: the epilogue recombines them with a two-round shuffle
+// reduce-scatter (each lane ends with Σ_ℓ 2^{8ℓ}·C_ℓ for one column of every group of four) and
+// reduces mod p with the same Barrett step.
+//
+// Converter data path per K-block (32 rows × 128 residues, 16 KB): TMA raw tiles (4 boxes of
+// 32 rows × 32 residues, SWIZZLE_128B) → LDS.128 (lane (r', ℓ') takes residues 16i + 4ℓ' .. +3 of
+// row q + 4r'; the row stride of 4 makes the 8 lanes of each LDS phase hit 8 distinct 16-B bank
+// groups under the swizzle) → PRMT 4×4 byte transpose → two shfl.xor rounds (4×4 word transpose
+// between the four lanes of a row) → 32 words = one 32-column TMEM row per lane → STTM.
+// Two converter groups (warps 8–11, 12–15) take alternate K-blocks; every ring length is even so a
+// stage always meets the same group (round 1's parity lesson, gemm_fused.cuh).
+// Warp roles (512 threads): w0 U^T TMA, w1 MMA issuer, w2 TMEM allocator, w3 raw X TMA,
+// w4–7 epilogue, w8–15 converters.
+#pragma once
+#include <cstdint>
+
+#include "kernels.cuh"
+#include "ptx.cuh"
+
+namespace ctpt {
+
+constexpr int FT_ROWS = 32;          // rows of X per tile (× 4 limbs = MMA M = 128)
+constexpr int FT_BK = 128;           // residues (K bytes of each limb row) per K-block
+constexpr int FT_MMA_K = 32;
+constexpr int FT_RAW_BYTES = FT_ROWS * FT_BK * 4;   // 16 KB: 4 TMA boxes of 32 rows × 32 residues
+constexpr int FT_THREADS = 512;
+constexpr int FT_AST = 8;            // limb (A) stages in TMEM, 32 columns each
+constexpr int FT_US = 4;             // U^T stages in shared memory
+// NPMAX = 256: one D buffer (256 columns) + 8 A stages; NPMAX = 128: two D buffers + 8 A stages
+__host__ __device__ constexpr int ft_u_bytes(int npmax) { return npmax * 128; }
+__host__ __device__ constexpr int ft_raw_stages(int npmax) { return npmax == 256 ? 6 : 10; }
+__host__ __device__ constexpr int ft_nbuf(int npmax) { return npmax == 256 ? 1 : 2; }
+__host__ __device__ constexpr int ft_smem_bytes(int npmax) {
+  return FT_US * ft_u_bytes(npmax) + ft_raw_stages(npmax) * FT_RAW_BYTES + 512 + 1024;
+}
+
+struct FusedTParams {
+  int64_t R;
+  int32_t j_off;       // first U column (col_begin)
+  int32_t plane;       // U digit plane (3rd TMA coordinate)
+  int32_t num_kb;      // ceil(d2p / 128)
+  int32_t num_tiles;   // ceil(R / 32)
+  int32_t np;          // MMA N = d3_loc rounded up to 16 (≤ NPMAX)
+  int32_t u_unsigned;  // U plane is u8 (U + u_offset, u_offset = 0 here) instead of balanced s8 digits
+  ModP m;
+  OutParams o;
+};
+
+// D[tmem] (+)= A[tmem] · B[smem]^T, kind::i8 (A from tensor memory).
+__device__ __forceinline__ void mma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// 32 lanes × 32 bit, 32 consecutive columns per thread: registers → TMEM.
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// 4×4 transpose of 32-bit words between the four lanes a = lane & 3 of a row group: on entry
+// lane a holds T[a][0..3] in w[0..3]; on exit lane a holds T[0..3][a] in w[0..3].
+__device__ __forceinline__ void transpose4_lanes(uint32_t (&w)[4], int a) {
+  // round 1 (xor 1): exchange the two words whose index parity differs from the lane's
+  const bool odd = a & 1;
+  {
+    const uint32_t s0 = odd ? w[0] : w[1], s1 = odd ? w[2] : w[3];
+    const uint32_t r0 = __shfl_xor_sync(0xffffffffu, s0, 1), r1 = __shfl_xor_sync(0xffffffffu, s1, 1);
+    // lane a keeps m ∈ {a&1, (a&1)+2}: T[a][m] and T[a^1][m]
+    if (odd) { w[0] = r0; w[2] = r1; } else { w[1] = r0; w[3] = r1; }
+  }
+  // now (even a): w = {T[a][0], T[a^1][0], T[a][2], T[a^1][2]}; (odd a): {T[a^1][1], T[a][1], T[a^1][3], T[a][3]}
+  // i.e. in both cases w[2x + y] = T[(a & ~1) | y][(a & 1) + 2x]
+  {
+    const bool hi = a & 2;
+    // lane a needs m = a: x = (a >> 1); it sends the pair with x' = 1 − (a >> 1)
+    const uint32_t s0 = hi ? w[0] : w[2], s1 = hi ? w[1] : w[3];
+    const uint32_t r0 = __shfl_xor_sync(0xffffffffu, s0, 2), r1 = __shfl_xor_sync(0xffffffffu, s1, 2);
+    // received T[(a^2) & ~1 | y][a] for y = 0, 1
+    const uint32_t k0 = hi ? w[2] : w[0], k1 = hi ? w[3] : w[1];  // own T[(a & ~1) | y][a]
+    // rows: a & ~1 ∈ {0, 2}; output order T[0][a], T[1][a], T[2][a], T[3][a]
+    if (hi) { w[0] = r0; w[1] = r1; w[2] = k0; w[3] = k1; }
+    else { w[0] = k0; w[1] = k1; w[2] = r0; w[3] = r1; }
+  }
+}
+
+template <int NPMAX>
+__global__ void __launch_bounds__(FT_THREADS, 1)
+    k_gemm_fused_t(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmX,
+                   const __grid_constant__ FusedTParams P) {
+  constexpr int U_BYTES = ft_u_bytes(NPMAX);
+  constexpr int RAW = ft_raw_stages(NPMAX);
+  constexpr int NBUF = ft_nbuf(NPMAX);
+  constexpr uint32_t A_COL0 = NBUF * NPMAX;  // TMEM columns [A_COL0, A_COL0 + 32·FT_AST) hold the limb stages
+  static_assert(A_COL0 + 32 * FT_AST <= 512, "TMEM budget");
+  static_assert(RAW % 2 == 0 && FT_AST % 2 == 0, "ring lengths must be even (two converter groups)");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t raw_base = sbase + FT_US * U_BYTES;
+  const uint32_t bar_base = raw_base + RAW * FT_RAW_BYTES;
+  auto u_full = [&](int s) { return bar_base + 8u * s; };
+  auto u_empty = [&](int s) { return bar_base + 8u * (FT_US + s); };
+  auto raw_full = [&](int s) { return bar_base + 8u * (2 * FT_US + s); };
+  auto raw_empty = [&](int s) { return bar_base + 8u * (2 * FT_US + RAW + s); };
+  auto a_full = [&](int s) { return bar_base + 8u * (2 * FT_US + 2 * RAW + s); };
+  auto a_empty = [&](int s) { return bar_base + 8u * (2 * FT_US + 2 * RAW + FT_AST + s); };
+  auto d_full = [&](int b) { return bar_base + 8u * (2 * FT_US + 2 * RAW + 2 * FT_AST + b); };
+  auto d_empty = [&](int b) { return bar_base + 8u * (2 * FT_US + 2 * RAW + 2 * FT_AST + 2 + b); };
+  constexpr int NBAR = 2 * FT_US + 2 * RAW + 2 * FT_AST + 4;
+  static_assert(8 * NBAR + 8 <= 512, "barrier area");
+  const uint32_t tmem_slot = bar_base + 8u * NBAR;
+  uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(smem + FT_US * U_BYTES + RAW * FT_RAW_BYTES + 8 * NBAR);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int32_t my_tiles =
+      (P.num_tiles > static_cast<int32_t>(blockIdx.x)) ? (P.num_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t n_it = static_cast<int64_t>(my_tiles) * P.num_kb;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmU);
+    tma_prefetch(&tmX);
+    for (int s = 0; s < FT_US; ++s) {
+      mbar_init(u_full(s), 1);
+      mbar_init(u_empty(s), 1);
+    }
+    for (int s = 0; s < RAW; ++s) {
+      mbar_init(raw_full(s), 1);
+      mbar_init(raw_empty(s), 4);  // the four converter warps of the group that consumed it
+    }
+    for (int s = 0; s < FT_AST; ++s) {
+      mbar_init(a_full(s), 4);
+      mbar_init(a_empty(s), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(d_full(b), 1);
+      mbar_init(d_empty(b), 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot_ptr;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- U^T TMA producer
+    if (lane == 0) {
+      const uint32_t ubytes = static_cast<uint32_t>(P.np) * 128u;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t it = 0; it < n_it; ++it) {
+        const int32_t kb = static_cast<int32_t>(it % P.num_kb);
+        mbar_wait(u_empty(stage), phase ^ 1);
+        mbar_arrive_expect_tx(u_full(stage), ubytes);
+        tma_load_3d(sbase + stage * U_BYTES, &tmU, u_full(stage), kb * FT_BK, P.j_off, P.plane);
+        if (++stage == FT_US) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      // A = u8 limbs, B = U^T digits (s8, or u8 in the unsigned-plane mode), D = s32
+      const uint32_t idesc = idesc_i8(128, static_cast<uint32_t>(P.np), /*a_signed=*/false, /*b_signed=*/!P.u_unsigned);
+      int us = 0, as = 0, acc = 0;
+      uint32_t uph = 0, aph = 0, acc_phase = 0;
+      for (int32_t t = 0; t < my_tiles; ++t) {
+        mbar_wait(d_empty(acc), acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * NPMAX;
+        for (int32_t kb = 0; kb < P.num_kb; ++kb) {
+          mbar_wait(a_full(as), aph);
+          mbar_wait(u_full(us), uph);
+          tc_fence_after();
+          const uint32_t su = sbase + us * U_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < FT_BK / FT_MMA_K; ++kk)
+            mma_i8_ts(d_tmem, tmem_base + A_COL0 + as * 32 + kk * (FT_MMA_K / 4), umma_desc_sw128(su + kk * FT_MMA_K),
+                      idesc, (kb | kk) != 0);
+          mma_commit(a_empty(as));  // the limb stage and the U^T stage are free once these MMAs are done
+          mma_commit(u_empty(us));
+          if (++as == FT_AST) { as = 0; aph ^= 1; }
+          if (++us == FT_US) { us = 0; uph ^= 1; }
+        }
+        mma_commit(d_full(acc));
+        if (++acc == NBUF) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp == 3) {
+    // ---------------------------------------------------------------- raw X TMA producer
+    if (lane == 0) {
+      int rs = 0;
+      uint32_t rphase = 0;
+      for (int64_t it = 0; it < n_it; ++it) {
+        const int32_t tr = static_cast<int32_t>(blockIdx.x) + static_cast<int32_t>(it / P.num_kb) * gridDim.x;
+        const int32_t kb = static_cast<int32_t>(it % P.num_kb);
+        mbar_wait(raw_empty(rs), rphase ^ 1);
+        mbar_arrive_expect_tx(raw_full(rs), FT_RAW_BYTES);
+        const uint32_t dst = raw_base + rs * FT_RAW_BYTES;
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          tma_load_2d(dst + b * 4096, &tmX, raw_full(rs), kb * FT_BK + 32 * b, tr * FT_ROWS);
+        if (++rs == RAW) { rs = 0; rphase ^= 1; }
+      }
+    }
+  } else if (warp < 8) {
+    // ---------------------------------------------------------------- epilogue (warps 4–7)
+    const int q = warp & 3;                 // TMEM lanes [32q, 32q + 32)
+    const int rp = lane >> 2, l4 = lane & 3;  // row q + 4·rp of the tile, limb l4
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int32_t t = 0; t < my_tiles; ++t) {
+      const int64_t tr = static_cast<int64_t>(blockIdx.x) + static_cast<int64_t>(t) * gridDim.x;
+      const int64_t row = tr * FT_ROWS + q + 4 * rp;
+      mbar_wait(d_full(acc), acc_phase);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * NPMAX;
+#pragma unroll 1
+      for (int c0 = 0; c0 < P.np; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32(t_row + c0, v);
+        tmem_ld_wait();
+        if (c0 + 32 >= P.np) {  // every column read: hand the accumulator back before the last stores
+          tc_fence_before();
+          mbar_arrive(d_empty(acc));
+        }
+        // reduce-scatter over the four limb lanes of this row: lane l4 ends with the full
+        // Σ_ℓ 2^{8ℓ} C_ℓ for column c0 + 4g + l4 of every group g of four columns
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          // round 1 (xor 1): keep columns s with (s & 1) == (l4 & 1), send the other two
+          const bool odd = l4 & 1;
+          const int32_t c0v = static_cast<int32_t>(v[4 * g]), c1v = static_cast<int32_t>(v[4 * g + 1]);
+          const int32_t c2v = static_cast<int32_t>(v[4 * g + 2]), c3v = static_cast<int32_t>(v[4 * g + 3]);
+          const int32_t k0 = odd ? c1v : c0v, k1 = odd ? c3v : c2v;  // kept: columns (l4 & 1), (l4 & 1) + 2
+          const int32_t s0 = odd ? c0v : c1v, s1 = odd ? c2v : c3v;  // sent to lane l4 ^ 1
+          const int32_t r0 = __shfl_xor_sync(0xffffffffu, s0, 1), r1 = __shfl_xor_sync(0xffffffffu, s1, 1);
+          // partial sums over limbs {l4, l4 ^ 1} for columns s = (l4 & 1) and (l4 & 1) + 2
+          const int sh_own = 8 * l4, sh_par = 8 * (l4 ^ 1);
+          const int64_t p0 = (static_cast<int64_t>(k0) << sh_own) + (static_cast<int64_t>(r0) << sh_par);
+          const int64_t p1 = (static_cast<int64_t>(k1) << sh_own) + (static_cast<int64_t>(r1) << sh_par);
+          // round 2 (xor 2): keep column s = l4 (p0 if l4 < 2 else p1), send the other
+          const bool hi = l4 & 2;
+          const int64_t keep = hi ? p1 : p0, send = hi ? p0 : p1;
+          const int64_t recv = static_cast<int64_t>(
+              (static_cast<uint64_t>(static_cast<uint32_t>(__shfl_xor_sync(0xffffffffu, static_cast<uint32_t>(send >> 32), 2))) << 32) |
+              static_cast<uint32_t>(__shfl_xor_sync(0xffffffffu, static_cast<uint32_t>(send), 2)));
+          const int64_t tsum = keep + recv;
+          const int64_t j = static_cast<int64_t>(c0) + 4 * g + l4;
+          if (j < P.o.d3_loc && row < P.o.R)
+            *out_ptr(P.o, j, row) = barrett64(static_cast<uint64_t>(tsum + static_cast<int64_t>(P.m.off)), P.m);
+        }
+      }
+      if (++acc == NBUF) { acc = 0; acc_phase ^= 1; }
+    }
+  } else {
+    // ---------------------------------------------------------------- converters (warps 8–15)
+    const int cw = warp - 8;
+    const int q = cw & 3, grp = cw >> 2;   // TMEM quadrant (warp % 4 == q, as tcgen05.st requires); K-block parity
+    const int rp = lane >> 2, l4 = lane & 3;
+    const int row = q + 4 * rp;            // row of the 32-row tile this lane's limb lane belongs to
+    const uint32_t t_lane = static_cast<uint32_t>(q * 32) << 16;
+    for (int64_t it = grp; it < n_it; it += 2) {
+      const int rs = static_cast<int>(it % RAW);
+      const int as = static_cast<int>(it % FT_AST);
+      mbar_wait(raw_full(rs), static_cast<uint32_t>((it / RAW) & 1));
+      const uint32_t raw = raw_base + rs * FT_RAW_BYTES;
+      uint32_t col[32];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        // residues 16i + 4·l4 .. +3 of this row: box i/2, 16-B chunk 4(i&1) + l4 of its 128-B row
+        const int cb = 4 * (i & 1) + l4;
+        const uint4 x = lds128(raw + (i >> 1) * 4096 + row * 128 + ((cb ^ (row & 7)) << 4));
+        uint32_t w[4];
+        byte_transpose4(x.x, x.y, x.z, x.w, w[0], w[1], w[2], w[3]);  // w[m] = limb m of the 4 residues
+        transpose4_lanes(w, l4);  // w[a] = limb l4 of residues 16i + 4a .. +3
+        col[4 * i + 0] = w[0];
+        col[4 * i + 1] = w[1];
+        col[4 * i + 2] = w[2];
+        col[4 * i + 3] = w[3];
+      }
+      fence_proxy_async_smem();  // release the raw tile only after its values are consumed
+      __syncwarp();
+      if (lane == 0) mbar_arrive(raw_empty(rs));
+      mbar_wait(a_empty(as), static_cast<uint32_t>(((it / FT_AST) & 1) ^ 1));
+      tc_fence_after();
+      tmem_st32(tmem_base + t_lane + A_COL0 + as * 32, col);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(a_full(as));
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem_base);
+  }
+}
+
+}  // namespace ctpt
