@@ -307,12 +307,16 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
         col[4 * i + 2] = w[2];
         col[4 * i + 3] = w[3];
       }
-      fence_proxy_async_smem();  // release the raw tile only after its values are consumed
-      __syncwarp();
-      if (lane == 0) mbar_arrive(raw_empty(rs));
       mbar_wait(a_empty(as), static_cast<uint32_t>(((it / FT_AST) & 1) ^ 1));
       tc_fence_after();
       tmem_st32(tmem_base + t_lane + A_COL0 + as * 32, col);
+      // The raw tile is handed back only here: the STTM takes every transposed word as an operand,
+      // so every LDS of the tile has completed (register computations such as the PRMTs and SHFLs
+      // may be scheduled past a fence; an asm operand may not), then a proxy fence orders the
+      // generic reads before the TMA's async-proxy refill.
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(raw_empty(rs));
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();

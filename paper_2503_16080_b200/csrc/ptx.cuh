@@ -3,6 +3,9 @@
 #pragma once
 #include <cstdint>
 #include <cuda.h>
+#ifdef CTPT_DEBUG_HANG
+#include <cstdio>
+#endif
 
 namespace ctpt {
 
@@ -23,6 +26,25 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t byt
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+#ifdef CTPT_DEBUG_HANG
+// Debug builds only (tools/ab_build.py -DCTPT_DEBUG_HANG): a wait that has not completed after
+// ~2^26 polls reports the barrier and traps instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  for (uint32_t n = 0; n < (1u << 26); ++n) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (done) return;
+  }
+  printf("ctpt hang: block %d thread %d barrier smem+%u parity %u\n", blockIdx.x, threadIdx.x, bar, parity);
+  __trap();
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
@@ -32,6 +54,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+#endif
 
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* m) {
