@@ -170,6 +170,11 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot_ptr;
+#ifdef CTPT_DEBUG_HANG
+  if (threadIdx.x == 0 && blockIdx.x < 2)
+    printf("fused_t block %d: tmem_base %u bar_base %u n_it %lld my_tiles %d\n", blockIdx.x, tmem_base, bar_base,
+           (long long)n_it, my_tiles);
+#endif
 
   if (warp == 0) {
     // ---------------------------------------------------------------- U^T TMA producer
@@ -231,7 +236,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
         if (++rs == RAW) { rs = 0; rphase ^= 1; }
       }
     }
-  } else if (warp < 8) {
+  } else if (warp >= 4 && warp < 8) {  // (warp 2, the TMEM allocator, idles until the dealloc)
     // ---------------------------------------------------------------- epilogue (warps 4–7)
     const int q = warp & 3;                 // TMEM lanes [32q, 32q + 32)
     const int rp = lane >> 2, l4 = lane & 3;  // row q + 4·rp of the tile, limb l4
@@ -281,7 +286,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
       }
       if (++acc == NBUF) { acc = 0; acc_phase ^= 1; }
     }
-  } else {
+  } else if (warp >= 8) {
     // ---------------------------------------------------------------- converters (warps 8–15)
     const int cw = warp - 8;
     const int q = cw & 3, grp = cw >> 2;   // TMEM quadrant (warp % 4 == q, as tcgen05.st requires); K-block parity

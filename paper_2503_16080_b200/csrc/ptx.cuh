@@ -28,10 +28,16 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 }
 #ifdef CTPT_DEBUG_HANG
 // Debug builds only (tools/ab_build.py -DCTPT_DEBUG_HANG): a wait that has not completed after
-// ~2^26 polls reports the barrier and traps instead of hanging the GPU.
+// 4 s (globaltimer) reports the barrier and traps instead of hanging the GPU.
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  const uint64_t t0 = globaltimer_ns();
   uint32_t done = 0;
-  for (uint32_t n = 0; n < (1u << 26); ++n) {
+  for (;;) {
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
@@ -40,6 +46,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "r"(bar), "r"(parity)
         : "memory");
     if (done) return;
+    if (globaltimer_ns() - t0 > 4000000000ull) break;
   }
   printf("ctpt hang: block %d thread %d barrier smem+%u parity %u\n", blockIdx.x, threadIdx.x, bar, parity);
   __trap();
