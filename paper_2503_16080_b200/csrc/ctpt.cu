@@ -359,8 +359,8 @@ ctpt_status tc_setup() {
     e = cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BYTES);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_fused<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(1));
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_fused<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(2));
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_fused_t<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, ft_smem_bytes(128));
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_fused_t<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, ft_smem_bytes(256));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_gemm_fused_t<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ft_smem_bytes(128, 2));
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
@@ -829,15 +829,17 @@ ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st) 
   P.o = g.o;
   P.o.accumulate = 0;
   P.o.w = 1;
-#ifndef CTPT_FUSED_SMEM_LIMBS  // A/B build switch (tools/ab_build.py): the limbs-in-shared-memory kernel below
-  {
-    // limbs in tensor memory (gemm_fused_t.cuh): 32-row tiles, MMA N = d3_loc rounded up to 16
+#ifndef CTPT_FUSED_SMEM_LIMBS  // A/B build switch (tools/ab_build.py): the limbs-in-shared-memory kernel for all d3
+  if (d.d3_loc <= 128) {
+    // limbs in tensor memory (gemm_fused_t.cuh): 64-row tiles (two 32-row sub-tiles sharing each U^T
+    // stage), MMA N = d3_loc rounded up to 16.  Measured against the limbs-in-shared-memory kernel
+    // on c4's ciphertexts: profiles/r02/fused_tmem_*; for 128 < d3_loc ≤ 256 that kernel stays.
     FusedTParams T;
     T.R = g.R;
     T.j_off = static_cast<int32_t>(d.j0);
     T.plane = g.plane0;
     T.num_kb = static_cast<int32_t>((d.d2p + FT_BK - 1) / FT_BK);
-    const int64_t ntt = (g.R + FT_ROWS - 1) / FT_ROWS;
+    const int64_t ntt = (g.R + ft_rows(2) - 1) / ft_rows(2);
     if (ntt > INT32_MAX) return fail(CTPT_ERR_SHAPE, "too many tiles");
     T.num_tiles = static_cast<int32_t>(ntt);
     T.np = static_cast<int32_t>((d.d3_loc + 15) / 16 * 16);
@@ -852,10 +854,7 @@ ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st) 
     const int64_t cap = grid_cap(g.max_ctas);
     const int64_t rounds = (ntt + cap - 1) / cap;
     const unsigned grid = static_cast<unsigned>((ntt + rounds - 1) / rounds);
-    if (T.np <= 128)
-      k_gemm_fused_t<128><<<grid, FT_THREADS, ft_smem_bytes(128), st>>>(tmUt, tmXt, T);
-    else
-      k_gemm_fused_t<256><<<grid, FT_THREADS, ft_smem_bytes(256), st>>>(tmUt, tmXt, T);
+    k_gemm_fused_t<128, 2><<<grid, FT_THREADS, ft_smem_bytes(128, 2), st>>>(tmUt, tmXt, T);
     CUDA_TRY(cudaGetLastError());
     return CTPT_OK;
   }

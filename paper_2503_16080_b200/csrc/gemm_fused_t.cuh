@@ -34,19 +34,28 @@
 
 namespace ctpt {
 
-constexpr int FT_ROWS = 32;          // rows of X per tile (× 4 limbs = MMA M = 128)
+constexpr int FT_SUB_ROWS = 32;      // rows of X per MMA (× 4 limbs = MMA M = 128)
 constexpr int FT_BK = 128;           // residues (K bytes of each limb row) per K-block
 constexpr int FT_MMA_K = 32;
-constexpr int FT_RAW_BYTES = FT_ROWS * FT_BK * 4;   // 16 KB: 4 TMA boxes of 32 rows × 32 residues
+constexpr int FT_BOX_BYTES = 4096;   // one raw TMA box: 32 rows × 32 residues
 constexpr int FT_THREADS = 512;
-constexpr int FT_AST = 8;            // limb (A) stages in TMEM, 32 columns each
 constexpr int FT_US = 4;             // U^T stages in shared memory
-// NPMAX = 256: one D buffer (256 columns) + 8 A stages; NPMAX = 128: two D buffers + 8 A stages
+// Two shapes (template <NPMAX, SUB>):
+//   SUB = 2, NPMAX = 128 (d3_loc ≤ 128): a tile is 64 rows = two 32-row sub-tiles that share each
+//     U^T stage (U^T is read from L2 once per 64 rows, as in gemm_fused.cuh); one D buffer of
+//     2 × 128 columns + 4 A stages of 2 × 32 columns; the 8 converter warps split every K-block
+//     (warp 8 + 4s + q: sub-tile s, quadrant q);
+//   SUB = 1, NPMAX = 256: 32-row tiles, one D buffer of 256 columns + 8 A stages of 32 columns;
+//     two converter groups of 4 warps take alternate K-blocks.  (Measured slower than the
+//     limbs-in-shared-memory kernel for 128 < d3 ≤ 256 — U^T is then re-read from L2 once per 32
+//     rows, 2 B per byte of X — so ctpt_matmul does not use it; profiles/r02/fused_tmem_v1/.)
+__host__ __device__ constexpr int ft_rows(int sub) { return 32 * sub; }
+__host__ __device__ constexpr int ft_raw_bytes(int sub) { return sub * 4 * FT_BOX_BYTES; }
 __host__ __device__ constexpr int ft_u_bytes(int npmax) { return npmax * 128; }
-__host__ __device__ constexpr int ft_raw_stages(int npmax) { return npmax == 256 ? 6 : 10; }
-__host__ __device__ constexpr int ft_nbuf(int npmax) { return npmax == 256 ? 1 : 2; }
-__host__ __device__ constexpr int ft_smem_bytes(int npmax) {
-  return FT_US * ft_u_bytes(npmax) + ft_raw_stages(npmax) * FT_RAW_BYTES + 512 + 1024;
+__host__ __device__ constexpr int ft_raw_stages(int npmax, int sub) { return sub == 2 ? 5 : (npmax == 256 ? 6 : 10); }
+__host__ __device__ constexpr int ft_ast(int sub) { return sub == 2 ? 4 : 8; }
+__host__ __device__ constexpr int ft_smem_bytes(int npmax, int sub) {
+  return FT_US * ft_u_bytes(npmax) + ft_raw_stages(npmax, sub) * ft_raw_bytes(sub) + 512 + 1024;
 }
 
 struct FusedTParams {
@@ -54,7 +63,7 @@ struct FusedTParams {
   int32_t j_off;       // first U column (col_begin)
   int32_t plane;       // U digit plane (3rd TMA coordinate)
   int32_t num_kb;      // ceil(d2p / 128)
-  int32_t num_tiles;   // ceil(R / 32)
+  int32_t num_tiles;   // ceil(R / (32·SUB))
   int32_t np;          // MMA N = d3_loc rounded up to 16 (≤ NPMAX)
   int32_t u_unsigned;  // U plane is u8 (U + u_offset, u_offset = 0 here) instead of balanced s8 digits
   ModP m;
@@ -110,21 +119,27 @@ __device__ __forceinline__ void transpose4_lanes(uint32_t (&w)[4], int a) {
   }
 }
 
-template <int NPMAX>
+template <int NPMAX, int SUB>
 __global__ void __launch_bounds__(FT_THREADS, 1)
     k_gemm_fused_t(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmX,
                    const __grid_constant__ FusedTParams P) {
   constexpr int U_BYTES = ft_u_bytes(NPMAX);
-  constexpr int RAW = ft_raw_stages(NPMAX);
-  constexpr int NBUF = ft_nbuf(NPMAX);
-  constexpr uint32_t A_COL0 = NBUF * NPMAX;  // TMEM columns [A_COL0, A_COL0 + 32·FT_AST) hold the limb stages
-  static_assert(A_COL0 + 32 * FT_AST <= 512, "TMEM budget");
-  static_assert(RAW % 2 == 0 && FT_AST % 2 == 0, "ring lengths must be even (two converter groups)");
+  constexpr int RAW = ft_raw_stages(NPMAX, SUB);
+  constexpr int RAW_BYTES = ft_raw_bytes(SUB);
+  constexpr int FT_AST = ft_ast(SUB);
+  constexpr int ROWS = ft_rows(SUB);
+  constexpr int NBUF = 1;                      // D: SUB × NPMAX columns (one buffer)
+  constexpr int D_COLS = SUB * NPMAX;
+  constexpr int ASTAGE_COLS = SUB * 32;         // one A stage: SUB sub-tiles × 32 columns (128 residues)
+  constexpr uint32_t A_COL0 = D_COLS;           // TMEM columns [A_COL0, 512) hold the limb stages
+  constexpr int GROUPS = SUB == 1 ? 2 : 1;      // converter groups taking alternate K-blocks
+  static_assert(A_COL0 + ASTAGE_COLS * FT_AST <= 512, "TMEM budget");
+  static_assert(RAW % GROUPS == 0 && FT_AST % GROUPS == 0, "ring lengths must be multiples of the group count");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
   const uint32_t raw_base = sbase + FT_US * U_BYTES;
-  const uint32_t bar_base = raw_base + RAW * FT_RAW_BYTES;
+  const uint32_t bar_base = raw_base + RAW * RAW_BYTES;
   auto u_full = [&](int s) { return bar_base + 8u * s; };
   auto u_empty = [&](int s) { return bar_base + 8u * (FT_US + s); };
   auto raw_full = [&](int s) { return bar_base + 8u * (2 * FT_US + s); };
@@ -136,7 +151,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
   constexpr int NBAR = 2 * FT_US + 2 * RAW + 2 * FT_AST + 4;
   static_assert(8 * NBAR + 8 <= 512, "barrier area");
   const uint32_t tmem_slot = bar_base + 8u * NBAR;
-  uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(smem + FT_US * U_BYTES + RAW * FT_RAW_BYTES + 8 * NBAR);
+  uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(smem + FT_US * U_BYTES + RAW * RAW_BYTES + 8 * NBAR);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -153,10 +168,10 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
     }
     for (int s = 0; s < RAW; ++s) {
       mbar_init(raw_full(s), 1);
-      mbar_init(raw_empty(s), 4);  // the four converter warps of the group that consumed it
+      mbar_init(raw_empty(s), 8 / GROUPS);  // the converter warps that consumed it
     }
     for (int s = 0; s < FT_AST; ++s) {
-      mbar_init(a_full(s), 4);
+      mbar_init(a_full(s), 8 / GROUPS);
       mbar_init(a_empty(s), 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -200,16 +215,20 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
       for (int32_t t = 0; t < my_tiles; ++t) {
         mbar_wait(d_empty(acc), acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * NPMAX;
+        const uint32_t d_tmem = tmem_base + acc * D_COLS;
         for (int32_t kb = 0; kb < P.num_kb; ++kb) {
           mbar_wait(a_full(as), aph);
           mbar_wait(u_full(us), uph);
           tc_fence_after();
           const uint32_t su = sbase + us * U_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < FT_BK / FT_MMA_K; ++kk)
-            mma_i8_ts(d_tmem, tmem_base + A_COL0 + as * 32 + kk * (FT_MMA_K / 4), umma_desc_sw128(su + kk * FT_MMA_K),
-                      idesc, (kb | kk) != 0);
+          for (int kk = 0; kk < FT_BK / FT_MMA_K; ++kk) {
+            const uint64_t bd = umma_desc_sw128(su + kk * FT_MMA_K);
+#pragma unroll
+            for (int sb = 0; sb < SUB; ++sb)  // the sub-tiles share the U^T stage
+              mma_i8_ts(d_tmem + sb * NPMAX, tmem_base + A_COL0 + as * ASTAGE_COLS + sb * 32 + kk * (FT_MMA_K / 4), bd,
+                        idesc, (kb | kk) != 0);
+          }
           mma_commit(a_empty(as));  // the limb stage and the U^T stage are free once these MMAs are done
           mma_commit(u_empty(us));
           if (++as == FT_AST) { as = 0; aph ^= 1; }
@@ -228,11 +247,14 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
         const int32_t tr = static_cast<int32_t>(blockIdx.x) + static_cast<int32_t>(it / P.num_kb) * gridDim.x;
         const int32_t kb = static_cast<int32_t>(it % P.num_kb);
         mbar_wait(raw_empty(rs), rphase ^ 1);
-        mbar_arrive_expect_tx(raw_full(rs), FT_RAW_BYTES);
-        const uint32_t dst = raw_base + rs * FT_RAW_BYTES;
+        mbar_arrive_expect_tx(raw_full(rs), RAW_BYTES);
+        const uint32_t dst = raw_base + rs * RAW_BYTES;
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
-          tma_load_2d(dst + b * 4096, &tmX, raw_full(rs), kb * FT_BK + 32 * b, tr * FT_ROWS);
+        for (int sb = 0; sb < SUB; ++sb)
+#pragma unroll
+          for (int b = 0; b < 4; ++b)  // box (sub-tile sb, residues 32b..): 32 rows × 128 B, SWIZZLE_128B
+            tma_load_2d(dst + (sb * 4 + b) * FT_BOX_BYTES, &tmX, raw_full(rs), kb * FT_BK + 32 * b,
+                        tr * ROWS + sb * FT_SUB_ROWS);
         if (++rs == RAW) { rs = 0; rphase ^= 1; }
       }
     }
@@ -244,16 +266,17 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
     uint32_t acc_phase = 0;
     for (int32_t t = 0; t < my_tiles; ++t) {
       const int64_t tr = static_cast<int64_t>(blockIdx.x) + static_cast<int64_t>(t) * gridDim.x;
-      const int64_t row = tr * FT_ROWS + q + 4 * rp;
       mbar_wait(d_full(acc), acc_phase);
       tc_fence_after();
-      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * NPMAX;
 #pragma unroll 1
-      for (int c0 = 0; c0 < P.np; c0 += 32) {
+      for (int chunk = 0; chunk < SUB * ((P.np + 31) / 32); ++chunk) {
+        const int sb = chunk / ((P.np + 31) / 32), c0 = 32 * (chunk % ((P.np + 31) / 32));
+        const int64_t row = tr * ROWS + sb * FT_SUB_ROWS + q + 4 * rp;
+        const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * D_COLS + sb * NPMAX;
         uint32_t v[32];
         tmem_ld32(t_row + c0, v);
         tmem_ld_wait();
-        if (c0 + 32 >= P.np) {  // every column read: hand the accumulator back before the last stores
+        if (chunk + 1 == SUB * ((P.np + 31) / 32)) {  // every column read: hand D back before the last stores
           tc_fence_before();
           mbar_arrive(d_empty(acc));
         }
@@ -289,21 +312,24 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
   } else if (warp >= 8) {
     // ---------------------------------------------------------------- converters (warps 8–15)
     const int cw = warp - 8;
-    const int q = cw & 3, grp = cw >> 2;   // TMEM quadrant (warp % 4 == q, as tcgen05.st requires); K-block parity
+    // TMEM quadrant q (warp % 4 == q, as tcgen05.st requires); hi = the K-block parity (SUB = 1:
+    // two groups on alternate K-blocks) or the sub-tile (SUB = 2: every K-block)
+    const int q = cw & 3, hi = cw >> 2;
+    const int grp = SUB == 1 ? hi : 0, sb = SUB == 1 ? 0 : hi;
     const int rp = lane >> 2, l4 = lane & 3;
-    const int row = q + 4 * rp;            // row of the 32-row tile this lane's limb lane belongs to
+    const int row = q + 4 * rp;            // row of the 32-row sub-tile this lane's limb lane belongs to
     const uint32_t t_lane = static_cast<uint32_t>(q * 32) << 16;
-    for (int64_t it = grp; it < n_it; it += 2) {
+    for (int64_t it = grp; it < n_it; it += GROUPS) {
       const int rs = static_cast<int>(it % RAW);
       const int as = static_cast<int>(it % FT_AST);
       mbar_wait(raw_full(rs), static_cast<uint32_t>((it / RAW) & 1));
-      const uint32_t raw = raw_base + rs * FT_RAW_BYTES;
+      const uint32_t raw = raw_base + rs * RAW_BYTES + sb * 4 * FT_BOX_BYTES;
       uint32_t col[32];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         // residues 16i + 4·l4 .. +3 of this row: box i/2, 16-B chunk 4(i&1) + l4 of its 128-B row
         const int cb = 4 * (i & 1) + l4;
-        const uint4 x = lds128(raw + (i >> 1) * 4096 + row * 128 + ((cb ^ (row & 7)) << 4));
+        const uint4 x = lds128(raw + (i >> 1) * FT_BOX_BYTES + row * 128 + ((cb ^ (row & 7)) << 4));
         uint32_t w[4];
         byte_transpose4(x.x, x.y, x.z, x.w, w[0], w[1], w[2], w[3]);  // w[m] = limb m of the 4 residues
         transpose4_lanes(w, l4);  // w[a] = limb l4 of residues 16i + 4a .. +3
@@ -314,7 +340,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
       }
       mbar_wait(a_empty(as), static_cast<uint32_t>(((it / FT_AST) & 1) ^ 1));
       tc_fence_after();
-      tmem_st32(tmem_base + t_lane + A_COL0 + as * 32, col);
+      tmem_st32(tmem_base + t_lane + A_COL0 + as * ASTAGE_COLS + sb * 32, col);
       // The raw tile is handed back only here: the STTM takes every transposed word as an operand,
       // so every LDS of the tile has completed (register computations such as the PRMTs and SHFLs
       // may be scheduled past a fence; an asm operand may not), then a proxy fence orders the

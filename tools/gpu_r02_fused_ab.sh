@@ -11,7 +11,7 @@ if grep -q "tests_rc=0" gpurun_out/r02/fused_ab/tests.log; then
   for rep in 1 2; do
     for v in tmem smem; do
       if [ $v = smem ]; then export CTPT_LIB=/tmp/libctpt_smemlimbs.so; else unset CTPT_LIB; fi
-      timeout 600 python tools/bench_skinny.py --L 2 --d3 64,128,160,192,256 --paths fused --steps 10 \
+      timeout 600 python tools/bench_skinny.py --L 2 --d3 32,64,96,128,192,256 --paths fused --steps 10 \
         > gpurun_out/r02/fused_ab/sweep_${v}_$rep.jsonl 2>> gpurun_out/r02/fused_ab/err.log
       python - <<PY
 import json
