@@ -361,6 +361,10 @@ ctpt_status tc_setup() {
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_fused<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(2));
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_gemm_fused_t<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ft_smem_bytes(128, 2));
+#ifdef CTPT_FUSED_T256
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_gemm_fused_t<256, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, ft_smem_bytes(256, 1));
+#endif
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
@@ -830,7 +834,12 @@ ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st) 
   P.o.accumulate = 0;
   P.o.w = 1;
 #ifndef CTPT_FUSED_SMEM_LIMBS  // A/B build switch (tools/ab_build.py): the limbs-in-shared-memory kernel for all d3
-  if (d.d3_loc <= 128) {
+#ifdef CTPT_FUSED_T256  // A/B build switch: 32-row limbs-in-TMEM tiles for 128 < d3_loc <= 256 too
+  constexpr int64_t kTmemMaxD3 = 256;
+#else
+  constexpr int64_t kTmemMaxD3 = 128;
+#endif
+  if (d.d3_loc <= kTmemMaxD3) {
     // limbs in tensor memory (gemm_fused_t.cuh): 64-row tiles (two 32-row sub-tiles sharing each U^T
     // stage), MMA N = d3_loc rounded up to 16.  Measured against the limbs-in-shared-memory kernel
     // on c4's ciphertexts: profiles/r02/fused_tmem_*; for 128 < d3_loc ≤ 256 that kernel stays.
@@ -839,7 +848,8 @@ ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st) 
     T.j_off = static_cast<int32_t>(d.j0);
     T.plane = g.plane0;
     T.num_kb = static_cast<int32_t>((d.d2p + FT_BK - 1) / FT_BK);
-    const int64_t ntt = (g.R + ft_rows(2) - 1) / ft_rows(2);
+    const int sub = d.d3_loc <= 128 ? 2 : 1;
+    const int64_t ntt = (g.R + ft_rows(sub) - 1) / ft_rows(sub);
     if (ntt > INT32_MAX) return fail(CTPT_ERR_SHAPE, "too many tiles");
     T.num_tiles = static_cast<int32_t>(ntt);
     T.np = static_cast<int32_t>((d.d3_loc + 15) / 16 * 16);
@@ -854,7 +864,13 @@ ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st) 
     const int64_t cap = grid_cap(g.max_ctas);
     const int64_t rounds = (ntt + cap - 1) / cap;
     const unsigned grid = static_cast<unsigned>((ntt + rounds - 1) / rounds);
-    k_gemm_fused_t<128, 2><<<grid, FT_THREADS, ft_smem_bytes(128, 2), st>>>(tmUt, tmXt, T);
+    if (sub == 2) {
+      k_gemm_fused_t<128, 2><<<grid, FT_THREADS, ft_smem_bytes(128, 2), st>>>(tmUt, tmXt, T);
+    } else {
+#ifdef CTPT_FUSED_T256
+      k_gemm_fused_t<256, 1><<<grid, FT_THREADS, ft_smem_bytes(256, 1), st>>>(tmUt, tmXt, T);
+#endif
+    }
     CUDA_TRY(cudaGetLastError());
     return CTPT_OK;
   }

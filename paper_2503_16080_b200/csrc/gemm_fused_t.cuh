@@ -6,22 +6,20 @@
 // out = Σ 2^{8ℓ} C_ℓ mod p), same "read X exactly once" schedule as gemm_fused.cuh,
 // but the operands swap roles so that the limbs never touch shared memory:
 //   MMA A = the limb tile in TMEM (tcgen05.mma …, [a-tmem]): M = 128 lanes = 32 rows of X × 4
-//           limbs — lane 4r'+ℓ of quadrant q holds limb ℓ of row q + 4r' of the tile, its 32-bit
-//           columns 4 consecutive residues' bytes (K-major);
+//           limbs — lane 16h + 8ℓ' + r of quadrant q holds limb 2h + ℓ' of row 8q + r of the
+//           tile, its 32-bit columns 4 consecutive residues' bytes (K-major);
 //   MMA B = U^T (N = d3_loc rounded up to 16, ≤ 256 rows × 128 B per K-block, TMA, SWIZZLE_128B);
-//   D     = 128 lanes × N columns: lane (r', ℓ) holds C_ℓ[row][j] for every j.
-// So the converters store their PRMT byte transposes with tcgen05.st (STTM, 256 B/clk) instead
-// of STS into a swizzled shared-memory image that the MMA then re-reads, and N is d3 itself (no
-// second M = 128 group padded to 256 columns for 128 < d3 < 256).  The four limb sums of an output
-// sit in four neighbouring lanes: the epilogue recombines them with a two-round shuffle
-// reduce-scatter (each lane ends with Σ_ℓ 2^{8ℓ}·C_ℓ for one column of every group of four) and
-// reduces mod p with the same Barrett step.
+//   D     = 128 lanes × N columns, same lane mapping: C_ℓ[row][j] for every j.
+// So the converters store their PRMT byte transposes with tcgen05.st (STTM) instead of STS into
+// a swizzled shared-memory image that the MMA then re-reads, and N is d3 itself (no M = 128 group
+// padded to 128 columns of U).  The .16x256b TMEM access shape (thread 4r + c ↔ lanes r, r + 8 ×
+// column pair c) matches that lane mapping: a converter thread that loaded 8 residues of row r
+// stores all four of their limbs, and an epilogue thread gets all four limb sums of its outputs —
+// no cross-lane exchange on either side (an earlier version with lane = 4r + ℓ needed shuffles
+// and selects for a 4×4 word transpose and was issue-bound: 51 % issue slots at d3 = 64).
 //
-// Converter data path per K-block (32 rows × 128 residues, 16 KB): TMA raw tiles (4 boxes of
-// 32 rows × 32 residues, SWIZZLE_128B) → LDS.128 (lane (r', ℓ') takes residues 16i + 4ℓ' .. +3 of
-// row q + 4r'; the row stride of 4 makes the 8 lanes of each LDS phase hit 8 distinct 16-B bank
-// groups under the swizzle) → PRMT 4×4 byte transpose → two shfl.xor rounds (4×4 word transpose
-// between the four lanes of a row) → 32 words = one 32-column TMEM row per lane → STTM.
+// Converter data path per K-block (32 rows × 128 residues, 16 KB per sub-tile): TMA raw tiles
+// (4 boxes of 32 rows × 32 residues, SWIZZLE_128B) → LDS.128 → PRMT 4×4 byte transpose → STTM.
 // Two converter groups (warps 8–11, 12–15) take alternate K-blocks; every ring length is even so a
 // stage always meets the same group (round 1's parity lesson, gemm_fused.cuh).
 // Warp roles (512 threads): w0 U^T TMA, w1 MMA issuer, w2 TMEM allocator, w3 raw X TMA,
@@ -92,31 +90,22 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32
       : "memory");
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-
-// 4×4 transpose of 32-bit words between the four lanes a = lane & 3 of a row group: on entry
-// lane a holds T[a][0..3] in w[0..3]; on exit lane a holds T[0..3][a] in w[0..3].
-__device__ __forceinline__ void transpose4_lanes(uint32_t (&w)[4], int a) {
-  // round 1 (xor 1): exchange the two words whose index parity differs from the lane's
-  const bool odd = a & 1;
-  {
-    const uint32_t s0 = odd ? w[0] : w[1], s1 = odd ? w[2] : w[3];
-    const uint32_t r0 = __shfl_xor_sync(0xffffffffu, s0, 1), r1 = __shfl_xor_sync(0xffffffffu, s1, 1);
-    // lane a keeps m ∈ {a&1, (a&1)+2}: T[a][m] and T[a^1][m]
-    if (odd) { w[0] = r0; w[2] = r1; } else { w[1] = r0; w[3] = r1; }
-  }
-  // now (even a): w = {T[a][0], T[a^1][0], T[a][2], T[a^1][2]}; (odd a): {T[a^1][1], T[a][1], T[a^1][3], T[a][3]}
-  // i.e. in both cases w[2x + y] = T[(a & ~1) | y][(a & 1) + 2x]
-  {
-    const bool hi = a & 2;
-    // lane a needs m = a: x = (a >> 1); it sends the pair with x' = 1 − (a >> 1)
-    const uint32_t s0 = hi ? w[0] : w[2], s1 = hi ? w[1] : w[3];
-    const uint32_t r0 = __shfl_xor_sync(0xffffffffu, s0, 2), r1 = __shfl_xor_sync(0xffffffffu, s1, 2);
-    // received T[(a^2) & ~1 | y][a] for y = 0, 1
-    const uint32_t k0 = hi ? w[2] : w[0], k1 = hi ? w[3] : w[1];  // own T[(a & ~1) | y][a]
-    // rows: a & ~1 ∈ {0, 2}; output order T[0][a], T[1][a], T[2][a], T[3][a]
-    if (hi) { w[0] = r0; w[1] = r1; w[2] = k0; w[3] = k1; }
-    else { w[0] = k0; w[1] = k1; w[2] = r0; w[3] = r1; }
-  }
+// .16x256b.x4: 16 TMEM lanes × 32 columns; thread t = 4r + c holds, for repetition k, the words
+// (lane r, column 8k + 2c), (lane r, 8k + 2c + 1), (lane r + 8, 8k + 2c), (lane r + 8, 8k + 2c + 1)
+// in registers 4k .. 4k + 3 (the mma accumulator-fragment pattern).
+__device__ __forceinline__ void tmem_st16x256_x4(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x256b.x4.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16x256_x4(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
 }
 
 template <int NPMAX, int SUB>
@@ -260,91 +249,88 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
     }
   } else if (warp >= 4 && warp < 8) {  // (warp 2, the TMEM allocator, idles until the dealloc)
     // ---------------------------------------------------------------- epilogue (warps 4–7)
-    const int q = warp & 3;                 // TMEM lanes [32q, 32q + 32)
-    const int rp = lane >> 2, l4 = lane & 3;  // row q + 4·rp of the tile, limb l4
+    // Quadrant q's lanes: 16h + 8ℓ' + r = limb 2h + ℓ' of tile row 8q + r.  Two .16x256b loads
+    // (lane blocks h = 0, 1) give thread t = 4r + c all four limb sums of row 8q + r for the
+    // columns 8k + 2c + {0, 1} of the 32-column chunk: the recombination is thread-local.
+    const int q = warp & 3;
+    const int r = lane >> 2, c = lane & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
+    const int nchunk = (P.np + 31) / 32;
     for (int32_t t = 0; t < my_tiles; ++t) {
       const int64_t tr = static_cast<int64_t>(blockIdx.x) + static_cast<int64_t>(t) * gridDim.x;
       mbar_wait(d_full(acc), acc_phase);
       tc_fence_after();
 #pragma unroll 1
-      for (int chunk = 0; chunk < SUB * ((P.np + 31) / 32); ++chunk) {
-        const int sb = chunk / ((P.np + 31) / 32), c0 = 32 * (chunk % ((P.np + 31) / 32));
-        const int64_t row = tr * ROWS + sb * FT_SUB_ROWS + q + 4 * rp;
-        const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * D_COLS + sb * NPMAX;
-        uint32_t v[32];
-        tmem_ld32(t_row + c0, v);
+      for (int chunk = 0; chunk < SUB * nchunk; ++chunk) {
+        const int sb = chunk / nchunk, c0 = 32 * (chunk % nchunk);
+        const int64_t row = tr * ROWS + sb * FT_SUB_ROWS + 8 * q + r;
+        const uint32_t t_col = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * D_COLS + sb * NPMAX + c0;
+        uint32_t lo[16], hi[16];  // limbs 0, 1 and limbs 2, 3
+        tmem_ld16x256_x4(t_col, lo);
+        tmem_ld16x256_x4(t_col + (16u << 16), hi);
         tmem_ld_wait();
-        if (chunk + 1 == SUB * ((P.np + 31) / 32)) {  // every column read: hand D back before the last stores
+        if (chunk + 1 == SUB * nchunk) {  // every column read: hand D back before the last stores
           tc_fence_before();
           mbar_arrive(d_empty(acc));
         }
-        // reduce-scatter over the four limb lanes of this row: lane l4 ends with the full
-        // Σ_ℓ 2^{8ℓ} C_ℓ for column c0 + 4g + l4 of every group g of four columns
 #pragma unroll
-        for (int g = 0; g < 8; ++g) {
-          // round 1 (xor 1): keep columns s with (s & 1) == (l4 & 1), send the other two
-          const bool odd = l4 & 1;
-          const int32_t c0v = static_cast<int32_t>(v[4 * g]), c1v = static_cast<int32_t>(v[4 * g + 1]);
-          const int32_t c2v = static_cast<int32_t>(v[4 * g + 2]), c3v = static_cast<int32_t>(v[4 * g + 3]);
-          const int32_t k0 = odd ? c1v : c0v, k1 = odd ? c3v : c2v;  // kept: columns (l4 & 1), (l4 & 1) + 2
-          const int32_t s0 = odd ? c0v : c1v, s1 = odd ? c2v : c3v;  // sent to lane l4 ^ 1
-          const int32_t r0 = __shfl_xor_sync(0xffffffffu, s0, 1), r1 = __shfl_xor_sync(0xffffffffu, s1, 1);
-          // partial sums over limbs {l4, l4 ^ 1} for columns s = (l4 & 1) and (l4 & 1) + 2
-          const int sh_own = 8 * l4, sh_par = 8 * (l4 ^ 1);
-          const int64_t p0 = (static_cast<int64_t>(k0) << sh_own) + (static_cast<int64_t>(r0) << sh_par);
-          const int64_t p1 = (static_cast<int64_t>(k1) << sh_own) + (static_cast<int64_t>(r1) << sh_par);
-          // round 2 (xor 2): keep column s = l4 (p0 if l4 < 2 else p1), send the other
-          const bool hi = l4 & 2;
-          const int64_t keep = hi ? p1 : p0, send = hi ? p0 : p1;
-          const int64_t recv = static_cast<int64_t>(
-              (static_cast<uint64_t>(static_cast<uint32_t>(__shfl_xor_sync(0xffffffffu, static_cast<uint32_t>(send >> 32), 2))) << 32) |
-              static_cast<uint32_t>(__shfl_xor_sync(0xffffffffu, static_cast<uint32_t>(send), 2)));
-          const int64_t tsum = keep + recv;
-          const int64_t j = static_cast<int64_t>(c0) + 4 * g + l4;
-          if (j < P.o.d3_loc && row < P.o.R)
-            *out_ptr(P.o, j, row) = barrett64(static_cast<uint64_t>(tsum + static_cast<int64_t>(P.m.off)), P.m);
-        }
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const uint32_t res = recombine_mod(static_cast<int32_t>(lo[4 * k + e]), static_cast<int32_t>(lo[4 * k + 2 + e]),
+                                               static_cast<int32_t>(hi[4 * k + e]), static_cast<int32_t>(hi[4 * k + 2 + e]), P.m);
+            const int64_t j = static_cast<int64_t>(c0) + 8 * k + 2 * c + e;
+            if (j < P.o.d3_loc && row < P.o.R) *out_ptr(P.o, j, row) = res;
+          }
       }
       if (++acc == NBUF) { acc = 0; acc_phase ^= 1; }
     }
   } else if (warp >= 8) {
     // ---------------------------------------------------------------- converters (warps 8–15)
+    // TMEM quadrant q (warp % 4 == q, as tcgen05.st requires) holds tile rows 8q .. 8q + 7: lane
+    // 16h + 8ℓ' + r = limb 2h + ℓ' of row 8q + r.  Thread t = 4r + c loads residues 32k + 8c .. +7
+    // of row 8q + r (two LDS.128 per repetition k; consecutive rows in an 8-lane phase differ in the
+    // swizzle's bit 0, so the 8 lanes hit 8 distinct 16-B bank groups), byte-transposes them
+    // (PRMT) into limb words and stores limbs 0–1 / 2–3 with two .16x256b.x4 STTMs whose fragment
+    // pattern is exactly (lane r | r + 8, columns 8k + 2c | + 1): no cross-lane exchange.
     const int cw = warp - 8;
-    // TMEM quadrant q (warp % 4 == q, as tcgen05.st requires); hi = the K-block parity (SUB = 1:
-    // two groups on alternate K-blocks) or the sub-tile (SUB = 2: every K-block)
+    // hi = the K-block parity (SUB = 1: two groups on alternate K-blocks) or the sub-tile (SUB = 2)
     const int q = cw & 3, hi = cw >> 2;
     const int grp = SUB == 1 ? hi : 0, sb = SUB == 1 ? 0 : hi;
-    const int rp = lane >> 2, l4 = lane & 3;
-    const int row = q + 4 * rp;            // row of the 32-row sub-tile this lane's limb lane belongs to
+    const int r = lane >> 2, c = lane & 3;
+    const int row = 8 * q + r;            // row of the 32-row sub-tile
     const uint32_t t_lane = static_cast<uint32_t>(q * 32) << 16;
     for (int64_t it = grp; it < n_it; it += GROUPS) {
       const int rs = static_cast<int>(it % RAW);
       const int as = static_cast<int>(it % FT_AST);
       mbar_wait(raw_full(rs), static_cast<uint32_t>((it / RAW) & 1));
       const uint32_t raw = raw_base + rs * RAW_BYTES + sb * 4 * FT_BOX_BYTES;
-      uint32_t col[32];
+      uint32_t l01[16], l23[16];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        // residues 16i + 4·l4 .. +3 of this row: box i/2, 16-B chunk 4(i&1) + l4 of its 128-B row
-        const int cb = 4 * (i & 1) + l4;
-        const uint4 x = lds128(raw + (i >> 1) * FT_BOX_BYTES + row * 128 + ((cb ^ (row & 7)) << 4));
-        uint32_t w[4];
-        byte_transpose4(x.x, x.y, x.z, x.w, w[0], w[1], w[2], w[3]);  // w[m] = limb m of the 4 residues
-        transpose4_lanes(w, l4);  // w[a] = limb l4 of residues 16i + 4a .. +3
-        col[4 * i + 0] = w[0];
-        col[4 * i + 1] = w[1];
-        col[4 * i + 2] = w[2];
-        col[4 * i + 3] = w[3];
+      for (int k = 0; k < 4; ++k) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          // residues 32k + 8c + 4e .. +3: box k, 16-B chunk 2c + e of row `row`
+          const int cb = 2 * c + e;
+          const uint4 x = lds128(raw + k * FT_BOX_BYTES + row * 128 + ((cb ^ (row & 7)) << 4));
+          uint32_t w0, w1, w2, w3;
+          byte_transpose4(x.x, x.y, x.z, x.w, w0, w1, w2, w3);  // wm = limb m of the 4 residues
+          l01[4 * k + e] = w0;
+          l01[4 * k + 2 + e] = w1;
+          l23[4 * k + e] = w2;
+          l23[4 * k + 2 + e] = w3;
+        }
       }
       mbar_wait(a_empty(as), static_cast<uint32_t>(((it / FT_AST) & 1) ^ 1));
       tc_fence_after();
-      tmem_st32(tmem_base + t_lane + A_COL0 + as * ASTAGE_COLS + sb * 32, col);
-      // The raw tile is handed back only here: the STTM takes every transposed word as an operand,
-      // so every LDS of the tile has completed (register computations such as the PRMTs and SHFLs
-      // may be scheduled past a fence; an asm operand may not), then a proxy fence orders the
-      // generic reads before the TMA's async-proxy refill.
+      const uint32_t ta = tmem_base + t_lane + A_COL0 + as * ASTAGE_COLS + sb * 32;
+      tmem_st16x256_x4(ta, l01);
+      tmem_st16x256_x4(ta + (16u << 16), l23);
+      // The raw tile is handed back only here: the STTMs take every limb word as an operand, so
+      // every LDS of the tile has completed (register computations such as the PRMTs may be
+      // scheduled past a fence; an asm operand may not), then a proxy fence orders the generic
+      // reads before the TMA's async-proxy refill.
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(raw_empty(rs));
