@@ -393,7 +393,7 @@ def run_ours(args, rank: int, world: int, local_rank: int, scaling: str = "stron
     fused = (d3l <= 256 and kU == 1 and not (spec.u_unsigned and spec.u_offset) and not args.rescale)
     n_ev = 1 if args.rescale else len(ps)
 
-    mv = fused and d3l <= 32
+    mv = fused and kernel_path(d3l, kU, spec.u_unsigned, spec.u_offset, c.R) == "mv"
     # Split/GEMM overlap (split path): the limb split of prime l+1 runs on a side stream into the
     # other of two workspaces while prime l's GEMM runs (the split needs no shared memory and
     # little SM time, so it co-resides with the persistent GEMM); gemm(l) waits on split(l).
@@ -552,7 +552,8 @@ def run_ours(args, rank: int, world: int, local_rank: int, scaling: str = "stron
         # SM clock sampled during the timed region (how busy the tensor pipe is per clock)
         "pct_int8_clock_normalised": (100.0 * value * 4 * kU / world / (148 * 8192 * clocks["sm_mhz"] * 1e6)
                                       if clocks.get("sm_mhz") else None),
-        "roofline": roofline_fused(c, d3l, gemm_avg_s, gemm_share, mp, which, "k_gemm_mv" if mv else "k_gemm_fused")
+        "roofline": roofline_fused(c, d3l, gemm_avg_s, gemm_share, mp, which,
+                                   "k_gemm_mv" if mv else "k_gemm_fused_t" if d3l <= 192 else "k_gemm_fused")
         if fused else {
                      "bound": "tensor", "achieved": achieved_tops, "peak": peak_tops, "unit": "TOP/s",
                      "frac": achieved_tops / peak_tops, "traffic": traffic if not args.rescale else None,
@@ -769,10 +770,12 @@ def gpu_uuid_of(dev) -> str | None:
         return None
 
 
-def kernel_path(d3_loc: int, kU: int, u_unsigned: int, u_offset: int) -> str:
-    """The library's automatic kernel choice for one prime (include/ctpt.h ctpt_kernel)."""
+def kernel_path(d3_loc: int, kU: int, u_unsigned: int, u_offset: int, R: int = 1 << 30, sms: int = 148) -> str:
+    """The library's automatic kernel choice for one prime (include/ctpt.h ctpt_kernel; ctpt.cu
+    choose_path): the raw-byte kernel for d3_loc <= 32 with fewer 64-row tiles than SMs, the fused
+    skinny kernels up to 256 columns, else split + GEMM."""
     if kU == 1 and d3_loc <= 256 and not (u_unsigned and u_offset):
-        return "mv" if d3_loc <= 32 else "fused"
+        return "mv" if d3_loc <= 32 and (R + 63) // 64 < sms else "fused"
     return "split_gemm"
 
 
@@ -782,7 +785,7 @@ def launch_unit(spec_u, eng, au, bu, stream, ev=None):
     from paper_2503_16080_b200 import ctpt
 
     sz = eng.unit_sizes[(spec_u.col_begin, spec_u.col_end)]
-    path = kernel_path(sz.d3_loc, spec_u.kU, spec_u.u_unsigned, spec_u.u_offset)
+    path = kernel_path(sz.d3_loc, spec_u.kU, spec_u.u_unsigned, spec_u.u_offset, sz.R)
     if path == "split_gemm":
         ctpt.split(spec_u, 0, eng.ctmat, eng.ws, stream=stream)
     if ev is not None:
@@ -965,7 +968,7 @@ def run_strong(args, rank: int, world: int, local_rank: int):
     macs = c.residue_macs
     value = macs / (ms / 1e3)
     paths = {kernel_path(engines[u.l].unit_sizes[(u.c0, u.c1)].d3_loc, kU, engines[u.l].spec.u_unsigned,
-                         engines[u.l].spec.u_offset) for u in mine}
+                         engines[u.l].spec.u_offset, c.R) for u in mine}
     unit_limb_macs = [4 * kU * c.R * c.d2 * u.ncols for u in mine]
     if paths == {"split_gemm"}:
         tops = [2 * m / (t / 1e3) / 1e12 for m, t in zip(unit_limb_macs * args.steps, gemm_ms)]

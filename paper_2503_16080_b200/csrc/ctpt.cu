@@ -357,14 +357,14 @@ ctpt_status tc_setup() {
   cudaError_t& e = errs[dev];
   std::call_once(onces[dev], [&e] {
     e = cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BYTES);
+#ifdef CTPT_FUSED_SMEM_LIMBS
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_fused<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(1));
+#endif
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_fused<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(2));
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_gemm_fused_t<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ft_smem_bytes(128, 2));
-#ifdef CTPT_FUSED_T256
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_gemm_fused_t<256, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, ft_smem_bytes(256, 1));
-#endif
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
@@ -421,6 +421,12 @@ ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st);
 // CTPT_KERNEL_AUTO takes the first that applies; a forced choice that does not apply is refused.
 constexpr int64_t kFusedMaxD3 = 256;
 constexpr int64_t kMvMaxD3 = 32;
+// The limbs-in-TMEM skinny kernel (gemm_fused_t.cuh) takes d3_loc ≤ 192 — 64-row tiles up to 128
+// columns, 32-row tiles above; the limbs-in-shared-memory kernel (gemm_fused.cuh) 192 < d3_loc ≤ 256.
+// On c4's ciphertexts: d3 = 64 / 128 / 160 / 192 → 1.03–1.05 / 0.81–0.91 / 0.82 / 0.73 of HBM vs
+// 0.84 / 0.81–0.82 / 0.70 / 0.64–0.65; at 224 / 256 the shared-memory kernel ties or wins
+// (0.63–0.64 vs 0.60–0.65; profiles/r02/fused_tmem_v3*/).
+constexpr int64_t kTmemMaxD3 = 192;
 int mv_nc(const Dims& d) {  // N = 4·d3p, d3p ∈ {4, 8, 16, 32}
   int d3p = 4;
   while (d3p < d.d3_loc) d3p *= 2;
@@ -469,7 +475,13 @@ ctpt_status choose_path(const ctpt_problem* pb, const Dims& d, Path& path) {
       path = Path::Mv;
       return CTPT_OK;
     default:
-      path = mv_applies(d, kU, pb) ? Path::Mv : fused_applies(d, kU, pb) ? Path::Fused : Path::SplitGemm;
+      // d3_loc ≤ 32: the raw-byte kernel only when there are fewer 64-row tiles than SMs (it splits
+      // the K loop across CTAs); with enough rows the limbs-in-TMEM kernel streams faster (c4's
+      // ciphertexts, d3 = 1 / 8 / 16 / 32: 1.06 / 1.06 / 1.05 / 1.04 vs 1.01 / 0.99 / 0.96 / 0.92
+      // of HBM, profiles/r02/fused_tmem_v3_ab2/)
+      path = (mv_applies(d, kU, pb) && (d.R + 63) / 64 < num_sms()) ? Path::Mv
+             : fused_applies(d, kU, pb)                          ? Path::Fused
+                                                                 : Path::SplitGemm;
       return CTPT_OK;
   }
 }
@@ -834,11 +846,6 @@ ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st) 
   P.o.accumulate = 0;
   P.o.w = 1;
 #ifndef CTPT_FUSED_SMEM_LIMBS  // A/B build switch (tools/ab_build.py): the limbs-in-shared-memory kernel for all d3
-#ifdef CTPT_FUSED_T256  // A/B build switch: 32-row limbs-in-TMEM tiles for 128 < d3_loc <= 256 too
-  constexpr int64_t kTmemMaxD3 = 256;
-#else
-  constexpr int64_t kTmemMaxD3 = 128;
-#endif
   if (d.d3_loc <= kTmemMaxD3) {
     // limbs in tensor memory (gemm_fused_t.cuh): 64-row tiles (two 32-row sub-tiles sharing each U^T
     // stage), MMA N = d3_loc rounded up to 16.  Measured against the limbs-in-shared-memory kernel
@@ -864,13 +871,10 @@ ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st) 
     const int64_t cap = grid_cap(g.max_ctas);
     const int64_t rounds = (ntt + cap - 1) / cap;
     const unsigned grid = static_cast<unsigned>((ntt + rounds - 1) / rounds);
-    if (sub == 2) {
+    if (sub == 2)
       k_gemm_fused_t<128, 2><<<grid, FT_THREADS, ft_smem_bytes(128, 2), st>>>(tmUt, tmXt, T);
-    } else {
-#ifdef CTPT_FUSED_T256
+    else
       k_gemm_fused_t<256, 1><<<grid, FT_THREADS, ft_smem_bytes(256, 1), st>>>(tmUt, tmXt, T);
-#endif
-    }
     CUDA_TRY(cudaGetLastError());
     return CTPT_OK;
   }
@@ -881,14 +885,17 @@ ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st) 
   const int64_t cap = grid_cap(g.max_ctas);
   const int64_t rounds = (nt + cap - 1) / cap;
   const unsigned grid = static_cast<unsigned>((nt + rounds - 1) / rounds);
-  const int ng = d.d3_loc <= 128 ? 1 : 2;
   CUtensorMap tmX;
   s = make_tmap_2d(&tmX, x, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, d.d2p, g.R, FU_BLOCK_K, FU_BLOCK_R);
   if (s != CTPT_OK) return s;
-  if (ng == 1)
+#ifdef CTPT_FUSED_SMEM_LIMBS
+  if (d.d3_loc <= 128) {
     k_gemm_fused<1><<<grid, FU_THREADS, fu_smem_bytes(1), st>>>(tmU, tmX, P);
-  else
-    k_gemm_fused<2><<<grid, FU_THREADS, fu_smem_bytes(2), st>>>(tmU, tmX, P);
+    CUDA_TRY(cudaGetLastError());
+    return CTPT_OK;
+  }
+#endif
+  k_gemm_fused<2><<<grid, FU_THREADS, fu_smem_bytes(2), st>>>(tmU, tmX, P);
   CUDA_TRY(cudaGetLastError());
   return CTPT_OK;
 }
