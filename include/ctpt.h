@@ -77,13 +77,16 @@ typedef enum {
 typedef enum { CTPT_RLWE = 0, CTPT_SHARED_S = 1, CTPT_SHARED_A = 2, CTPT_STRUCT_A = 3 } ctpt_format;
 
 /* Which kernel path ctpt_matmul / ctpt_matmul_host run per prime (ctpt_problem.kernel).  AUTO:
- * the raw-byte kernel k_gemm_mv when d3_loc ≤ 32, the fused skinny kernel k_gemm_fused when
- * d3_loc ≤ 256, else the limb split + k_gemm_tc (the first two need kU = 1 and u_offset = 0).
- * A forced choice that does not apply returns CTPT_ERR_UNSUPPORTED. */
+ * the raw-byte kernel k_gemm_mv when d3_loc ≤ 32 and R has fewer 64-row tiles than the GPU has
+ * SMs, the fused skinny kernels when d3_loc ≤ 256, else the limb split + k_gemm_tc (the first two
+ * need kU = 1 and u_offset = 0).  A forced choice that does not apply returns
+ * CTPT_ERR_UNSUPPORTED. */
 typedef enum {
   CTPT_KERNEL_AUTO = 0,
   CTPT_KERNEL_SPLIT_GEMM = 1, /* k_split[_rows] + k_gemm_tc (tcgen05, any d3, any kU)            */
-  CTPT_KERNEL_FUSED = 2,      /* k_gemm_fused: split in the GEMM's load path (d3_loc ≤ 256)       */
+  CTPT_KERNEL_FUSED = 2,      /* split in the GEMM's load path, X read once: k_gemm_fused_t (limbs
+                                 in tensor memory, d3_loc ≤ 192) or k_gemm_fused (limbs in shared
+                                 memory, 192 < d3_loc ≤ 256)                                      */
   CTPT_KERNEL_MV = 3          /* k_gemm_mv: raw residue bytes × expanded U (d3_loc ≤ 32)          */
 } ctpt_kernel;
 
@@ -214,9 +217,11 @@ ctpt_status ctpt_gemm(const ctpt_problem* prob, int32_t l, const void* d_ws, siz
  * P:982; Table 4's d3 ∈ {1, 2^6, 2^7}).  For prime index l: the same
  * (A·U mod p, B·U mod p) as ctpt_split + ctpt_gemm, but the limb split runs inside the GEMM's
  * load path, reading the int32 residues of d_ctmat exactly once (no workspace): the regime is
- * HBM-bound and this saves the split's write + re-read.  ctpt_matmul (and ctpt_matmul_host)
- * choose this kernel automatically for every prime when 32 < d3_loc ≤ 256 and kU = 1
- * (ctpt_problem.kernel overrides that).  Outputs as for ctpt_gemm.
+ * HBM-bound and this saves the split's write + re-read.  d3_loc ≤ 192: k_gemm_fused_t (the limbs
+ * go to tensor memory as the MMA's A operand, U^T is B); 192 < d3_loc ≤ 256: k_gemm_fused (limbs
+ * in shared memory).  ctpt_matmul (and ctpt_matmul_host) choose these kernels automatically when
+ * d3_loc ≤ 256 and kU = 1 (see ctpt_kernel; ctpt_problem.kernel overrides).  Outputs as for
+ * ctpt_gemm.
  * CTPT_ERR_UNSUPPORTED when kU ≠ 1 or d3_loc > 256.  Never synchronises. */
 ctpt_status ctpt_gemm_fused(const ctpt_problem* prob, int32_t l, const void* d_ctmat, const void* d_plain,
                             uint32_t* d_AU_l, uint32_t* d_BU_l, void* stream);

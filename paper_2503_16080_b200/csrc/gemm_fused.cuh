@@ -226,6 +226,7 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
       uint32_t lw[FU_ROWS_PER_WARP][4];
 #pragma unroll
       for (int i = 0; i < FU_ROWS_PER_WARP; ++i) {
+        CTPT_CHECK(sraw + (cw + FU_CONV_WARPS * i) * 512 + lane * 16 + 16 <= raw_base + RAW * RAW_BYTES);
         const uint4 v = lds128(sraw + (cw + FU_CONV_WARPS * i) * 512 + lane * 16);
         byte_transpose4(v.x, v.y, v.z, v.w, lw[i][0], lw[i][1], lw[i][2], lw[i][3]);
       }

@@ -174,11 +174,6 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot_ptr;
-#ifdef CTPT_DEBUG_HANG
-  if (threadIdx.x == 0 && blockIdx.x < 2)
-    printf("fused_t block %d: tmem_base %u bar_base %u n_it %lld my_tiles %d\n", blockIdx.x, tmem_base, bar_base,
-           (long long)n_it, my_tiles);
-#endif
 
   if (warp == 0) {
     // ---------------------------------------------------------------- U^T TMA producer
@@ -281,7 +276,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
             const uint32_t res = recombine_mod(static_cast<int32_t>(lo[4 * k + e]), static_cast<int32_t>(lo[4 * k + 2 + e]),
                                                static_cast<int32_t>(hi[4 * k + e]), static_cast<int32_t>(hi[4 * k + 2 + e]), P.m);
             const int64_t j = static_cast<int64_t>(c0) + 8 * k + 2 * c + e;
-            if (j < P.o.d3_loc && row < P.o.R) *out_ptr(P.o, j, row) = res;
+            if (j < P.o.d3_loc && row < P.o.R) store_out(P.o, P.m, j, row, res);  // (+ the Rescale epilogue)
           }
       }
       if (++acc == NBUF) { acc = 0; acc_phase ^= 1; }
@@ -313,7 +308,9 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
         for (int e = 0; e < 2; ++e) {
           // residues 32k + 8c + 4e .. +3: box k, 16-B chunk 2c + e of row `row`
           const int cb = 2 * c + e;
-          const uint4 x = lds128(raw + k * FT_BOX_BYTES + row * 128 + ((cb ^ (row & 7)) << 4));
+          const uint32_t a = raw + k * FT_BOX_BYTES + row * 128 + ((cb ^ (row & 7)) << 4);
+          CTPT_CHECK(a >= raw_base && a + 16 <= raw_base + RAW * RAW_BYTES);
+          const uint4 x = lds128(a);
           uint32_t w0, w1, w2, w3;
           byte_transpose4(x.x, x.y, x.z, x.w, w0, w1, w2, w3);  // wm = limb m of the 4 residues
           l01[4 * k + e] = w0;
@@ -325,6 +322,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
       mbar_wait(a_empty(as), static_cast<uint32_t>(((it / FT_AST) & 1) ^ 1));
       tc_fence_after();
       const uint32_t ta = tmem_base + t_lane + A_COL0 + as * ASTAGE_COLS + sb * 32;
+      CTPT_CHECK(A_COL0 + as * ASTAGE_COLS + sb * 32 + 32 <= 512);
       tmem_st16x256_x4(ta, l01);
       tmem_st16x256_x4(ta + (16u << 16), l23);
       // The raw tile is handed back only here: the STTMs take every limb word as an operand, so

@@ -243,6 +243,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const int64_t r0 = r_tile + h * 32;
           finish_rows<32>(P.o, P.m, j, r0, res, j < P.o.d3_loc);
           const uint32_t buf = stg + h * TC_OUT_HALF_BYTES;
+          CTPT_CHECK(buf >= out_base && buf + TC_OUT_HALF_BYTES <= out_base + TC_OUT_BYTES);
+          CTPT_CHECK(r0 + 32 <= (r0 < P.o.rows_A ? P.o.rows_A : P.o.rows_A + P.o.d1));  // inside A' or B
           if (lane == 0) bulk_wait_read<1>();  // this half's previous store has read its buffer
           __syncwarp();
 #pragma unroll

@@ -3,6 +3,8 @@
 #pragma once
 #include <cstdint>
 
+#include "ptx.cuh"
+
 namespace ctpt {
 
 // ------------------------------------------------------------------------------------------
@@ -320,6 +322,7 @@ struct OutParams {
 };
 
 __device__ __forceinline__ uint32_t* out_ptr(const OutParams& o, int64_t j, int64_t r) {
+  CTPT_CHECK(j >= 0 && j < o.d3_loc && r >= 0 && r < o.R);
   return (r < o.rows_A) ? o.AU + j * o.rows_A + r : o.BU + j * o.d1 + (r - o.rows_A);
 }
 
@@ -416,6 +419,7 @@ __device__ __forceinline__ void finish_rows(const OutParams& o, const ModP& m, i
 __device__ __forceinline__ void store16(const OutParams& o, const ModP& m, int64_t j, int64_t r0, uint32_t (&res)[16]) {
   const bool in_a = (r0 + 15 < o.rows_A), in_b = (r0 >= o.rows_A);
   if (((o.rows_A & 3) == 0) && ((o.d1 & 3) == 0) && r0 + 15 < o.R && (in_a || in_b)) {
+    CTPT_CHECK(out_ptr(o, j, r0 + 15) == out_ptr(o, j, r0) + 15);
     uint4* q = reinterpret_cast<uint4*>(out_ptr(o, j, r0));
     if (o.rowcorr) {
       const uint4* rc = reinterpret_cast<const uint4*>(o.rowcorr + r0);

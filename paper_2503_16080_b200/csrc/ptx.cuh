@@ -3,8 +3,28 @@
 #pragma once
 #include <cstdint>
 #include <cuda.h>
+#if defined(CTPT_DEBUG_CHECKS) && !defined(CTPT_DEBUG_HANG)
+#define CTPT_DEBUG_HANG
+#endif
 #ifdef CTPT_DEBUG_HANG
 #include <cstdio>
+#endif
+// CTPT_CHECK(cond): in debug builds (tools/ab_build.py -DCTPT_DEBUG_CHECKS; compute-sanitizer is
+// closed on this pool) a failed bounds / invariant check prints the site and traps; compiled out
+// otherwise.
+#ifdef CTPT_DEBUG_CHECKS
+#define CTPT_CHECK(cond)                                                                                  \
+  do {                                                                                                    \
+    if (!(cond)) {                                                                                        \
+      printf("ctpt check failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, blockIdx.x, \
+             threadIdx.x);                                                                                \
+      __trap();                                                                                           \
+    }                                                                                                     \
+  } while (0)
+#else
+#define CTPT_CHECK(cond) \
+  do {                   \
+  } while (0)
 #endif
 
 namespace ctpt {

@@ -1,8 +1,15 @@
 #!/usr/bin/env python
-"""Small cases of every kernel path for compute-sanitizer (racecheck / synccheck / memcheck),
-each checked against the oracle so a sanitizer run is also a parity run.
+"""Small cases of every kernel path, each checked against the oracle, for checked builds.
 
-    compute-sanitizer --tool racecheck python tools/sanitize_cases.py [--cases a,b,...]
+compute-sanitizer is closed on this GPU pool (runs under it left GPUs needing a reset), so the
+substitute is (a) a debug build of the library with device-side bounds / invariant checks that
+trap with the failing site, and mbarrier waits that trap with the barrier after 4 s instead of
+hanging (`python tools/ab_build.py /tmp/dbg.so -DCTPT_DEBUG_CHECKS`, loaded with CTPT_LIB), and
+(b) stress repetitions that change the schedule (grid caps 1 … 148 CTAs, so each CTA loops over a
+different number of tiles and the rings wrap at different points) and compare every output with
+the oracle each time — a race that corrupts data shows up as a mismatch.
+
+    CTPT_LIB=/tmp/dbg.so python tools/sanitize_cases.py [--cases a,b,...] [--stress 5]
 
 Cases (kept small: the sanitizers slow kernels down 10–100×):
   gemm          limb split + k_gemm_tc, 3 primes, ragged R / d2 / d3 (several tiles, 2 raster groups)
@@ -36,7 +43,20 @@ from gpu_helpers import oracle_outputs, run_gpu  # noqa: E402
 R, S, A = ctgen.RLWE, ctgen.SHARED_S, ctgen.SHARED_A
 
 
+STRESS = [0]  # grid caps cycled through by --stress
+
+
 def check(name, fmt, N, k, d2, d3, L, seed=0, u_bound=8, **kw):
+    bad = 0
+    for i, cap in enumerate(STRESS):
+        kw2 = dict(kw)
+        if cap and "max_ctas" not in kw:
+            kw2["max_ctas"] = cap
+        bad += _check1(name, fmt, N, k, d2, d3, L, seed + i, u_bound, **kw2)
+    return bad
+
+
+def _check1(name, fmt, N, k, d2, d3, L, seed=0, u_bound=8, **kw):
     d1 = N * k
     ps = ctgen.primes(L)
     ct = ctgen.encrypt(fmt, N, d1, d2, seed, 20, ps)
@@ -47,7 +67,7 @@ def check(name, fmt, N, k, d2, d3, L, seed=0, u_bound=8, **kw):
         wa, wb = oracle_outputs(fmt, N, d1, ct.a_polys[l], ct.b_polys[l], U, p)
         bad += int(np.count_nonzero(AU[l] != wa)) + int(np.count_nonzero(BU[l] != wb))
     print(f"{name}: fmt={fmt} N={N} k={k} d2={d2} d3={d3} L={L} kU={eng.spec.kU} u8={eng.spec.u_unsigned} "
-          f"mismatches={bad}", flush=True)
+          f"max_ctas={kw.get('max_ctas', 0)} mismatches={bad}", flush=True)
     return bad
 
 
@@ -167,7 +187,10 @@ CASES = {
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cases", default=",".join(CASES))
+    ap.add_argument("--stress", type=int, default=1, help="repetitions per case with grid caps 0, 1, 3, 7, 37, ...")
     args = ap.parse_args()
+    caps = [0, 1, 3, 7, 37, 148, 2, 5, 19, 64]
+    STRESS[:] = [caps[i % len(caps)] for i in range(max(1, args.stress))]
     bad = 0
     for name in args.cases.split(","):
         bad += CASES[name]()
