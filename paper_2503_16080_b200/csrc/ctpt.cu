@@ -192,12 +192,28 @@ size_t ws_bytes_needed(const ctpt_problem* pb, const Dims& d) {
   return overlap_on(pb, d) ? ws_ovl_off(pb, d) + ws_ovl_bytes(pb, d) : ws_base_bytes(pb, d);
 }
 
-ModP make_modp(uint32_t p) {
+// Barrett constants for p; with nonneg_limbs (u8 limbs × the u8 U plane: every limb sum C_ℓ ≥ 0)
+// also the Montgomery recombination of kernels.cuh recombine_mod (redc = 2 when d2·255·255 < 2^30
+// bounds every C_ℓ below 2^30, else 1).
+ModP make_modp(uint32_t p, bool nonneg_limbs = false, int64_t d2 = 0) {
   ModP m;
+  memset(&m, 0, sizeof(m));
   m.p = p;
   m.mu = static_cast<uint64_t>((static_cast<unsigned __int128>(1) << 64) / p);
   const uint64_t two56 = 1ULL << 56;
   m.off = ((two56 + p - 1) / p) * static_cast<uint64_t>(p);
+#ifdef CTPT_NO_REDC  // A/B build switch (tools/ab_build.py): Barrett on the int64 recombination everywhere
+  nonneg_limbs = false;
+#endif
+  if (nonneg_limbs && d2 * 255LL * 255LL < (1LL << 31)) {
+    m.redc = (d2 * 255LL * 255LL < (1LL << 30)) ? 2 : 1;
+    uint32_t inv = p;  // p·inv ≡ 1 (mod 2^k), Newton doubling k = 3 → 48
+    for (int i = 0; i < 5; ++i) inv *= 2u - p * inv;
+    m.pinv = 0u - inv;
+    for (int l = 0; l < 4; ++l)
+      m.w[l] = static_cast<uint32_t>((static_cast<unsigned __int128>(1) << (8 * l + 32)) % p);
+    m.p32 = static_cast<uint64_t>(p) << 32;
+  }
   return m;
 }
 
@@ -736,7 +752,7 @@ ctpt_status launch_split(const uint32_t* x, int64_t rows, int64_t d2p, void* lim
 
 ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
   const Dims& d = g.d;
-  const ModP m = make_modp(g.p);
+  const ModP m = make_modp(g.p, g.u_unsigned != 0, d.d2);
   if (simt) {
     for (int i = 0; i < g.kU; ++i) {
       SimtParams S;
@@ -841,7 +857,7 @@ ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st) 
   if (nt > INT32_MAX) return fail(CTPT_ERR_SHAPE, "too many tiles");
   P.num_tiles = static_cast<int32_t>(nt);
   P.u_unsigned = g.u_unsigned;
-  P.m = make_modp(g.p);
+  P.m = make_modp(g.p, g.u_unsigned != 0, d.d2);
   P.o = g.o;
   P.o.accumulate = 0;
   P.o.w = 1;
@@ -931,7 +947,7 @@ ctpt_status launch_mv(const GemmArgs& g, const uint32_t* x, void* mv_ws, cudaStr
   P.u_unsigned = g.u_unsigned;
   P.partial = reinterpret_cast<int32_t*>(w + mp.part_off);
   P.tickets = reinterpret_cast<uint32_t*>(w + mp.ticket_off);
-  P.m = make_modp(g.p);
+  P.m = make_modp(g.p, g.u_unsigned != 0, d.d2);
   P.o = g.o;
   P.o.accumulate = 0;
   P.o.w = 1;

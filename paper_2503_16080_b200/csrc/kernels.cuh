@@ -15,6 +15,11 @@ struct ModP {
   uint32_t p;
   uint64_t mu;   // floor(2^64 / p)
   uint64_t off;  // p * ceil(2^56 / p): makes t + off non-negative for |t| < 2^56
+  // Montgomery form of the recombination (limb sums known non-negative: u8 limbs × the u8 U plane)
+  int32_t redc;  // 0: Barrett on the int64 sum; 1: Montgomery, sums < 2^31; 2: Montgomery, sums < 2^30
+  uint32_t pinv; // −p^{−1} mod 2^32
+  uint32_t w[4]; // 2^{8ℓ + 32} mod p
+  uint64_t p32;  // p · 2^32
 };
 
 // r = x mod p for x < 2^64 (Barrett with a 64-bit reciprocal; q_est ∈ {q-1, q}).
@@ -26,8 +31,26 @@ __device__ __forceinline__ uint32_t barrett64(uint64_t x, const ModP& m) {
   return static_cast<uint32_t>(r);
 }
 
-// t = C0 + 2^8 C1 + 2^16 C2 + 2^24 C3 (exact in int64), reduced to [0, p).
+// t = C0 + 2^8 C1 + 2^16 C2 + 2^24 C3 (the exact limb recombination), reduced to [0, p).
+//  * redc = 0 (general, C_ℓ signed): t in int64, Barrett — ≈ 30 instructions per output;
+//  * redc > 0 (C_ℓ ≥ 0: u8 limbs × the u8 U plane, C_ℓ < 2^31 by the d2 ≤ 33025 refusal):
+//    x = Σ_ℓ C_ℓ·w_ℓ with w_ℓ = 2^{8ℓ+32} mod p (four IMAD.WIDE.U32), so x ≡ t·2^32 (mod p), then
+//    one Montgomery reduction REDC(x) = x·2^{−32} mod p ≡ t: q = x·(−p^{−1}) mod 2^32,
+//    y = (x + q·p) / 2^32 < 2p, one min-subtract — ≈ 8 instructions.  REDC needs x < p·2^32:
+//    redc = 2 when every C_ℓ < 2^30 (then x < 4·2^30·p), redc = 1 subtracts p·2^32 once
+//    (x < 4·2^31·p = 2·p·2^32).  The epilogue's ALU work is the issue-rate limit of the
+//    k_gemm_tc epilogue warps, which drain a tile in the time the MMAs compute the next.
 __device__ __forceinline__ uint32_t recombine_mod(int32_t c0, int32_t c1, int32_t c2, int32_t c3, const ModP& m) {
+  if (m.redc) {
+    uint64_t x = static_cast<uint64_t>(static_cast<uint32_t>(c0)) * m.w[0];
+    x += static_cast<uint64_t>(static_cast<uint32_t>(c1)) * m.w[1];
+    x += static_cast<uint64_t>(static_cast<uint32_t>(c2)) * m.w[2];
+    x += static_cast<uint64_t>(static_cast<uint32_t>(c3)) * m.w[3];
+    if (m.redc == 1) x = (x >= m.p32) ? x - m.p32 : x;
+    const uint32_t q = static_cast<uint32_t>(x) * m.pinv;
+    const uint32_t y = static_cast<uint32_t>((x + static_cast<uint64_t>(q) * m.p) >> 32);  // < 2p
+    return min(y, y - m.p);  // y − p wraps above y when y < p
+  }
   int64_t t = static_cast<int64_t>(c0) + (static_cast<int64_t>(c1) << 8) + (static_cast<int64_t>(c2) << 16) +
               (static_cast<int64_t>(c3) << 24);
   return barrett64(static_cast<uint64_t>(t + static_cast<int64_t>(m.off)), m);
@@ -336,7 +359,11 @@ __device__ __forceinline__ uint32_t rescale_last(uint32_t v, uint32_t xl, const 
   return barrett64(static_cast<uint64_t>(d) * o.p_last_inv, m);
 }
 
-__device__ __forceinline__ uint32_t sub_mod(uint32_t a, uint32_t b, uint32_t p) { return a >= b ? a - b : a + (p - b); }
+// (a − b) mod p for a, b ∈ [0, p): d = a − b wraps above p exactly when a < b
+__device__ __forceinline__ uint32_t sub_mod(uint32_t a, uint32_t b, uint32_t p) {
+  const uint32_t d = a - b;
+  return min(d, d + p);
+}
 
 // Standalone RNS Rescale of residue arrays (Alg. 7 step 2 on Ã's polynomials):
 // in [L][n] canonical residues → out [L−1][n] = ⌊x / p_{L−1}⌉ mod p_l.
