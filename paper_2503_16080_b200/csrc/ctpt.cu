@@ -442,7 +442,10 @@ constexpr int64_t kMvMaxD3 = 32;
 // On c4's ciphertexts: d3 = 64 / 128 / 160 / 192 → 1.03–1.05 / 0.81–0.91 / 0.82 / 0.73 of HBM vs
 // 0.84 / 0.81–0.82 / 0.70 / 0.64–0.65; at 224 / 256 the shared-memory kernel ties or wins
 // (0.63–0.64 vs 0.60–0.65; profiles/r02/fused_tmem_v3*/).
-constexpr int64_t kTmemMaxD3 = 192;
+#ifndef CTPT_FUSED_TMEM_MAXD3  // A/B build switch (tools/ab_build.py -DCTPT_FUSED_TMEM_MAXD3=256)
+#define CTPT_FUSED_TMEM_MAXD3 192
+#endif
+constexpr int64_t kTmemMaxD3 = CTPT_FUSED_TMEM_MAXD3;
 int mv_nc(const Dims& d) {  // N = 4·d3p, d3p ∈ {4, 8, 16, 32}
   int d3p = 4;
   while (d3p < d.d3_loc) d3p *= 2;
