@@ -40,6 +40,7 @@ def main():
 
     import torch
 
+    import bench
     import ctgen
     from paper_2503_16080_b200 import ctpt
     from paper_2503_16080_b200.engine import CpmmEngine
@@ -78,7 +79,7 @@ def main():
             def step(evs=None):
                 for l in range(len(ps)):
                     au, bu = AU[l * d3 * ra:], BU[l * d3 * c.d1:]
-                    if path == "mv" or (path == "auto" and d3 <= 32):
+                    if path == "mv" or (path == "auto" and bench.kernel_path(d3, 1, 0, 0, R) == "mv"):
                         if evs is not None:
                             evs[l][0].record(stream)
                         ctpt.gemm_mv(sp, l, eng.ctmat, eng.plain, au, bu, eng.ws, stream=stream)
@@ -97,6 +98,7 @@ def main():
             for _ in range(args.warmup):
                 step()
             torch.cuda.synchronize()
+            clk = bench.ClockSampler(torch.device("cuda", torch.cuda.current_device()))
             evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in ps]
                    for _ in range(args.steps)]
             t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -105,6 +107,7 @@ def main():
                 step(evs[s])
             t1.record(stream)
             torch.cuda.synchronize()
+            clocks = clk.stop()
             ms_step = t0.elapsed_time(t1) / args.steps
             k_ms = statistics.mean(a.elapsed_time(b) for row in evs for (a, b) in row)
             alg_bytes = 4 * R * d2 + d3 * d2 + 4 * R * d3
@@ -113,12 +116,14 @@ def main():
             print(json.dumps({
                 "sweep": "skinny", "path": path, "d3": d3, "L": len(ps), "R": R, "d2": d2,
                 "ms_per_step": ms_step, "residue_macs_per_s": macs / (ms_step / 1e3),
-                "kernel": ("k_gemm_mv" if path == "mv" or (path == "auto" and d3 <= 32) else
-                           "k_gemm_fused" if path.startswith("fused") or path == "auto" else "k_gemm_tc (after k_split)"),
+                "kernel": ("k_gemm_mv" if path == "mv" or (path == "auto" and bench.kernel_path(d3, 1, 0, 0, R) == "mv") else
+                           ("k_gemm_fused_t" if d3 <= 192 else "k_gemm_fused") if path.startswith("fused") or path == "auto"
+                           else "k_gemm_tc (after k_split)"),
                 "avg_launch_ms": k_ms,
                 "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
                              "frac": gbs / hbm_peak, "per_launch_bytes": alg_bytes},
                 "step_gbs_algorithmic": len(ps) * alg_bytes / (ms_step / 1e3) / 1e9,
+                "clocks": clocks,
             }), flush=True)
         del AU, BU
 
