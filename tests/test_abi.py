@@ -121,3 +121,46 @@ def test_split_overlap_workspace_and_validation(ctpt):
     assert resc.workspace_bytes == ctpt.query_sizes(_spec(ctpt, d3=300, primes=ps, rescale=1)).workspace_bytes
     with pytest.raises(ctpt.CtptError, match="ERR_ARG"):
         ctpt.query_sizes(_spec(ctpt, primes=ps, split_overlap=2))
+
+
+def test_schedule_fields_validated_without_gpu(ctpt):
+    """ctpt_problem.kernel / raster_group / max_ctas: out-of-range values are refused on the host;
+    a forced kernel that does not apply to the problem is refused by ctpt_matmul before any CUDA
+    call (ERR_UNSUPPORTED), never replaced by another path."""
+    for kw in (dict(kernel=4), dict(kernel=-1), dict(raster_group=-1), dict(max_ctas=-2)):
+        with pytest.raises(ctpt.CtptError, match="ERR_ARG"):
+            ctpt.query_sizes(_spec(ctpt, **kw))
+    ctpt.query_sizes(_spec(ctpt, kernel=ctpt.KERNEL_FUSED, raster_group=3, max_ctas=7))
+    lib = ctpt.raw_lib()
+    fake = ctypes.c_void_p(256)  # never dereferenced
+    ws = 1 << 30
+    pb = _spec(ctpt, d3=300, kernel=ctpt.KERNEL_FUSED).cstruct()        # d3_loc > 256
+    assert lib.ctpt_matmul(ctypes.byref(pb), fake, fake, fake, fake, fake, ws, None) == 6
+    pb = _spec(ctpt, d3=40, kernel=ctpt.KERNEL_MV).cstruct()            # d3_loc > 32
+    assert lib.ctpt_matmul(ctypes.byref(pb), fake, fake, fake, fake, fake, ws, None) == 6
+    pb = _spec(ctpt, d3=20, kU=2, kernel=ctpt.KERNEL_MV).cstruct()      # kU > 1
+    assert lib.ctpt_matmul(ctypes.byref(pb), fake, fake, fake, fake, fake, ws, None) == 6
+    assert b"needs" in lib.ctpt_last_error()
+
+
+def test_version_names_the_source_hash(ctpt):
+    """ctpt_version() carries src=<sha256 prefix of csrc/ + include/>, the hash build() compiles in."""
+    import __graft_entry__
+
+    assert ctpt.source_hash() == __graft_entry__.source_hash()
+
+
+def test_ipc_and_peer_entry_points_validate_without_gpu(ctpt):
+    """The multi-GPU gather plumbing refuses null arguments on the host (CTPT_ERR_ARG)."""
+    lib = ctpt.raw_lib()
+    h = (ctypes.c_char * ctpt.IPC_HANDLE_BYTES)()
+    off = ctypes.c_uint64(0)
+    base, ptr = ctypes.c_void_p(), ctypes.c_void_p()
+    assert lib.ctpt_ipc_export(None, ctypes.cast(h, ctypes.c_void_p), ctypes.byref(off)) == 1
+    assert lib.ctpt_ipc_export(ctypes.c_void_p(256), None, ctypes.byref(off)) == 1
+    assert lib.ctpt_ipc_open(None, 0, ctypes.byref(base), ctypes.byref(ptr)) == 1
+    assert lib.ctpt_ipc_open(ctypes.cast(h, ctypes.c_void_p), 0, None, ctypes.byref(ptr)) == 1
+    assert lib.ctpt_ipc_close(None) == 1
+    assert lib.ctpt_peer_access(0, 0, None) == 1
+    can = ctypes.c_int32(0)
+    assert lib.ctpt_peer_access(3, 3, ctypes.byref(can)) == 0 and can.value == 1  # a device reaches itself
