@@ -67,6 +67,8 @@ def parse():
                     help="Algorithm 6 with step 2 (SURVEY.md §8(f) row 3): U real uniform[-1,1) encoded at "
                          "Δ_U = the last prime (per-prime residues, kU = 4), RNS Rescale by that prime "
                          "fused into the other primes' epilogues")
+    ap.add_argument("--raster-group", type=int, default=0,
+                    help="k_gemm_tc raster group in j-tiles (ctpt_problem.raster_group; 0 = the library's choice)")
     ap.add_argument("--mode", default="auto", choices=["auto", "strong", "weak"],
                     help="auto: ONE problem strong-scaled over the ranks (N > 1, or a config whose inputs and "
                          "outputs do not fit one device-resident problem, i.e. c5: the primes stream through "
@@ -375,7 +377,7 @@ def run_ours(args, rank: int, world: int, local_rank: int, scaling: str = "stron
     want = args.split_overlap == "on" or (args.split_overlap == "auto" and c.d3 <= 8192)
     inkernel_split = want and not args.rescale and len(ps) >= 2 and not args.overlap
     eng = CpmmEngine(ctpt.Spec(c.fmt, c.N, c.d1, c.d2, c.d3, ps, rescale=int(args.rescale),
-                               split_overlap=int(inkernel_split)), dev)
+                               split_overlap=int(inkernel_split), raster_group=args.raster_group), dev)
     a_dev = torch.from_numpy(ct.a_polys.view(np.int32)).to(dev)
     b_dev = torch.from_numpy(ct.b_polys.view(np.int32)).to(dev)
     eng.layout(a_dev, b_dev, validate=True)
