@@ -33,6 +33,10 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--d3", default="1,16,32,64,128,256")
+    ap.add_argument("--u-shift", type=int, default=0,
+                    help="add this to U (e.g. 8: U in [0, 16], so the u8 plane needs no row correction)")
+    ap.add_argument("--plane", default="auto", choices=["auto", "always", "never"],
+                    help="the U plane mode (engine.precompute's `unsigned`): always = u8, never = s8 digits")
     ap.add_argument("--paths", default="auto,fused,split+gemm",
                     help="auto = ctpt_matmul's choice per prime (mv for d3 <= 32, else fused); fused = the "
                          "converter kernel (ctpt_gemm_fused); mv = ctpt_gemm_mv; split+gemm")
@@ -57,7 +61,8 @@ def main():
     eng = CpmmEngine(ctpt.Spec(c.fmt, c.N, c.d1, c.d2, d3max, ps), "cuda")
     eng.layout(ct.a_polys, ct.b_polys)
     del ct
-    kU = eng.precompute(U)
+    U = U + args.u_shift
+    kU = eng.precompute(U, unsigned=args.plane)
     assert kU == 1
     stream = torch.cuda.current_stream()
     R, d2 = c.R, c.d2
@@ -114,7 +119,8 @@ def main():
             macs = len(ps) * R * d2 * d3
             gbs = alg_bytes / (k_ms / 1e3) / 1e9
             print(json.dumps({
-                "sweep": "skinny", "path": path, "d3": d3, "L": len(ps), "R": R, "d2": d2,
+                "sweep": "skinny", "path": path, "d3": d3, "u_plane": "u8" if eng.spec.u_unsigned else "s8",
+                "u_offset": eng.spec.u_offset, "L": len(ps), "R": R, "d2": d2,
                 "ms_per_step": ms_step, "residue_macs_per_s": macs / (ms_step / 1e3),
                 "kernel": ("k_gemm_mv" if path == "mv" or (path == "auto" and bench.kernel_path(d3, 1, 0, 0, R) == "mv") else
                            ("k_gemm_fused_t" if d3 <= 192 else "k_gemm_fused") if path.startswith("fused") or path == "auto"
