@@ -408,11 +408,13 @@ struct GemmArgs {
   SplitJob sj;           // the next prime's limb split, run inside the first pass (sj.x = nullptr: none)
   int raster_group;      // k_gemm_tc raster group (0: automatic)
   int max_ctas;          // cap on the persistent grids (0: one CTA per SM)
+  int64_t u_offset;      // unsigned-U plane offset (the fused skinny kernel forms the row sums itself)
 };
 // GemmArgs fields that come straight from the problem
 void gemm_args_from_problem(GemmArgs& g, const ctpt_problem* pb) {
   g.raster_group = pb->raster_group;
   g.max_ctas = pb->max_ctas;
+  g.u_offset = pb->u_unsigned ? pb->u_offset : 0;
 }
 // persistent grid size: one CTA per SM (or the caller's cap, e.g. SMs left to a concurrent
 // communication kernel), never more than the work units
@@ -476,17 +478,26 @@ MvPlan mv_plan(const Dims& d) {
   m.total = m.ticket_off + align256(static_cast<size_t>(m.tiles) * 4);
   return m;
 }
+// the limbs-in-TMEM kernel forms the unsigned-U row sums itself; the other skinny kernels need u_offset = 0
 bool fused_applies(const Dims& d, int kU, const ctpt_problem* pb) {
+#ifdef CTPT_FUSED_SMEM_LIMBS  // A/B build: the limbs-in-shared-memory kernel has no row sums
   return kU == 1 && d.d3_loc <= kFusedMaxD3 && !needs_rowcorr(pb);
+#else
+  return kU == 1 && d.d3_loc <= kFusedMaxD3 && (!needs_rowcorr(pb) || d.d3_loc <= kTmemMaxD3);
+#endif
 }
-bool mv_applies(const Dims& d, int kU, const ctpt_problem* pb) { return fused_applies(d, kU, pb) && d.d3_loc <= kMvMaxD3; }
+bool mv_applies(const Dims& d, int kU, const ctpt_problem* pb) {
+  return kU == 1 && d.d3_loc <= kMvMaxD3 && !needs_rowcorr(pb);
+}
 enum class Path { SplitGemm, Fused, Mv };
 ctpt_status choose_path(const ctpt_problem* pb, const Dims& d, Path& path) {
   const int kU = pb->kU <= 0 ? 1 : pb->kU;
   switch (pb->kernel) {
     case CTPT_KERNEL_SPLIT_GEMM: path = Path::SplitGemm; return CTPT_OK;
     case CTPT_KERNEL_FUSED:
-      if (!fused_applies(d, kU, pb)) return fail(CTPT_ERR_UNSUPPORTED, "fused kernel needs kU = 1, d3_loc <= 256 and u_offset = 0");
+      if (!fused_applies(d, kU, pb))
+        return fail(CTPT_ERR_UNSUPPORTED, "fused kernels need kU = 1 and d3_loc <= 256 (u_offset != 0: d3_loc <= %lld)",
+                    static_cast<long long>(kTmemMaxD3));
       path = Path::Fused;
       return CTPT_OK;
     case CTPT_KERNEL_MV:
@@ -844,6 +855,8 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
 ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st) {
   const Dims& d = g.d;
   if (g.kU != 1 || d.d3_loc > kFusedMaxD3) return fail(CTPT_ERR_UNSUPPORTED, "fused kernel needs kU = 1 and d3_loc <= 256");
+  if (g.u_offset != 0 && d.d3_loc > kTmemMaxD3)
+    return fail(CTPT_ERR_UNSUPPORTED, "u_offset != 0 needs d3_loc <= %lld for the fused kernels", static_cast<long long>(kTmemMaxD3));
   ctpt_status s = tc_setup();
   if (s != CTPT_OK) return s;
   CUtensorMap tmU;
@@ -880,8 +893,10 @@ ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st) 
     T.num_tiles = static_cast<int32_t>(ntt);
     T.np = static_cast<int32_t>((d.d3_loc + 15) / 16 * 16);
     T.u_unsigned = g.u_unsigned;
+    T.off_mod = static_cast<uint32_t>(((g.u_offset % static_cast<int64_t>(g.p)) + g.p) % g.p);
     T.m = P.m;
     T.o = P.o;
+    T.o.rowcorr = nullptr;  // the kernel forms the row sums while it splits X
     CUtensorMap tmUt, tmXt;
     s = make_tmap_u8(&tmUt, g.planes, d.d2, d.d3, g.nplanes, d.d2p, d.d3 * d.d2p, FT_BK, static_cast<uint32_t>(T.np), 1);
     if (s != CTPT_OK) return s;
@@ -1007,7 +1022,8 @@ ctpt_status ctpt_gemm_fused(const ctpt_problem* pb, int32_t l, const void* d_ctm
   ctpt_status s = check_problem(pb, d);
   if (s != CTPT_OK) return s;
   if (pb->rescale) return fail(CTPT_ERR_UNSUPPORTED, "Rescale needs every prime: use ctpt_matmul");
-  if (needs_rowcorr(pb)) return fail(CTPT_ERR_UNSUPPORTED, "the fused kernel does not form row sums (u_offset != 0)");
+  if (needs_rowcorr(pb) && d.d3_loc > kTmemMaxD3)
+    return fail(CTPT_ERR_UNSUPPORTED, "u_offset != 0 needs d3_loc <= %lld for the fused kernels", static_cast<long long>(kTmemMaxD3));
   if (l < 0 || l >= d.L) return fail(CTPT_ERR_ARG, "prime index %d out of range", l);
   if (!d_ctmat || !d_plain || (!d_AU_l && d.rows_A > 0) || !d_BU_l) return fail(CTPT_ERR_ARG, "null device pointer");
   GemmArgs g{};

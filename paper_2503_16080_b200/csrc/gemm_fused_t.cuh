@@ -52,8 +52,9 @@ __host__ __device__ constexpr int ft_raw_bytes(int sub) { return sub * 4 * FT_BO
 __host__ __device__ constexpr int ft_u_bytes(int npmax) { return npmax * 128; }
 __host__ __device__ constexpr int ft_raw_stages(int npmax, int sub) { return sub == 2 ? 5 : (npmax == 256 ? 6 : 10); }
 __host__ __device__ constexpr int ft_ast(int sub) { return sub == 2 ? 4 : 8; }
+// + 512 B of barriers, 1 KB of row-sum partials (unsigned-U row correction), 1 KB of alignment slack
 __host__ __device__ constexpr int ft_smem_bytes(int npmax, int sub) {
-  return FT_US * ft_u_bytes(npmax) + ft_raw_stages(npmax, sub) * ft_raw_bytes(sub) + 512 + 1024;
+  return FT_US * ft_u_bytes(npmax) + ft_raw_stages(npmax, sub) * ft_raw_bytes(sub) + 512 + 1024 + 1024;
 }
 
 struct FusedTParams {
@@ -63,9 +64,11 @@ struct FusedTParams {
   int32_t num_kb;      // ceil(d2p / 128)
   int32_t num_tiles;   // ceil(R / (32·SUB))
   int32_t np;          // MMA N = d3_loc rounded up to 16 (≤ NPMAX)
-  int32_t u_unsigned;  // U plane is u8 (U + u_offset, u_offset = 0 here) instead of balanced s8 digits
+  int32_t u_unsigned;  // U plane is u8 (U' = U + u_offset) instead of balanced s8 digits
+  uint32_t off_mod;    // u_offset mod p: the epilogue subtracts u_offset·Σ_k X[r][k] (row sums formed by the
+                       // converters while they split X); 0: no correction
   ModP m;
-  OutParams o;
+  OutParams o;         // o.rowcorr is not used (the row sums are formed in-kernel)
 };
 
 // D[tmem] (+)= A[tmem] · B[smem]^T, kind::i8 (A from tensor memory).
@@ -137,8 +140,15 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
   auto a_empty = [&](int s) { return bar_base + 8u * (2 * FT_US + 2 * RAW + FT_AST + s); };
   auto d_full = [&](int b) { return bar_base + 8u * (2 * FT_US + 2 * RAW + 2 * FT_AST + b); };
   auto d_empty = [&](int b) { return bar_base + 8u * (2 * FT_US + 2 * RAW + 2 * FT_AST + 2 + b); };
-  constexpr int NBAR = 2 * FT_US + 2 * RAW + 2 * FT_AST + 4;
+  // row-sum partials of tile t live in buffer t & 1: full = every converter warp wrote its partials,
+  // empty = every epilogue thread read them
+  auto rows_full = [&](int b) { return bar_base + 8u * (2 * FT_US + 2 * RAW + 2 * FT_AST + 4 + b); };
+  auto rows_empty = [&](int b) { return bar_base + 8u * (2 * FT_US + 2 * RAW + 2 * FT_AST + 6 + b); };
+  constexpr int NBAR = 2 * FT_US + 2 * RAW + 2 * FT_AST + 8;
   static_assert(8 * NBAR + 8 <= 512, "barrier area");
+  // rsum[buf][sub-tile][group][32 rows] u64 partial row sums (1 KB)
+  uint64_t* rsum = reinterpret_cast<uint64_t*>(smem + FT_US * U_BYTES + RAW * RAW_BYTES + 512);
+  static_assert(2 * SUB * GROUPS * 32 * 8 <= 1024, "row-sum area");
   const uint32_t tmem_slot = bar_base + 8u * NBAR;
   uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(smem + FT_US * U_BYTES + RAW * RAW_BYTES + 8 * NBAR);
 
@@ -166,6 +176,8 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(d_full(b), 1);
       mbar_init(d_empty(b), 128);
+      mbar_init(rows_full(b), 8);    // the 8 converter warps
+      mbar_init(rows_empty(b), 128); // the 128 epilogue threads
     }
     fence_mbar_init();
   }
@@ -254,6 +266,19 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
     const int nchunk = (P.np + 31) / 32;
     for (int32_t t = 0; t < my_tiles; ++t) {
       const int64_t tr = static_cast<int64_t>(blockIdx.x) + static_cast<int64_t>(t) * gridDim.x;
+      // unsigned-U plane: X·U = X·U' − u_offset·Σ_k X[r][k]; this thread's rows' corrections
+      uint32_t corr[SUB];
+      if (P.off_mod) {
+        mbar_wait(rows_full(t & 1), static_cast<uint32_t>((t >> 1) & 1));
+#pragma unroll
+        for (int sb = 0; sb < SUB; ++sb) {
+          uint64_t sum = 0;
+#pragma unroll
+          for (int g = 0; g < GROUPS; ++g) sum += rsum[(((t & 1) * SUB + sb) * GROUPS + g) * 32 + 8 * q + r];
+          corr[sb] = static_cast<uint32_t>(static_cast<uint64_t>(barrett64(sum, P.m)) * P.off_mod % P.m.p);
+        }
+        mbar_arrive(rows_empty(t & 1));
+      }
       mbar_wait(d_full(acc), acc_phase);
       tc_fence_after();
 #pragma unroll 1
@@ -273,8 +298,9 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
         for (int k = 0; k < 4; ++k)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const uint32_t res = recombine_mod(static_cast<int32_t>(lo[4 * k + e]), static_cast<int32_t>(lo[4 * k + 2 + e]),
-                                               static_cast<int32_t>(hi[4 * k + e]), static_cast<int32_t>(hi[4 * k + 2 + e]), P.m);
+            uint32_t res = recombine_mod(static_cast<int32_t>(lo[4 * k + e]), static_cast<int32_t>(lo[4 * k + 2 + e]),
+                                         static_cast<int32_t>(hi[4 * k + e]), static_cast<int32_t>(hi[4 * k + 2 + e]), P.m);
+            if (P.off_mod) res = sub_mod(res, sb == 0 ? corr[0] : corr[SUB - 1], P.m.p);
             const int64_t j = static_cast<int64_t>(c0) + 8 * k + 2 * c + e;
             if (j < P.o.d3_loc && row < P.o.R) store_out(P.o, P.m, j, row, res);  // (+ the Rescale epilogue)
           }
@@ -296,46 +322,69 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
     const int r = lane >> 2, c = lane & 3;
     const int row = 8 * q + r;            // row of the 32-row sub-tile
     const uint32_t t_lane = static_cast<uint32_t>(q * 32) << 16;
-    for (int64_t it = grp; it < n_it; it += GROUPS) {
-      const int rs = static_cast<int>(it % RAW);
-      const int as = static_cast<int>(it % FT_AST);
-      mbar_wait(raw_full(rs), static_cast<uint32_t>((it / RAW) & 1));
-      const uint32_t raw = raw_base + rs * RAW_BYTES + sb * 4 * FT_BOX_BYTES;
-      uint32_t l01[16], l23[16];
+    // Global iterations it ≡ grp (mod GROUPS), walked tile by tile so that every tile's row-sum
+    // partials are flushed — also by a group that has no K-block in the tile (num_kb = 1)
+    for (int32_t t = 0; t < my_tiles; ++t) {
+      const int64_t it0 = static_cast<int64_t>(t) * P.num_kb;
+      uint32_t lsum[4] = {0u, 0u, 0u, 0u};  // Σ of each limb over this thread's residues of the tile
+      for (int64_t it = it0 + ((grp - it0 % GROUPS) + GROUPS) % GROUPS; it < it0 + P.num_kb; it += GROUPS) {
+        const int rs = static_cast<int>(it % RAW);
+        const int as = static_cast<int>(it % FT_AST);
+        mbar_wait(raw_full(rs), static_cast<uint32_t>((it / RAW) & 1));
+        const uint32_t raw = raw_base + rs * RAW_BYTES + sb * 4 * FT_BOX_BYTES;
+        uint32_t l01[16], l23[16];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < 4; ++k) {
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          // residues 32k + 8c + 4e .. +3: box k, 16-B chunk 2c + e of row `row`
-          const int cb = 2 * c + e;
-          const uint32_t a = raw + k * FT_BOX_BYTES + row * 128 + ((cb ^ (row & 7)) << 4);
-          CTPT_CHECK(a >= raw_base && a + 16 <= raw_base + RAW * RAW_BYTES);
-          const uint4 x = lds128(a);
-          uint32_t w0, w1, w2, w3;
-          byte_transpose4(x.x, x.y, x.z, x.w, w0, w1, w2, w3);  // wm = limb m of the 4 residues
-          l01[4 * k + e] = w0;
-          l01[4 * k + 2 + e] = w1;
-          l23[4 * k + e] = w2;
-          l23[4 * k + 2 + e] = w3;
+          for (int e = 0; e < 2; ++e) {
+            // residues 32k + 8c + 4e .. +3: box k, 16-B chunk 2c + e of row `row`
+            const int cb = 2 * c + e;
+            const uint32_t a = raw + k * FT_BOX_BYTES + row * 128 + ((cb ^ (row & 7)) << 4);
+            CTPT_CHECK(a >= raw_base && a + 16 <= raw_base + RAW * RAW_BYTES);
+            const uint4 x = lds128(a);
+            uint32_t w0, w1, w2, w3;
+            byte_transpose4(x.x, x.y, x.z, x.w, w0, w1, w2, w3);  // wm = limb m of the 4 residues
+            l01[4 * k + e] = w0;
+            l01[4 * k + 2 + e] = w1;
+            l23[4 * k + e] = w2;
+            l23[4 * k + 2 + e] = w3;
+            if (P.off_mod) {  // byte sums of each limb (IDP4A): Σ_k x[k] = Σ_ℓ 2^{8ℓ} Σ_k x_ℓ[k]
+              lsum[0] = __dp4a(w0, 0x01010101u, lsum[0]);
+              lsum[1] = __dp4a(w1, 0x01010101u, lsum[1]);
+              lsum[2] = __dp4a(w2, 0x01010101u, lsum[2]);
+              lsum[3] = __dp4a(w3, 0x01010101u, lsum[3]);
+            }
+          }
         }
+        mbar_wait(a_empty(as), static_cast<uint32_t>(((it / FT_AST) & 1) ^ 1));
+        tc_fence_after();
+        const uint32_t ta = tmem_base + t_lane + A_COL0 + as * ASTAGE_COLS + sb * 32;
+        CTPT_CHECK(A_COL0 + as * ASTAGE_COLS + sb * 32 + 32 <= 512);
+        tmem_st16x256_x4(ta, l01);
+        tmem_st16x256_x4(ta + (16u << 16), l23);
+        // The raw tile is handed back only here: the STTMs take every limb word as an operand, so
+        // every LDS of the tile has completed (register computations such as the PRMTs may be
+        // scheduled past a fence; an asm operand may not), then a proxy fence orders the generic
+        // reads before the TMA's async-proxy refill.
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(raw_empty(rs));
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(a_full(as));
       }
-      mbar_wait(a_empty(as), static_cast<uint32_t>(((it / FT_AST) & 1) ^ 1));
-      tc_fence_after();
-      const uint32_t ta = tmem_base + t_lane + A_COL0 + as * ASTAGE_COLS + sb * 32;
-      CTPT_CHECK(A_COL0 + as * ASTAGE_COLS + sb * 32 + 32 <= 512);
-      tmem_st16x256_x4(ta, l01);
-      tmem_st16x256_x4(ta + (16u << 16), l23);
-      // The raw tile is handed back only here: the STTMs take every limb word as an operand, so
-      // every LDS of the tile has completed (register computations such as the PRMTs may be
-      // scheduled past a fence; an asm operand may not), then a proxy fence orders the generic
-      // reads before the TMA's async-proxy refill.
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(raw_empty(rs));
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(a_full(as));
+      if (P.off_mod) {
+        // this warp's partial row sums of tile t: Σ_ℓ 2^{8ℓ}·lsum_ℓ, summed over the 4 threads of a row
+        uint64_t part = static_cast<uint64_t>(lsum[0]) + (static_cast<uint64_t>(lsum[1]) << 8) +
+                        (static_cast<uint64_t>(lsum[2]) << 16) + (static_cast<uint64_t>(lsum[3]) << 24);
+        part += __shfl_xor_sync(0xffffffffu, part, 1);
+        part += __shfl_xor_sync(0xffffffffu, part, 2);
+        mbar_wait(rows_empty(t & 1), static_cast<uint32_t>(((t >> 1) & 1) ^ 1));
+        if (c == 0) rsum[(((t & 1) * SUB + sb) * GROUPS + grp) * 32 + row] = part;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(rows_full(t & 1));
+      }
     }
   }
 

@@ -13,6 +13,10 @@ import torch
 
 from . import ctpt
 
+# ctpt.cu kTmemMaxD3: the largest d3_loc the limbs-in-TMEM skinny kernel (which forms the unsigned-U
+# row sums itself) takes under CTPT_KERNEL_AUTO
+TMEM_MAX_D3 = 192
+
 
 def _u32_to_dev(a: np.ndarray, device) -> torch.Tensor:
     a = np.ascontiguousarray(a, dtype=np.uint32)
@@ -49,9 +53,14 @@ class CpmmEngine:
 
     # -- a2: plaintext precompute ------------------------------------------------------------
     def precompute(self, U, unsigned: str = "auto") -> int:
-        """U's digit planes.  unsigned="auto" stores one u8 plane U + u_offset when the problem is
-        in the GEMM regime (d3_loc > 256: lower tensor-core switching power under the power cap)
-        and U spans ≤ 255 values; "never" forces balanced s8 digits; "always" requires the u8 plane."""
+        """U's digit planes.  unsigned="auto" stores one u8 plane U + u_offset (lower tensor-core
+        switching power under the 1000 W cap than sign-extended s8 digits: +5 % on the GEMM, +2–10 %
+        in the power-bound skinny regime, profiles/r01/power_operands_c3gemm.jsonl,
+        profiles/r02/u8_skinny_probe/) when U spans ≤ 255 values and the kernel ctpt_matmul will pick
+        can correct for u_offset: k_gemm_tc (d3_loc > 256) and the limbs-in-TMEM skinny kernel
+        (d3_loc ≤ TMEM_MAX_D3, which forms the row sums itself) — not the raw-byte kernel (d3_loc ≤ 32
+        with fewer 64-row tiles than SMs) nor the shared-memory skinny kernel.  "never" forces balanced
+        s8 digits; "always" requires the u8 plane."""
         Ud = U if isinstance(U, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(U, dtype=np.int64))
         Ud = Ud.to(self.device)
         self.spec.kU = 4  # size the buffer for the worst case first
@@ -59,7 +68,10 @@ class CpmmEngine:
         sz = ctpt.query_sizes(self.spec)
         self.plain = torch.empty(sz.plain_bytes, dtype=torch.uint8, device=self.device)
         self.spec.plain_per_prime = 0
-        want_u8 = unsigned == "always" or (unsigned == "auto" and self.sizes.d3_loc > 256 and self.spec.d2 <= 33025)
+        d3l = self.sizes.d3_loc
+        sms = torch.cuda.get_device_properties(self.device).multi_processor_count
+        u8_kernel = d3l > 256 or (d3l <= TMEM_MAX_D3 and not (d3l <= 32 and (self.sizes.R + 63) // 64 < sms))
+        want_u8 = unsigned == "always" or (unsigned == "auto" and u8_kernel and self.spec.d2 <= 33025)
         if want_u8:
             self.spec.kU = 1
             try:

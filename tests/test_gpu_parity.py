@@ -815,3 +815,20 @@ def test_forced_kernel_refusals():
         run_gpu(fmt, N, N, d2, 300, ps, ct.a_polys, ct.b_polys, U=U, kernel=FUSED)
     with pytest.raises(ctpt.CtptError, match="ERR_UNSUPPORTED"):
         run_gpu(fmt, N, N, d2, 40, ps, ct.a_polys, ct.b_polys, U=U[:, :40], kernel=MV_K)
+
+
+@pytest.mark.parametrize("shape,max_ctas", [
+    ((S, 64, 3, 1000, 1, 2), 0),      # CP-Mv through the TMEM kernel with u_offset
+    ((A, 128, 4, 520, 64, 1), 0),
+    ((S, 32, 5, 384, 128, 2), 1),     # one CTA loops over every tile: the row-sum buffers wrap
+    ((A, 16, 3, 77, 129, 2), 0),      # 32-row tiles (d3 > 128), one K-block: a converter group with no K-block
+    ((R, 1024, 1, 2056, 160, 1), 3),
+    ((S, 128, 2, 100, 192, 1), 1),    # num_kb = 1 with 32-row tiles, several tiles per CTA
+], ids=lambda s: str(s))
+def test_skinny_unsigned_plane_row_sums(shape, max_ctas):
+    """The limbs-in-TMEM skinny kernel with the u8 plane U' = U + u_offset: the converters form
+    Σ_k X[r][k] (IDP4A byte sums of the limbs) while they split X, the epilogue subtracts
+    u_offset·Σ_k X[r][k] mod p (X·U = X·U' − u_offset·rowsum) — against the oracle, forced and
+    automatic kernel choice, several tiles per CTA."""
+    _check(*shape, unsigned="always", kernel=FUSED, max_ctas=max_ctas)
+    _check(*shape, unsigned="always", max_ctas=max_ctas, seed=3)
