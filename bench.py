@@ -555,7 +555,7 @@ def run_ours(args, rank: int, world: int, local_rank: int, scaling: str = "stron
         "pct_int8_clock_normalised": (100.0 * value * 4 * kU / world / (148 * 8192 * clocks["sm_mhz"] * 1e6)
                                       if clocks.get("sm_mhz") else None),
         "roofline": roofline_fused(c, d3l, gemm_avg_s, gemm_share, mp, which,
-                                   "k_gemm_mv" if mv else "k_gemm_fused_t" if d3l <= 192 else "k_gemm_fused")
+                                   "k_gemm_mv" if mv else "k_gemm_fused_t")
         if fused else {
                      "bound": "tensor", "achieved": achieved_tops, "peak": peak_tops, "unit": "TOP/s",
                      "frac": achieved_tops / peak_tops, "traffic": traffic if not args.rescale else None,
@@ -573,7 +573,7 @@ def run_ours(args, rank: int, world: int, local_rank: int, scaling: str = "stron
                      "dram_frac": (traffic / gemm_avg_s / 1e9 / float(mp["hbm_gbs"]))
                      if traffic and not args.rescale else None},
         "e2e": e2e,
-        # per prime: k_split[_rows] + kU x k_gemm_tc, or one k_gemm_fused / k_gemm_mv (+ k_expand_u)
+        # per prime: k_split[_rows] + kU x k_gemm_tc, or one k_gemm_fused_t / k_gemm_mv (+ k_expand_u)
         "gpu_launches": ((1 + kU * len(ps)) if inkernel_split else
                          (2 if mv else 1 if fused else 1 + kU) * len(ps)) * args.steps,
         "split_overlap": overlap,
@@ -665,8 +665,8 @@ def cublaslt_ratio(limb_macs_per_s: float, elapsed_ms: float):
     return {"ratio": 2 * limb_macs_per_s / 1e12 / float(pr[key]), "cublaslt_tops": pr[key], "which": key}
 
 
-def roofline_fused(c, d3l, launch_s, share, mp, which, kernel="k_gemm_fused"):
-    """HBM roofline of k_gemm_fused (skinny U): algorithmic bytes per launch (one prime) = 4·R·d2
+def roofline_fused(c, d3l, launch_s, share, mp, which, kernel="k_gemm_fused_t"):
+    """HBM roofline of the skinny kernels (k_gemm_fused_t, k_gemm_mv): algorithmic bytes per launch (one prime) = 4·R·d2
     (X int32, read once) + d3·d2 (U digits) + 4·R·d3 (outputs)."""
     alg = 4 * c.R * c.d2 + d3l * c.d2 + 4 * c.R * d3l
     gbs = alg / launch_s / 1e9

@@ -78,15 +78,14 @@ typedef enum { CTPT_RLWE = 0, CTPT_SHARED_S = 1, CTPT_SHARED_A = 2, CTPT_STRUCT_
 
 /* Which kernel path ctpt_matmul / ctpt_matmul_host run per prime (ctpt_problem.kernel).  AUTO:
  * the raw-byte kernel k_gemm_mv when d3_loc ≤ 32 and R has fewer 64-row tiles than the GPU has
- * SMs, the fused skinny kernels when d3_loc ≤ 256, else the limb split + k_gemm_tc (the first two
- * need kU = 1 and u_offset = 0).  A forced choice that does not apply returns
- * CTPT_ERR_UNSUPPORTED. */
+ * SMs, the fused skinny kernels when d3_loc ≤ 256, else the limb split + k_gemm_tc.  The first two
+ * need kU = 1; k_gemm_mv also needs u_offset = 0 (k_gemm_fused_t forms the unsigned-U row sums
+ * itself).  A forced choice that does not apply returns CTPT_ERR_UNSUPPORTED. */
 typedef enum {
   CTPT_KERNEL_AUTO = 0,
   CTPT_KERNEL_SPLIT_GEMM = 1, /* k_split[_rows] + k_gemm_tc (tcgen05, any d3, any kU)            */
-  CTPT_KERNEL_FUSED = 2,      /* split in the GEMM's load path, X read once: k_gemm_fused_t (limbs
-                                 in tensor memory, d3_loc ≤ 192) or k_gemm_fused (limbs in shared
-                                 memory, 192 < d3_loc ≤ 256)                                      */
+  CTPT_KERNEL_FUSED = 2,      /* k_gemm_fused_t: split in the GEMM's load path, X read once, the
+                                 limbs in tensor memory as the MMA's A operand (d3_loc ≤ 256)      */
   CTPT_KERNEL_MV = 3          /* k_gemm_mv: raw residue bytes × expanded U (d3_loc ≤ 32)          */
 } ctpt_kernel;
 
@@ -178,8 +177,9 @@ ctpt_status ctpt_plain_precompute(const ctpt_problem* prob, const int64_t* d_U, 
 
 /* Unsigned-U plaintext precompute: the same U as ctpt_plain_precompute, stored as ONE u8 plane
  * U' = U + u_offset ∈ [0, 255] with u_offset = max(0, −min U) (*u_offset_out).  The product is
- * unchanged — X·U = X·U' − u_offset·(Σ_k X[r][k]) — and ctpt_split forms the per-row sums while
- * it reads X, so the epilogue subtracts u_offset·Σ_k X[r][k] mod p (an O(R) correction, the
+ * unchanged — X·U = X·U' − u_offset·(Σ_k X[r][k]) — and ctpt_split (or, in the skinny regime, the
+ * limbs-in-TMEM kernel's converters) forms the per-row sums while it reads X, so the epilogue
+ * subtracts u_offset·Σ_k X[r][k] mod p (an O(R) correction, the
  * same bookkeeping as the paper's chop with digits of one sign).  Why: the tensor
  * cores' switching energy depends on the operand bits, and at the 1000 W cap a non-negative
  * small U (no sign-extended high bits) sustains ≈ 5 % more int8 ops
@@ -217,11 +217,11 @@ ctpt_status ctpt_gemm(const ctpt_problem* prob, int32_t l, const void* d_ws, siz
  * P:982; Table 4's d3 ∈ {1, 2^6, 2^7}).  For prime index l: the same
  * (A·U mod p, B·U mod p) as ctpt_split + ctpt_gemm, but the limb split runs inside the GEMM's
  * load path, reading the int32 residues of d_ctmat exactly once (no workspace): the regime is
- * HBM-bound and this saves the split's write + re-read.  d3_loc ≤ 192: k_gemm_fused_t (the limbs
- * go to tensor memory as the MMA's A operand, U^T is B); 192 < d3_loc ≤ 256: k_gemm_fused (limbs
- * in shared memory).  ctpt_matmul (and ctpt_matmul_host) choose these kernels automatically when
- * d3_loc ≤ 256 and kU = 1 (see ctpt_kernel; ctpt_problem.kernel overrides).  Outputs as for
- * ctpt_gemm.
+ * HBM-bound and this saves the split's write + re-read.  The kernel (k_gemm_fused_t) keeps the
+ * limbs in tensor memory as the MMA's A operand (U^T is B) and, with the unsigned-U plane, forms
+ * the row sums Σ_k X[r][k] for the u_offset correction while it splits X.  ctpt_matmul (and
+ * ctpt_matmul_host) choose it automatically when d3_loc ≤ 256 and kU = 1 (see ctpt_kernel;
+ * ctpt_problem.kernel overrides).  Outputs as for ctpt_gemm.
  * CTPT_ERR_UNSUPPORTED when kU ≠ 1 or d3_loc > 256.  Never synchronises. */
 ctpt_status ctpt_gemm_fused(const ctpt_problem* prob, int32_t l, const void* d_ctmat, const void* d_plain,
                             uint32_t* d_AU_l, uint32_t* d_BU_l, void* stream);

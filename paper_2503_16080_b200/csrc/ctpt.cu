@@ -13,7 +13,6 @@
 
 #include "../../include/ctpt.h"
 #include "gemm_tc.cuh"
-#include "gemm_fused.cuh"
 #include "gemm_fused_t.cuh"
 #include "gemm_mv.cuh"
 #include "kernels.cuh"
@@ -373,10 +372,6 @@ ctpt_status tc_setup() {
   cudaError_t& e = errs[dev];
   std::call_once(onces[dev], [&e] {
     e = cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BYTES);
-#ifdef CTPT_FUSED_SMEM_LIMBS
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_fused<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(1));
-#endif
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_fused<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, fu_smem_bytes(2));
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_gemm_fused_t<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ft_smem_bytes(128, 2));
     if (e == cudaSuccess)
@@ -439,15 +434,6 @@ ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st);
 // CTPT_KERNEL_AUTO takes the first that applies; a forced choice that does not apply is refused.
 constexpr int64_t kFusedMaxD3 = 256;
 constexpr int64_t kMvMaxD3 = 32;
-// The limbs-in-TMEM skinny kernel (gemm_fused_t.cuh) takes d3_loc ≤ 192 — 64-row tiles up to 128
-// columns, 32-row tiles above; the limbs-in-shared-memory kernel (gemm_fused.cuh) 192 < d3_loc ≤ 256.
-// On c4's ciphertexts: d3 = 64 / 128 / 160 / 192 → 1.03–1.05 / 0.81–0.91 / 0.82 / 0.73 of HBM vs
-// 0.84 / 0.81–0.82 / 0.70 / 0.64–0.65; at 224 / 256 the shared-memory kernel ties or wins
-// (0.63–0.64 vs 0.60–0.65; profiles/r02/fused_tmem_v3*/).
-#ifndef CTPT_FUSED_TMEM_MAXD3  // A/B build switch (tools/ab_build.py -DCTPT_FUSED_TMEM_MAXD3=256)
-#define CTPT_FUSED_TMEM_MAXD3 192
-#endif
-constexpr int64_t kTmemMaxD3 = CTPT_FUSED_TMEM_MAXD3;
 int mv_nc(const Dims& d) {  // N = 4·d3p, d3p ∈ {4, 8, 16, 32}
   int d3p = 4;
   while (d3p < d.d3_loc) d3p *= 2;
@@ -480,11 +466,8 @@ MvPlan mv_plan(const Dims& d) {
 }
 // the limbs-in-TMEM kernel forms the unsigned-U row sums itself; the other skinny kernels need u_offset = 0
 bool fused_applies(const Dims& d, int kU, const ctpt_problem* pb) {
-#ifdef CTPT_FUSED_SMEM_LIMBS  // A/B build: the limbs-in-shared-memory kernel has no row sums
-  return kU == 1 && d.d3_loc <= kFusedMaxD3 && !needs_rowcorr(pb);
-#else
-  return kU == 1 && d.d3_loc <= kFusedMaxD3 && (!needs_rowcorr(pb) || d.d3_loc <= kTmemMaxD3);
-#endif
+  (void)pb;
+  return kU == 1 && d.d3_loc <= kFusedMaxD3;
 }
 bool mv_applies(const Dims& d, int kU, const ctpt_problem* pb) {
   return kU == 1 && d.d3_loc <= kMvMaxD3 && !needs_rowcorr(pb);
@@ -495,9 +478,7 @@ ctpt_status choose_path(const ctpt_problem* pb, const Dims& d, Path& path) {
   switch (pb->kernel) {
     case CTPT_KERNEL_SPLIT_GEMM: path = Path::SplitGemm; return CTPT_OK;
     case CTPT_KERNEL_FUSED:
-      if (!fused_applies(d, kU, pb))
-        return fail(CTPT_ERR_UNSUPPORTED, "fused kernels need kU = 1 and d3_loc <= 256 (u_offset != 0: d3_loc <= %lld)",
-                    static_cast<long long>(kTmemMaxD3));
+      if (!fused_applies(d, kU, pb)) return fail(CTPT_ERR_UNSUPPORTED, "the fused kernel needs kU = 1 and d3_loc <= 256");
       path = Path::Fused;
       return CTPT_OK;
     case CTPT_KERNEL_MV:
@@ -855,81 +836,44 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
 ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st) {
   const Dims& d = g.d;
   if (g.kU != 1 || d.d3_loc > kFusedMaxD3) return fail(CTPT_ERR_UNSUPPORTED, "fused kernel needs kU = 1 and d3_loc <= 256");
-  if (g.u_offset != 0 && d.d3_loc > kTmemMaxD3)
-    return fail(CTPT_ERR_UNSUPPORTED, "u_offset != 0 needs d3_loc <= %lld for the fused kernels", static_cast<long long>(kTmemMaxD3));
   ctpt_status s = tc_setup();
   if (s != CTPT_OK) return s;
-  CUtensorMap tmU;
-  s = make_tmap_u8(&tmU, g.planes, d.d2, d.d3, g.nplanes, d.d2p, d.d3 * d.d2p, FU_BLOCK_K, 128, 1);
+  // limbs in tensor memory (gemm_fused_t.cuh): 64-row tiles (two 32-row sub-tiles sharing each U^T
+  // stage) up to 128 columns, 32-row tiles above; MMA N = d3_loc rounded up to 16; the unsigned-U
+  // row sums formed in the converters.  (The round-1 limbs-in-shared-memory kernel lost at every
+  // width: profiles/r02/fused_tmem_v3*/, fused_rowsum/; removed.)
+  FusedTParams T;
+  T.R = g.R;
+  T.j_off = static_cast<int32_t>(d.j0);
+  T.plane = g.plane0;
+  T.num_kb = static_cast<int32_t>((d.d2p + FT_BK - 1) / FT_BK);
+  const int sub = d.d3_loc <= 128 ? 2 : 1;
+  const int64_t ntt = (g.R + ft_rows(sub) - 1) / ft_rows(sub);
+  if (ntt > INT32_MAX) return fail(CTPT_ERR_SHAPE, "too many tiles");
+  T.num_tiles = static_cast<int32_t>(ntt);
+  T.np = static_cast<int32_t>((d.d3_loc + 15) / 16 * 16);
+  T.u_unsigned = g.u_unsigned;
+  T.off_mod = static_cast<uint32_t>(((g.u_offset % static_cast<int64_t>(g.p)) + g.p) % g.p);
+  T.m = make_modp(g.p, g.u_unsigned != 0, d.d2);
+  T.o = g.o;
+  T.o.accumulate = 0;
+  T.o.w = 1;
+  T.o.rowcorr = nullptr;  // the kernel forms the row sums while it splits X
+  CUtensorMap tmU, tmX;
+  s = make_tmap_u8(&tmU, g.planes, d.d2, d.d3, g.nplanes, d.d2p, d.d3 * d.d2p, FT_BK, static_cast<uint32_t>(T.np), 1);
   if (s != CTPT_OK) return s;
-  FusedParams P;
-  P.x = x;
-  P.R = g.R;
-  P.d2p = d.d2p;
-  P.j_off = static_cast<int32_t>(d.j0);
-  P.plane = g.plane0;
-  P.num_kb = static_cast<int32_t>((d.d2p + FU_BLOCK_K - 1) / FU_BLOCK_K);
-  const int64_t nt = (g.R + FU_BLOCK_R - 1) / FU_BLOCK_R;
-  if (nt > INT32_MAX) return fail(CTPT_ERR_SHAPE, "too many tiles");
-  P.num_tiles = static_cast<int32_t>(nt);
-  P.u_unsigned = g.u_unsigned;
-  P.m = make_modp(g.p, g.u_unsigned != 0, d.d2);
-  P.o = g.o;
-  P.o.accumulate = 0;
-  P.o.w = 1;
-#ifndef CTPT_FUSED_SMEM_LIMBS  // A/B build switch (tools/ab_build.py): the limbs-in-shared-memory kernel for all d3
-  if (d.d3_loc <= kTmemMaxD3) {
-    // limbs in tensor memory (gemm_fused_t.cuh): 64-row tiles (two 32-row sub-tiles sharing each U^T
-    // stage), MMA N = d3_loc rounded up to 16.  Measured against the limbs-in-shared-memory kernel
-    // on c4's ciphertexts: profiles/r02/fused_tmem_*; for 128 < d3_loc ≤ 256 that kernel stays.
-    FusedTParams T;
-    T.R = g.R;
-    T.j_off = static_cast<int32_t>(d.j0);
-    T.plane = g.plane0;
-    T.num_kb = static_cast<int32_t>((d.d2p + FT_BK - 1) / FT_BK);
-    const int sub = d.d3_loc <= 128 ? 2 : 1;
-    const int64_t ntt = (g.R + ft_rows(sub) - 1) / ft_rows(sub);
-    if (ntt > INT32_MAX) return fail(CTPT_ERR_SHAPE, "too many tiles");
-    T.num_tiles = static_cast<int32_t>(ntt);
-    T.np = static_cast<int32_t>((d.d3_loc + 15) / 16 * 16);
-    T.u_unsigned = g.u_unsigned;
-    T.off_mod = static_cast<uint32_t>(((g.u_offset % static_cast<int64_t>(g.p)) + g.p) % g.p);
-    T.m = P.m;
-    T.o = P.o;
-    T.o.rowcorr = nullptr;  // the kernel forms the row sums while it splits X
-    CUtensorMap tmUt, tmXt;
-    s = make_tmap_u8(&tmUt, g.planes, d.d2, d.d3, g.nplanes, d.d2p, d.d3 * d.d2p, FT_BK, static_cast<uint32_t>(T.np), 1);
-    if (s != CTPT_OK) return s;
-    s = make_tmap_u32_sw128(&tmXt, x, d.d2p, g.R);
-    if (s != CTPT_OK) return s;
-    const int64_t cap = grid_cap(g.max_ctas);
-    const int64_t rounds = (ntt + cap - 1) / cap;
-    const unsigned grid = static_cast<unsigned>((ntt + rounds - 1) / rounds);
-    if (sub == 2)
-      k_gemm_fused_t<128, 2><<<grid, FT_THREADS, ft_smem_bytes(128, 2), st>>>(tmUt, tmXt, T);
-    else
-      k_gemm_fused_t<256, 1><<<grid, FT_THREADS, ft_smem_bytes(256, 1), st>>>(tmUt, tmXt, T);
-    CUDA_TRY(cudaGetLastError());
-    return CTPT_OK;
-  }
-#endif
-  // balanced persistent grid: the same number of rounds as min(nt, SMs) CTAs would take, spread
+  s = make_tmap_u32_sw128(&tmX, x, d.d2p, g.R);
+  if (s != CTPT_OK) return s;
+  // balanced persistent grid: the same number of rounds as min(tiles, SMs) CTAs would take, spread
   // over as few CTAs as that needs, so no round ends with most SMs idle behind a few stragglers
   // (an HBM-bound CTA can pull more than 1/148 of the bandwidth; profiles/r01/fused_balanced_grid/)
   const int64_t cap = grid_cap(g.max_ctas);
-  const int64_t rounds = (nt + cap - 1) / cap;
-  const unsigned grid = static_cast<unsigned>((nt + rounds - 1) / rounds);
-  CUtensorMap tmX;
-  s = make_tmap_2d(&tmX, x, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, d.d2p, g.R, FU_BLOCK_K, FU_BLOCK_R);
-  if (s != CTPT_OK) return s;
-#ifdef CTPT_FUSED_SMEM_LIMBS
-  if (d.d3_loc <= 128) {
-    k_gemm_fused<1><<<grid, FU_THREADS, fu_smem_bytes(1), st>>>(tmU, tmX, P);
-    CUDA_TRY(cudaGetLastError());
-    return CTPT_OK;
-  }
-#endif
-  k_gemm_fused<2><<<grid, FU_THREADS, fu_smem_bytes(2), st>>>(tmU, tmX, P);
+  const int64_t rounds = (ntt + cap - 1) / cap;
+  const unsigned grid = static_cast<unsigned>((ntt + rounds - 1) / rounds);
+  if (sub == 2)
+    k_gemm_fused_t<128, 2><<<grid, FT_THREADS, ft_smem_bytes(128, 2), st>>>(tmU, tmX, T);
+  else
+    k_gemm_fused_t<256, 1><<<grid, FT_THREADS, ft_smem_bytes(256, 1), st>>>(tmU, tmX, T);
   CUDA_TRY(cudaGetLastError());
   return CTPT_OK;
 }
@@ -1022,8 +966,6 @@ ctpt_status ctpt_gemm_fused(const ctpt_problem* pb, int32_t l, const void* d_ctm
   ctpt_status s = check_problem(pb, d);
   if (s != CTPT_OK) return s;
   if (pb->rescale) return fail(CTPT_ERR_UNSUPPORTED, "Rescale needs every prime: use ctpt_matmul");
-  if (needs_rowcorr(pb) && d.d3_loc > kTmemMaxD3)
-    return fail(CTPT_ERR_UNSUPPORTED, "u_offset != 0 needs d3_loc <= %lld for the fused kernels", static_cast<long long>(kTmemMaxD3));
   if (l < 0 || l >= d.L) return fail(CTPT_ERR_ARG, "prime index %d out of range", l);
   if (!d_ctmat || !d_plain || (!d_AU_l && d.rows_A > 0) || !d_BU_l) return fail(CTPT_ERR_ARG, "null device pointer");
   GemmArgs g{};

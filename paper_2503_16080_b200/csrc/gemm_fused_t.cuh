@@ -1,10 +1,14 @@
 // gemm_fused_t.cuh — the skinny-U limb GEMM with the limb split fused into its load path and the
-// byte limbs kept in TENSOR MEMORY (32 < d3 ≤ 256; Table 4's d3 ∈ {2^6,
-// 2^7}).
+// byte limbs kept in TENSOR MEMORY (d3 ≤ 256, CP-Mv at d3 = 1 included;
+// Table 4's d3 ∈ {1, 2^6, 2^7}; CP-Mv).
 //
-// Same contraction and epilogue arithmetic as gemm_tc.cuh / gemm_fused.cuh (C_ℓ = X_ℓ·U over Z,
-// out = Σ 2^{8ℓ} C_ℓ mod p), same "read X exactly once" schedule as gemm_fused.cuh,
-// but the operands swap roles so that the limbs never touch shared memory:
+// Same contraction and epilogue arithmetic as gemm_tc.cuh (C_ℓ = X_ℓ·U over Z, out = Σ 2^{8ℓ} C_ℓ
+// mod p).  Below the ridge (≈ d3 limb MACs per byte of X) the step is HBM-bound, so
+// the schedule reads X exactly once: a tile is 64 (or 32) rows of X × ALL of U's d3_loc columns ×
+// the full K loop, and the int32 residues are split into their four base-2^8 digits on the way in
+// (no limb workspace: 4 B of HBM per residue instead of split + GEMM's 4 + 4 + 4).  Round 1's
+// kernel kept the limbs in shared memory as the MMA's B operand with U^T as A (M = 128 columns
+// of U); this one swaps the operand roles so that the limbs never touch shared memory:
 //   MMA A = the limb tile in TMEM (tcgen05.mma …, [a-tmem]): M = 128 lanes = 32 rows of X × 4
 //           limbs — lane 16h + 8ℓ' + r of quadrant q holds limb 2h + ℓ' of row 8q + r of the
 //           tile, its 32-bit columns 4 consecutive residues' bytes (K-major);
@@ -20,8 +24,12 @@
 //
 // Converter data path per K-block (32 rows × 128 residues, 16 KB per sub-tile): TMA raw tiles
 // (4 boxes of 32 rows × 32 residues, SWIZZLE_128B) → LDS.128 → PRMT 4×4 byte transpose → STTM.
-// Two converter groups (warps 8–11, 12–15) take alternate K-blocks; every ring length is even so a
-// stage always meets the same group (round 1's parity lesson, gemm_fused.cuh).
+// Two converter groups (warps 8–11, 12–15) take alternate K-blocks for 32-row tiles; every ring
+// length is then even so a stage always meets the same group (round 1's parity lesson: a group
+// two phases behind once passed a barrier of the other group's fill).
+// Unsigned-U plane (U' = U + u_offset): the converters also form Σ_k X[r][k] (IDP4A byte sums of
+// the limb words), flushed per tile through shared memory; the epilogue subtracts
+// u_offset·Σ_k X[r][k] mod p.
 // Warp roles (512 threads): w0 U^T TMA, w1 MMA issuer, w2 TMEM allocator, w3 raw X TMA,
 // w4–7 epilogue, w8–15 converters.
 #pragma once
@@ -40,13 +48,12 @@ constexpr int FT_THREADS = 512;
 constexpr int FT_US = 4;             // U^T stages in shared memory
 // Two shapes (template <NPMAX, SUB>):
 //   SUB = 2, NPMAX = 128 (d3_loc ≤ 128): a tile is 64 rows = two 32-row sub-tiles that share each
-//     U^T stage (U^T is read from L2 once per 64 rows, as in gemm_fused.cuh); one D buffer of
+//     U^T stage (U^T is read from L2 once per 64 rows); one D buffer of
 //     2 × 128 columns + 4 A stages of 2 × 32 columns; the 8 converter warps split every K-block
 //     (warp 8 + 4s + q: sub-tile s, quadrant q);
-//   SUB = 1, NPMAX = 256: 32-row tiles, one D buffer of 256 columns + 8 A stages of 32 columns;
-//     two converter groups of 4 warps take alternate K-blocks.  (Measured slower than the
-//     limbs-in-shared-memory kernel for 128 < d3 ≤ 256 — U^T is then re-read from L2 once per 32
-//     rows, 2 B per byte of X — so ctpt_matmul does not use it; profiles/r02/fused_tmem_v1/.)
+//   SUB = 1, NPMAX = 256 (128 < d3_loc ≤ 256): 32-row tiles (a 64-row D would need all 512 TMEM
+//     columns), one D buffer of 256 columns + 8 A stages of 32 columns; two converter groups of 4
+//     warps take alternate K-blocks; U^T is read from L2 once per 32 rows.
 __host__ __device__ constexpr int ft_rows(int sub) { return 32 * sub; }
 __host__ __device__ constexpr int ft_raw_bytes(int sub) { return sub * 4 * FT_BOX_BYTES; }
 __host__ __device__ constexpr int ft_u_bytes(int npmax) { return npmax * 128; }

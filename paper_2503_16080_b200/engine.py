@@ -13,9 +13,9 @@ import torch
 
 from . import ctpt
 
-# ctpt.cu kTmemMaxD3: the largest d3_loc the limbs-in-TMEM skinny kernel (which forms the unsigned-U
-# row sums itself) takes under CTPT_KERNEL_AUTO
-TMEM_MAX_D3 = 192
+# the largest d3_loc the limbs-in-TMEM skinny kernel (which forms the unsigned-U row sums itself)
+# takes under CTPT_KERNEL_AUTO (ctpt.cu kFusedMaxD3)
+TMEM_MAX_D3 = 256
 
 
 def _u32_to_dev(a: np.ndarray, device) -> torch.Tensor:
@@ -59,8 +59,8 @@ class CpmmEngine:
         profiles/r02/u8_skinny_probe/) when U spans ≤ 255 values and the kernel ctpt_matmul will pick
         can correct for u_offset: k_gemm_tc (d3_loc > 256) and the limbs-in-TMEM skinny kernel
         (d3_loc ≤ TMEM_MAX_D3, which forms the row sums itself) — not the raw-byte kernel (d3_loc ≤ 32
-        with fewer 64-row tiles than SMs) nor the shared-memory skinny kernel.  "never" forces balanced
-        s8 digits; "always" requires the u8 plane."""
+        with fewer 64-row tiles than SMs).  "never" forces balanced s8 digits; "always" requires the
+        u8 plane."""
         Ud = U if isinstance(U, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(U, dtype=np.int64))
         Ud = Ud.to(self.device)
         self.spec.kU = 4  # size the buffer for the worst case first

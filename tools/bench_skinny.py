@@ -123,7 +123,7 @@ def main():
                 "u_offset": eng.spec.u_offset, "L": len(ps), "R": R, "d2": d2,
                 "ms_per_step": ms_step, "residue_macs_per_s": macs / (ms_step / 1e3),
                 "kernel": ("k_gemm_mv" if path == "mv" or (path == "auto" and bench.kernel_path(d3, 1, 0, 0, R) == "mv") else
-                           ("k_gemm_fused_t" if d3 <= 192 else "k_gemm_fused") if path.startswith("fused") or path == "auto"
+                           "k_gemm_fused_t" if path.startswith("fused") or path == "auto"
                            else "k_gemm_tc (after k_split)"),
                 "avg_launch_ms": k_ms,
                 "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
