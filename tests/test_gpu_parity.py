@@ -155,9 +155,9 @@ def test_skinny_fused(shape):
 
 @pytest.mark.parametrize("cols", [(0, 129), (20, 220), (44, 300), (171, 300)])
 def test_skinny_column_shards(cols):
-    """k_gemm_fused on column blocks [c0, c1) of a wider U (129..256 columns: the second MMA group
-    holds U^T rows j_off + 128.. — partly past the block and, for (171, 300), past d3), with ragged R
-    (not a multiple of the 64-row tile) and more CTAs than tiles."""
+    """k_gemm_fused_t on column blocks [c0, c1) of a wider U (129..256 columns: 32-row tiles, U^T
+    rows j_off .. j_off + N partly past the block and, for (171, 300), past d3), with ragged R (not a
+    multiple of the tile) and more CTAs than tiles."""
     _check(A, 64, 3, 333, 300, 2, col_begin=cols[0], col_end=cols[1], seed=5, kernel=FUSED)
     _check(S, 512, 9, 300, 300, 1, col_begin=cols[0], col_end=cols[1], seed=6, kernel=FUSED)  # R = 9216: 144 tiles
 

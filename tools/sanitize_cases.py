@@ -15,8 +15,9 @@ Cases (kept small: the sanitizers slow kernels down 10–100×):
   gemm          limb split + k_gemm_tc, 3 primes, ragged R / d2 / d3 (several tiles, 2 raster groups)
   gemm_side     the same with split_overlap = 1 (prime l+1 split by warps 2–3 inside GEMM l)
   gemm_u8       the unsigned-U plane (row-sum correction in the epilogue), k_U = 2 (accumulating passes)
-  fused_wrap    the skinny kernels with long K (65 k-blocks: the rings wrap many times): k_gemm_fused_t
-                (d3 ≤ 128, limbs in TMEM) and k_gemm_fused (NG = 2), and one CTA looping over 4–8 tiles
+  fused_wrap    the skinny kernel k_gemm_fused_t with long K (65 k-blocks: the rings wrap many times),
+                64-row (d3 ≤ 128) and 32-row tiles, the u8 plane's in-kernel row sums, and one CTA
+                looping over 4–8 tiles
   mv_tickets    k_gemm_mv with the K loop split into units that meet on an atomic ticket
   layout        k_layout_v4 (16-byte) and k_layout (4-byte) with validate = 1
   host          ctpt_matmul_host (three streams, double-buffered staging), split + GEMM and fused chunks
@@ -174,7 +175,9 @@ CASES = {
     "fused_wrap": lambda: check("fused_wrap", A, 64, 2, 8200, 100, 1, kernel=2) +
                           check("fused_wrap", S, 32, 3, 8200, 200, 1, kernel=2) +
                           check("fused_multi", S, 32, 4, 520, 100, 1, kernel=2, max_ctas=1) +
-                          check("fused_multi", S, 32, 4, 520, 200, 1, kernel=2, max_ctas=1),
+                          check("fused_multi", S, 32, 4, 520, 200, 1, kernel=2, max_ctas=1) +
+                          check("fused_u8", S, 32, 4, 520, 100, 1, kernel=2, unsigned="always", max_ctas=1) +
+                          check("fused_u8", A, 64, 2, 8200, 200, 1, kernel=2, unsigned="always"),
     "mv_tickets": lambda: check("mv_tickets", S, 512, 2, 8200, 3, 1, kernel=3) +
                           check("mv_tickets", A, 64, 3, 4112, 20, 2, kernel=3),
     "layout": case_layout,
