@@ -45,23 +45,28 @@ constexpr int FT_BK = 128;           // residues (K bytes of each limb row) per 
 constexpr int FT_MMA_K = 32;
 constexpr int FT_BOX_BYTES = 4096;   // one raw TMA box: 32 rows × 32 residues
 constexpr int FT_THREADS = 512;
-constexpr int FT_US = 4;             // U^T stages in shared memory
-// Two shapes (template <NPMAX, SUB>):
-//   SUB = 2, NPMAX = 128 (d3_loc ≤ 128): a tile is 64 rows = two 32-row sub-tiles that share each
-//     U^T stage (U^T is read from L2 once per 64 rows); one D buffer of
-//     2 × 128 columns + 4 A stages of 2 × 32 columns; the 8 converter warps split every K-block
-//     (warp 8 + 4s + q: sub-tile s, quadrant q);
-//   SUB = 1, NPMAX = 256 (128 < d3_loc ≤ 256): 32-row tiles (a 64-row D would need all 512 TMEM
+// Shapes (template <NPMAX, SUB>):
+//   SUB = 2 (d3_loc ≤ 192): a tile is 64 rows = two 32-row sub-tiles that share each U^T stage
+//     (U^T is read from L2 once per 64 rows); one D buffer of 2 × NPMAX columns and the rest of
+//     TMEM as A stages of 2 × 32 columns (NPMAX = 128 / 160 / 192: 4 / 3 / 2 stages); the 8
+//     converter warps split every K-block (warp 8 + 4s + q: sub-tile s, quadrant q);
+//   SUB = 1, NPMAX = 256 (192 < d3_loc ≤ 256): 32-row tiles (a 64-row D would need all 512 TMEM
 //     columns), one D buffer of 256 columns + 8 A stages of 32 columns; two converter groups of 4
 //     warps take alternate K-blocks; U^T is read from L2 once per 32 rows.
 __host__ __device__ constexpr int ft_rows(int sub) { return 32 * sub; }
 __host__ __device__ constexpr int ft_raw_bytes(int sub) { return sub * 4 * FT_BOX_BYTES; }
 __host__ __device__ constexpr int ft_u_bytes(int npmax) { return npmax * 128; }
-__host__ __device__ constexpr int ft_raw_stages(int npmax, int sub) { return sub == 2 ? 5 : (npmax == 256 ? 6 : 10); }
-__host__ __device__ constexpr int ft_ast(int sub) { return sub == 2 ? 4 : 8; }
+// U^T stages in shared memory; raw X stages (≥ 128 KB in flight per SM where it fits beside U^T)
+__host__ __device__ constexpr int ft_us(int npmax, int sub) { return (sub == 2 && npmax == 160) ? 3 : 4; }
+__host__ __device__ constexpr int ft_raw_stages(int npmax, int sub) {
+  return sub == 2 ? (npmax == 192 ? 4 : 5) : (npmax == 256 ? 6 : 10);
+}
+__host__ __device__ constexpr int ft_ast(int npmax, int sub) {
+  return sub == 2 ? ((512 - 2 * npmax) / 64 < 4 ? (512 - 2 * npmax) / 64 : 4) : 8;
+}
 // + 512 B of barriers, 1 KB of row-sum partials (unsigned-U row correction), 1 KB of alignment slack
 __host__ __device__ constexpr int ft_smem_bytes(int npmax, int sub) {
-  return FT_US * ft_u_bytes(npmax) + ft_raw_stages(npmax, sub) * ft_raw_bytes(sub) + 512 + 1024 + 1024;
+  return ft_us(npmax, sub) * ft_u_bytes(npmax) + ft_raw_stages(npmax, sub) * ft_raw_bytes(sub) + 512 + 1024 + 1024;
 }
 
 struct FusedTParams {
@@ -125,7 +130,10 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
   constexpr int U_BYTES = ft_u_bytes(NPMAX);
   constexpr int RAW = ft_raw_stages(NPMAX, SUB);
   constexpr int RAW_BYTES = ft_raw_bytes(SUB);
-  constexpr int FT_AST = ft_ast(SUB);
+  constexpr int FT_AST = ft_ast(NPMAX, SUB);
+  constexpr int FT_US = ft_us(NPMAX, SUB);
+  static_assert(ft_smem_bytes(NPMAX, SUB) <= 232448, "shared memory per CTA");
+  static_assert(FT_AST >= 2, "at least two limb stages (convert one while the MMA reads the other)");
   constexpr int ROWS = ft_rows(SUB);
   constexpr int NBUF = 1;                      // D: SUB × NPMAX columns (one buffer)
   constexpr int D_COLS = SUB * NPMAX;
