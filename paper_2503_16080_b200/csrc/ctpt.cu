@@ -379,6 +379,8 @@ ctpt_status tc_setup() {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_gemm_fused_t<192, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ft_smem_bytes(192, 2));
     if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_gemm_fused_t<224, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ft_smem_bytes(224, 2));
+    if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_gemm_fused_t<256, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, ft_smem_bytes(256, 1));
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_mv<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, MV_SMEM_BYTES);
@@ -843,7 +845,7 @@ ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st) 
   ctpt_status s = tc_setup();
   if (s != CTPT_OK) return s;
   // limbs in tensor memory (gemm_fused_t.cuh): 64-row tiles (two 32-row sub-tiles sharing each U^T
-  // stage) up to 192 columns, 32-row tiles above; MMA N = d3_loc rounded up to 16; the unsigned-U
+  // stage) up to 224 columns, 32-row tiles above; MMA N = d3_loc rounded up to 16; the unsigned-U
   // row sums formed in the converters.  (The round-1 limbs-in-shared-memory kernel lost at every
   // width: profiles/r02/fused_tmem_v3*/, fused_rowsum/; removed.)
   FusedTParams T;
@@ -852,7 +854,7 @@ ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st) 
   T.plane = g.plane0;
   T.num_kb = static_cast<int32_t>((d.d2p + FT_BK - 1) / FT_BK);
 #ifndef CTPT_FT_SUB2_MAX
-#define CTPT_FT_SUB2_MAX 192  // widest d3_loc on 64-row tiles (A/B builds: 128 = round 2's first cut)
+#define CTPT_FT_SUB2_MAX 224  // widest d3_loc on 64-row tiles (A/B builds: 192 = 32-row tiles above)
 #endif
   const int sub = d.d3_loc <= CTPT_FT_SUB2_MAX ? 2 : 1;
   const int64_t ntt = (g.R + ft_rows(sub) - 1) / ft_rows(sub);
@@ -881,8 +883,10 @@ ctpt_status launch_fused(const GemmArgs& g, const uint32_t* x, cudaStream_t st) 
     k_gemm_fused_t<128, 2><<<grid, FT_THREADS, ft_smem_bytes(128, 2), st>>>(tmU, tmX, T);
   else if (sub == 2 && d.d3_loc <= 160)
     k_gemm_fused_t<160, 2><<<grid, FT_THREADS, ft_smem_bytes(160, 2), st>>>(tmU, tmX, T);
-  else if (sub == 2)
+  else if (sub == 2 && d.d3_loc <= 192)
     k_gemm_fused_t<192, 2><<<grid, FT_THREADS, ft_smem_bytes(192, 2), st>>>(tmU, tmX, T);
+  else if (sub == 2)
+    k_gemm_fused_t<224, 2><<<grid, FT_THREADS, ft_smem_bytes(224, 2), st>>>(tmU, tmX, T);
   else
     k_gemm_fused_t<256, 1><<<grid, FT_THREADS, ft_smem_bytes(256, 1), st>>>(tmU, tmX, T);
   CUDA_TRY(cudaGetLastError());

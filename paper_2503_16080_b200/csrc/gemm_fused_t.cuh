@@ -46,23 +46,30 @@ constexpr int FT_MMA_K = 32;
 constexpr int FT_BOX_BYTES = 4096;   // one raw TMA box: 32 rows × 32 residues
 constexpr int FT_THREADS = 512;
 // Shapes (template <NPMAX, SUB>):
-//   SUB = 2 (d3_loc ≤ 192): a tile is 64 rows = two 32-row sub-tiles that share each U^T stage
+//   SUB = 2 (d3_loc ≤ 224): a tile is 64 rows = two 32-row sub-tiles that share each U^T stage
 //     (U^T is read from L2 once per 64 rows); one D buffer of 2 × NPMAX columns and the rest of
-//     TMEM as A stages of 2 × 32 columns (NPMAX = 128 / 160 / 192: 4 / 3 / 2 stages); the 8
-//     converter warps split every K-block (warp 8 + 4s + q: sub-tile s, quadrant q);
-//   SUB = 1, NPMAX = 256 (192 < d3_loc ≤ 256): 32-row tiles (a 64-row D would need all 512 TMEM
+//     TMEM as A stages of 2 × AW columns, AW = 32 (a K-block, 128 residues) or 16 (half a
+//     K-block): NPMAX = 128 / 160 / 192 / 224 → 4 / 3 / 2 / 2 stages of AW = 32 / 32 / 32 / 16;
+//     the 8 converter warps split every K-block (warp 8 + 4s + q: sub-tile s, quadrant q);
+//   SUB = 1, NPMAX = 256 (224 < d3_loc ≤ 256): 32-row tiles (a 64-row D would need all 512 TMEM
 //     columns), one D buffer of 256 columns + 8 A stages of 32 columns; two converter groups of 4
 //     warps take alternate K-blocks; U^T is read from L2 once per 32 rows.
 __host__ __device__ constexpr int ft_rows(int sub) { return 32 * sub; }
 __host__ __device__ constexpr int ft_raw_bytes(int sub) { return sub * 4 * FT_BOX_BYTES; }
 __host__ __device__ constexpr int ft_u_bytes(int npmax) { return npmax * 128; }
 // U^T stages in shared memory; raw X stages (≥ 128 KB in flight per SM where it fits beside U^T)
-__host__ __device__ constexpr int ft_us(int npmax, int sub) { return (sub == 2 && npmax == 160) ? 3 : 4; }
+__host__ __device__ constexpr int ft_us(int npmax, int sub) { return (sub == 2 && npmax >= 160 && npmax != 192) ? 3 : 4; }
 __host__ __device__ constexpr int ft_raw_stages(int npmax, int sub) {
-  return sub == 2 ? (npmax == 192 ? 4 : 5) : (npmax == 256 ? 6 : 10);
+  return sub == 2 ? (npmax >= 192 ? 4 : 5) : (npmax == 256 ? 6 : 10);
 }
+#ifndef CTPT_FT_AW_FROM
+#define CTPT_FT_AW_FROM 224  // narrowest NPMAX with half-K-block limb stages (A/B builds)
+#endif
+// TMEM columns per sub-tile in one limb stage: 32 = a whole K-block, 16 = half of one
+__host__ __device__ constexpr int ft_aw(int npmax, int sub) { return (sub == 2 && npmax >= CTPT_FT_AW_FROM) ? 16 : 32; }
 __host__ __device__ constexpr int ft_ast(int npmax, int sub) {
-  return sub == 2 ? ((512 - 2 * npmax) / 64 < 4 ? (512 - 2 * npmax) / 64 : 4) : 8;
+  return sub == 2 ? ((512 - 2 * npmax) / (2 * ft_aw(npmax, sub)) < 4 ? (512 - 2 * npmax) / (2 * ft_aw(npmax, sub)) : 4)
+                  : 8;
 }
 // + 512 B of barriers, 1 KB of row-sum partials (unsigned-U row correction), 1 KB of alignment slack
 __host__ __device__ constexpr int ft_smem_bytes(int npmax, int sub) {
@@ -115,6 +122,11 @@ __device__ __forceinline__ void tmem_st16x256_x4(uint32_t taddr, const uint32_t 
       "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
       : "memory");
 }
+__device__ __forceinline__ void tmem_st16x256_x2(uint32_t taddr, const uint32_t (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.16x256b.x2.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
 __device__ __forceinline__ void tmem_ld16x256_x4(uint32_t taddr, uint32_t (&v)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -137,7 +149,9 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
   constexpr int ROWS = ft_rows(SUB);
   constexpr int NBUF = 1;                      // D: SUB × NPMAX columns (one buffer)
   constexpr int D_COLS = SUB * NPMAX;
-  constexpr int ASTAGE_COLS = SUB * 32;         // one A stage: SUB sub-tiles × 32 columns (128 residues)
+  constexpr int AW = ft_aw(NPMAX, SUB);          // columns per sub-tile of one A stage (4 residues each)
+  constexpr int HPK = 32 / AW;                   // A stages per K-block
+  constexpr int ASTAGE_COLS = SUB * AW;          // one A stage: SUB sub-tiles × AW columns
   constexpr uint32_t A_COL0 = D_COLS;           // TMEM columns [A_COL0, 512) hold the limb stages
   constexpr int GROUPS = SUB == 1 ? 2 : 1;      // converter groups taking alternate K-blocks
   static_assert(A_COL0 + ASTAGE_COLS * FT_AST <= 512, "TMEM budget");
@@ -228,21 +242,25 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * D_COLS;
         for (int32_t kb = 0; kb < P.num_kb; ++kb) {
-          mbar_wait(a_full(as), aph);
           mbar_wait(u_full(us), uph);
-          tc_fence_after();
           const uint32_t su = sbase + us * U_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < FT_BK / FT_MMA_K; ++kk) {
-            const uint64_t bd = umma_desc_sw128(su + kk * FT_MMA_K);
+          for (int hh = 0; hh < HPK; ++hh) {
+            mbar_wait(a_full(as), aph);
+            tc_fence_after();
 #pragma unroll
-            for (int sb = 0; sb < SUB; ++sb)  // the sub-tiles share the U^T stage
-              mma_i8_ts(d_tmem + sb * NPMAX, tmem_base + A_COL0 + as * ASTAGE_COLS + sb * 32 + kk * (FT_MMA_K / 4), bd,
-                        idesc, (kb | kk) != 0);
+            for (int k2 = 0; k2 < AW / 8; ++k2) {  // MMA K = 32 residues = 8 columns
+              const int kk = hh * (AW / 8) + k2;
+              const uint64_t bd = umma_desc_sw128(su + kk * FT_MMA_K);
+#pragma unroll
+              for (int sb = 0; sb < SUB; ++sb)  // the sub-tiles share the U^T stage
+                mma_i8_ts(d_tmem + sb * NPMAX, tmem_base + A_COL0 + as * ASTAGE_COLS + sb * AW + k2 * (FT_MMA_K / 4), bd,
+                          idesc, (kb | kk) != 0);
+            }
+            mma_commit(a_empty(as));  // the limb stage is free once these MMAs are done
+            if (++as == FT_AST) { as = 0; aph ^= 1; }
           }
-          mma_commit(a_empty(as));  // the limb stage and the U^T stage are free once these MMAs are done
-          mma_commit(u_empty(us));
-          if (++as == FT_AST) { as = 0; aph ^= 1; }
+          mma_commit(u_empty(us));  // and the U^T stage once the whole K-block's are
           if (++us == FT_US) { us = 0; uph ^= 1; }
         }
         mma_commit(d_full(acc));
@@ -344,7 +362,6 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
       uint32_t lsum[4] = {0u, 0u, 0u, 0u};  // Σ of each limb over this thread's residues of the tile
       for (int64_t it = it0 + ((grp - it0 % GROUPS) + GROUPS) % GROUPS; it < it0 + P.num_kb; it += GROUPS) {
         const int rs = static_cast<int>(it % RAW);
-        const int as = static_cast<int>(it % FT_AST);
         mbar_wait(raw_full(rs), static_cast<uint32_t>((it / RAW) & 1));
         const uint32_t raw = raw_base + rs * RAW_BYTES + sb * 4 * FT_BOX_BYTES;
         uint32_t l01[16], l23[16];
@@ -371,23 +388,55 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
             }
           }
         }
-        mbar_wait(a_empty(as), static_cast<uint32_t>(((it / FT_AST) & 1) ^ 1));
-        tc_fence_after();
-        const uint32_t ta = tmem_base + t_lane + A_COL0 + as * ASTAGE_COLS + sb * 32;
-        CTPT_CHECK(A_COL0 + as * ASTAGE_COLS + sb * 32 + 32 <= 512);
-        tmem_st16x256_x4(ta, l01);
-        tmem_st16x256_x4(ta + (16u << 16), l23);
-        // The raw tile is handed back only here: the STTMs take every limb word as an operand, so
-        // every LDS of the tile has completed (register computations such as the PRMTs may be
-        // scheduled past a fence; an asm operand may not), then a proxy fence orders the generic
-        // reads before the TMA's async-proxy refill.
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(raw_empty(rs));
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(a_full(as));
+        if constexpr (HPK == 1) {
+          const int as = static_cast<int>(it % FT_AST);
+          mbar_wait(a_empty(as), static_cast<uint32_t>(((it / FT_AST) & 1) ^ 1));
+          tc_fence_after();
+          const uint32_t ta = tmem_base + t_lane + A_COL0 + as * ASTAGE_COLS + sb * 32;
+          CTPT_CHECK(A_COL0 + as * ASTAGE_COLS + sb * 32 + 32 <= 512);
+          tmem_st16x256_x4(ta, l01);
+          tmem_st16x256_x4(ta + (16u << 16), l23);
+          // The raw tile is handed back only here: the STTMs take every limb word as an operand, so
+          // every LDS of the tile has completed (register computations such as the PRMTs may be
+          // scheduled past a fence; an asm operand may not), then a proxy fence orders the generic
+          // reads before the TMA's async-proxy refill.
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(raw_empty(rs));
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(a_full(as));
+        } else {
+          // half-K-block stages (AW = 16): repetitions 0–1 (residues 0..63) into stage n = 2·it,
+          // 2–3 into stage 2·it + 1 — the .x2 fragment of each half is registers 0..7 / 8..15
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int64_t n = it * 2 + hh;
+            const int as = static_cast<int>(n % FT_AST);
+            mbar_wait(a_empty(as), static_cast<uint32_t>(((n / FT_AST) & 1) ^ 1));
+            tc_fence_after();
+            const uint32_t ta = tmem_base + t_lane + A_COL0 + as * ASTAGE_COLS + sb * AW;
+            CTPT_CHECK(A_COL0 + as * ASTAGE_COLS + sb * AW + AW <= 512);
+            uint32_t h01[8], h23[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              h01[i] = l01[8 * hh + i];
+              h23[i] = l23[8 * hh + i];
+            }
+            tmem_st16x256_x2(ta, h01);
+            tmem_st16x256_x2(ta + (16u << 16), h23);
+            if (hh == 1) {  // every limb word of the K-block is an STTM operand by now: release the raw tile
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(raw_empty(rs));
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(a_full(as));
+          }
+        }
       }
       if (P.off_mod) {
         // this warp's partial row sums of tile t: Σ_ℓ 2^{8ℓ}·lsum_ℓ, summed over the 4 threads of a row

@@ -132,7 +132,8 @@ def test_column_shard_both_kernels(gemm_kernel):
 # ------------------------------------------------------------------ skinny regime (§8(f) row 1)
 SKINNY = [
     # fmt, N, k, d2, d3, L — d3 across the fused kernel's shapes: 1 (CP-Mv), < 128, = 128 (64-row
-    # tiles, 4 limb stages), 129..160 (3 stages), 161..192 (2 stages), 193..256 (32-row tiles);
+    # tiles, 4 limb stages), 129..160 (3 stages), 161..192 (2 stages), 193..224 (2 half-K-block
+    # stages), 225..256 (32-row tiles);
     # ragged R and d2 (not multiples of 64 / 128), long K so the 2- and 3-stage rings wrap
     (S, 64, 3, 1000, 1, 2),
     (R, 512, 1, 130, 2, 1),
@@ -144,6 +145,8 @@ SKINNY = [
     (A, 32, 5, 300, 176, 1),
     (A, 128, 2, 3000, 192, 1),
     (R, 1024, 1, 2056, 200, 1),
+    (S, 32, 5, 1000, 224, 1),
+    (A, 64, 3, 900, 240, 1),
     (S, 128, 2, 640, 256, 1),
     (A, 8, 2, 16, 256, 1),       # R = 24 rows < one tile
     (SA, 256, 2, 700, 1, 2),     # Algorithm 7 CP-Mv: the output is a shared-s vector
@@ -161,7 +164,7 @@ def test_skinny_fused(shape):
 @pytest.mark.parametrize("cols", [(0, 129), (20, 220), (44, 300), (171, 300)])
 def test_skinny_column_shards(cols):
     """k_gemm_fused_t on column blocks [c0, c1) of a wider U (129 columns: 64-row tiles with 3 limb
-    stages; 200 and 256: 32-row tiles; U^T rows j_off .. j_off + N partly past the block and, for
+    stages; 200: 64-row tiles with half-K-block stages; 256: 32-row tiles; U^T rows j_off .. j_off + N partly past the block and, for
     (171, 300), past d3), with ragged R (not a multiple of the tile) and more CTAs than tiles."""
     _check(A, 64, 3, 333, 300, 2, col_begin=cols[0], col_end=cols[1], seed=5, kernel=FUSED)
     _check(S, 512, 9, 300, 300, 1, col_begin=cols[0], col_end=cols[1], seed=6, kernel=FUSED)  # R = 9216: 144 tiles

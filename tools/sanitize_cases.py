@@ -16,7 +16,8 @@ Cases (kept small: the sanitizers slow kernels down 10–100×):
   gemm_side     the same with split_overlap = 1 (prime l+1 split by warps 2–3 inside GEMM l)
   gemm_u8       the unsigned-U plane (row-sum correction in the epilogue), k_U = 2 (accumulating passes)
   fused_wrap    the skinny kernel k_gemm_fused_t with long K (65 k-blocks: the rings wrap many times),
-                64-row tiles with 4 / 3 / 2 limb stages (d3 ≤ 128 / 160 / 192) and 32-row tiles, the u8 plane's in-kernel row sums, and one CTA
+                64-row tiles with 4 / 3 / 2 limb stages (d3 ≤ 128 / 160 / 192), 2 half-K-block stages
+                (≤ 224) and 32-row tiles (≤ 256), the u8 plane's in-kernel row sums, and one CTA
                 looping over 4–8 tiles
   mv_tickets    k_gemm_mv with the K loop split into units that meet on an atomic ticket
   layout        k_layout_v4 (16-byte) and k_layout (4-byte) with validate = 1
@@ -176,6 +177,7 @@ CASES = {
                           check("fused_wrap", S, 32, 3, 8200, 200, 1, kernel=2) +
                           check("fused_wrap", A, 64, 2, 8200, 150, 1, kernel=2) +
                           check("fused_wrap", S, 32, 3, 8200, 190, 1, kernel=2) +
+                          check("fused_wrap", A, 64, 2, 8200, 250, 1, kernel=2) +
                           check("fused_multi", S, 32, 4, 520, 100, 1, kernel=2, max_ctas=1) +
                           check("fused_multi", S, 32, 4, 520, 200, 1, kernel=2, max_ctas=1) +
                           check("fused_multi", S, 32, 4, 520, 180, 1, kernel=2, max_ctas=1) +
