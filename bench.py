@@ -1010,18 +1010,19 @@ def run_strong(args, rank: int, world: int, local_rank: int):
         for eng in engines.values():
             eng.ctmat = None
         torch.cuda.empty_cache()
-        outs, hws_bytes = [], 0
-        for u, sp in zip(mine, specs):
+        outs = []
+        for u in mine:
             sz = engines[u.l].unit_sizes[(u.c0, u.c1)]
             outs.append((torch.empty(max(1, sz.out_AU_bytes // 4), dtype=torch.int32).pin_memory(),
                          torch.empty(sz.out_BU_bytes // 4, dtype=torch.int32).pin_memory()))
-            hws_bytes = max(hws_bytes, ctpt.host_workspace_bytes(sp, 0))
-        hws = torch.empty(hws_bytes, dtype=torch.uint8, device=dev)
+        hws = torch.empty(ctpt.host_workspace_bytes_units(specs, 0), dtype=torch.uint8, device=dev)
+        h_a = [host_ct[u.l][0] for u in mine]
+        h_b = [host_ct[u.l][1] for u in mine]
+        h_plain = [engines[u.l].plain for u in mine]
 
-        def hstep():
-            for u, sp, (au, bu) in zip(mine, specs, outs):
-                a_h, b_h = host_ct[u.l]
-                ctpt.matmul_host(sp, a_h, b_h, engines[u.l].plain, au, bu, hws, stream=stream)
+        def hstep():  # every unit of this rank in ONE copy / compute pipeline (ctpt_matmul_host_units)
+            ctpt.matmul_host_units(specs, h_a, h_b, h_plain, [o[0] for o in outs], [o[1] for o in outs], hws,
+                                   stream=stream)
 
         hstep()
         torch.cuda.synchronize(dev)
@@ -1045,8 +1046,9 @@ def run_strong(args, rank: int, world: int, local_rank: int):
         h2d, d2h = int(vals[1].item()), int(vals[2].item())
         e2e = {"value": macs / (hms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": hms, "steps": args.e2e_steps,
-               "path": "per rank: pinned host ciphertexts -> ctpt_matmul_host per unit (chunked H2D || layout + "
-                       "split + GEMM || D2H) -> pinned host outputs (the sharded result in host memory)"}
+               "path": "per rank: pinned host ciphertexts -> ctpt_matmul_host_units over the rank's units (one "
+                       "chunked H2D || layout + split + GEMM || D2H pipeline) -> pinned host outputs (the sharded "
+                       "result in host memory)"}
 
     # ---------------------------------------------------------------- gather parity on sampled columns
     sample = None

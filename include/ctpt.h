@@ -270,7 +270,7 @@ ctpt_status ctpt_gemm_mv(const ctpt_problem* prob, int32_t l, const void* d_ctma
  * ctpt_layout + ctpt_matmul, but the per-column ciphertexts h_a_polys / h_b_polys (layouts as
  * for ctpt_layout) and the outputs h_AU / h_BU (layouts as for ctpt_matmul) live in host
  * memory.  The stacked X of each prime is processed in row chunks of `chunk_rows` (≤ 0: about
- * R/4, rounded to 64); the host→device copy of one chunk, the layout + split + GEMM of the
+ * R/6, rounded to 64); the host→device copy of one chunk, the layout + split + GEMM of the
  * previous one and the device→host copy of the one before run concurrently (two internal
  * copy streams forked from and joined back into `stream`).  Host buffers must be page-locked
  * (cudaHostAlloc / cudaHostRegister) for the copies to overlap.  d_plain as for ctpt_matmul;
@@ -281,6 +281,24 @@ ctpt_status ctpt_host_workspace_bytes(const ctpt_problem* prob, int64_t chunk_ro
 ctpt_status ctpt_matmul_host(const ctpt_problem* prob, const uint32_t* h_a_polys, const uint32_t* h_b_polys,
                              const void* d_plain, uint32_t* h_AU, uint32_t* h_BU, void* d_ws, size_t ws_bytes,
                              int64_t chunk_rows, void* stream);
+
+/* The host executor over n UNITS in one pipeline (e.g. a rank's (prime, column-block) units of
+ * the multi-GPU plan, or the primes of one problem held in separate host
+ * buffers): unit u is problem probs[u] with host inputs h_a_polys[u] / h_b_polys[u], plaintext
+ * d_plains[u] and host outputs h_AUs[u] / h_BUs[u], each exactly as for ctpt_matmul_host.  The
+ * chunks of all units flow through one set of staging buffers and copy streams, so unit u+1's
+ * first copies overlap unit u's last GEMMs and copies: one pipeline fill and one drain per call
+ * instead of one per unit (n calls of ctpt_matmul_host on one stream serialise, since each joins
+ * its device→host stream back into `stream` before the next forks).  d_ws: at least
+ * ctpt_host_workspace_bytes_units(n, probs, chunk_rows) bytes (each staging region sized for the
+ * largest unit).  Every unit is validated before anything is enqueued; errors as for
+ * ctpt_matmul_host (CTPT_ERR_ARG for n < 1).  ctpt_matmul_host(p, …) ≡ the n = 1 case. */
+ctpt_status ctpt_host_workspace_bytes_units(int32_t n, const ctpt_problem* probs, int64_t chunk_rows,
+                                            size_t* bytes);
+ctpt_status ctpt_matmul_host_units(int32_t n, const ctpt_problem* probs, const uint32_t* const* h_a_polys,
+                                   const uint32_t* const* h_b_polys, const void* const* d_plains,
+                                   uint32_t* const* h_AUs, uint32_t* const* h_BUs, void* d_ws, size_t ws_bytes,
+                                   int64_t chunk_rows, void* stream);
 
 /* ctpt_gemm for prime l with the limb split of prime l+1 fused in (prob->split_overlap = 1,
  * no rescale, L ≥ 2): while prime l's MMAs run, two otherwise idle warps of every CTA split

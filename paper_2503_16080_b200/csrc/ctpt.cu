@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "../../include/ctpt.h"
 #include "gemm_tc.cuh"
@@ -1259,41 +1260,87 @@ struct StreamSet {
   }
 };
 
+// The staging buffers of one pipeline serve every unit of a batch: each region is sized for the
+// largest unit.
+struct HostWs {
+  size_t in_bytes = 0, cm_bytes = 0, limb_bytes = 0, out_bytes = 0, corr_bytes = 0, mv_bytes = 0;
+  size_t total() const { return 2 * in_bytes + cm_bytes + limb_bytes + 2 * out_bytes + corr_bytes + mv_bytes; }
+  void cover(const HostPlan& h) {
+    in_bytes = std::max(in_bytes, h.in_bytes);
+    cm_bytes = std::max(cm_bytes, h.cm_bytes);
+    limb_bytes = std::max(limb_bytes, h.limb_bytes);
+    out_bytes = std::max(out_bytes, h.out_bytes);
+    corr_bytes = std::max(corr_bytes, h.corr_bytes);
+    mv_bytes = std::max(mv_bytes, h.mv_bytes);
+  }
+};
+
+ctpt_status host_ws_units(int32_t n, const ctpt_problem* probs, int64_t chunk_rows, HostWs& ws) {
+  if (n < 1 || !probs) return fail(CTPT_ERR_ARG, "need n >= 1 problems");
+  for (int32_t u = 0; u < n; ++u) {
+    Dims d;
+    ctpt_status s = check_problem(probs + u, d);
+    if (s != CTPT_OK) return s;
+    if (probs[u].rescale) return fail(CTPT_ERR_UNSUPPORTED, "ctpt_matmul_host does not Rescale (use ctpt_matmul)");
+    ws.cover(host_plan(d, chunk_rows));
+  }
+  return CTPT_OK;
+}
+
 }  // namespace
 
 extern "C" {
 
 ctpt_status ctpt_host_workspace_bytes(const ctpt_problem* pb, int64_t chunk_rows, size_t* bytes) {
-  Dims d;
-  ctpt_status s = check_problem(pb, d);
-  if (s != CTPT_OK) return s;
+  return ctpt_host_workspace_bytes_units(1, pb, chunk_rows, bytes);
+}
+
+ctpt_status ctpt_host_workspace_bytes_units(int32_t n, const ctpt_problem* probs, int64_t chunk_rows, size_t* bytes) {
   if (!bytes) return fail(CTPT_ERR_ARG, "bytes is NULL");
-  *bytes = host_plan(d, chunk_rows).total;
+  HostWs ws;
+  ctpt_status s = host_ws_units(n, probs, chunk_rows, ws);
+  if (s != CTPT_OK) return s;
+  *bytes = ws.total();
   return CTPT_OK;
 }
 
 ctpt_status ctpt_matmul_host(const ctpt_problem* pb, const uint32_t* h_a, const uint32_t* h_b, const void* d_plain,
                              uint32_t* h_AU, uint32_t* h_BU, void* d_ws, size_t ws_bytes, int64_t chunk_rows,
                              void* stream) {
-  Dims d;
-  ctpt_status s = check_problem(pb, d);
+  return ctpt_matmul_host_units(1, pb, &h_a, &h_b, &d_plain, &h_AU, &h_BU, d_ws, ws_bytes, chunk_rows, stream);
+}
+
+ctpt_status ctpt_matmul_host_units(int32_t n, const ctpt_problem* probs, const uint32_t* const* h_as,
+                                   const uint32_t* const* h_bs, const void* const* d_plains, uint32_t* const* h_AUs,
+                                   uint32_t* const* h_BUs, void* d_ws, size_t ws_bytes, int64_t chunk_rows,
+                                   void* stream) {
+  HostWs hw;
+  ctpt_status s = host_ws_units(n, probs, chunk_rows, hw);
   if (s != CTPT_OK) return s;
-  if (pb->rescale) return fail(CTPT_ERR_UNSUPPORTED, "ctpt_matmul_host does not Rescale (use ctpt_matmul)");
-  if (((!h_a || !h_AU) && d.rows_A > 0) || !h_b || !d_plain || !h_BU || !d_ws) return fail(CTPT_ERR_ARG, "null pointer");
-  const HostPlan hp = host_plan(d, chunk_rows);
-  if (ws_bytes < hp.total) return fail(CTPT_ERR_ARG, "workspace too small (%zu < %zu)", ws_bytes, hp.total);
-  Path path;
-  s = choose_path(pb, d, path);
-  if (s != CTPT_OK) return s;
+  if (!h_as || !h_bs || !d_plains || !h_AUs || !h_BUs || !d_ws) return fail(CTPT_ERR_ARG, "null pointer");
+  if (ws_bytes < hw.total()) return fail(CTPT_ERR_ARG, "workspace too small (%zu < %zu)", ws_bytes, hw.total());
+  for (int32_t u = 0; u < n; ++u) {  // validate every unit before enqueueing anything
+    Dims d;
+    check_problem(probs + u, d);
+    if (((!h_as[u] || !h_AUs[u]) && d.rows_A > 0) || !h_bs[u] || !d_plains[u] || !h_BUs[u])
+      return fail(CTPT_ERR_ARG, "null pointer (unit %d)", u);
+  }
+  std::vector<Path> paths(static_cast<size_t>(n));
+  for (int32_t u = 0; u < n; ++u) {
+    Dims d;
+    check_problem(probs + u, d);
+    s = choose_path(probs + u, d, paths[static_cast<size_t>(u)]);
+    if (s != CTPT_OK) return s;
+  }
   cudaStream_t sc = static_cast<cudaStream_t>(stream);
   uint8_t* w = static_cast<uint8_t*>(d_ws);
-  uint32_t* in[2] = {reinterpret_cast<uint32_t*>(w), reinterpret_cast<uint32_t*>(w + hp.in_bytes)};
-  uint32_t* cm = reinterpret_cast<uint32_t*>(w + 2 * hp.in_bytes);
-  void* limbs = w + 2 * hp.in_bytes + hp.cm_bytes;
-  uint32_t* ob[2] = {reinterpret_cast<uint32_t*>(w + 2 * hp.in_bytes + hp.cm_bytes + hp.limb_bytes),
-                     reinterpret_cast<uint32_t*>(w + 2 * hp.in_bytes + hp.cm_bytes + hp.limb_bytes + hp.out_bytes)};
-  uint32_t* corr = reinterpret_cast<uint32_t*>(w + 2 * hp.in_bytes + hp.cm_bytes + hp.limb_bytes + 2 * hp.out_bytes);
-  uint8_t* mvws = w + 2 * hp.in_bytes + hp.cm_bytes + hp.limb_bytes + 2 * hp.out_bytes + hp.corr_bytes;
+  uint32_t* in[2] = {reinterpret_cast<uint32_t*>(w), reinterpret_cast<uint32_t*>(w + hw.in_bytes)};
+  uint32_t* cm = reinterpret_cast<uint32_t*>(w + 2 * hw.in_bytes);
+  void* limbs = w + 2 * hw.in_bytes + hw.cm_bytes;
+  uint32_t* ob[2] = {reinterpret_cast<uint32_t*>(w + 2 * hw.in_bytes + hw.cm_bytes + hw.limb_bytes),
+                     reinterpret_cast<uint32_t*>(w + 2 * hw.in_bytes + hw.cm_bytes + hw.limb_bytes + hw.out_bytes)};
+  uint32_t* corr = reinterpret_cast<uint32_t*>(w + 2 * hw.in_bytes + hw.cm_bytes + hw.limb_bytes + 2 * hw.out_bytes);
+  uint8_t* mvws = w + 2 * hw.in_bytes + hw.cm_bytes + hw.limb_bytes + 2 * hw.out_bytes + hw.corr_bytes;
 
   StreamSet ss;
   CUDA_TRY(cudaStreamCreateWithFlags(&ss.h2d, cudaStreamNonBlocking));
@@ -1310,69 +1357,79 @@ ctpt_status ctpt_matmul_host(const ctpt_problem* pb, const uint32_t* h_a, const 
   CUDA_TRY(cudaStreamWaitEvent(ss.h2d, ev_start, 0));
   CUDA_TRY(cudaStreamWaitEvent(ss.d2h, ev_start, 0));
 
-  GemmArgs g{};
-  gemm_args_from_problem(g, pb);
-  g.d = d;
-  g.kU = pb->kU <= 0 ? 1 : pb->kU;
-  g.planes = reinterpret_cast<const int8_t*>(static_cast<const uint8_t*>(d_plain) + kHeader);
-  g.nplanes = pb->plain_per_prime ? d.L * g.kU : g.kU;
-  g.limbs = limbs;
-  g.u_unsigned = pb->u_unsigned;
-  if (needs_rowcorr(pb)) g.o.rowcorr = corr;
-  const bool fused = path != Path::SplitGemm;
-  const bool mv = path == Path::Mv;
-
+  // One pipeline over every (unit, prime, row chunk): the chunk counter `it` and the staging
+  // buffers run on across unit boundaries, so unit u+1's first copies overlap unit u's last GEMMs
+  // and copies (one fill and one drain per call, not per unit).
   int64_t it = 0;
-  for (int l = 0; l < d.L; ++l) {
-    const uint32_t* a_l = h_a + static_cast<int64_t>(l) * d.d2 * d.rows_A;
-    const uint32_t* b_l = h_b + static_cast<int64_t>(l) * d.d2 * d.d1;
-    uint32_t* AU_l = h_AU + static_cast<int64_t>(l) * d.d3_loc * d.rows_A;
-    uint32_t* BU_l = h_BU + static_cast<int64_t>(l) * d.d3_loc * d.d1;
-    for (int64_t r0 = 0; r0 < d.R; r0 += hp.chunk, ++it) {
-      const int b = static_cast<int>(it & 1);
-      const int64_t r1 = std::min(d.R, r0 + hp.chunk), rows = r1 - r0;
-      const int64_t na = std::max<int64_t>(0, std::min(r1, d.rows_A) - r0), nb = rows - na;
-      const int64_t rb0 = r0 + na - d.rows_A;  // first B row of the chunk (if nb > 0)
-      // 1. host → device: the chunk's rows of every ciphertext column, packed col-major [d2][rows]
-      if (it >= 2) CUDA_TRY(cudaStreamWaitEvent(ss.h2d, in_free[b], 0));
-      if (na)
-        CUDA_TRY(cudaMemcpy2DAsync(in[b], rows * 4, a_l + r0, d.rows_A * 4, na * 4, d.d2, cudaMemcpyHostToDevice,
-                                   ss.h2d));
-      if (nb)
-        CUDA_TRY(cudaMemcpy2DAsync(in[b] + na, rows * 4, b_l + rb0, d.d1 * 4, nb * 4, d.d2, cudaMemcpyHostToDevice,
-                                   ss.h2d));
-      CUDA_TRY(cudaEventRecord(in_ready[b], ss.h2d));
-      // 2. layout + split + GEMM on the caller's stream
-      CUDA_TRY(cudaStreamWaitEvent(sc, in_ready[b], 0));
-      s = launch_layout_cols(in[b], cm, rows, d.d2, d.d2p, sc);
-      if (s != CTPT_OK) return s;
-      CUDA_TRY(cudaEventRecord(in_free[b], sc));
-      if (!fused) {
-        s = launch_split_prime(pb, cm, rows, d.d2p, pb->primes[l], limbs, corr, sc);
+  for (int32_t u = 0; u < n; ++u) {
+    const ctpt_problem* pb = probs + u;
+    Dims d;
+    check_problem(pb, d);
+    const HostPlan hp = host_plan(d, chunk_rows);
+    const Path path = paths[static_cast<size_t>(u)];
+    GemmArgs g{};
+    gemm_args_from_problem(g, pb);
+    g.d = d;
+    g.kU = pb->kU <= 0 ? 1 : pb->kU;
+    g.planes = reinterpret_cast<const int8_t*>(static_cast<const uint8_t*>(d_plains[u]) + kHeader);
+    g.nplanes = pb->plain_per_prime ? d.L * g.kU : g.kU;
+    g.limbs = limbs;
+    g.u_unsigned = pb->u_unsigned;
+    if (needs_rowcorr(pb)) g.o.rowcorr = corr;
+    const bool fused = path != Path::SplitGemm;
+    const bool mv = path == Path::Mv;
+
+    for (int l = 0; l < d.L; ++l) {
+      const uint32_t* a_l = h_as[u] + static_cast<int64_t>(l) * d.d2 * d.rows_A;
+      const uint32_t* b_l = h_bs[u] + static_cast<int64_t>(l) * d.d2 * d.d1;
+      uint32_t* AU_l = h_AUs[u] + static_cast<int64_t>(l) * d.d3_loc * d.rows_A;
+      uint32_t* BU_l = h_BUs[u] + static_cast<int64_t>(l) * d.d3_loc * d.d1;
+      for (int64_t r0 = 0; r0 < d.R; r0 += hp.chunk, ++it) {
+        const int b = static_cast<int>(it & 1);
+        const int64_t r1 = std::min(d.R, r0 + hp.chunk), rows = r1 - r0;
+        const int64_t na = std::max<int64_t>(0, std::min(r1, d.rows_A) - r0), nb = rows - na;
+        const int64_t rb0 = r0 + na - d.rows_A;  // first B row of the chunk (if nb > 0)
+        // 1. host → device: the chunk's rows of every ciphertext column, packed col-major [d2][rows]
+        if (it >= 2) CUDA_TRY(cudaStreamWaitEvent(ss.h2d, in_free[b], 0));
+        if (na)
+          CUDA_TRY(cudaMemcpy2DAsync(in[b], rows * 4, a_l + r0, d.rows_A * 4, na * 4, d.d2, cudaMemcpyHostToDevice,
+                                     ss.h2d));
+        if (nb)
+          CUDA_TRY(cudaMemcpy2DAsync(in[b] + na, rows * 4, b_l + rb0, d.d1 * 4, nb * 4, d.d2, cudaMemcpyHostToDevice,
+                                     ss.h2d));
+        CUDA_TRY(cudaEventRecord(in_ready[b], ss.h2d));
+        // 2. layout + split + GEMM on the caller's stream
+        CUDA_TRY(cudaStreamWaitEvent(sc, in_ready[b], 0));
+        s = launch_layout_cols(in[b], cm, rows, d.d2, d.d2p, sc);
         if (s != CTPT_OK) return s;
+        CUDA_TRY(cudaEventRecord(in_free[b], sc));
+        if (!fused) {
+          s = launch_split_prime(pb, cm, rows, d.d2p, pb->primes[l], limbs, corr, sc);
+          if (s != CTPT_OK) return s;
+        }
+        if (it >= 2) CUDA_TRY(cudaStreamWaitEvent(sc, out_free[b], 0));
+        g.R = rows;
+        g.p = pb->primes[l];
+        g.plane0 = plane_index(pb, l, 0);
+        g.o.AU = ob[b];
+        g.o.BU = ob[b];
+        g.o.rows_A = rows;
+        g.o.d1 = 0;
+        g.o.R = rows;
+        g.o.d3_loc = d.d3_loc;
+        s = mv ? launch_mv(g, cm, mvws, sc) : fused ? launch_fused(g, cm, sc) : launch_gemm(g, sc, false);
+        if (s != CTPT_OK) return s;
+        CUDA_TRY(cudaEventRecord(out_ready[b], sc));
+        // 3. device → host: rows [r0, r1) of every output column
+        CUDA_TRY(cudaStreamWaitEvent(ss.d2h, out_ready[b], 0));
+        if (na)
+          CUDA_TRY(cudaMemcpy2DAsync(AU_l + r0, d.rows_A * 4, ob[b], rows * 4, na * 4, d.d3_loc,
+                                     cudaMemcpyDeviceToHost, ss.d2h));
+        if (nb)
+          CUDA_TRY(cudaMemcpy2DAsync(BU_l + rb0, d.d1 * 4, ob[b] + na, rows * 4, nb * 4, d.d3_loc,
+                                     cudaMemcpyDeviceToHost, ss.d2h));
+        CUDA_TRY(cudaEventRecord(out_free[b], ss.d2h));
       }
-      if (it >= 2) CUDA_TRY(cudaStreamWaitEvent(sc, out_free[b], 0));
-      g.R = rows;
-      g.p = pb->primes[l];
-      g.plane0 = plane_index(pb, l, 0);
-      g.o.AU = ob[b];
-      g.o.BU = ob[b];
-      g.o.rows_A = rows;
-      g.o.d1 = 0;
-      g.o.R = rows;
-      g.o.d3_loc = d.d3_loc;
-      s = mv ? launch_mv(g, cm, mvws, sc) : fused ? launch_fused(g, cm, sc) : launch_gemm(g, sc, false);
-      if (s != CTPT_OK) return s;
-      CUDA_TRY(cudaEventRecord(out_ready[b], sc));
-      // 3. device → host: rows [r0, r1) of every output column
-      CUDA_TRY(cudaStreamWaitEvent(ss.d2h, out_ready[b], 0));
-      if (na)
-        CUDA_TRY(cudaMemcpy2DAsync(AU_l + r0, d.rows_A * 4, ob[b], rows * 4, na * 4, d.d3_loc, cudaMemcpyDeviceToHost,
-                                   ss.d2h));
-      if (nb)
-        CUDA_TRY(cudaMemcpy2DAsync(BU_l + rb0, d.d1 * 4, ob[b] + na, rows * 4, nb * 4, d.d3_loc,
-                                   cudaMemcpyDeviceToHost, ss.d2h));
-      CUDA_TRY(cudaEventRecord(out_free[b], ss.d2h));
     }
   }
   // join: the caller's stream completes only after the last device→host copy

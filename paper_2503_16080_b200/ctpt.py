@@ -78,6 +78,10 @@ _sig = {
                                       ctypes.c_int64, _P, _P, _P, ctypes.c_size_t, _P]),
     "ctpt_host_workspace_bytes": (ctypes.c_int, [_PP, ctypes.c_int64, ctypes.POINTER(ctypes.c_size_t)]),
     "ctpt_matmul_host": (ctypes.c_int, [_PP, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, ctypes.c_int64, _P]),
+    "ctpt_host_workspace_bytes_units": (ctypes.c_int, [ctypes.c_int32, _PP, ctypes.c_int64,
+                                                       ctypes.POINTER(ctypes.c_size_t)]),
+    "ctpt_matmul_host_units": (ctypes.c_int, [ctypes.c_int32, _PP, _P, _P, _P, _P, _P, _P, ctypes.c_size_t,
+                                              ctypes.c_int64, _P]),
     "ctpt_ipc_export": (ctypes.c_int, [_P, _P, ctypes.POINTER(ctypes.c_uint64)]),
     "ctpt_ipc_open": (ctypes.c_int, [_P, ctypes.c_uint64, ctypes.POINTER(_P), ctypes.POINTER(_P)]),
     "ctpt_ipc_close": (ctypes.c_int, [_P]),
@@ -278,6 +282,34 @@ def matmul_host(spec: Spec, a_polys_h, b_polys_h, plain, AU_h, BU_h, ws, chunk_r
     pb = spec.cstruct()
     _check(_lib.ctpt_matmul_host(ctypes.byref(pb), _ptr(a_polys_h), _ptr(b_polys_h), _ptr(plain), _ptr(AU_h),
                                  _ptr(BU_h), _ptr(ws), ws.numel() * ws.element_size(), chunk_rows, _stream(stream)))
+
+
+def _problems(specs) -> ctypes.Array:
+    """A C array of ctpt_problem (the prime arrays kept alive on the array object)."""
+    structs = [sp.cstruct() for sp in specs]
+    arr = (Problem * len(structs))(*structs)
+    arr._keep = [pb._keep for pb in structs]
+    return arr
+
+
+def _ptrs(ts) -> ctypes.Array:
+    return (ctypes.c_void_p * len(ts))(*[_ptr(t).value for t in ts])
+
+
+def host_workspace_bytes_units(specs, chunk_rows: int = 0) -> int:
+    arr = _problems(specs)
+    n = ctypes.c_size_t(0)
+    _check(_lib.ctpt_host_workspace_bytes_units(len(specs), ctypes.cast(arr, _PP), chunk_rows, ctypes.byref(n)))
+    return n.value
+
+
+def matmul_host_units(specs, a_polys_h, b_polys_h, plains, AU_h, BU_h, ws, chunk_rows: int = 0, stream=None):
+    """ctpt_matmul_host_units: unit u = (specs[u], a_polys_h[u], b_polys_h[u], plains[u], AU_h[u], BU_h[u]),
+    all units in one copy / compute pipeline (host tensors pinned)."""
+    arr = _problems(specs)
+    lists = [_ptrs(x) for x in (a_polys_h, b_polys_h, plains, AU_h, BU_h)]
+    _check(_lib.ctpt_matmul_host_units(len(specs), ctypes.cast(arr, _PP), *[ctypes.cast(x, _P) for x in lists],
+                                       _ptr(ws), ws.numel() * ws.element_size(), chunk_rows, _stream(stream)))
 
 
 IPC_HANDLE_BYTES = 64  # CTPT_IPC_HANDLE_BYTES

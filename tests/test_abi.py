@@ -2,6 +2,7 @@
 arguments on the host (no GPU needed: validation and size queries touch no device)."""
 import ctypes
 import os
+import types
 
 import pytest
 
@@ -164,3 +165,32 @@ def test_ipc_and_peer_entry_points_validate_without_gpu(ctpt):
     assert lib.ctpt_peer_access(0, 0, None) == 1
     can = ctypes.c_int32(0)
     assert lib.ctpt_peer_access(3, 3, ctypes.byref(can)) == 0 and can.value == 1  # a device reaches itself
+
+
+def test_host_units_workspace_and_validation_without_gpu(ctpt):
+    """ctpt_host_workspace_bytes_units: n = 1 is ctpt_host_workspace_bytes; a batch is sized for its
+    largest unit in every staging region; n < 1, a Rescale unit, or a bad unit anywhere in the
+    batch is refused before anything is enqueued (no device pointer is touched)."""
+    a = _spec(ctpt, d3=300)
+    b = _spec(ctpt, d3=40, col_begin=10, col_end=30)
+    one = ctpt.host_workspace_bytes_units([a], 64)
+    assert one == ctpt.host_workspace_bytes(a, 64)
+    both = ctpt.host_workspace_bytes_units([a, b], 64)
+    assert both >= max(one, ctpt.host_workspace_bytes(b, 64))
+    assert ctpt.host_workspace_bytes_units([b, a], 64) == both
+    lib = ctpt.raw_lib()
+    n = ctypes.c_size_t(0)
+    assert lib.ctpt_host_workspace_bytes_units(0, ctypes.cast(ctpt._problems([a]), ctpt._PP), 64, ctypes.byref(n)) == 1
+    with pytest.raises(ctpt.CtptError, match="ERR_UNSUPPORTED"):
+        ctpt.host_workspace_bytes_units([a, _spec(ctpt, d3=300, rescale=1, primes=[2147352577, 2146959361])], 0)
+    with pytest.raises(ctpt.CtptError, match="ERR_ARG"):
+        ctpt.host_workspace_bytes_units([a, _spec(ctpt, kernel=4)], 0)
+    fake = 256  # never dereferenced: the null host pointer of unit 1 is refused first
+    ws_t = types.SimpleNamespace(data_ptr=lambda: 256, numel=lambda: both, element_size=lambda: 1)
+    with pytest.raises(ctpt.CtptError, match="ERR_ARG"):
+        ctpt.matmul_host_units([a, b], [fake, fake], [fake, None], [fake, fake], [fake, fake], [fake, fake], ws_t,
+                               chunk_rows=64, stream=0)
+    with pytest.raises(ctpt.CtptError, match="workspace too small"):
+        ctpt.matmul_host_units([a, b], [fake] * 2, [fake] * 2, [fake] * 2, [fake] * 2, [fake] * 2,
+                               types.SimpleNamespace(data_ptr=lambda: 256, numel=lambda: one - 1,
+                                                     element_size=lambda: 1), chunk_rows=64, stream=0)

@@ -423,6 +423,43 @@ def test_matmul_host_pipeline(fmt, N, k, d2, d3, L, u_bound, chunk, cols):
         assert np.array_equal(AU[l], wa) and np.array_equal(BU[l], wb)
 
 
+@pytest.mark.parametrize("chunk", [0, 64, 192])
+def test_matmul_host_units_one_pipeline(chunk):
+    """ctpt_matmul_host_units: the units of a 3-rank plan's rank (one prime each, column blocks of
+    different widths, so the skinny fused kernel, the raw-byte kernel and split + GEMM alternate
+    along one pipeline, staging buffers sized for the largest unit) == the oracle, unit by unit."""
+    import torch
+
+    from paper_2503_16080_b200 import ctpt
+    from paper_2503_16080_b200.engine import CpmmEngine
+
+    fmt, N, k, d2, d3, L = A, 64, 3, 200, 600, 3
+    d1 = N * k
+    ps = ctgen.primes(L)
+    ct = ctgen.encrypt(fmt, N, d1, d2, 6, 20, ps)
+    U = ctgen.U_matrix(6, d2, d3, 8)
+    units = [(0, 0, 600), (1, 0, 300), (1, 300, 301), (2, 17, 250), (0, 599, 600), (2, 250, 600)]
+    specs, plains, a_h, b_h, outs = [], [], [], [], []
+    for l, c0, c1 in units:
+        eng = CpmmEngine(ctpt.Spec(fmt, N, d1, d2, d3, [ps[l]], c0, c1), "cuda")
+        eng.precompute(U)
+        specs.append(eng.spec)
+        plains.append(eng.plain)
+        a_h.append(torch.from_numpy(np.ascontiguousarray(ct.a_polys[l]).view(np.int32)).pin_memory())
+        b_h.append(torch.from_numpy(np.ascontiguousarray(ct.b_polys[l]).view(np.int32)).pin_memory())
+        outs.append((torch.zeros(eng.sizes.out_AU_bytes // 4, dtype=torch.int32).pin_memory(),
+                     torch.zeros(eng.sizes.out_BU_bytes // 4, dtype=torch.int32).pin_memory()))
+    ws_bytes = ctpt.host_workspace_bytes_units(specs, chunk)
+    assert ws_bytes >= max(ctpt.host_workspace_bytes(sp, chunk) for sp in specs)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    ctpt.matmul_host_units(specs, a_h, b_h, plains, [o[0] for o in outs], [o[1] for o in outs], ws, chunk_rows=chunk)
+    torch.cuda.synchronize()
+    for (l, c0, c1), (au, bu) in zip(units, outs):
+        wa, wb = oracle_outputs(fmt, N, d1, ct.a_polys[l], ct.b_polys[l], U, ps[l], cols=np.arange(c0, c1))
+        assert np.array_equal(au.numpy().view(np.uint32).reshape(c1 - c0, N), wa), (l, c0, c1)
+        assert np.array_equal(bu.numpy().view(np.uint32).reshape(c1 - c0, d1), wb), (l, c0, c1)
+
+
 def test_shard_units_on_one_gpu():
     """Every unit of a 4-rank plan (L = 3 primes: column-split units) computed through
     shard.gpu_compute_fn on this GPU and placed as rank 0's gather would place it == the oracle."""
