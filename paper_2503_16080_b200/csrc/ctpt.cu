@@ -1260,6 +1260,22 @@ struct StreamSet {
   }
 };
 
+#ifdef CTPT_HOST_TRACE
+// Diagnostic build only (tools/ab_build.py OUT.so -DCTPT_HOST_TRACE): timing events around every
+// chunk's H2D, compute and D2H; the call synchronises at the end and prints the timeline (ms from
+// the fork) to stderr.  The release library never synchronises in ctpt_matmul_host*.
+struct HostTrace {
+  std::vector<cudaEvent_t> ev;
+  cudaEvent_t rec(cudaStream_t st) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    ev.push_back(e);
+    return e;
+  }
+};
+#endif
+
 // The staging buffers of one pipeline serve every unit of a batch: each region is sized for the
 // largest unit.
 struct HostWs {
@@ -1356,6 +1372,13 @@ ctpt_status ctpt_matmul_host_units(int32_t n, const ctpt_problem* probs, const u
   CUDA_TRY(cudaEventRecord(ev_start, sc));
   CUDA_TRY(cudaStreamWaitEvent(ss.h2d, ev_start, 0));
   CUDA_TRY(cudaStreamWaitEvent(ss.d2h, ev_start, 0));
+#ifdef CTPT_HOST_TRACE
+  HostTrace tr;
+  tr.rec(sc);
+#define CTPT_TRACE(st) tr.rec(st)
+#else
+#define CTPT_TRACE(st) ((void)0)
+#endif
 
   // One pipeline over every (unit, prime, row chunk): the chunk counter `it` and the staging
   // buffers run on across unit boundaries, so unit u+1's first copies overlap unit u's last GEMMs
@@ -1391,6 +1414,7 @@ ctpt_status ctpt_matmul_host_units(int32_t n, const ctpt_problem* probs, const u
         const int64_t rb0 = r0 + na - d.rows_A;  // first B row of the chunk (if nb > 0)
         // 1. host → device: the chunk's rows of every ciphertext column, packed col-major [d2][rows]
         if (it >= 2) CUDA_TRY(cudaStreamWaitEvent(ss.h2d, in_free[b], 0));
+        CTPT_TRACE(ss.h2d);
         if (na)
           CUDA_TRY(cudaMemcpy2DAsync(in[b], rows * 4, a_l + r0, d.rows_A * 4, na * 4, d.d2, cudaMemcpyHostToDevice,
                                      ss.h2d));
@@ -1398,8 +1422,10 @@ ctpt_status ctpt_matmul_host_units(int32_t n, const ctpt_problem* probs, const u
           CUDA_TRY(cudaMemcpy2DAsync(in[b] + na, rows * 4, b_l + rb0, d.d1 * 4, nb * 4, d.d2, cudaMemcpyHostToDevice,
                                      ss.h2d));
         CUDA_TRY(cudaEventRecord(in_ready[b], ss.h2d));
+        CTPT_TRACE(ss.h2d);
         // 2. layout + split + GEMM on the caller's stream
         CUDA_TRY(cudaStreamWaitEvent(sc, in_ready[b], 0));
+        CTPT_TRACE(sc);
         s = launch_layout_cols(in[b], cm, rows, d.d2, d.d2p, sc);
         if (s != CTPT_OK) return s;
         CUDA_TRY(cudaEventRecord(in_free[b], sc));
@@ -1408,6 +1434,7 @@ ctpt_status ctpt_matmul_host_units(int32_t n, const ctpt_problem* probs, const u
           if (s != CTPT_OK) return s;
         }
         if (it >= 2) CUDA_TRY(cudaStreamWaitEvent(sc, out_free[b], 0));
+        CTPT_TRACE(sc);
         g.R = rows;
         g.p = pb->primes[l];
         g.plane0 = plane_index(pb, l, 0);
@@ -1420,8 +1447,10 @@ ctpt_status ctpt_matmul_host_units(int32_t n, const ctpt_problem* probs, const u
         s = mv ? launch_mv(g, cm, mvws, sc) : fused ? launch_fused(g, cm, sc) : launch_gemm(g, sc, false);
         if (s != CTPT_OK) return s;
         CUDA_TRY(cudaEventRecord(out_ready[b], sc));
+        CTPT_TRACE(sc);
         // 3. device → host: rows [r0, r1) of every output column
         CUDA_TRY(cudaStreamWaitEvent(ss.d2h, out_ready[b], 0));
+        CTPT_TRACE(ss.d2h);
         if (na)
           CUDA_TRY(cudaMemcpy2DAsync(AU_l + r0, d.rows_A * 4, ob[b], rows * 4, na * 4, d.d3_loc,
                                      cudaMemcpyDeviceToHost, ss.d2h));
@@ -1429,12 +1458,26 @@ ctpt_status ctpt_matmul_host_units(int32_t n, const ctpt_problem* probs, const u
           CUDA_TRY(cudaMemcpy2DAsync(BU_l + rb0, d.d1 * 4, ob[b] + na, rows * 4, nb * 4, d.d3_loc,
                                      cudaMemcpyDeviceToHost, ss.d2h));
         CUDA_TRY(cudaEventRecord(out_free[b], ss.d2h));
+        CTPT_TRACE(ss.d2h);
       }
     }
   }
   // join: the caller's stream completes only after the last device→host copy
   CUDA_TRY(cudaEventRecord(ev_end, ss.d2h));
   CUDA_TRY(cudaStreamWaitEvent(sc, ev_end, 0));
+#ifdef CTPT_HOST_TRACE
+  // per chunk: h2d start, h2d end, compute start (input ready), GEMM start (output buffer free),
+  // compute end, d2h start, d2h end — ms from the fork
+  cudaStreamSynchronize(sc);
+  for (size_t i = 1; i + 7 <= tr.ev.size(); i += 7) {
+    float t[7];
+    for (int k = 0; k < 7; ++k) cudaEventElapsedTime(&t[k], tr.ev[0], tr.ev[i + k]);
+    fprintf(stderr, "trace chunk %zu h2d %.3f %.3f comp %.3f %.3f %.3f d2h %.3f %.3f\n", (i - 1) / 7, t[0], t[1], t[2],
+            t[3], t[4], t[5], t[6]);
+  }
+  for (auto e : tr.ev) cudaEventDestroy(e);
+#endif
+#undef CTPT_TRACE
   return CTPT_OK;
 }
 
