@@ -596,7 +596,7 @@ static ctpt_status plain_common(const ctpt_problem* pb, const int64_t* d_U, cons
     long long init[2] = {LLONG_MAX, LLONG_MIN};
     CUDA_TRY(cudaMemcpyAsync(hdr, init, 16, cudaMemcpyHostToDevice, st));
     const int64_t n = d.d2 * d.d3;
-    k_minmax_i64<<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 4096)), 256, 0, st>>>(
+    k_minmax_i64<<<static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((n + 2047) / 2048, 8LL * num_sms()))), 256, 0, st>>>(
         d_U, n, reinterpret_cast<long long*>(hdr));
     CUDA_TRY(cudaGetLastError());
     long long mm[2];
@@ -640,7 +640,8 @@ static ctpt_status plain_common(const ctpt_problem* pb, const int64_t* d_U, cons
     for (int i = 0; i < d.L; ++i) P.p_arr[i] = pb->primes[i];
     nblk_z = d.L;
   }
-  dim3 grid(static_cast<unsigned>((d.d2p + 31) / 32), static_cast<unsigned>((d.d3 + 31) / 32), nblk_z);
+  dim3 grid(static_cast<unsigned>((d.d2p + PLAIN_TK - 1) / PLAIN_TK), static_cast<unsigned>((d.d3 + PLAIN_TJ - 1) / PLAIN_TJ),
+           nblk_z);
   if (grid.y > 65535) return fail(CTPT_ERR_SHAPE, "d3 too large for the precompute grid");
   k_plain<<<grid, 256, 0, st>>>(P);
   CUDA_TRY(cudaGetLastError());

@@ -249,14 +249,36 @@ __global__ void __launch_bounds__(256) k_split_rows(const uint4* __restrict__ x,
 // Plaintext precompute (§8(a) a2): U int64 [d2][d3] → balanced int8 digits of the centred
 // residue, written transposed (U^T, K-major) as planes [kU][d3][d2p].
 // ------------------------------------------------------------------------------------------
-__global__ void k_minmax_i64(const int64_t* __restrict__ u, int64_t n, long long* mm /*[2]: min, max*/) {
+// min / max of n int64 values: 16-byte loads, four in flight per thread per iteration (a grid of a
+// few CTAs per SM streams 2 GB at HBM speed), warp shuffles, one atomic pair per warp.
+__global__ void __launch_bounds__(256) k_minmax_i64(const int64_t* __restrict__ u, int64_t n, long long* mm /*[2]: min, max*/) {
   long long lo = LLONG_MAX, hi = LLONG_MIN;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    long long v = u[i];
+  auto take = [&](long long v) {
     lo = v < lo ? v : lo;
     hi = v > hi ? v : hi;
+  };
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nthr = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const bool vec = (reinterpret_cast<uintptr_t>(u) & 15) == 0;
+  const int64_t n2 = vec ? n / 2 : 0;  // 16-byte pairs
+  const longlong2* u2 = reinterpret_cast<const longlong2*>(u);
+  int64_t i = tid;
+  for (; i + 3 * nthr < n2; i += 4 * nthr) {
+    longlong2 v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = __ldcs(u2 + i + q * nthr);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      take(v[q].x);
+      take(v[q].y);
+    }
   }
+  for (; i < n2; i += nthr) {
+    const longlong2 v = __ldcs(u2 + i);
+    take(v.x);
+    take(v.y);
+  }
+  for (int64_t k = 2 * n2 + tid; k < n; k += nthr) take(u[k]);
   for (int o = 16; o; o >>= 1) {
     long long a = __shfl_xor_sync(0xffffffffu, lo, o), b = __shfl_xor_sync(0xffffffffu, hi, o);
     lo = a < lo ? a : lo;
@@ -287,16 +309,23 @@ struct PlainParams {
   uint32_t p_arr[64];
 };
 
-// grid: (ceil(d2p/32), ceil(d3/32), L or 1); block 32x8.  Reads coalesce along j, writes along k.
+// Tile: 128 k × 32 j; grid: (ceil(d2p/128), ceil(d3/32), L or 1); block 256 = 32 (j) × 8.  Reads
+// coalesce along j (a warp reads 32 consecutive entries of U's row k); the digits are transposed
+// through shared memory ([32 j][132 B]: the 33-word row pitch makes the byte writes of a warp hit
+// 32 distinct banks) and written as one 16-byte store per thread (a warp writes 4 rows j of
+// 128 contiguous k bytes).
+constexpr int PLAIN_TK = 128, PLAIN_TJ = 32, PLAIN_PITCH = PLAIN_TK + 4;
 __global__ void __launch_bounds__(256) k_plain(const __grid_constant__ PlainParams P) {
-  __shared__ int8_t t[4][32][33];
+  __shared__ __align__(16) uint8_t t[4][PLAIN_TJ][PLAIN_PITCH];
   const int l = blockIdx.z;
-  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * 32, j0 = static_cast<int64_t>(blockIdx.y) * 32;
+  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * PLAIN_TK, j0 = static_cast<int64_t>(blockIdx.y) * PLAIN_TJ;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  for (int kk = ty; kk < 32; kk += 8) {
-    const int64_t k = k0 + kk, j = j0 + tx;
+  const int64_t j = j0 + tx;
+  for (int kk = ty; kk < PLAIN_TK; kk += 8) {
+    const int64_t k = k0 + kk;
+    const bool in = k < P.d2 && j < P.d3;
     int64_t x = 0;
-    if (k < P.d2 && j < P.d3) {
+    if (in) {
       if (P.rns) {
         const uint32_t p = P.p_arr[l];
         const uint32_t v = P.ures[(static_cast<int64_t>(l) * P.d2 + k) * P.d3 + j];
@@ -306,20 +335,21 @@ __global__ void __launch_bounds__(256) k_plain(const __grid_constant__ PlainPara
       }
     }
     if (P.unsigned_plane) {
-      t[0][kk][tx] = (k < P.d2 && j < P.d3) ? static_cast<int8_t>(static_cast<uint8_t>(x + P.u_offset)) : 0;
+      t[0][tx][kk] = in ? static_cast<uint8_t>(x + P.u_offset) : 0;
     } else {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) t[i][kk][tx] = (i < P.kU) ? balanced_digit(x) : 0;
+      for (int i = 0; i < 4; ++i) t[i][tx][kk] = (i < P.kU) ? static_cast<uint8_t>(balanced_digit(x)) : 0;
     }
   }
   __syncthreads();
-  for (int jj = ty; jj < 32; jj += 8) {
-    const int64_t j = j0 + jj, k = k0 + tx;
-    if (j < P.d3 && k < P.d2p) {
-      for (int i = 0; i < P.kU; ++i) {
-        const int64_t plane = static_cast<int64_t>(l) * P.kU + i;
-        P.planes[(plane * P.d3 + j) * P.d2p + k] = t[i][tx][jj];
-      }
+  // thread → row jj = threadIdx / 8, 16-byte chunk c = threadIdx % 8 (k = k0 + 16c .. +15)
+  const int jj = threadIdx.x >> 3, c = threadIdx.x & 7;
+  const int64_t jw = j0 + jj, kw = k0 + 16 * c;
+  if (jw < P.d3 && kw < P.d2p) {  // d2p is a multiple of 16 (of 128), so a chunk never straddles it
+    for (int i = 0; i < P.kU; ++i) {
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(&t[i][jj][16 * c]);
+      const int64_t plane = static_cast<int64_t>(l) * P.kU + i;
+      *reinterpret_cast<uint4*>(P.planes + (plane * P.d3 + jw) * P.d2p + kw) = make_uint4(src[0], src[1], src[2], src[3]);
     }
   }
 }
