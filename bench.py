@@ -375,7 +375,8 @@ def run_ours(args, rank: int, world: int, local_rank: int, scaling: str = "stron
     ps, ct, U, gen_s = make_inputs(c, seed, max(1, cores // world))
 
     want = args.split_overlap == "on" or (args.split_overlap == "auto" and c.d3 <= 8192)
-    inkernel_split = want and not args.rescale and len(ps) >= 2 and not args.overlap
+    # only the split + GEMM path has a split pass to hide (d3 <= 256 runs the fused kernels)
+    inkernel_split = want and not args.rescale and len(ps) >= 2 and not args.overlap and c.d3 > 256
     eng = CpmmEngine(ctpt.Spec(c.fmt, c.N, c.d1, c.d2, c.d3, ps, rescale=int(args.rescale),
                                split_overlap=int(inkernel_split), raster_group=args.raster_group), dev)
     a_dev = torch.from_numpy(ct.a_polys.view(np.int32)).to(dev)
@@ -392,7 +393,7 @@ def run_ours(args, rank: int, world: int, local_rank: int, scaling: str = "stron
     stream = torch.cuda.current_stream(dev)
     d3l, ra = sizes.d3_loc, sizes.rows_A
     # the library's automatic kernel choice (include/ctpt.h ctpt_kernel), stage by stage
-    fused = (d3l <= 256 and kU == 1 and not (spec.u_unsigned and spec.u_offset) and not args.rescale)
+    fused = d3l <= 256 and kU == 1 and not args.rescale  # the fused / raw-byte kernels (no limb split pass)
     n_ev = 1 if args.rescale else len(ps)
 
     mv = fused and kernel_path(d3l, kU, spec.u_unsigned, spec.u_offset, c.R) == "mv"
@@ -774,11 +775,14 @@ def gpu_uuid_of(dev) -> str | None:
 
 def kernel_path(d3_loc: int, kU: int, u_unsigned: int, u_offset: int, R: int = 1 << 30, sms: int = 148) -> str:
     """The library's automatic kernel choice for one prime (include/ctpt.h ctpt_kernel; ctpt.cu
-    choose_path): the raw-byte kernel for d3_loc <= 32 with fewer 64-row tiles than SMs, the fused
-    skinny kernels up to 256 columns, else split + GEMM."""
-    if kU == 1 and d3_loc <= 256 and not (u_unsigned and u_offset):
-        return "mv" if d3_loc <= 32 and (R + 63) // 64 < sms else "fused"
-    return "split_gemm"
+    choose_path): the raw-byte kernel for d3_loc <= 32 with fewer 64-row tiles than SMs (and no
+    unsigned-U row correction), the limbs-in-TMEM skinny kernel up to 256 columns (it forms the u8
+    plane's row sums itself), else split + GEMM."""
+    if kU != 1 or d3_loc > 256:
+        return "split_gemm"
+    if d3_loc <= 32 and not (u_unsigned and u_offset) and (R + 63) // 64 < sms:
+        return "mv"
+    return "fused"
 
 
 def launch_unit(spec_u, eng, au, bu, stream, ev=None):

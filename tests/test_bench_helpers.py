@@ -23,7 +23,9 @@ def test_kernel_path_mirrors_the_library_choice():
     """bench.kernel_path = ctpt.cu choose_path under CTPT_KERNEL_AUTO (launch counting, roofline)."""
     assert bench.kernel_path(16384, 1, 1, 8) == "split_gemm"   # c3: u8 plane with offset
     assert bench.kernel_path(256, 1, 0, 0) == "fused"
-    assert bench.kernel_path(256, 1, 1, 8) == "split_gemm"     # fused kernel has no row correction
+    assert bench.kernel_path(256, 1, 1, 8) == "fused"          # the fused kernel forms the row sums itself
+    assert bench.kernel_path(257, 1, 1, 8) == "split_gemm"
+    assert bench.kernel_path(32, 1, 1, 8, R=8192) == "fused"    # raw-byte kernel: no row correction
     assert bench.kernel_path(32, 1, 0, 0, R=8192) == "mv"       # 128 tiles of 64 rows < 148 SMs
     assert bench.kernel_path(32, 1, 0, 0, R=65536) == "fused"   # enough rows: limbs-in-TMEM kernel
     assert bench.kernel_path(100, 2, 0, 0) == "split_gemm"     # kU > 1
