@@ -69,6 +69,8 @@ def parse():
                          "fused into the other primes' epilogues")
     ap.add_argument("--raster-group", type=int, default=0,
                     help="k_gemm_tc raster group in j-tiles (ctpt_problem.raster_group; 0 = the library's choice)")
+    ap.add_argument("--max-ctas", type=int, default=0,
+                    help="cap on the persistent grids (ctpt_problem.max_ctas; 0 = one CTA per SM)")
     ap.add_argument("--mode", default="auto", choices=["auto", "strong", "weak"],
                     help="auto: ONE problem strong-scaled over the ranks (N > 1, or a config whose inputs and "
                          "outputs do not fit one device-resident problem, i.e. c5: the primes stream through "
@@ -378,7 +380,8 @@ def run_ours(args, rank: int, world: int, local_rank: int, scaling: str = "stron
     # only the split + GEMM path has a split pass to hide (d3 <= 256 runs the fused kernels)
     inkernel_split = want and not args.rescale and len(ps) >= 2 and not args.overlap and c.d3 > 256
     eng = CpmmEngine(ctpt.Spec(c.fmt, c.N, c.d1, c.d2, c.d3, ps, rescale=int(args.rescale),
-                               split_overlap=int(inkernel_split), raster_group=args.raster_group), dev)
+                               split_overlap=int(inkernel_split), raster_group=args.raster_group,
+                               max_ctas=args.max_ctas), dev)
     a_dev = torch.from_numpy(ct.a_polys.view(np.int32)).to(dev)
     b_dev = torch.from_numpy(ct.b_polys.view(np.int32)).to(dev)
     eng.layout(a_dev, b_dev, validate=True)
