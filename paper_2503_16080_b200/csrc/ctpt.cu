@@ -804,6 +804,24 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
   const int64_t fit = (32LL << 20) / std::max<int64_t>(per_panel, 1);
   P.group_j = static_cast<int32_t>(std::min<int64_t>(std::max<int64_t>(fit, TC_GROUP_J_DEFAULT), P.tiles_j));
   if (g.raster_group > 0) P.group_j = g.raster_group;
+  // Serpentine K order when one wave's operand footprint exceeds L2: per K byte a wave touches the
+  // group's U^T panel (128·group_j B) and the X limb rows of ≈ SMs / group_j r-tiles (256 B each).
+  // c4 / c5 (K = 32768): 144 MB per wave, the next wave would re-read the whole panel from DRAM —
+  // reversing K on odd waves starts it on the lines the last wave touched (c4 GEMM: 33.4 → 27.9 GB
+  // of DRAM reads per launch, bench +1.0 %); c3 (72 MB, fits) loses 1.5 % with it, so it stays off
+  // there (profiles/r02/serpentine/).
+  {
+    const double wave_bytes = static_cast<double>(P.num_kb) * TC_BLOCK_K *
+                              (static_cast<double>(TC_BLOCK_J) * P.group_j +
+                               4.0 * TC_BLOCK_R * static_cast<double>(num_sms()) / P.group_j);
+    P.serpentine = wave_bytes > 100.0e6 ? 1 : 0;
+  }
+#ifdef CTPT_TC_NO_SERPENTINE  // A/B measurement build only (tools/ab_build.py): K always ascending
+  P.serpentine = 0;
+#endif
+#ifdef CTPT_TC_SERPENTINE_ALWAYS
+  P.serpentine = 1;
+#endif
   P.u_unsigned = g.u_unsigned;
   P.m = m;
   // TMA-store epilogue: a tile's 64 rows must lie inside A' or inside B' (rows_A, d1 multiples of

@@ -92,6 +92,9 @@ struct TcParams {
   int32_t num_tiles;
   int32_t group_j;    // tiles visited in groups of group_j j-tiles (L2 reuse of U panels)
   int32_t u_unsigned; // U plane is u8 (U + u_offset) instead of balanced s8 digits
+  int32_t serpentine; // odd waves (tile iteration (tile − blockIdx) / grid) walk K backwards, so the U^T
+                      // panel lines a wave touched last are the next wave's first reads (L2 reuse when
+                      // the group's U^T panel + a wave's X rows exceed L2, e.g. K = 32768)
   int32_t tma_store;  // epilogue stages each 32 × 32 output block in shared memory and writes it with
                       // one TMA store (tmAU / tmBU); needs rows_A and d1 multiples of 64 (a tile's 64
                       // rows lie inside A' or B') and device-local outputs; else 16-byte STG stores
@@ -157,10 +160,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int32_t tile = blockIdx.x; tile < P.num_tiles; tile += gridDim.x) {
+      int32_t wave = 0;
+      for (int32_t tile = blockIdx.x; tile < P.num_tiles; tile += gridDim.x, ++wave) {
         int32_t tj, tr;
         tc_tile_coords(tile, P, tj, tr);
-        for (int32_t kb = 0; kb < P.num_kb; ++kb) {
+        const bool back = P.serpentine && (wave & 1);
+        for (int32_t kb0 = 0; kb0 < P.num_kb; ++kb0) {
+          // the MMA warp accumulates in stage order; integer sums do not depend on the K order
+          const int32_t kb = back ? P.num_kb - 1 - kb0 : kb0;
           mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t su = sbase + stage * TC_STAGE_BYTES;
           mbar_arrive_expect_tx(full_bar(stage), TC_STAGE_BYTES);
