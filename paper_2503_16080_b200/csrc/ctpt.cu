@@ -819,7 +819,7 @@ ctpt_status launch_gemm(const GemmArgs& g, cudaStream_t st, bool simt) {
 #ifdef CTPT_TC_NO_SERPENTINE  // A/B measurement build only (tools/ab_build.py): K always ascending
   P.serpentine = 0;
 #endif
-#ifdef CTPT_TC_SERPENTINE_ALWAYS
+#ifdef CTPT_TC_SERPENTINE_ALWAYS  // A/B measurement build only
   P.serpentine = 1;
 #endif
   P.u_unsigned = g.u_unsigned;
