@@ -517,10 +517,10 @@ def run_ours(args, rank: int, world: int, local_rank: int, scaling: str = "stron
     gemm_avg_s = statistics.mean(gemm_ms) / 1e3
     limb_macs_launch = 4 * kU * c.R * c.d2 * c.d3 * (len(ps) if args.rescale else 1)
     achieved_tops = 2 * limb_macs_launch / gemm_avg_s / 1e12
-    # int8 = 2 x bf16 (the guide's nominal ratio).  Burst peak for a timed region shorter than
-    # MEASURED_PEAKS' 4-s sustained loop (the clocks have not settled at the power cap yet),
-    # sustained peak for longer runs.
-    peak_key = "bf16_tflops" if elapsed_ms < 2000.0 else "bf16_tflops_sustained"
+    # int8 = 2 x bf16 (the guide's nominal ratio).  Burst peak for a timed region well short of
+    # MEASURED_PEAKS' 4-s sustained loop (< 1.5 s: the clocks have not settled at the power cap yet),
+    # sustained peak for longer runs (c4's 20 steps take ~2.0 s: a 2-s cut flipped box to box).
+    peak_key = "bf16_tflops" if elapsed_ms < 1500.0 else "bf16_tflops_sustained"
     peak_tops = 2 * float(mp[peak_key])
     traffic = None
     try:
@@ -665,7 +665,7 @@ def cublaslt_ratio(limb_macs_per_s: float, elapsed_ms: float):
             pr = json.load(f)
     except OSError:
         return None
-    key = "burst_tops" if elapsed_ms < 2000.0 else "sustained_tops"
+    key = "burst_tops" if elapsed_ms < 1500.0 else "sustained_tops"
     return {"ratio": 2 * limb_macs_per_s / 1e12 / float(pr[key]), "cublaslt_tops": pr[key], "which": key}
 
 
@@ -981,7 +981,7 @@ def run_strong(args, rank: int, world: int, local_rank: int):
     unit_limb_macs = [4 * kU * c.R * c.d2 * u.ncols for u in mine]
     if paths == {"split_gemm"}:
         tops = [2 * m / (t / 1e3) / 1e12 for m, t in zip(unit_limb_macs * args.steps, gemm_ms)]
-        peak_key = "bf16_tflops" if ms * args.steps < 2000.0 else "bf16_tflops_sustained"
+        peak_key = "bf16_tflops" if ms * args.steps < 1500.0 else "bf16_tflops_sustained"
         ach = 2 * sum(unit_limb_macs) * args.steps / (sum(gemm_ms) / 1e3) / 1e12
         roof = {"bound": "tensor", "achieved": ach, "peak": 2 * float(mp[peak_key]), "unit": "TOP/s",
                 "frac": ach / (2 * float(mp[peak_key])), "traffic": None, "kernel": "k_gemm_tc",
@@ -1179,7 +1179,7 @@ def run_modmm(args, rank: int, world: int, local_rank: int):
     value = world * macs / (ms / 1e3)
     mp, which = peaks()
     tops = 2 * 16 * macs / (ms / 1e3) / 1e12
-    peak_key = "bf16_tflops" if ms * args.steps < 2000.0 else "bf16_tflops_sustained"
+    peak_key = "bf16_tflops" if ms * args.steps < 1500.0 else "bf16_tflops_sustained"
     result = {
         "metric": "Mod-PP-MM residue-MACs/s (full residues both sides, 16384^3 x 3 primes)", "value": value,
         "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
