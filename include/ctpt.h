@@ -270,7 +270,8 @@ ctpt_status ctpt_gemm_mv(const ctpt_problem* prob, int32_t l, const void* d_ctma
  * ctpt_layout + ctpt_matmul, but the per-column ciphertexts h_a_polys / h_b_polys (layouts as
  * for ctpt_layout) and the outputs h_AU / h_BU (layouts as for ctpt_matmul) live in host
  * memory.  The stacked X of each prime is processed in row chunks of `chunk_rows` (≤ 0: about
- * R/6, rounded to 64); the host→device copy of one chunk, the layout + split + GEMM of the
+ * R/6 rows, rounded to 64 and cut separately within A's and within B's rows, so no chunk straddles
+ * the two parts); the host→device copy of one chunk, the layout + split + GEMM of the
  * previous one and the device→host copy of the one before run concurrently (two internal
  * copy streams forked from and joined back into `stream`).  Host buffers must be page-locked
  * (cudaHostAlloc / cudaHostRegister) for the copies to overlap.  d_plain as for ctpt_matmul;

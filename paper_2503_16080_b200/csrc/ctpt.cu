@@ -1225,15 +1225,33 @@ namespace {
 struct HostPlan {
   int64_t chunk;  // rows of X per chunk (multiple of 64)
   size_t in_bytes, cm_bytes, limb_bytes, out_bytes, corr_bytes, mv_bytes, total;
+  std::vector<std::pair<int64_t, int64_t>> pieces;  // the row chunks [r0, r1) of one prime, in order
 };
 
 HostPlan host_plan(const Dims& d, int64_t chunk_rows) {
   HostPlan h;
-  // default: ~6 chunks per prime (c3: 97 ms/step = 86 % of the concurrent-PCIe floor, vs 110 ms
-  // with 4 chunks; profiles/r01/e2e_chunk_sweep.txt)
-  int64_t c = chunk_rows > 0 ? chunk_rows : (d.R + 5) / 6;
-  c = (c + 63) / 64 * 64;
-  c = std::max<int64_t>(64, std::min<int64_t>(c, (d.R + 63) / 64 * 64));
+  const int64_t Rr = (d.R + 63) / 64 * 64;
+  if (chunk_rows > 0) {  // fixed chunks of chunk_rows (rounded to 64); a chunk may straddle A / B
+    const int64_t c = std::max<int64_t>(64, std::min<int64_t>((chunk_rows + 63) / 64 * 64, Rr));
+    for (int64_t r0 = 0; r0 < d.R; r0 += c) h.pieces.emplace_back(r0, std::min(d.R, r0 + c));
+  } else {
+    // default: ~6 chunks per prime (c3: 97 ms/step = 86 % of the concurrent-PCIe floor, vs 110 ms
+    // with 4 chunks; profiles/r01/e2e_chunk_sweep.txt), cut separately within A's rows and B's rows
+    // (a chunk up to 5/4 of the target is not split), so no copy carries a few-hundred-row sliver
+    // of the other part: every 2-D copy moves the chunk's full width (an A part of rows_A ≤ 1.25 ×
+    // target rows is one copy whose width is the whole host pitch)
+    const int64_t target = std::max<int64_t>(64, ((d.R + 5) / 6 + 63) / 64 * 64);
+    const int64_t seg[2][2] = {{0, d.rows_A}, {d.rows_A, d.R}};
+    for (const auto& sg : seg) {
+      const int64_t len = sg[1] - sg[0];
+      if (len <= 0) continue;
+      const int64_t n = len * 4 <= target * 5 ? 1 : (len + target - 1) / target;
+      const int64_t piece = ((len + n - 1) / n + 63) / 64 * 64;
+      for (int64_t r0 = sg[0]; r0 < sg[1]; r0 += piece) h.pieces.emplace_back(r0, std::min(sg[1], r0 + piece));
+    }
+  }
+  int64_t c = 64;
+  for (const auto& pc : h.pieces) c = std::max(c, pc.second - pc.first);
   h.chunk = c;
   h.in_bytes = align256(static_cast<size_t>(d.d2) * c * 4);
   h.cm_bytes = align256(static_cast<size_t>(c) * d.d2p * 4);
@@ -1426,9 +1444,9 @@ ctpt_status ctpt_matmul_host_units(int32_t n, const ctpt_problem* probs, const u
       const uint32_t* b_l = h_bs[u] + static_cast<int64_t>(l) * d.d2 * d.d1;
       uint32_t* AU_l = h_AUs[u] + static_cast<int64_t>(l) * d.d3_loc * d.rows_A;
       uint32_t* BU_l = h_BUs[u] + static_cast<int64_t>(l) * d.d3_loc * d.d1;
-      for (int64_t r0 = 0; r0 < d.R; r0 += hp.chunk, ++it) {
+      for (size_t pi = 0; pi < hp.pieces.size(); ++pi, ++it) {
         const int b = static_cast<int>(it & 1);
-        const int64_t r1 = std::min(d.R, r0 + hp.chunk), rows = r1 - r0;
+        const int64_t r0 = hp.pieces[pi].first, r1 = hp.pieces[pi].second, rows = r1 - r0;
         const int64_t na = std::max<int64_t>(0, std::min(r1, d.rows_A) - r0), nb = rows - na;
         const int64_t rb0 = r0 + na - d.rows_A;  // first B row of the chunk (if nb > 0)
         // 1. host → device: the chunk's rows of every ciphertext column, packed col-major [d2][rows]
