@@ -1,7 +1,6 @@
 #!/bin/bash
-# Round 2, HEAD (aligned host chunks): the -m gpu suite, smoke, the bench
-# lines, the reference arm, the default bench's launch list, and the DRAM bytes of c4's GEMM with the
-# next prime's split inside (the bench default for c4; profiles/gemm_dram_bytes.json).
+# Round 2, HEAD (aligned host chunks): the bench lines, the reference arm, smoke, the -m gpu suite
+# and the default bench's launch list.
 O=gpurun_out/r02/final5; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
 timeout 900 python bench.py > $O/bench_c3.json 2> $O/bench_c3.err; echo "bench_rc=$?" >> $O/bench_c3.err
