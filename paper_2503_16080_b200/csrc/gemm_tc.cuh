@@ -129,9 +129,17 @@ __device__ __forceinline__ void tc_tile_coords(int32_t tile, const TcParams& P, 
 }
 
 // One CTA's walk over its (tile, k-block) steps: tiles blockIdx.x, + gridDim.x, …; K ascending, or
-// descending on odd waves with P.serpentine.
+// descending on odd waves with P.serpentine.  The tile's coordinates are computed once per tile
+// (tc_tile_coords divides; per k-block that made the single producer thread the kernel's pace).
 struct TcStep {
-  int32_t tile, wave, kb0;
+  int32_t tile, wave, kb0, tj, tr;
+  __device__ __forceinline__ void start(int32_t first_tile, const TcParams& P) {
+    tile = first_tile;
+    wave = 0;
+    kb0 = 0;
+    tj = tr = 0;
+    if (tile < P.num_tiles) tc_tile_coords(tile, P, tj, tr);
+  }
   __device__ __forceinline__ int32_t kb(const TcParams& P) const {
     return (P.serpentine && (wave & 1)) ? P.num_kb - 1 - kb0 : kb0;
   }
@@ -140,6 +148,7 @@ struct TcStep {
       kb0 = 0;
       tile += gridDim.x;
       ++wave;
+      if (tile < P.num_tiles) tc_tile_coords(tile, P, tj, tr);
     }
   }
 };
@@ -203,28 +212,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // MMAs while the L2-resident U^T runs TC_US ahead (no deadlock: X step n waits for the MMA of
     // step n − TC_XS, whose U^T was issued at step n − TC_XS + TC_XS − TC_US ≤ n − 1).
     if (lane == 0) {
-      TcStep sx{static_cast<int32_t>(blockIdx.x), 0, 0}, su = sx;
+      TcStep sx, su;
+      sx.start(static_cast<int32_t>(blockIdx.x), P);
+      su = sx;
       int xs = 0, us = 0;
       uint32_t xph = 0, uph = 0;
       int32_t n = 0;
       while (sx.tile < P.num_tiles || su.tile < P.num_tiles) {
         if (sx.tile < P.num_tiles) {
-          int32_t tj, tr;
-          tc_tile_coords(sx.tile, P, tj, tr);
           const int32_t kb = sx.kb(P);  // the MMA warp accumulates in stage order; integer sums do not depend on K order
           mbar_wait(xempty_bar(xs), xph ^ 1);
           mbar_arrive_expect_tx(xfull_bar(xs), TC_X_BYTES);
-          tma_load_5d(xbase + xs * TC_X_BYTES, &tmX, xfull_bar(xs), 0, 0, 0, kb, tr);  // one 32-KB limb tile
+          tma_load_5d(xbase + xs * TC_X_BYTES, &tmX, xfull_bar(xs), 0, 0, 0, kb, sx.tr);  // one 32-KB limb tile
           if (++xs == TC_XS) { xs = 0; xph ^= 1; }
           sx.next(P);
         }
         if (su.tile < P.num_tiles && (n >= TC_XS - TC_US || sx.tile >= P.num_tiles)) {
-          int32_t tj, tr;
-          tc_tile_coords(su.tile, P, tj, tr);
           const int32_t kb = su.kb(P);
           mbar_wait(uempty_bar(us), uph ^ 1);
           mbar_arrive_expect_tx(ufull_bar(us), TC_U_BYTES);
-          tma_load_3d(ubase + us * TC_U_BYTES, &tmU, ufull_bar(us), kb * TC_BLOCK_K, P.j_off + tj * TC_BLOCK_J, P.plane);
+          tma_load_3d(ubase + us * TC_U_BYTES, &tmU, ufull_bar(us), kb * TC_BLOCK_K, P.j_off + su.tj * TC_BLOCK_J, P.plane);
           if (++us == TC_US) { us = 0; uph ^= 1; }
           su.next(P);
         }
