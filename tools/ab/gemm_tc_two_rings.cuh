@@ -11,7 +11,7 @@
 //   D = 128 lanes × 256 int32 columns: lane j holds C_ℓ[r][j] at column ℓ·64 + r, so one
 //   epilogue thread owns all four limb sums of its 64 outputs — recombination needs no
 //   data exchange.  One MMA (M=128, N=256, K=32) per 32-byte K step.
-// Tiles: 128 (j) × 64 (r) outputs, K-block 128 bytes, 4-stage TMA→SMEM ring (48 KB/stage),
+// Tiles: 128 (j) × 64 (r) outputs, K-block 128 bytes, TMA→SMEM rings for U^T (16 KB/stage) and X (32 KB/stage),
 // double-buffered TMEM accumulators (2 × 256 columns = all 512).
 // Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator, w4–7 epilogue.
 // Persistent: grid = min(#tiles, #SMs); tiles visited in groups of GROUP_J j-tiles so the
@@ -27,18 +27,34 @@ namespace ctpt {
 constexpr int TC_BLOCK_J = 128;   // MMA M (output columns per tile)
 constexpr int TC_BLOCK_R = 64;    // rows of X per tile (× 4 limbs = MMA N = 256)
 constexpr int TC_BLOCK_K = 128;   // bytes of K per stage (one 128-B swizzle row)
-constexpr int TC_STAGES = 4;
+// Two TMA rings: U^T tiles (L2-resident, 16 KB) and X limb tiles (streamed from DRAM, 32 KB), each
+// with its own depth, so the operand that misses L2 can run further ahead (A/B builds:
+// -DCTPT_TC_XS=5 -DCTPT_TC_US=3 -DCTPT_TC_OUT_HALVES=1; default 4 + 4 stages, two staging halves).
+#ifndef CTPT_TC_XS
+#define CTPT_TC_XS 4
+#endif
+#ifndef CTPT_TC_US
+#define CTPT_TC_US 4
+#endif
+#ifndef CTPT_TC_OUT_HALVES
+#define CTPT_TC_OUT_HALVES 2
+#endif
+constexpr int TC_XS = CTPT_TC_XS;  // X limb-tile stages
+constexpr int TC_US = CTPT_TC_US;  // U^T-tile stages
+static_assert(TC_XS >= TC_US, "the X ring runs ahead of the U^T ring");
 constexpr int TC_MMA_K = 32;      // K per kind::i8 MMA
 constexpr int TC_U_BYTES = TC_BLOCK_J * TC_BLOCK_K;            // 16 KB
 constexpr int TC_X_BYTES = 4 * TC_BLOCK_R * TC_BLOCK_K;        // 32 KB
-constexpr int TC_STAGE_BYTES = TC_U_BYTES + TC_X_BYTES;        // 48 KB
+constexpr int TC_RING_BYTES = TC_US * TC_U_BYTES + TC_XS * TC_X_BYTES;  // 192 KB (4 + 4)
 constexpr int TC_ACC_COLS = 4 * TC_BLOCK_R;                    // 256
 constexpr int TC_THREADS = 256;
-// TMA-store epilogue: per epilogue warp two 4-KB staging halves ([32 columns j][32 rows r] uint32,
-// SWIZZLE_128B), one TMA store per half
+// TMA-store epilogue: per epilogue warp TC_OUT_HALVES 4-KB staging buffers ([32 columns j][32 rows
+// r] uint32, SWIZZLE_128B), one TMA store per 32-row half
 constexpr int TC_OUT_HALF_BYTES = 32 * 32 * 4;
-constexpr int TC_OUT_BYTES = 4 * 2 * TC_OUT_HALF_BYTES;         // 32 KB
-constexpr int TC_SMEM_BYTES = TC_STAGES * TC_STAGE_BYTES + TC_OUT_BYTES + 256 + 1024;
+constexpr int TC_OUT_HALVES = CTPT_TC_OUT_HALVES;
+constexpr int TC_OUT_BYTES = 4 * TC_OUT_HALVES * TC_OUT_HALF_BYTES;  // 32 KB
+constexpr int TC_SMEM_BYTES = TC_RING_BYTES + TC_OUT_BYTES + 256 + 1024;
+static_assert(TC_SMEM_BYTES <= 232448, "k_gemm_tc shared memory exceeds 227 KB");
 constexpr int TC_GROUP_J_DEFAULT = 16;  // measured best of {8,16,32,64,128} on c3 (profiles/r01)
 
 // The limb split of the NEXT prime, run by the GEMM's two otherwise idle warps (2 and 3) while
@@ -112,6 +128,31 @@ __device__ __forceinline__ void tc_tile_coords(int32_t tile, const TcParams& P, 
   tr = rem / gj;
 }
 
+// One CTA's walk over its (tile, k-block) steps: tiles blockIdx.x, + gridDim.x, …; K ascending, or
+// descending on odd waves with P.serpentine.  The tile's coordinates are computed once per tile
+// (tc_tile_coords divides; per k-block that made the single producer thread the kernel's pace).
+struct TcStep {
+  int32_t tile, wave, kb0, tj, tr;
+  __device__ __forceinline__ void start(int32_t first_tile, const TcParams& P) {
+    tile = first_tile;
+    wave = 0;
+    kb0 = 0;
+    tj = tr = 0;
+    if (tile < P.num_tiles) tc_tile_coords(tile, P, tj, tr);
+  }
+  __device__ __forceinline__ int32_t kb(const TcParams& P) const {
+    return (P.serpentine && (wave & 1)) ? P.num_kb - 1 - kb0 : kb0;
+  }
+  __device__ __forceinline__ void next(const TcParams& P) {
+    if (++kb0 == P.num_kb) {
+      kb0 = 0;
+      tile += gridDim.x;
+      ++wave;
+      if (tile < P.num_tiles) tc_tile_coords(tile, P, tj, tr);
+    }
+  }
+};
+
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmX,
               const __grid_constant__ CUtensorMap tmAU, const __grid_constant__ CUtensorMap tmBU,
@@ -119,15 +160,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
-  const uint32_t out_base = sbase + TC_STAGES * TC_STAGE_BYTES;  // 1024-B aligned (SWIZZLE_128B atoms)
+  const uint32_t ubase = sbase;                            // U^T ring: TC_US × 16 KB
+  const uint32_t xbase = sbase + TC_US * TC_U_BYTES;       // X ring: TC_XS × 32 KB
+  const uint32_t out_base = sbase + TC_RING_BYTES;  // 1024-B aligned (SWIZZLE_128B atoms)
   const uint32_t bar_base = out_base + TC_OUT_BYTES;
-  auto full_bar = [&](int s) { return bar_base + 8u * s; };
-  auto empty_bar = [&](int s) { return bar_base + 8u * (TC_STAGES + s); };
-  auto tfull_bar = [&](int b) { return bar_base + 8u * (2 * TC_STAGES + b); };
-  auto tempty_bar = [&](int b) { return bar_base + 8u * (2 * TC_STAGES + 2 + b); };
-  const uint32_t tmem_slot = bar_base + 8u * (2 * TC_STAGES + 4);
-  uint32_t* tmem_slot_ptr =
-      reinterpret_cast<uint32_t*>(smem + TC_STAGES * TC_STAGE_BYTES + TC_OUT_BYTES + 8 * (2 * TC_STAGES + 4));
+  auto xfull_bar = [&](int s) { return bar_base + 8u * s; };
+  auto xempty_bar = [&](int s) { return bar_base + 8u * (TC_XS + s); };
+  auto ufull_bar = [&](int s) { return bar_base + 8u * (2 * TC_XS + s); };
+  auto uempty_bar = [&](int s) { return bar_base + 8u * (2 * TC_XS + TC_US + s); };
+  constexpr int NB = 2 * TC_XS + 2 * TC_US;
+  auto tfull_bar = [&](int b) { return bar_base + 8u * (NB + b); };
+  auto tempty_bar = [&](int b) { return bar_base + 8u * (NB + 2 + b); };
+  const uint32_t tmem_slot = bar_base + 8u * (NB + 4);
+  static_assert(8 * (NB + 5) <= 256, "barrier block");
+  uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(smem + TC_RING_BYTES + TC_OUT_BYTES + 8 * (NB + 4));
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -139,9 +185,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tma_prefetch(&tmAU);
       tma_prefetch(&tmBU);
     }
-    for (int s = 0; s < TC_STAGES; ++s) {
-      mbar_init(full_bar(s), 1);
-      mbar_init(empty_bar(s), 1);
+    for (int s = 0; s < TC_XS; ++s) {
+      mbar_init(xfull_bar(s), 1);
+      mbar_init(xempty_bar(s), 1);
+    }
+    for (int s = 0; s < TC_US; ++s) {
+      mbar_init(ufull_bar(s), 1);
+      mbar_init(uempty_bar(s), 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull_bar(b), 1);
@@ -157,32 +207,43 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
+    // One thread walks the CTA's (tile, k-block) sequence twice: X limb tiles for step n and U^T
+    // tiles for step n − (TC_XS − TC_US), so the DRAM-streamed X runs TC_XS stages ahead of the
+    // MMAs while the L2-resident U^T runs TC_US ahead (no deadlock: X step n waits for the MMA of
+    // step n − TC_XS, whose U^T was issued at step n − TC_XS + TC_XS − TC_US ≤ n − 1).
     if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      int32_t wave = 0;
-      for (int32_t tile = blockIdx.x; tile < P.num_tiles; tile += gridDim.x, ++wave) {
-        int32_t tj, tr;
-        tc_tile_coords(tile, P, tj, tr);
-        const bool back = P.serpentine && (wave & 1);
-        for (int32_t kb0 = 0; kb0 < P.num_kb; ++kb0) {
-          // the MMA warp accumulates in stage order; integer sums do not depend on the K order
-          const int32_t kb = back ? P.num_kb - 1 - kb0 : kb0;
-          mbar_wait(empty_bar(stage), phase ^ 1);
-          const uint32_t su = sbase + stage * TC_STAGE_BYTES;
-          mbar_arrive_expect_tx(full_bar(stage), TC_STAGE_BYTES);
-          tma_load_3d(su, &tmU, full_bar(stage), kb * TC_BLOCK_K, P.j_off + tj * TC_BLOCK_J, P.plane);
-          tma_load_5d(su + TC_U_BYTES, &tmX, full_bar(stage), 0, 0, 0, kb, tr);  // one 32-KB limb tile
-          if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
+      TcStep sx, su;
+      sx.start(static_cast<int32_t>(blockIdx.x), P);
+      su = sx;
+      int xs = 0, us = 0;
+      uint32_t xph = 0, uph = 0;
+      int32_t n = 0;
+      while (sx.tile < P.num_tiles || su.tile < P.num_tiles) {
+        if (sx.tile < P.num_tiles) {
+          const int32_t kb = sx.kb(P);  // the MMA warp accumulates in stage order; integer sums do not depend on K order
+          mbar_wait(xempty_bar(xs), xph ^ 1);
+          mbar_arrive_expect_tx(xfull_bar(xs), TC_X_BYTES);
+          tma_load_5d(xbase + xs * TC_X_BYTES, &tmX, xfull_bar(xs), 0, 0, 0, kb, sx.tr);  // one 32-KB limb tile
+          if (++xs == TC_XS) { xs = 0; xph ^= 1; }
+          sx.next(P);
         }
+        if (su.tile < P.num_tiles && (n >= TC_XS - TC_US || sx.tile >= P.num_tiles)) {
+          const int32_t kb = su.kb(P);
+          mbar_wait(uempty_bar(us), uph ^ 1);
+          mbar_arrive_expect_tx(ufull_bar(us), TC_U_BYTES);
+          tma_load_3d(ubase + us * TC_U_BYTES, &tmU, ufull_bar(us), kb * TC_BLOCK_K, P.j_off + su.tj * TC_BLOCK_J, P.plane);
+          if (++us == TC_US) { us = 0; uph ^= 1; }
+          su.next(P);
+        }
+        ++n;
       }
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
     if (lane == 0) {
       const uint32_t idesc = idesc_i8(TC_BLOCK_J, TC_ACC_COLS, /*a_signed=*/!P.u_unsigned, /*b_signed=*/false);
-      int stage = 0;
-      uint32_t phase = 0;
+      int xs = 0, us = 0;
+      uint32_t xph = 0, uph = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int32_t tile = blockIdx.x; tile < P.num_tiles; tile += gridDim.x) {
@@ -190,17 +251,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * TC_ACC_COLS;
         for (int32_t kb = 0; kb < P.num_kb; ++kb) {
-          mbar_wait(full_bar(stage), phase);
+          mbar_wait(ufull_bar(us), uph);
+          mbar_wait(xfull_bar(xs), xph);
           tc_fence_after();
-          const uint32_t su = sbase + stage * TC_STAGE_BYTES;
+          const uint32_t sa = ubase + us * TC_U_BYTES;
+          const uint32_t sb = xbase + xs * TC_X_BYTES;
 #pragma unroll
           for (int kk = 0; kk < TC_BLOCK_K / TC_MMA_K; ++kk) {
-            const uint64_t ad = umma_desc_sw128(su + kk * TC_MMA_K);
-            const uint64_t bd = umma_desc_sw128(su + TC_U_BYTES + kk * TC_MMA_K);
+            const uint64_t ad = umma_desc_sw128(sa + kk * TC_MMA_K);
+            const uint64_t bd = umma_desc_sw128(sb + kk * TC_MMA_K);
             mma_i8(d_tmem, ad, bd, idesc, (kb | kk) != 0);
           }
-          mma_commit(empty_bar(stage));  // frees the SMEM stage once these MMAs have read it
-          if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
+          mma_commit(uempty_bar(us));  // frees the SMEM stages once these MMAs have read them
+          mma_commit(xempty_bar(xs));
+          if (++us == TC_US) { us = 0; uph ^= 1; }
+          if (++xs == TC_XS) { xs = 0; xph ^= 1; }
         }
         mma_commit(tfull_bar(acc));  // accumulator ready for the epilogue
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
@@ -212,7 +277,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else {
     // ---------------------------------------------------------------- epilogue (warps 4–7)
     const int quad = warp & 3;  // TMEM lanes [32·quad, 32·quad + 32)
-    const uint32_t stg = out_base + quad * 2 * TC_OUT_HALF_BYTES;  // this warp's two staging halves
+    const uint32_t stg = out_base + quad * TC_OUT_HALVES * TC_OUT_HALF_BYTES;  // this warp's staging buffers
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int32_t tile = blockIdx.x; tile < P.num_tiles; tile += gridDim.x) {
@@ -249,10 +314,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                                    static_cast<int32_t>(v2[i]), static_cast<int32_t>(v3[i]), P.m);
           const int64_t r0 = r_tile + h * 32;
           finish_rows<32>(P.o, P.m, j, r0, res, j < P.o.d3_loc);
-          const uint32_t buf = stg + h * TC_OUT_HALF_BYTES;
+          const uint32_t buf = stg + (h % TC_OUT_HALVES) * TC_OUT_HALF_BYTES;
           CTPT_CHECK(buf >= out_base && buf + TC_OUT_HALF_BYTES <= out_base + TC_OUT_BYTES);
           CTPT_CHECK(r0 + 32 <= (r0 < P.o.rows_A ? P.o.rows_A : P.o.rows_A + P.o.d1));  // inside A' or B
-          if (lane == 0) bulk_wait_read<1>();  // this half's previous store has read its buffer
+          if (lane == 0) bulk_wait_read<TC_OUT_HALVES - 1>();  // this buffer's previous store has read it
           __syncwarp();
 #pragma unroll
           for (int c = 0; c < 8; ++c)
