@@ -393,6 +393,8 @@ def test_general_U_residues_rns():
     (S, 64, 3, 300, 256, 2, 8, 128, (0, 0)),        # fused skinny kernel on each chunk
     (R, 512, 1, 200, 600, 1, 8, 320, (100, 101)),   # d3_loc = 1 (CP-Mv) column shard
     (A, 64, 4, 300, 520, 2, 8, 192, (0, 0)),        # unsigned-U plane: row sums per chunk
+    (S, 2048, 2, 130, 300, 2, 8, 0, (0, 0)),        # default chunks of >= 1024 rows: graded first / last chunk
+    (A, 2048, 4, 72, 64, 1, 8, 0, (0, 0)),          # the same through the fused skinny kernel, A / B parts
 ])
 def test_matmul_host_pipeline(fmt, N, k, d2, d3, L, u_bound, chunk, cols):
     """ctpt_matmul_host (host buffers, chunked 3-stream pipeline) == the oracle."""
