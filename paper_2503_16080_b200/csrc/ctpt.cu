@@ -1265,27 +1265,6 @@ HostPlan host_plan(const Dims& d, int64_t chunk_rows) {
   return h;
 }
 
-// Cut the first (head) or last piece of a prime's chunk list into a quarter (rounded to 64 rows, at
-// the outer end) and the rest; pieces under 1024 rows stay whole.  Sub-pieces are no larger than the
-// plan's chunk, so the staging buffers sized by host_plan cover them.
-#ifndef CTPT_HOST_GRADED
-#define CTPT_HOST_GRADED 0
-#endif
-[[maybe_unused]] void graded_split(std::vector<std::pair<int64_t, int64_t>>& pieces, bool head) {
-  if (pieces.empty()) return;
-  const auto pc = head ? pieces.front() : pieces.back();
-  const int64_t len = pc.second - pc.first;
-  if (len < 1024) return;
-  const int64_t q = (len / 4 + 63) / 64 * 64;
-  if (head) {
-    pieces.front() = {pc.first + q, pc.second};
-    pieces.insert(pieces.begin(), {pc.first, pc.first + q});
-  } else {
-    pieces.back() = {pc.first, pc.second - q};
-    pieces.emplace_back(pc.second - q, pc.second);
-  }
-}
-
 ctpt_status launch_layout_cols(const uint32_t* a_colmajor, uint32_t* x, int64_t rows, int64_t d2, int64_t d2p,
                                cudaStream_t st) {
   LayoutParams P;
@@ -1465,19 +1444,9 @@ ctpt_status ctpt_matmul_host_units(int32_t n, const ctpt_problem* probs, const u
       const uint32_t* b_l = h_bs[u] + static_cast<int64_t>(l) * d.d2 * d.d1;
       uint32_t* AU_l = h_AUs[u] + static_cast<int64_t>(l) * d.d3_loc * d.rows_A;
       uint32_t* BU_l = h_BUs[u] + static_cast<int64_t>(l) * d.d3_loc * d.d1;
-      std::vector<std::pair<int64_t, int64_t>> pieces = hp.pieces;
-#if CTPT_HOST_GRADED
-      // Graded ends (default plan only): the call's very first chunk and very last chunk are cut
-      // into a quarter + the rest, so the pipeline's fill (nothing overlaps the first host→device
-      // copy) and drain (nothing overlaps the last GEMM + device→host copy) are a quarter as long.
-      if (chunk_rows <= 0) {
-        if (u == 0 && l == 0) graded_split(pieces, /*head=*/true);
-        if (u == n - 1 && l == d.L - 1) graded_split(pieces, /*head=*/false);
-      }
-#endif
-      for (size_t pi = 0; pi < pieces.size(); ++pi, ++it) {
+      for (size_t pi = 0; pi < hp.pieces.size(); ++pi, ++it) {
         const int b = static_cast<int>(it & 1);
-        const int64_t r0 = pieces[pi].first, r1 = pieces[pi].second, rows = r1 - r0;
+        const int64_t r0 = hp.pieces[pi].first, r1 = hp.pieces[pi].second, rows = r1 - r0;
         const int64_t na = std::max<int64_t>(0, std::min(r1, d.rows_A) - r0), nb = rows - na;
         const int64_t rb0 = r0 + na - d.rows_A;  // first B row of the chunk (if nb > 0)
         // 1. host → device: the chunk's rows of every ciphertext column, packed col-major [d2][rows]
