@@ -178,19 +178,27 @@ __device__ void die_sched_setup(const TcParams& P, DieSched& S) {
       for (int w = 0; w < 2; ++w) {
         uint32_t z;
         asm volatile("and.b32 %0, %1, 0;" : "=r"(z) : "r"(v));  // opaque zero: the next load depends on this one
-        asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p + z) : "memory");
+        // an atomic is performed in the line's HOME partition (a plain load would hit the copy the
+        // first read left in this die's partition: every SM measured the same latency that way)
+        asm volatile("atom.global.add.u32 %0, [%1], 0;" : "=r"(v) : "l"(p + z) : "memory");
       }
       const long long c0 = clock64();
       for (int w = 0; w < 8; ++w) {
         uint32_t z;
         asm volatile("and.b32 %0, %1, 0;" : "=r"(z) : "r"(v));  // opaque zero: the next load depends on this one
-        asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p + z) : "memory");
+        // an atomic is performed in the line's HOME partition (a plain load would hit the copy the
+        // first read left in this die's partition: every SM measured the same latency that way)
+        asm volatile("atom.global.add.u32 %0, [%1], 0;" : "=r"(v) : "l"(p + z) : "memory");
       }
       const long long c1 = clock64();
       lat[k] = static_cast<uint32_t>(c1 - c0) + (v & 0u);
       sum += lat[k];
     }
     g_sm_die[sm] = lat[0] * 16u > sum ? 2 : 1;
+    if (blockIdx.x < 3 || blockIdx.x > gridDim.x - 3)
+      printf("ctpt die probe: cta %d sm %u lat/8 = %u %u %u %u %u %u %u %u | %u %u %u %u %u %u %u %u\n", blockIdx.x, sm,
+             lat[0] / 8, lat[1] / 8, lat[2] / 8, lat[3] / 8, lat[4] / 8, lat[5] / 8, lat[6] / 8, lat[7] / 8, lat[8] / 8,
+             lat[9] / 8, lat[10] / 8, lat[11] / 8, lat[12] / 8, lat[13] / 8, lat[14] / 8, lat[15] / 8);
     __threadfence();
     // everyone waits for the end of the stagger window before the GEMM's traffic starts
     while (die_timer_ns() - t0 < static_cast<uint64_t>(gridDim.x + 4) * 10000ull) {}
