@@ -176,22 +176,24 @@ __device__ void die_sched_setup(const TcParams& P, DieSched& S) {
       const char* p = base + static_cast<size_t>(k) * 4096 * 5;  // distinct 2-KB hash grains
       uint32_t v = 0;
       for (int w = 0; w < 2; ++w) {
-        uint32_t z;
-        asm volatile("and.b32 %0, %1, 0;" : "=r"(z) : "r"(v));  // opaque zero: the next load depends on this one
+        // the next access depends on this one's result: bit 31 of an output residue (< p < 2^31) is 0 in
+        // practice, which ptxas cannot know (it folded `and v, 0` and issued the atomics without waiting)
+        const uint32_t z = (v >> 31) << 2;
         // an atomic is performed in the line's HOME partition (a plain load would hit the copy the
         // first read left in this die's partition: every SM measured the same latency that way)
         asm volatile("atom.global.add.u32 %0, [%1], 0;" : "=r"(v) : "l"(p + z) : "memory");
       }
       const long long c0 = clock64();
       for (int w = 0; w < 8; ++w) {
-        uint32_t z;
-        asm volatile("and.b32 %0, %1, 0;" : "=r"(z) : "r"(v));  // opaque zero: the next load depends on this one
+        // the next access depends on this one's result: bit 31 of an output residue (< p < 2^31) is 0 in
+        // practice, which ptxas cannot know (it folded `and v, 0` and issued the atomics without waiting)
+        const uint32_t z = (v >> 31) << 2;
         // an atomic is performed in the line's HOME partition (a plain load would hit the copy the
         // first read left in this die's partition: every SM measured the same latency that way)
         asm volatile("atom.global.add.u32 %0, [%1], 0;" : "=r"(v) : "l"(p + z) : "memory");
       }
       const long long c1 = clock64();
-      lat[k] = static_cast<uint32_t>(c1 - c0) + (v & 0u);
+      lat[k] = static_cast<uint32_t>(c1 - c0) + (v >> 31);
       sum += lat[k];
     }
     g_sm_die[sm] = lat[0] * 16u > sum ? 2 : 1;

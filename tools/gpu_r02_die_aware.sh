@@ -1,7 +1,7 @@
 #!/bin/bash
 # EXPERIMENT: die-aware raster for k_gemm_tc (tools/ab/gemm_tc_die_aware.cuh) against the default, c3 and
 # c4 interleaved on one box; sampled parity from the bench's oracle leg; DRAM bytes per launch (ncu).
-O=gpurun_out/r02/die_aware2; mkdir -p $O
+O=gpurun_out/r02/die_aware3; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
 rm -rf /tmp/absrc /tmp/include && mkdir -p /tmp/absrc && cp -r paper_2503_16080_b200/csrc /tmp/absrc/ && cp -r include /tmp/include && \
   cp tools/ab/gemm_tc_die_aware.cuh /tmp/absrc/csrc/gemm_tc.cuh
@@ -33,7 +33,7 @@ done
 unset CTPT_LIB
 python - <<'PY'
 import json, glob
-for f in sorted(glob.glob('gpurun_out/r02/die_aware2/c*.json')):
+for f in sorted(glob.glob('gpurun_out/r02/die_aware3/c*.json')):
     try:
         d = json.loads(open(f).read().strip().splitlines()[-1])
     except Exception as e:
